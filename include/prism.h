@@ -1,0 +1,208 @@
+/*
+ * prism.h — C ABI of the B200-native PrismLLM hot path (graph expansion + replay).
+ *
+ * What this library computes (PAPER.md = /root/reference/PAPER.md, "P:NNNN" = its line):
+ *   - P:976-982 (§5.1, PrismTrace): the execution graph answers "what operations are executed,
+ *     in what order, and how long"; nodes are compute spans or communication events with a
+ *     duration; edges are *directional* ("one operation must complete before another begins")
+ *     or *synchronization* ("all participating nodes must reach the operation before any can
+ *     proceed (e.g., collectives or matched send-receive pairs)").
+ *   - P:1099 (§5.2): "execution graphs are identical across DP groups" -> the input is a set of
+ *     per-pipeline-stage op templates which prism_build_graph expands over TP/PP/DP/EP.
+ *   - P:1295-1298 (§6.1): virtual ranks "wait for the recorded duration" at compute nodes and
+ *     rendezvous at communication nodes -> prism_replay computes the ASAP schedule of every rank.
+ *   - P:1573 (§8.1) iteration time = elapsed time of one step; P:1578 peak memory as
+ *     max_memory_allocated -> prism_replay / prism_peak_memory.
+ * Readings of silent points (Z1..Z16) are listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *   - Every call returns prism_status (0 = PRISM_OK). Nothing is thrown across the ABI.
+ *     On error prism_last_error() returns a thread-local, human-readable detail string.
+ *   - Every time is int64 nanoseconds, every size int64 bytes. No floating point on the path.
+ *   - Input arrays are HOST pointers owned by the caller and copied during the call.
+ *   - Output arrays are HOST pointers owned by the caller, unless the name says _dev.
+ *   - A prism_graph owns its device buffers (allocated through prism_set_allocator's hooks,
+ *     cudaMallocAsync if none) and releases them in prism_destroy_graph.
+ *   - A graph handle is not thread-safe; distinct handles are independent.
+ *   - All device work runs on the stream given at build time (prism_build_opts.stream).
+ *   - There is no CPU fallback: without a CUDA device every compute call returns PRISM_E_CUDA.
+ */
+#ifndef PRISM_H
+#define PRISM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRISM_ABI_VERSION 1
+
+typedef int32_t prism_status;
+enum {
+  PRISM_OK = 0,
+  PRISM_E_INVALID_ARG = 1,       /* null pointer, size out of range, capacity too small       */
+  PRISM_E_INVALID_SPEC = 2,      /* topology invalid: degrees < 1, ep does not divide dp, ... */
+  PRISM_E_GA_TOO_SMALL = 3,      /* reserved (schedule generators)                */
+  PRISM_E_TEMPLATE_MISMATCH = 4, /* a sync group is missing members or members disagree      */
+  PRISM_E_DEADLOCK = 5,          /* the sync structure is cyclic: replay could never finish   */
+  PRISM_E_NEGATIVE_MEMORY = 6,   /* a rank's running allocation would drop below zero        */
+  PRISM_E_UNKNOWN_RANK = 7,      /* rank outside [0, world)                                   */
+  PRISM_E_UNKNOWN_LABEL = 8,     /* reserved (what-if label overrides)                       */
+  PRISM_E_NOT_REPLAYED = 9,      /* query before any prism_replay with record != 0            */
+  PRISM_E_OOM = 10,              /* device allocation failed                                  */
+  PRISM_E_CUDA = 11,             /* CUDA runtime error / no device                            */
+  PRISM_E_NCCL = 12              /* cross-shard exchange failed                               */
+};
+
+/* Opaque graph handle; owns device buffers. */
+typedef struct prism_graph_s *prism_graph_t;
+
+/* ---- input format ------------------------------------------------------------------------ */
+
+/* Node kinds ("a computation span or a communication event"). */
+enum { PRISM_KIND_COMPUTE = 0, PRISM_KIND_COLLECTIVE = 1, PRISM_KIND_P2P = 2 };
+
+/* Collective types (P:1444-1450 decomposition; informational except that all members of one
+ * group must agree on it). */
+enum { PRISM_COLL_AR = 0, PRISM_COLL_RS = 1, PRISM_COLL_AG = 2, PRISM_COLL_A2A = 3,
+       PRISM_COLL_BCAST = 4, PRISM_COLL_BARRIER = 5 };
+
+/* Communicator-group roles ("DP, TP, PP"; EP/EDP from the EP column of P:1983-1989).
+ * The numeric values are also the role field of the group perturbation uid. */
+enum { PRISM_ROLE_TP = 1, PRISM_ROLE_DP = 2, PRISM_ROLE_EP = 3, PRISM_ROLE_EDP = 4,
+       PRISM_ROLE_WORLD = 5, PRISM_ROLE_P2P = 6 };
+
+/* Batched point-to-point messages of one P2P node, between ring neighbours of the pipeline
+ * (next = (stage+1) mod pp, prev = (stage-1) mod pp). The k-th SEND_NEXT of stage s pairs with
+ * the k-th RECV_PREV of stage s+1 (same tp/dp coordinates); the k-th SEND_PREV of stage s pairs
+ * with the k-th RECV_NEXT of stage s-1. Each message is a 2-member synchronization group
+ * ("matched send-receive pairs"); a node with several messages finishes when all of them
+ * have finished (reading Z3). */
+enum { PRISM_P2P_SEND_NEXT = 1, PRISM_P2P_RECV_PREV = 2, PRISM_P2P_SEND_PREV = 4,
+       PRISM_P2P_RECV_NEXT = 8 };
+
+/* Rank numbering (reading Z1). TP_PP_DP: r = tp_i + tp*(pp_i + pp*dp_i) (TP fastest).
+ * MEGATRON ("tp-cp-ep-dp-pp"): r = tp_i + tp*(dp_i + dp*pp_i). EP is carved out of DP:
+ * ep_i = dp_i % ep, edp_i = dp_i / ep, in both orders. */
+enum { PRISM_ORDER_TP_PP_DP = 0, PRISM_ORDER_MEGATRON = 1 };
+
+typedef struct {
+  int32_t tp, pp, dp, ep; /* world = tp*pp*dp; ep >= 1 divides dp                              */
+  int32_t vpp;            /* informational (the schedule lives in the templates, reading Z16) */
+  int32_t rank_order;     /* PRISM_ORDER_*                                                    */
+} prism_topology;
+
+/* One op of a per-stage template. 48 bytes, natural alignment, little-endian. */
+typedef struct {
+  uint8_t kind;      /* PRISM_KIND_*                                                          */
+  uint8_t coll;      /* PRISM_COLL_* (COLLECTIVE only)                                        */
+  uint8_t role;      /* PRISM_ROLE_TP..WORLD (COLLECTIVE only)                                */
+  uint8_t p2p_mask;  /* PRISM_P2P_* bits, nonzero (P2P only)                                  */
+  uint8_t stream;    /* must be 0 (single stream per rank)                                    */
+  uint8_t pad0[3];
+  uint32_t label;    /* user tag (queries / what-if); not interpreted                         */
+  uint32_t pad1;
+  int64_t dur_ns;    /* >= 0, <= 2^40. For sync ops: this member's duration of the occurrence */
+  int64_t bytes;     /* payload, informational                                                */
+  int64_t mem_alloc; /* >= 0: allocated at the op's start                                     */
+  int64_t mem_free;  /* >= 0: freed at the op's finish                                        */
+} prism_op;
+
+typedef struct {
+  const prism_op *ops;       /* concatenated templates, n_ops entries                          */
+  int64_t n_ops;
+  const int64_t *tmpl_ptr;   /* [pp+1]: stage s runs ops[tmpl_ptr[s] .. tmpl_ptr[s+1]) in order;
+                                every rank of stage s runs the same template           */
+  const int64_t *static_mem; /* [pp]: bytes resident for the whole iteration on stage-s ranks   */
+} prism_templates;
+
+/* Device-memory hooks (the Python binding routes these to PyTorch's caching allocator). */
+typedef void *(*prism_alloc_fn)(size_t bytes, void *stream, void *ctx);
+typedef void (*prism_free_fn)(void *ptr, void *stream, void *ctx);
+
+typedef struct {
+  void *stream;           /* cudaStream_t all device work of this graph is issued on (NULL = legacy
+                             default stream)                                                  */
+  int32_t device;         /* CUDA device ordinal, -1 = current                                 */
+  int32_t n_shards;       /* 1 (multi-GPU sharding is reserved for a later ABI revision)        */
+  int32_t shard_index;    /* 0                                                                */
+  int32_t reserved;
+} prism_build_opts;
+
+/* Scenario batch for what-if sweeps (re-time without structural change).
+ * Scenario k gets perturbed durations d' = (d * (65536 + delta)) >> 16 with
+ * delta = ((h >> 40) mod (2*amp+1)) - amp, h = splitmix64(seed ^ k*0x9E3779B97F4A7C15 ^
+ * uid*0xBF58476D1CE4E5B9); uid = (rank<<32)|template_index for compute nodes and
+ * (role<<56)|(gid<<24)|occurrence for sync groups (exact text in DESIGN.md §3, Z8).
+ * Scenario 0, and every node kind whose bit (1<<kind) is clear in kind_mask, is unperturbed. */
+typedef struct {
+  int32_t n;          /* S >= 1 scenarios                                                     */
+  int32_t amp_q16;    /* 0 .. 65535                                                           */
+  uint64_t seed;
+  uint32_t kind_mask; /* bit (1<<PRISM_KIND_*) = perturb that kind                             */
+  int32_t record;     /* nonzero: keep every node's finish time for prism_query_rank           */
+} prism_scenarios;
+
+/* ---- entry points ------------------------------------------------------------------------ */
+
+const char *prism_status_string(prism_status s);
+const char *prism_last_error(void);
+int32_t prism_abi_version(void);
+
+/* Install device allocation hooks used by subsequent prism_build_graph calls (NULL, NULL =
+ * cudaMallocAsync/cudaFreeAsync). Process-global; not thread-safe against concurrent builds. */
+prism_status prism_set_allocator(prism_alloc_fn alloc, prism_free_fn free_fn, void *ctx);
+
+/* Rows a1-a5: expand the per-stage templates over the topology into the device-resident CSR
+ * DAG: node SoA (rank, duration, kind, label, alloc/free), per-node sync-group lists, sync-group
+ * CSR (members, shared duration = max of members' dur_ns (Z2), perturbation uid, level) sorted
+ * by level. Validates everything on the host before any launch:
+ *   PRISM_E_INVALID_SPEC       bad topology
+ *   PRISM_E_INVALID_ARG        malformed op (unknown kind/role, negative duration/bytes, stream!=0,
+ *                              P2P with pp==1, empty p2p_mask, dur > 2^40), N or M >= 2^31
+ *   PRISM_E_TEMPLATE_MISMATCH  a P2P message without its partner, WORLD collectives whose count or
+ *                              collective type differ between stages
+ *   PRISM_E_DEADLOCK           the synchronization structure has a cycle
+ *   PRISM_E_NEGATIVE_MEMORY    a template's running allocation drops below zero (program order)
+ * On success *out owns the graph. Blocks until the device work is complete. */
+prism_status prism_build_graph(const prism_topology *topo, const prism_templates *tmpl,
+                               const prism_build_opts *opts, prism_graph_t *out);
+
+/* Rows a6-a8: replay all ranks over the graph for S scenarios (ASAP, integer ns, reading Z4/Z5):
+ * a compute node starts when its stream predecessor finishes; a sync group starts at the max of
+ * its members' ready times (segmented max) and lasts its (perturbed) duration; a sync node
+ * finishes at the max over its groups. Writes the iteration time T_k = max finish (ns) of each
+ * scenario to iter_ns_out[k] (host, n entries). Synchronizes the stream. */
+prism_status prism_replay(prism_graph_t g, const prism_scenarios *sc, int64_t *iter_ns_out);
+
+/* Same as prism_replay but asynchronous: writes T_k into iter_ns_dev_out (DEVICE pointer, n
+ * int64) on the graph's stream and returns without synchronizing. */
+prism_status prism_replay_async(prism_graph_t g, const prism_scenarios *sc, int64_t *iter_ns_dev_out);
+
+/* Row a9: per-rank peak memory in bytes, peak_r = static_mem[stage(r)] + max(0, max prefix sum of
+ * the rank's events +alloc at op start / -free at op finish ordered by (time, event index)); for
+ * single-stream ranks this is program order (Z6), so the result does not depend on
+ * the scenario and no replay is required. Writes world entries to peak_bytes_out (host). */
+prism_status prism_peak_memory(prism_graph_t g, int64_t *peak_bytes_out);
+prism_status prism_peak_memory_async(prism_graph_t g, int64_t *peak_bytes_dev_out);
+
+/* Per-op start and finish times of one rank in one scenario of the last recorded replay, in
+ * program order, plus the rank's coordinates (tp, pp, dp, ep, edp). If cap < the rank's op count
+ * the call writes the count to *n_ops_out and returns PRISM_E_INVALID_ARG.
+ * PRISM_E_NOT_REPLAYED if no replay with record != 0 has run; PRISM_E_UNKNOWN_RANK. */
+prism_status prism_query_rank(prism_graph_t g, int32_t rank, int32_t scenario, int64_t *start_ns,
+                              int64_t *finish_ns, int64_t cap, int64_t *n_ops_out,
+                              int32_t coords_out[5]);
+
+/* out[0..9]: world, nodes, sync groups, memberships, levels, quotient groups, sync nodes,
+ * max group size, bytes of device graph structure, replay launches per call. */
+prism_status prism_graph_stats(prism_graph_t g, int64_t out[10]);
+
+void prism_destroy_graph(prism_graph_t g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRISM_H */

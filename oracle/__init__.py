@@ -1,0 +1,146 @@
+"""CPU oracle for the PrismLLM hot path — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package. The product path
+(``paper_2605_15617_b200``) never imports it and fails loudly without its CUDA library.
+
+``prism_oracle.cpp`` is a plain discrete-event replayer with its own template expansion
+(PAPER.md P:982, P:1099, P:1298, P:1573, P:1578 — see the file header); ``brute.py`` is a
+pure-Python path enumeration for tiny graphs used to pin the DES itself.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+from typing import Dict, Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "prism_oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+STATUS = {0: "OK", 1: "INVALID_ARG", 2: "INVALID_SPEC", 4: "TEMPLATE_MISMATCH", 5: "DEADLOCK",
+          6: "NEGATIVE_MEMORY"}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with g++ (building the checker is not using it)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-pthread", _SRC,
+                               "-o", tmp])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            P = ctypes.c_void_p
+            lib.oracle_expand.argtypes = [P, P, ctypes.c_int64, P, P, P, P, P, P, P, P,
+                                          ctypes.c_char_p, ctypes.c_int]
+            lib.oracle_expand.restype = ctypes.c_int
+            lib.oracle_replay.argtypes = [P, P, ctypes.c_int64, P, P, ctypes.c_int32, ctypes.c_int32,
+                                          ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32, P, P, P,
+                                          P, P, ctypes.c_int32, ctypes.c_char_p, ctypes.c_int]
+            lib.oracle_replay.restype = ctypes.c_int
+            lib.oracle_splitmix64.argtypes = [ctypes.c_uint64]
+            lib.oracle_splitmix64.restype = ctypes.c_uint64
+            lib.oracle_perturb.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32,
+                                           ctypes.c_uint64, ctypes.c_int32]
+            lib.oracle_perturb.restype = ctypes.c_int64
+            _lib = lib
+    return _lib
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _topo_buf(topo) -> np.ndarray:
+    return np.array([topo.tp, topo.pp, topo.dp, topo.ep, topo.vpp, topo.rank_order], dtype=np.int32)
+
+
+def _inputs(tm):
+    ops = np.ascontiguousarray(tm.ops)
+    ptr = np.ascontiguousarray(tm.tmpl_ptr, dtype=np.int64)
+    st = np.ascontiguousarray(tm.static_mem, dtype=np.int64)
+    return ops, ptr, st
+
+
+def expand(tm) -> Dict[str, np.ndarray]:
+    """The oracle's expanded sync groups: uid, dur, level, member node ids (sorted)."""
+    lib = _load()
+    topo = _topo_buf(tm.topo)
+    ops, ptr, st = _inputs(tm)
+    stats = np.zeros(8, dtype=np.int64)
+    err = ctypes.create_string_buffer(512)
+    s = lib.oracle_expand(_ptr(topo), _ptr(ops), len(ops), _ptr(ptr), _ptr(st), _ptr(stats),
+                          None, None, None, None, None, err, 512)
+    if s:
+        raise OracleError(s, err.value.decode())
+    G, M = int(stats[2]), int(stats[3])
+    uid = np.zeros(G, np.uint64)
+    dur = np.zeros(G, np.int64)
+    gptr = np.zeros(G + 1, np.int64)
+    mem = np.zeros(M, np.int32)
+    lvl = np.zeros(G, np.int64)
+    s = lib.oracle_expand(_ptr(topo), _ptr(ops), len(ops), _ptr(ptr), _ptr(st), _ptr(stats),
+                          _ptr(uid), _ptr(dur), _ptr(gptr), _ptr(mem), _ptr(lvl), err, 512)
+    if s:
+        raise OracleError(s, err.value.decode())
+    return {"stats": stats, "uid": uid, "dur": dur, "ptr": gptr, "mem": mem, "level": lvl,
+            "world": int(stats[0]), "nodes": int(stats[1]), "groups": G, "memberships": M,
+            "levels": int(stats[4]), "sync_nodes": int(stats[5]), "max_group": int(stats[6])}
+
+
+def replay(tm, n_scen: int = 1, *, seed: int = 0x5EED, amp_q16: int = 0, kind_mask: int = 0,
+           scen_first: int = 0, times: bool = False, peaks: bool = True, threads: int = 1):
+    """Replay scenarios scen_first .. scen_first+n_scen-1. Returns a dict with
+    iter [S], rank_end [S, W], peak [S, W] (if peaks), start/finish [S, N] (if times)."""
+    lib = _load()
+    topo = _topo_buf(tm.topo)
+    ops, ptr, st = _inputs(tm)
+    W = tm.topo.world
+    N = tm.n_nodes
+    it = np.zeros(n_scen, np.int64)
+    re = np.zeros((n_scen, W), np.int64)
+    pk = np.zeros((n_scen, W), np.int64) if peaks else None
+    s0 = np.zeros((n_scen, N), np.int64) if times else None
+    f0 = np.zeros((n_scen, N), np.int64) if times else None
+    err = ctypes.create_string_buffer(512)
+    s = lib.oracle_replay(_ptr(topo), _ptr(ops), len(ops), _ptr(ptr), _ptr(st), scen_first, n_scen,
+                          seed, amp_q16, kind_mask, _ptr(it), _ptr(re), _ptr(pk), _ptr(s0), _ptr(f0),
+                          threads, err, 512)
+    if s:
+        raise OracleError(s, err.value.decode())
+    out = {"iter": it, "rank_end": re}
+    if peaks:
+        out["peak"] = pk
+    if times:
+        out["start"] = s0
+        out["finish"] = f0
+    return out
+
+
+def splitmix64(x: int) -> int:
+    return int(_load().oracle_splitmix64(x & (2**64 - 1)))
+
+
+def perturb(d: int, uid: int, k: int, seed: int, amp: int) -> int:
+    return int(_load().oracle_perturb(d, uid & (2**64 - 1), k, seed & (2**64 - 1), amp))

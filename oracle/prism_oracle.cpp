@@ -1,0 +1,472 @@
+// prism_oracle.cpp — TEST INFRASTRUCTURE ONLY (the parity authority for the CUDA path).
+//
+// Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+// load this library. It shares no code, header, table or helper with paper_2605_15617_b200/:
+// the template record layout below is re-declared here from the input format (48-byte prism_op,
+// written by workloads/), and every step is re-derived from the paper's definitions.
+//
+// What it computes, step by step (PAPER.md = /root/reference/PAPER.md):
+//   1. Expansion (§5.2 "execution graphs are identical across DP groups"): every rank of
+//      pipeline stage s runs template s; nodes are numbered rank-major in program order.
+//   2. Communicator groups (§6.2 "DP, TP, PP" groups; EP/EDP from P:1983-1989): the k-th
+//      collective of role R in a rank's template joins the k-th occurrence of the rank's
+//      concrete R group; each P2P message is a 2-member "matched send-receive pair".
+//   3. Replay (P:982 directional vs synchronization edges; "waits for the recorded
+//      duration"; "shift the receive to occur after the send ... propagating"):
+//      a discrete-event simulation with a min-heap of (time, node) finish events. A node is
+//      released when its stream predecessor finishes; a compute node finishes dur' later; a
+//      sync node arrives at each of its groups; when a group has all members, it starts at the
+//      max of their arrival times and lasts its duration; a member finishes when all of its
+//      groups have finished (max). Iteration time = max finish.
+//   4. Peak memory (P:1578 max_memory_allocated): per rank, events +alloc at op start and
+//      -free at op finish sorted by (time, event index), prefix-summed; peak = static + max(0,
+//      max prefix). A negative running total is an error.
+// Readings of silent points are DESIGN.md §3 (Z1-Z16); the perturbation formula is Z8's text.
+// Parity pins for this file: tests/test_oracle_pins.py (closed forms, brute force, SPEC worked
+// examples, invariants).
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <queue>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <utility>
+#include <vector>
+
+namespace {
+
+struct Op {  // one template record, 48 bytes (input format)
+  uint8_t kind, coll, role, p2p_mask, stream, pad0[3];
+  uint32_t label, pad1;
+  int64_t dur, bytes, alloc, free_;
+};
+static_assert(sizeof(Op) == 48, "record layout");
+
+struct Topo {
+  int32_t tp, pp, dp, ep, vpp, order;
+};
+
+enum { OK = 0, E_INVALID_ARG = 1, E_INVALID_SPEC = 2, E_MISMATCH = 4, E_DEADLOCK = 5, E_NEGMEM = 6 };
+
+struct Coords {
+  int64_t tp, pp, dp, ep, edp;
+};
+
+Coords coords_of(const Topo &t, int64_t r) {
+  Coords c;
+  c.tp = r % t.tp;
+  if (t.order == 1) {  // tp-cp-ep-dp-pp: TP fastest, then DP, then PP
+    c.dp = (r / t.tp) % t.dp;
+    c.pp = r / ((int64_t)t.tp * t.dp);
+  } else {  // TP fastest, then PP, then DP
+    c.pp = (r / t.tp) % t.pp;
+    c.dp = r / ((int64_t)t.tp * t.pp);
+  }
+  c.ep = c.dp % t.ep;
+  c.edp = c.dp / t.ep;
+  return c;
+}
+
+int64_t rank_of(const Topo &t, int64_t tp_i, int64_t pp_i, int64_t dp_i) {
+  if (t.order == 1) return tp_i + (int64_t)t.tp * (dp_i + (int64_t)t.dp * pp_i);
+  return tp_i + (int64_t)t.tp * (pp_i + (int64_t)t.pp * dp_i);
+}
+
+// Concrete group id of a role for a rank (closed form in its coordinates).
+int64_t group_id(const Topo &t, int role, const Coords &c) {
+  switch (role) {
+    case 1: return c.pp + (int64_t)t.pp * c.dp;                        // TP: one per (pp, dp)
+    case 2: return c.tp + (int64_t)t.tp * c.pp;                        // DP: one per (tp, pp)
+    case 3: return c.tp + (int64_t)t.tp * (c.pp + (int64_t)t.pp * c.edp);  // EP: per (tp, pp, edp)
+    case 4: return c.tp + (int64_t)t.tp * (c.pp + (int64_t)t.pp * c.ep);   // EDP: per (tp, pp, ep)
+    default: return 0;                                                 // WORLD
+  }
+}
+
+int64_t role_size(const Topo &t, int role) {
+  switch (role) {
+    case 1: return t.tp;
+    case 2: return t.dp;
+    case 3: return t.ep;
+    case 4: return t.dp / t.ep;
+    default: return (int64_t)t.tp * t.pp * t.dp;
+  }
+}
+
+uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// Reading Z8: d' = (d * (65536 + delta)) >> 16, delta = ((h >> 40) mod (2 amp + 1)) - amp.
+int64_t perturb(int64_t d, uint64_t uid, int k, uint64_t seed, int amp) {
+  if (k == 0 || amp == 0) return d;
+  uint64_t x = seed ^ ((uint64_t)k * 0x9E3779B97F4A7C15ULL) ^ (uid * 0xBF58476D1CE4E5B9ULL);
+  uint64_t h = splitmix64(x);
+  int64_t delta = (int64_t)((h >> 40) % (uint64_t)(2 * amp + 1)) - amp;
+  return (d * (65536 + delta)) >> 16;
+}
+
+struct Group {
+  int role = 0;       // 1..5 collectives, 6 P2P message
+  int coll = -1;
+  uint64_t uid = 0;
+  int64_t dur = 0;    // max over members' op durations (reading Z2)
+  int64_t expect = 0; // expected member count
+  std::vector<int32_t> members;
+  int senders = 0, receivers = 0;
+};
+
+struct Graph {
+  int64_t W = 0, N = 0;
+  std::vector<int64_t> rank_base;  // [W+1]
+  std::vector<int32_t> node_rank;
+  std::vector<int32_t> node_tidx;
+  std::vector<const Op *> node_op;
+  std::vector<std::vector<int32_t>> node_groups;  // group indices per node (in insertion order)
+  std::vector<Group> groups;
+  std::vector<int64_t> static_of_rank;
+  std::string err;
+};
+
+int expand(const Topo &t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
+           const int64_t *static_mem, Graph &g) {
+  if (t.tp < 1 || t.pp < 1 || t.dp < 1 || t.ep < 1 || t.dp % t.ep != 0 || (t.order != 0 && t.order != 1)) {
+    g.err = "invalid topology";
+    return E_INVALID_SPEC;
+  }
+  if (tmpl_ptr[0] != 0 || tmpl_ptr[t.pp] != n_ops) { g.err = "tmpl_ptr"; return E_INVALID_ARG; }
+  for (int s = 0; s < t.pp; ++s)
+    if (tmpl_ptr[s + 1] < tmpl_ptr[s]) { g.err = "tmpl_ptr not monotone"; return E_INVALID_ARG; }
+  for (int64_t i = 0; i < n_ops; ++i) {
+    const Op &o = ops[i];
+    bool ok = o.kind <= 2 && o.stream == 0 && o.dur >= 0 && o.dur <= (1LL << 40) && o.bytes >= 0 &&
+              o.alloc >= 0 && o.free_ >= 0;
+    if (o.kind == 1) ok = ok && o.role >= 1 && o.role <= 5 && o.coll <= 5;
+    if (o.kind == 2) ok = ok && o.p2p_mask >= 1 && o.p2p_mask <= 15 && t.pp > 1;
+    if (!ok) { g.err = "malformed op " + std::to_string(i); return E_INVALID_ARG; }
+  }
+  // memory never negative in program order (per template; every rank of a stage shares it)
+  for (int s = 0; s < t.pp; ++s) {
+    int64_t run = 0;
+    for (int64_t i = tmpl_ptr[s]; i < tmpl_ptr[s + 1]; ++i) {
+      run += ops[i].alloc;
+      run -= ops[i].free_;
+      if (run < 0) { g.err = "negative memory in stage " + std::to_string(s); return E_NEGMEM; }
+    }
+  }
+  const int64_t W = (int64_t)t.tp * t.pp * t.dp;
+  g.W = W;
+  g.rank_base.assign(W + 1, 0);
+  for (int64_t r = 0; r < W; ++r) {
+    Coords c = coords_of(t, r);
+    g.rank_base[r + 1] = g.rank_base[r] + (tmpl_ptr[c.pp + 1] - tmpl_ptr[c.pp]);
+  }
+  g.N = g.rank_base[W];
+  g.node_rank.resize(g.N);
+  g.node_tidx.resize(g.N);
+  g.node_op.resize(g.N);
+  g.node_groups.assign(g.N, {});
+  g.static_of_rank.resize(W);
+
+  // key: (role, gid, occurrence) -> group index
+  std::map<std::tuple<int, int64_t, int64_t>, int32_t> index;
+  auto get_group = [&](int role, int64_t gid, int64_t occ) -> int32_t {
+    auto key = std::make_tuple(role, gid, occ);
+    auto it = index.find(key);
+    if (it != index.end()) return it->second;
+    int32_t id = (int32_t)g.groups.size();
+    Group G;
+    G.role = role;
+    G.uid = ((uint64_t)role << 56) | ((uint64_t)gid << 24) | (uint64_t)occ;
+    G.expect = role == 6 ? 2 : role_size(t, role);
+    g.groups.push_back(G);
+    index.emplace(key, id);
+    return id;
+  };
+
+  for (int64_t r = 0; r < W; ++r) {
+    Coords c = coords_of(t, r);
+    int64_t s = c.pp;
+    g.static_of_rank[r] = static_mem[s];
+    int64_t prev_rank = rank_of(t, c.tp, (s - 1 + t.pp) % t.pp, c.dp);
+    int64_t next_rank = rank_of(t, c.tp, (s + 1) % t.pp, c.dp);
+    int64_t occ_role[6] = {0, 0, 0, 0, 0, 0};
+    int64_t occ_bit[4] = {0, 0, 0, 0};
+    for (int64_t i = tmpl_ptr[s]; i < tmpl_ptr[s + 1]; ++i) {
+      int64_t ti = i - tmpl_ptr[s];
+      int32_t n = (int32_t)(g.rank_base[r] + ti);
+      const Op &o = ops[i];
+      g.node_rank[n] = (int32_t)r;
+      g.node_tidx[n] = (int32_t)ti;
+      g.node_op[n] = &o;
+      if (o.kind == 1) {
+        int64_t occ = occ_role[o.role]++;
+        int32_t gi = get_group(o.role, group_id(t, o.role, c), occ);
+        Group &G = g.groups[gi];
+        if (G.coll < 0) G.coll = o.coll;
+        else if (G.coll != o.coll) { g.err = "collective type mismatch"; return E_MISMATCH; }
+        G.members.push_back(n);
+        G.dur = std::max(G.dur, o.dur);
+        g.node_groups[n].push_back(gi);
+      } else if (o.kind == 2) {
+        for (int b = 0; b < 4; ++b) {
+          if (!(o.p2p_mask & (1 << b))) continue;
+          int64_t occ = occ_bit[b]++;
+          int64_t sender, dir;
+          bool is_send;
+          switch (b) {
+            case 0: sender = r; dir = 0; is_send = true; break;            // SEND_NEXT
+            case 1: sender = prev_rank; dir = 0; is_send = false; break;   // RECV_PREV
+            case 2: sender = r; dir = 1; is_send = true; break;            // SEND_PREV
+            default: sender = next_rank; dir = 1; is_send = false; break;  // RECV_NEXT
+          }
+          int32_t gi = get_group(6, sender * 2 + dir, occ);
+          Group &G = g.groups[gi];
+          G.members.push_back(n);
+          G.dur = std::max(G.dur, o.dur);
+          if (is_send) G.senders++; else G.receivers++;
+          g.node_groups[n].push_back(gi);
+        }
+      }
+    }
+  }
+  for (size_t gi = 0; gi < g.groups.size(); ++gi) {
+    Group &G = g.groups[gi];
+    if ((int64_t)G.members.size() != G.expect || (G.role == 6 && (G.senders != 1 || G.receivers != 1))) {
+      g.err = "sync group " + std::to_string(gi) + " (role " + std::to_string(G.role) + ") has " +
+              std::to_string(G.members.size()) + " of " + std::to_string(G.expect) + " members";
+      return E_MISMATCH;
+    }
+    std::sort(G.members.begin(), G.members.end());
+  }
+  return OK;
+}
+
+int64_t node_dur(const Graph &g, int32_t n, int k, uint64_t seed, int amp, uint32_t mask) {
+  const Op *o = g.node_op[n];
+  if (!(mask & 1u)) return o->dur;
+  uint64_t uid = ((uint64_t)g.node_rank[n] << 32) | (uint64_t)(uint32_t)g.node_tidx[n];
+  return perturb(o->dur, uid, k, seed, amp);
+}
+
+int64_t group_dur(const Group &G, int k, uint64_t seed, int amp, uint32_t mask) {
+  uint32_t bit = G.role == 6 ? 4u : 2u;
+  if (!(mask & bit)) return G.dur;
+  return perturb(G.dur, G.uid, k, seed, amp);
+}
+
+// Discrete-event replay of one scenario. gdur[gi] and ndur(n) are the (perturbed) durations.
+int replay(const Graph &g, const std::function<int64_t(int32_t)> &ndur,
+           const std::vector<int64_t> &gdur, std::vector<int64_t> &start,
+           std::vector<int64_t> &finish, std::string &err) {
+  const int64_t N = g.N;
+  start.assign(N, 0);
+  finish.assign(N, 0);
+  std::vector<int32_t> pend(N, 0);
+  std::vector<int64_t> contrib(N, 0), gstart_max(N, 0);
+  for (int64_t n = 0; n < N; ++n) pend[n] = (int32_t)g.node_groups[n].size();
+  std::vector<int32_t> arrived(g.groups.size(), 0);
+  std::vector<int64_t> gready(g.groups.size(), 0);
+  using Ev = std::pair<int64_t, int32_t>;
+  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> heap;
+  int64_t done = 0;
+
+  auto release = [&](int32_t n, int64_t t) {
+    if (g.node_groups[n].empty()) {  // compute span: wait out the duration
+      start[n] = t;
+      heap.push({t + ndur(n), n});
+      return;
+    }
+    for (int32_t gi : g.node_groups[n]) {  // synchronization: all must reach it
+      arrived[gi]++;
+      gready[gi] = std::max(gready[gi], t);
+      const Group &G = g.groups[gi];
+      if (arrived[gi] == (int32_t)G.members.size()) {
+        int64_t gs = gready[gi];
+        int64_t gf = gs + gdur[gi];
+        for (int32_t m : G.members) {
+          contrib[m] = std::max(contrib[m], gf);
+          gstart_max[m] = std::max(gstart_max[m], gs);
+          if (--pend[m] == 0) {
+            start[m] = gstart_max[m];
+            heap.push({contrib[m], m});
+          }
+        }
+      }
+    }
+  };
+  for (int64_t r = 0; r < g.W; ++r)
+    if (g.rank_base[r + 1] > g.rank_base[r]) release((int32_t)g.rank_base[r], 0);
+  while (!heap.empty()) {
+    Ev e = heap.top();
+    heap.pop();
+    int32_t n = e.second;
+    finish[n] = e.first;
+    ++done;
+    int32_t r = g.node_rank[n];
+    if (n + 1 < g.rank_base[r + 1]) release(n + 1, e.first);
+  }
+  if (done != N) {
+    int64_t incomplete = 0;
+    for (size_t gi = 0; gi < g.groups.size(); ++gi)
+      if (arrived[gi] != (int32_t)g.groups[gi].members.size()) ++incomplete;
+    err = "deadlock: " + std::to_string(N - done) + " nodes never finished, " +
+          std::to_string(incomplete) + " sync groups incomplete";
+    return E_DEADLOCK;
+  }
+  return OK;
+}
+
+int peak_memory(const Graph &g, const std::vector<int64_t> &start, const std::vector<int64_t> &finish,
+                int64_t *peak_out, std::string &err) {
+  for (int64_t r = 0; r < g.W; ++r) {
+    // (time, event index, delta): +alloc at start (index 2i), -free at finish (index 2i+1)
+    std::vector<std::tuple<int64_t, int64_t, int64_t>> ev;
+    for (int64_t n = g.rank_base[r]; n < g.rank_base[r + 1]; ++n) {
+      int64_t i = n - g.rank_base[r];
+      ev.emplace_back(start[n], 2 * i, g.node_op[n]->alloc);
+      ev.emplace_back(finish[n], 2 * i + 1, -g.node_op[n]->free_);
+    }
+    std::sort(ev.begin(), ev.end());
+    int64_t run = 0, best = 0;
+    for (auto &e : ev) {
+      run += std::get<2>(e);
+      if (run < 0) { err = "negative memory on rank " + std::to_string(r); return E_NEGMEM; }
+      best = std::max(best, run);
+    }
+    peak_out[r] = g.static_of_rank[r] + best;
+  }
+  return OK;
+}
+
+thread_local std::string g_last;
+
+void put_err(char *err, int errlen, const std::string &m) {
+  g_last = m;
+  if (err && errlen > 0) {
+    std::snprintf(err, (size_t)errlen, "%s", m.c_str());
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// stats_out[8]: world, nodes, groups, memberships, levels, sync nodes, max group size, 0.
+// level_out (optional, [n_groups]): level of each group in the oracle's group order.
+// Group export (optional): grp_uid_out[G], grp_dur_out[G], grp_ptr_out[G+1], grp_mem_out[M].
+int oracle_expand(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
+                  const int64_t *static_mem, int64_t *stats_out, uint64_t *grp_uid_out,
+                  int64_t *grp_dur_out, int64_t *grp_ptr_out, int32_t *grp_mem_out,
+                  int64_t *grp_level_out, char *err, int errlen) {
+  Graph g;
+  int st = expand(*t, ops, n_ops, tmpl_ptr, static_mem, g);
+  if (st) { put_err(err, errlen, g.err); return st; }
+  int64_t M = 0, sync_nodes = 0, maxsz = 0;
+  for (auto &G : g.groups) { M += (int64_t)G.members.size(); maxsz = std::max<int64_t>(maxsz, G.members.size()); }
+  for (int64_t n = 0; n < g.N; ++n) sync_nodes += !g.node_groups[n].empty();
+  // Levels (reading of SURVEY §8 a5): lvl(g) = 1 + max over members n of lvl(prev-sync(n)),
+  // lvl(node) = max over its groups, 0 before the first sync node. This is exactly the replay
+  // with every compute span lasting 0 and every group lasting 1: the finish time of a sync node
+  // is then its level (finish(prev-sync) = ready(n); group finish = max ready + 1).
+  std::vector<int64_t> lv_start, lv_fin, unit(g.groups.size(), 1);
+  std::string e2;
+  st = replay(g, [](int32_t) { return (int64_t)0; }, unit, lv_start, lv_fin, e2);
+  if (st) { put_err(err, errlen, e2); return st; }
+  int64_t levels = 0;
+  std::vector<int64_t> glevel(g.groups.size(), 0);
+  for (size_t gi = 0; gi < g.groups.size(); ++gi) {
+    int64_t mx = 0;
+    for (int32_t m : g.groups[gi].members) {
+      // ready(m) = finish of its stream predecessor (0 if first)
+      int32_t r = g.node_rank[m];
+      int64_t ready = (m > g.rank_base[r]) ? lv_fin[m - 1] : 0;
+      mx = std::max(mx, ready);
+    }
+    glevel[gi] = mx + 1;
+    levels = std::max(levels, glevel[gi]);
+  }
+  if (stats_out) {
+    stats_out[0] = g.W; stats_out[1] = g.N; stats_out[2] = (int64_t)g.groups.size(); stats_out[3] = M;
+    stats_out[4] = levels; stats_out[5] = sync_nodes; stats_out[6] = maxsz; stats_out[7] = 0;
+  }
+  if (grp_ptr_out) {
+    int64_t off = 0;
+    for (size_t gi = 0; gi < g.groups.size(); ++gi) {
+      const Group &G = g.groups[gi];
+      if (grp_uid_out) grp_uid_out[gi] = G.uid;
+      if (grp_dur_out) grp_dur_out[gi] = G.dur;
+      if (grp_level_out) grp_level_out[gi] = glevel[gi];
+      grp_ptr_out[gi] = off;
+      for (int32_t m : G.members) grp_mem_out[off++] = m;
+    }
+    grp_ptr_out[g.groups.size()] = off;
+  }
+  return OK;
+}
+
+// Replays n_scen scenarios (scenario indices k = scen_first .. scen_first+n_scen-1).
+// iter_out[n_scen] (required); rank_end_out[n_scen][W], peak_out[n_scen][W],
+// start_out/finish_out[n_scen][N] optional (NULL = not written). n_threads >= 1.
+int oracle_replay(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
+                  const int64_t *static_mem, int32_t scen_first, int32_t n_scen, uint64_t seed,
+                  int32_t amp, uint32_t kind_mask, int64_t *iter_out, int64_t *rank_end_out,
+                  int64_t *peak_out, int64_t *start_out, int64_t *finish_out, int32_t n_threads,
+                  char *err, int errlen) {
+  if (n_scen < 0 || amp < 0 || amp > 65535 || n_threads < 1 || !iter_out) {
+    put_err(err, errlen, "bad arguments");
+    return E_INVALID_ARG;
+  }
+  Graph g;
+  int st = expand(*t, ops, n_ops, tmpl_ptr, static_mem, g);
+  if (st) { put_err(err, errlen, g.err); return st; }
+  std::vector<int> status(n_scen, OK);
+  std::vector<std::string> msgs(n_scen);
+  auto work = [&](int tid) {
+    std::vector<int64_t> start, finish, gd(g.groups.size());
+    for (int j = tid; j < n_scen; j += n_threads) {
+      int k = scen_first + j;
+      for (size_t gi = 0; gi < g.groups.size(); ++gi) gd[gi] = group_dur(g.groups[gi], k, seed, amp, kind_mask);
+      auto nd = [&](int32_t n) { return node_dur(g, n, k, seed, amp, kind_mask); };
+      int s2 = replay(g, nd, gd, start, finish, msgs[j]);
+      if (s2) { status[j] = s2; continue; }
+      int64_t T = 0;
+      for (int64_t n = 0; n < g.N; ++n) T = std::max(T, finish[n]);
+      iter_out[j] = T;
+      if (rank_end_out)
+        for (int64_t r = 0; r < g.W; ++r)
+          rank_end_out[(int64_t)j * g.W + r] = g.rank_base[r + 1] > g.rank_base[r] ? finish[g.rank_base[r + 1] - 1] : 0;
+      if (peak_out) {
+        int s3 = peak_memory(g, start, finish, peak_out + (int64_t)j * g.W, msgs[j]);
+        if (s3) { status[j] = s3; continue; }
+      }
+      if (start_out) std::copy(start.begin(), start.end(), start_out + (int64_t)j * g.N);
+      if (finish_out) std::copy(finish.begin(), finish.end(), finish_out + (int64_t)j * g.N);
+    }
+  };
+  int nt = std::min<int>(n_threads, std::max(1, n_scen));
+  if (nt == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int i = 0; i < nt; ++i) th.emplace_back(work, i);
+    for (auto &x : th) x.join();
+  }
+  for (int j = 0; j < n_scen; ++j)
+    if (status[j]) { put_err(err, errlen, msgs[j]); return status[j]; }
+  return OK;
+}
+
+uint64_t oracle_splitmix64(uint64_t x) { return splitmix64(x); }
+int64_t oracle_perturb(int64_t d, uint64_t uid, int32_t k, uint64_t seed, int32_t amp) {
+  return perturb(d, uid, k, seed, amp);
+}
+
+}  // extern "C"
