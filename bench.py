@@ -1,0 +1,357 @@
+#!/usr/bin/env python3
+"""bench.py — the PrismLLM hot path on B200: expand + replay + peak-memory per step.
+
+One step = one pass of every SURVEY.md §8(a) row over one synthetic input: prism_build_graph
+(a1-a5: coordinates, groups, CSR DAG, levels) of the BASELINE.json workload, prism_replay of S
+perturbed what-if scenarios (a6-a8) and prism_peak_memory (a9), all through the C ABI.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--scenarios 64]
+  python bench.py --impl reference ...   (the CPU oracle on a bounded sample of the workload)
+
+Prints ONE JSON line on rank 0. Metric: replayed graph ops/s = nodes x scenarios / step time
+(plus emulated iterations/s = scenarios / step time in "extra"). Multi-GPU: one process per GPU
+(torchrun); every rank replays its own replica of the workload (row e sharding is not used by
+this bench yet: "replicas", weak scaling); time = max over ranks of the device-timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "replayed graph ops/sec (node-scenarios/s) at 8192 ranks"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (the recipe's clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(int(float(r[1])) for r in self.rows if r[1].replace(".", "").isdigit())
+        mx = max(int(float(r[2])) for r in self.rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def algorithmic_bytes(st, S: int, record: bool = True):
+    """SURVEY.md §8(d) / DESIGN.md §6 algorithmic bytes of one replay (rows a6-a8) and one
+    build (a1-a4) and one peak scan (a9)."""
+    N, G, M, W = st["nodes"], st["groups"], st["memberships"], st["world"]
+    replay = (N * S * 8 if record else 0) + G * S * 16 + N * 16 + M * 8 + W * S * 8
+    build = N * 41 + M * 8 + G * 24
+    peak = N * 16 + W * 8
+    return {"replay": replay, "build": build, "peak": peak}
+
+
+def run_prism(args):
+    import numpy as np
+    import torch
+
+    import paper_2605_15617_b200 as prism
+    import workloads as w
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    prism.use_torch_allocator()
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+    tm = w.config(args.config)
+    S = args.scenarios
+    kw = dict(amp_q16=args.amp, kind_mask=7, seed=0x5EED)
+    iter_dev = torch.zeros(S, dtype=torch.int64, device="cuda")
+    peak_dev = torch.zeros(tm.topo.world, dtype=torch.int64, device="cuda")
+
+    graphs = []
+
+    def step():
+        # the previous step's graph is released first (its buffers return to the caching
+        # allocator and are reused by this build); the last one survives the timed region
+        while graphs:
+            graphs.pop().close()
+        g = prism.Graph(tm, stream=sh)
+        g.replay_async(iter_dev.data_ptr(), S, record=True, **kw)
+        g.peak_memory_async(peak_dev.data_ptr())
+        graphs.append(g)
+
+    for _ in range(args.warmup):
+        step()
+        for g in graphs:
+            g.close()
+        graphs.clear()
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    iters = iter_dev.cpu().numpy().copy()
+    st = graphs[0].stats()
+    launches_per_step = st["replay_launches"] + 3 + 1  # expand: rank tables, nodes, groups; peak
+    for g in graphs:
+        g.close()
+    graphs.clear()
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    units = st["nodes"] * S
+    value = ws * units / (ms_step / 1e3)
+
+    # ---- per-kernel-group device times (profiled graph, CUDA events on the launching stream)
+    gp = prism.Graph(tm, stream=sh, profile=True)
+    prof = {"expand": [], "levels": [], "tail": [], "reduce": [], "peak": []}
+    for i in range(3):
+        gp.replay_async(iter_dev.data_ptr(), S, record=True, **kw)
+        gp.peak_memory_async(peak_dev.data_ptr())
+        t = gp.last_timing()
+        for k in ("levels", "tail", "reduce", "peak"):
+            prof[k].append(t[k])
+    prof["expand"].append(gp.last_timing()["expand"])
+    gp.close()
+    med = {k: sorted(v)[len(v) // 2] for k, v in prof.items()}
+    ab = algorithmic_bytes(st, S)
+    replay_ms = med["levels"] + med["tail"] + med["reduce"]
+    peak_bw, peak_src = _peaks()
+    achieved = ab["replay"] / (replay_ms / 1e3) / 1e9
+
+    # ---- e2e: the public API with HOST buffers (H2D of templates, D2H of results) -------------
+    e2e_ms = None
+    h2d = int(tm.ops.nbytes + tm.tmpl_ptr.nbytes + tm.static_mem.nbytes)
+    d2h = S * 8 + tm.topo.world * 8
+    if True:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = max(1, min(args.steps, 3))
+        for _ in range(reps):
+            g = prism.Graph(tm, stream=sh)
+            it_host = g.replay(S, record=True, **kw)
+            pk_host = g.peak_memory()
+            g.close()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / reps
+        assert (it_host == iters).all()
+    if ws > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    if rank != 0:
+        return None
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args)
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get(str(S))
+        except Exception:
+            traffic = None
+    out = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "node-scenarios/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int64",
+        "data": "synthetic (seeded templates, BASELINE.json config shapes; DESIGN.md §4)",
+        "config": {
+            "workload": f"{args.config}: {w.CONFIG_DESCRIPTIONS[args.config]}",
+            "ranks": tm.topo.world, "nodes": st["nodes"], "sync_groups": st["groups"],
+            "memberships": st["memberships"], "levels": st["levels"], "scenarios": S,
+            "amp_q16": args.amp, "record_times": True,
+            "parallelism": f"replicas{ws}" if ws > 1 else "single-gpu",
+            "l2": "working set (fin[N][S] = %.1f GB) > 126 MB L2; no flush needed" % (st["nodes"] * S * 8 / 1e9),
+        },
+        "extra": {
+            "emulated_iterations_per_s": round(ws * S / (ms_step / 1e3), 2),
+            "iteration_time_ns_scenario0": int(iters[0]),
+            "device_ms": {k: round(v, 4) for k, v in med.items()},
+        },
+        "roofline": {
+            "bound": "hbm",
+            "kernel": "replay (level_kernel x levels + tail_kernel + reduce_iter_kernel)",
+            "achieved": round(achieved, 1),
+            "peak": peak_bw,
+            "peak_source": peak_src,
+            "unit": "GB/s",
+            "frac": round(achieved / peak_bw, 4),
+            "alg_bytes_per_call": ab["replay"],
+            "traffic": traffic,
+        },
+        "e2e": {"value": round(ws * units / (e2e_ms / 1e3), 1), "unit": "node-scenarios/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    return out
+
+
+def cpu_baseline(args, sample_dp: int = 8):
+    """The oracle as it stands, on a bounded sample of the same workload: the C5 templates with
+    DP cut to `sample_dp` replicas, nproc scenarios (one thread each), expansion included."""
+    import oracle
+    import workloads as w
+
+    full = w.config(args.config)
+    t = full.topo
+    dp = min(t.dp, sample_dp)
+    while t.dp % dp:
+        dp -= 1
+    ep = t.ep if dp % t.ep == 0 else 1
+    tm = w.Templates(w.Topology(t.tp, t.pp, dp, ep, t.vpp, t.rank_order), full.ops, full.tmpl_ptr,
+                     full.static_mem)
+    cores = os.cpu_count() or 1
+    S = max(1, min(args.scenarios, cores))
+    oracle.build()
+    t0 = time.perf_counter()
+    r = oracle.replay(tm, S, amp_q16=args.amp, kind_mask=7, peaks=True, threads=S)
+    dt = time.perf_counter() - t0
+    return {"value": round(tm.n_nodes * S / dt, 1), "unit": "node-scenarios/s", "cores": min(S, cores),
+            "kind": "oracle", "seconds": round(dt, 2),
+            "sample": f"{args.config} templates at dp={dp} ({tm.topo.world} of {t.world} ranks, "
+                      f"{tm.n_nodes} nodes), {S} scenarios, one thread each, expansion + DES + peak"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle timed on the box's host cores (rank 0 only)."""
+    ws, rank, local = _dist()
+    if rank != 0:
+        return None
+    import oracle
+    import workloads as w
+
+    full = w.config(args.config)
+    t = full.topo
+    dp = min(t.dp, 4)
+    tm = w.Templates(w.Topology(t.tp, t.pp, dp, t.ep if dp % t.ep == 0 else 1, t.vpp, t.rank_order),
+                     full.ops, full.tmpl_ptr, full.static_mem)
+    cores = os.cpu_count() or 1
+    S = max(1, min(args.scenarios, cores))
+    oracle.build()
+    for _ in range(min(args.warmup, 1)):
+        oracle.replay(tm, 1, amp_q16=args.amp, kind_mask=7)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.replay(tm, S, amp_q16=args.amp, kind_mask=7, peaks=True, threads=S)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = round(tm.n_nodes * S / dt, 1)
+    sample = (f"{args.config} templates at dp={dp} ({tm.topo.world} of {t.world} ranks, {tm.n_nodes} "
+              f"nodes), {S} scenarios one thread each")
+    return {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "node-scenarios/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": {"workload": f"{args.config}: {w.CONFIG_DESCRIPTIONS[args.config]}",
+                                        "scenarios": S, "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "node-scenarios/s", "cores": min(S, cores), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "node-scenarios/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--scenarios", type=int, default=64)
+    ap.add_argument("--amp", type=int, default=6554)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.config = args.config.upper()
+    if args.warmup < 3 and args.impl == "prism":
+        args.warmup = 3
+    out = run_reference(args) if args.impl == "reference" else run_prism(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws > 1 and args.impl == "prism":
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

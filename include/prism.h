@@ -39,6 +39,12 @@ extern "C" {
 
 #define PRISM_ABI_VERSION 1
 
+#if defined(__GNUC__)
+#define PRISM_API __attribute__((visibility("default")))
+#else
+#define PRISM_API
+#endif
+
 typedef int32_t prism_status;
 enum {
   PRISM_OK = 0,
@@ -128,8 +134,10 @@ typedef struct {
   int32_t device;         /* CUDA device ordinal, -1 = current                                 */
   int32_t n_shards;       /* 1 (multi-GPU sharding is reserved for a later ABI revision)        */
   int32_t shard_index;    /* 0                                                                */
-  int32_t reserved;
+  int32_t flags;          /* PRISM_BUILD_PROFILE: record CUDA events around every kernel group */
 } prism_build_opts;
+
+enum { PRISM_BUILD_PROFILE = 1 };
 
 /* Scenario batch for what-if sweeps (re-time without structural change).
  * Scenario k gets perturbed durations d' = (d * (65536 + delta)) >> 16 with
@@ -147,13 +155,13 @@ typedef struct {
 
 /* ---- entry points ------------------------------------------------------------------------ */
 
-const char *prism_status_string(prism_status s);
-const char *prism_last_error(void);
-int32_t prism_abi_version(void);
+PRISM_API const char *prism_status_string(prism_status s);
+PRISM_API const char *prism_last_error(void);
+PRISM_API int32_t prism_abi_version(void);
 
 /* Install device allocation hooks used by subsequent prism_build_graph calls (NULL, NULL =
  * cudaMallocAsync/cudaFreeAsync). Process-global; not thread-safe against concurrent builds. */
-prism_status prism_set_allocator(prism_alloc_fn alloc, prism_free_fn free_fn, void *ctx);
+PRISM_API prism_status prism_set_allocator(prism_alloc_fn alloc, prism_free_fn free_fn, void *ctx);
 
 /* Rows a1-a5: expand the per-stage templates over the topology into the device-resident CSR
  * DAG: node SoA (rank, duration, kind, label, alloc/free), per-node sync-group lists, sync-group
@@ -167,40 +175,59 @@ prism_status prism_set_allocator(prism_alloc_fn alloc, prism_free_fn free_fn, vo
  *   PRISM_E_DEADLOCK           the synchronization structure has a cycle
  *   PRISM_E_NEGATIVE_MEMORY    a template's running allocation drops below zero (program order)
  * On success *out owns the graph. Blocks until the device work is complete. */
-prism_status prism_build_graph(const prism_topology *topo, const prism_templates *tmpl,
+PRISM_API prism_status prism_build_graph(const prism_topology *topo, const prism_templates *tmpl,
                                const prism_build_opts *opts, prism_graph_t *out);
+
+/* Host-only dry run of prism_build_graph's validation and quotient plan (no device needed):
+ * out[0..7] = world, nodes, sync groups, memberships, levels, quotient groups, sync nodes,
+ * max group size. Same error statuses as prism_build_graph. */
+PRISM_API prism_status prism_plan(const prism_topology *topo, const prism_templates *tmpl, int64_t out[8]);
 
 /* Rows a6-a8: replay all ranks over the graph for S scenarios (ASAP, integer ns, reading Z4/Z5):
  * a compute node starts when its stream predecessor finishes; a sync group starts at the max of
  * its members' ready times (segmented max) and lasts its (perturbed) duration; a sync node
  * finishes at the max over its groups. Writes the iteration time T_k = max finish (ns) of each
  * scenario to iter_ns_out[k] (host, n entries). Synchronizes the stream. */
-prism_status prism_replay(prism_graph_t g, const prism_scenarios *sc, int64_t *iter_ns_out);
+PRISM_API prism_status prism_replay(prism_graph_t g, const prism_scenarios *sc, int64_t *iter_ns_out);
 
 /* Same as prism_replay but asynchronous: writes T_k into iter_ns_dev_out (DEVICE pointer, n
  * int64) on the graph's stream and returns without synchronizing. */
-prism_status prism_replay_async(prism_graph_t g, const prism_scenarios *sc, int64_t *iter_ns_dev_out);
+PRISM_API prism_status prism_replay_async(prism_graph_t g, const prism_scenarios *sc, int64_t *iter_ns_dev_out);
 
 /* Row a9: per-rank peak memory in bytes, peak_r = static_mem[stage(r)] + max(0, max prefix sum of
  * the rank's events +alloc at op start / -free at op finish ordered by (time, event index)); for
  * single-stream ranks this is program order (Z6), so the result does not depend on
  * the scenario and no replay is required. Writes world entries to peak_bytes_out (host). */
-prism_status prism_peak_memory(prism_graph_t g, int64_t *peak_bytes_out);
-prism_status prism_peak_memory_async(prism_graph_t g, int64_t *peak_bytes_dev_out);
+PRISM_API prism_status prism_peak_memory(prism_graph_t g, int64_t *peak_bytes_out);
+PRISM_API prism_status prism_peak_memory_async(prism_graph_t g, int64_t *peak_bytes_dev_out);
 
 /* Per-op start and finish times of one rank in one scenario of the last recorded replay, in
  * program order, plus the rank's coordinates (tp, pp, dp, ep, edp). If cap < the rank's op count
  * the call writes the count to *n_ops_out and returns PRISM_E_INVALID_ARG.
  * PRISM_E_NOT_REPLAYED if no replay with record != 0 has run; PRISM_E_UNKNOWN_RANK. */
-prism_status prism_query_rank(prism_graph_t g, int32_t rank, int32_t scenario, int64_t *start_ns,
+PRISM_API prism_status prism_query_rank(prism_graph_t g, int32_t rank, int32_t scenario, int64_t *start_ns,
                               int64_t *finish_ns, int64_t cap, int64_t *n_ops_out,
                               int32_t coords_out[5]);
 
 /* out[0..9]: world, nodes, sync groups, memberships, levels, quotient groups, sync nodes,
  * max group size, bytes of device graph structure, replay launches per call. */
-prism_status prism_graph_stats(prism_graph_t g, int64_t out[10]);
+PRISM_API prism_status prism_graph_stats(prism_graph_t g, int64_t out[10]);
 
-void prism_destroy_graph(prism_graph_t g);
+PRISM_API void prism_destroy_graph(prism_graph_t g);
+
+/* Device time (ms, CUDA events on the graph's stream) of the last call of each kernel group of a
+ * graph built with PRISM_BUILD_PROFILE: out[0] expand (a1-a4, last build), out[1] level loop of the
+ * last replay (a5-a7), out[2] tail (a6), out[3] iteration reduce (a8), out[4] peak scan (a9).
+ * Synchronizes on the recorded events. PRISM_E_INVALID_ARG if profiling is off. */
+PRISM_API prism_status prism_last_timing(prism_graph_t g, float out[5]);
+
+/* Test hook: copy one device array of the graph to host memory (bytes = capacity of host_out).
+ * which: 0 rank_ptr[W+1] i32, 1 node_rank[N] i32, 2 node_dur[N] i64, 3 node_kind[N] u8,
+ * 4 node_label[N] u32, 5 node_alloc[N] i64, 6 node_free[N] i64, 7 node_prev_sync[N] i32,
+ * 8 node_gptr[N+1] i32, 9 node_grp[M] i32, 10 grp_ptr[G+1] i32, 11 grp_mem[M] i32,
+ * 12 grp_dur[G] i64, 13 grp_uid[G] u64, 14 grp_level[G] i32, 15 fin[N][S_pad] i64 (last
+ * recorded replay; S_pad = S rounded up to the replay's scenario chunk). */
+PRISM_API prism_status prism_debug_export(prism_graph_t g, int32_t which, void *host_out, int64_t bytes);
 
 #ifdef __cplusplus
 }

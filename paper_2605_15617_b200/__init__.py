@@ -1,0 +1,270 @@
+"""paper_2605_15617_b200 — B200-native hot path of PrismLLM's hybrid emulation (arXiv 2605.15617).
+
+A thin ctypes binding over the C ABI of ``libprism_b200.so`` (``include/prism.h``): argument
+marshalling only, every step of the path runs in the CUDA kernels of ``csrc/``. PyTorch supplies
+device memory (caching allocator hooks), the stream and, for multi-GPU runs, the process group.
+
+There is no CPU fallback: if the library or a CUDA device is missing, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, Optional
+
+import numpy as np
+
+__all__ = ["lib", "Graph", "plan", "PrismError", "build_library", "LIB_PATH", "EXPORTED_SYMBOLS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libprism_b200.so")
+
+EXPORTED_SYMBOLS = [
+    "prism_status_string", "prism_last_error", "prism_abi_version", "prism_set_allocator",
+    "prism_build_graph", "prism_replay", "prism_replay_async", "prism_peak_memory",
+    "prism_peak_memory_async", "prism_query_rank", "prism_graph_stats", "prism_destroy_graph",
+    "prism_debug_export", "prism_plan", "prism_last_timing",
+]
+
+STATUS_NAMES = {
+    0: "PRISM_OK", 1: "PRISM_E_INVALID_ARG", 2: "PRISM_E_INVALID_SPEC", 3: "PRISM_E_GA_TOO_SMALL",
+    4: "PRISM_E_TEMPLATE_MISMATCH", 5: "PRISM_E_DEADLOCK", 6: "PRISM_E_NEGATIVE_MEMORY",
+    7: "PRISM_E_UNKNOWN_RANK", 8: "PRISM_E_UNKNOWN_LABEL", 9: "PRISM_E_NOT_REPLAYED",
+    10: "PRISM_E_OOM", 11: "PRISM_E_CUDA", 12: "PRISM_E_NCCL",
+}
+
+
+class PrismError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.name = STATUS_NAMES.get(status, str(status))
+        super().__init__(f"{self.name}: {msg}")
+
+
+class _Topology(ctypes.Structure):
+    _fields_ = [("tp", ctypes.c_int32), ("pp", ctypes.c_int32), ("dp", ctypes.c_int32),
+                ("ep", ctypes.c_int32), ("vpp", ctypes.c_int32), ("rank_order", ctypes.c_int32)]
+
+
+class _Templates(ctypes.Structure):
+    _fields_ = [("ops", ctypes.c_void_p), ("n_ops", ctypes.c_int64), ("tmpl_ptr", ctypes.c_void_p),
+                ("static_mem", ctypes.c_void_p)]
+
+
+class _BuildOpts(ctypes.Structure):
+    _fields_ = [("stream", ctypes.c_void_p), ("device", ctypes.c_int32), ("n_shards", ctypes.c_int32),
+                ("shard_index", ctypes.c_int32), ("flags", ctypes.c_int32)]
+
+
+class _Scenarios(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("amp_q16", ctypes.c_int32), ("seed", ctypes.c_uint64),
+                ("kind_mask", ctypes.c_uint32), ("record", ctypes.c_int32)]
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+
+_lib = None
+_hooks = None
+
+
+def build_library(force: bool = False, verbose: bool = False) -> str:
+    from . import build as _b
+
+    return _b.build(force=force, verbose=verbose)
+
+
+def lib():
+    """Load libprism_b200.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.c_void_p
+        L.prism_status_string.restype = ctypes.c_char_p
+        L.prism_status_string.argtypes = [ctypes.c_int32]
+        L.prism_last_error.restype = ctypes.c_char_p
+        L.prism_abi_version.restype = ctypes.c_int32
+        L.prism_set_allocator.argtypes = [_ALLOC_FN, _FREE_FN, P]
+        L.prism_build_graph.argtypes = [P, P, P, ctypes.POINTER(P)]
+        L.prism_replay.argtypes = [P, P, P]
+        L.prism_replay_async.argtypes = [P, P, P]
+        L.prism_peak_memory.argtypes = [P, P]
+        L.prism_peak_memory_async.argtypes = [P, P]
+        L.prism_query_rank.argtypes = [P, ctypes.c_int32, ctypes.c_int32, P, P, ctypes.c_int64, P, P]
+        L.prism_graph_stats.argtypes = [P, P]
+        L.prism_destroy_graph.argtypes = [P]
+        L.prism_destroy_graph.restype = None
+        L.prism_debug_export.argtypes = [P, ctypes.c_int32, P, ctypes.c_int64]
+        L.prism_plan.argtypes = [P, P, P]
+        L.prism_last_timing.argtypes = [P, P]
+        for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
+                     "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
+                     "prism_graph_stats", "prism_debug_export", "prism_plan",
+                     "prism_last_timing"):
+            getattr(L, name).restype = ctypes.c_int32
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != 0:
+        raise PrismError(status, lib().prism_last_error().decode(errors="replace"))
+
+
+def use_torch_allocator() -> None:
+    """Route the library's device allocations through PyTorch's caching allocator."""
+    global _hooks
+    import torch
+
+    def _alloc(nbytes, stream, ctx):
+        try:
+            return int(torch.cuda.caching_allocator_alloc(int(nbytes), stream=int(stream or 0)))
+        except Exception:  # allocation failure -> NULL -> PRISM_E_OOM
+            return None
+
+    def _free(ptr, stream, ctx):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    _hooks = (_ALLOC_FN(_alloc), _FREE_FN(_free))
+    _check(lib().prism_set_allocator(_hooks[0], _hooks[1], None))
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+DEBUG_ARRAYS = {
+    "rank_ptr": (0, np.int32), "node_rank": (1, np.int32), "node_dur": (2, np.int64),
+    "node_kind": (3, np.uint8), "node_label": (4, np.uint32), "node_alloc": (5, np.int64),
+    "node_free": (6, np.int64), "node_prev_sync": (7, np.int32), "node_gptr": (8, np.int32),
+    "node_grp": (9, np.int32), "grp_ptr": (10, np.int32), "grp_mem": (11, np.int32),
+    "grp_dur": (12, np.int64), "grp_uid": (13, np.uint64), "grp_level": (14, np.int32),
+}
+
+
+def _marshal(templates):
+    t = templates.topo
+    topo = _Topology(t.tp, t.pp, t.dp, t.ep, getattr(t, "vpp", 1), getattr(t, "rank_order", 0))
+    ops = np.ascontiguousarray(templates.ops)
+    if ops.dtype.itemsize != 48:
+        raise ValueError("ops must use the 48-byte prism_op record layout")
+    ptr = np.ascontiguousarray(templates.tmpl_ptr, dtype=np.int64)
+    static = np.ascontiguousarray(templates.static_mem, dtype=np.int64)
+    tm = _Templates(ops.ctypes.data if len(ops) else None, len(ops), ptr.ctypes.data, static.ctypes.data)
+    return topo, tm, (ops, ptr, static)
+
+
+def plan(templates) -> Dict[str, int]:
+    """Host-only validation + quotient plan (prism_plan): sizes of the graph that would be built."""
+    topo, tm, keep = _marshal(templates)
+    out = np.zeros(8, np.int64)
+    _check(lib().prism_plan(ctypes.byref(topo), ctypes.byref(tm), _ptr(out)))
+    keys = ["world", "nodes", "groups", "memberships", "levels", "quotient_groups", "sync_nodes",
+            "max_group"]
+    return dict(zip(keys, (int(x) for x in out)))
+
+
+class Graph:
+    """An expanded execution graph resident on one GPU (prism_build_graph)."""
+
+    def __init__(self, templates, *, stream: Optional[int] = None, device: int = -1,
+                 profile: bool = False):
+        L = lib()
+        self.topo = templates.topo
+        self._topo, self._tm, self._keep = _marshal(templates)
+        self._opts = _BuildOpts(stream or 0, device, 1, 0, 1 if profile else 0)
+        h = ctypes.c_void_p()
+        self._h = None
+        _check(L.prism_build_graph(ctypes.byref(self._topo), ctypes.byref(self._tm),
+                                   ctypes.byref(self._opts), ctypes.byref(h)))
+        self._h = h
+        self._stats = None
+
+    # ---------------------------------------------------------------- lifetime
+    def close(self):
+        if self._h is not None and _lib is not None:
+            _lib.prism_destroy_graph(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---------------------------------------------------------------- calls
+    def stats(self) -> Dict[str, int]:
+        out = np.zeros(10, np.int64)
+        _check(lib().prism_graph_stats(self._h, _ptr(out)))
+        keys = ["world", "nodes", "groups", "memberships", "levels", "quotient_groups", "sync_nodes",
+                "max_group", "structure_bytes", "replay_launches"]
+        return dict(zip(keys, (int(x) for x in out)))
+
+    def last_timing(self) -> Dict[str, float]:
+        """Device ms of the last expand / level loop / tail / reduce / peak (profile=True graphs)."""
+        out = np.zeros(5, np.float32)
+        _check(lib().prism_last_timing(self._h, _ptr(out)))
+        return dict(zip(["expand", "levels", "tail", "reduce", "peak"], (float(x) for x in out)))
+
+    @staticmethod
+    def _scen(n, seed, amp_q16, kind_mask, record):
+        return _Scenarios(int(n), int(amp_q16), int(seed) & (2**64 - 1), int(kind_mask), int(bool(record)))
+
+    def replay(self, n: int = 1, *, seed: int = 0x5EED, amp_q16: int = 0, kind_mask: int = 0,
+               record: bool = True) -> np.ndarray:
+        """Iteration time (ns) of each of n scenarios (host result, synchronizing)."""
+        out = np.zeros(n, np.int64)
+        sc = self._scen(n, seed, amp_q16, kind_mask, record)
+        _check(lib().prism_replay(self._h, ctypes.byref(sc), _ptr(out)))
+        return out
+
+    def replay_async(self, iter_dev_ptr: int, n: int = 1, *, seed: int = 0x5EED, amp_q16: int = 0,
+                     kind_mask: int = 0, record: bool = True) -> None:
+        """Asynchronous replay writing n int64 iteration times to a DEVICE pointer."""
+        sc = self._scen(n, seed, amp_q16, kind_mask, record)
+        _check(lib().prism_replay_async(self._h, ctypes.byref(sc), ctypes.c_void_p(iter_dev_ptr)))
+
+    def peak_memory(self) -> np.ndarray:
+        out = np.zeros(self.topo.tp * self.topo.pp * self.topo.dp, np.int64)
+        _check(lib().prism_peak_memory(self._h, _ptr(out)))
+        return out
+
+    def peak_memory_async(self, peak_dev_ptr: int) -> None:
+        _check(lib().prism_peak_memory_async(self._h, ctypes.c_void_p(peak_dev_ptr)))
+
+    def query_rank(self, rank: int, scenario: int = 0):
+        """(start[n_ops], finish[n_ops], coords(tp, pp, dp, ep, edp)) of one rank."""
+        n = ctypes.c_int64(0)
+        coords = np.zeros(5, np.int32)
+        st = lib().prism_query_rank(self._h, rank, scenario, None, None, 0, ctypes.byref(n), _ptr(coords))
+        if st not in (0, 1):
+            _check(st)
+        start = np.zeros(max(1, n.value), np.int64)
+        fin = np.zeros(max(1, n.value), np.int64)
+        _check(lib().prism_query_rank(self._h, rank, scenario, _ptr(start), _ptr(fin), n.value, None, None))
+        return start[: n.value], fin[: n.value], tuple(int(c) for c in coords)
+
+    def export(self, name: str, scen_pad: int = 0) -> np.ndarray:
+        """Copy one device CSR array to the host (tests)."""
+        st = self.stats()
+        if name == "fin":
+            which, dt, count = 15, np.int64, st["nodes"] * scen_pad
+        else:
+            which, dt = DEBUG_ARRAYS[name]
+            W, N, G, M = st["world"], st["nodes"], st["groups"], st["memberships"]
+            count = {"rank_ptr": W + 1, "node_gptr": N + 1, "grp_ptr": G + 1, "node_grp": M,
+                     "grp_mem": M}.get(name)
+            if count is None:
+                count = G if name.startswith("grp_") else N
+        out = np.zeros(max(1, count), dt)
+        _check(lib().prism_debug_export(self._h, which, _ptr(out), out.nbytes))
+        return out[:count]

@@ -1,0 +1,519 @@
+// abi.cu — the C ABI (include/prism.h): graph handles, device memory, launch orchestration.
+//
+// prism_build_graph = host validation + quotient plan (plan.cpp) -> H2D of the per-stage tables
+// (KBs) -> expand kernels (rows a1-a4) on the caller's stream. prism_replay = one level_kernel
+// launch per frontier level (rows a5-a7), then tail + reduce (a8). prism_peak_memory = peak_kernel
+// (a9). No CPU fallback: every compute entry point fails with PRISM_E_CUDA without a device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "graph.h"
+
+using namespace prism;
+
+namespace {
+
+thread_local std::string t_err;
+std::mutex g_alloc_mu;
+prism_alloc_fn g_alloc = nullptr;
+prism_free_fn g_free = nullptr;
+void *g_alloc_ctx = nullptr;
+
+prism_status fail(prism_status s, const std::string &m) {
+  t_err = m;
+  return s;
+}
+
+#define CU(call)                                                                             \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(e_ == cudaErrorMemoryAllocation ? PRISM_E_OOM : PRISM_E_CUDA,              \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                       \
+  } while (0)
+
+}  // namespace
+
+struct prism_graph_s {
+  Plan plan;
+  DevGraph dg{};
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  prism_alloc_fn alloc = nullptr;
+  prism_free_fn free_fn = nullptr;
+  void *ctx = nullptr;
+  std::vector<std::pair<void *, size_t>> blocks;  // structure allocations
+  int64_t structure_bytes = 0;
+  // replay state
+  int64_t *fin = nullptr;
+  size_t fin_bytes = 0;
+  int64_t *gfin = nullptr;
+  size_t gfin_bytes = 0;
+  int64_t *rank_end = nullptr;
+  size_t rank_end_bytes = 0;
+  int64_t *iter = nullptr;
+  size_t iter_bytes = 0;
+  int64_t *scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int recorded = 0;
+  ScenParams last{};
+  int32_t last_Sp = 0;
+  // tile plan cache (depends on lanes)
+  int tiles_lanes = -1;
+  Tile *tiles = nullptr;
+  size_t tiles_bytes = 0;
+  std::vector<int32_t> lvl_tile_ptr, lvl_max_cnt;
+  int64_t launches = 0;
+  bool oom = false;
+  // profiling events: 0/1 expand, 2/3 levels, 4 tail end, 5 reduce end, 6/7 peak
+  bool profile = false;
+  cudaEvent_t ev[8] = {};
+  bool ev_done[8] = {};
+  void rec(int i) {
+    if (profile) {
+      cudaEventRecord(ev[i], stream);
+      ev_done[i] = true;
+    }
+  }
+
+  void *dalloc(size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    void *p = nullptr;
+    if (alloc) {
+      p = alloc(bytes, (void *)stream, ctx);
+    } else if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
+      p = nullptr;
+    }
+    return p;
+  }
+  void dfree(void *p) {
+    if (!p) return;
+    if (free_fn) free_fn(p, (void *)stream, ctx);
+    else cudaFreeAsync(p, stream);
+  }
+  template <class T>
+  T *take(size_t count) {  // structure allocation, freed with the graph
+    size_t b = count * sizeof(T);
+    void *p = dalloc(b);
+    if (p) {
+      blocks.emplace_back(p, b);
+      structure_bytes += (int64_t)b;
+    } else {
+      oom = true;
+    }
+    return (T *)p;
+  }
+  template <class T>
+  bool ensure(T *&p, size_t &cap, size_t bytes) {
+    if (cap >= bytes && p) return true;
+    dfree(p);
+    p = (T *)dalloc(bytes);
+    cap = p ? bytes : 0;
+    return p != nullptr;
+  }
+  ~prism_graph_s() {
+    dfree(fin);
+    dfree(gfin);
+    dfree(rank_end);
+    dfree(iter);
+    dfree(scratch);
+    dfree(tiles);
+    for (auto &b : blocks) dfree(b.first);
+    cudaStreamSynchronize(stream);
+    for (auto &e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+extern "C" {
+
+const char *prism_status_string(prism_status s) {
+  switch (s) {
+    case PRISM_OK: return "PRISM_OK";
+    case PRISM_E_INVALID_ARG: return "PRISM_E_INVALID_ARG";
+    case PRISM_E_INVALID_SPEC: return "PRISM_E_INVALID_SPEC";
+    case PRISM_E_GA_TOO_SMALL: return "PRISM_E_GA_TOO_SMALL";
+    case PRISM_E_TEMPLATE_MISMATCH: return "PRISM_E_TEMPLATE_MISMATCH";
+    case PRISM_E_DEADLOCK: return "PRISM_E_DEADLOCK";
+    case PRISM_E_NEGATIVE_MEMORY: return "PRISM_E_NEGATIVE_MEMORY";
+    case PRISM_E_UNKNOWN_RANK: return "PRISM_E_UNKNOWN_RANK";
+    case PRISM_E_UNKNOWN_LABEL: return "PRISM_E_UNKNOWN_LABEL";
+    case PRISM_E_NOT_REPLAYED: return "PRISM_E_NOT_REPLAYED";
+    case PRISM_E_OOM: return "PRISM_E_OOM";
+    case PRISM_E_CUDA: return "PRISM_E_CUDA";
+    case PRISM_E_NCCL: return "PRISM_E_NCCL";
+    default: return "PRISM_E_UNKNOWN_STATUS";
+  }
+}
+
+const char *prism_last_error(void) { return t_err.c_str(); }
+
+int32_t prism_abi_version(void) { return PRISM_ABI_VERSION; }
+
+prism_status prism_set_allocator(prism_alloc_fn alloc, prism_free_fn free_fn, void *ctx) {
+  if ((alloc == nullptr) != (free_fn == nullptr)) return fail(PRISM_E_INVALID_ARG, "alloc and free hooks must be set together");
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  g_alloc = alloc;
+  g_free = free_fn;
+  g_alloc_ctx = ctx;
+  return PRISM_OK;
+}
+
+prism_status prism_plan(const prism_topology *topo, const prism_templates *tmpl, int64_t out[8]) {
+  if (!topo || !tmpl || !out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  Plan plan;
+  std::string err;
+  prism_status st = plan_graph(*topo, *tmpl, plan, err);
+  if (st != PRISM_OK) return fail(st, err);
+  out[0] = plan.W;
+  out[1] = plan.N;
+  out[2] = plan.G;
+  out[3] = plan.M;
+  out[4] = plan.levels;
+  out[5] = (int64_t)plan.q.size();
+  out[6] = plan.sync_nodes;
+  out[7] = plan.max_group;
+  return PRISM_OK;
+}
+
+prism_status prism_build_graph(const prism_topology *topo, const prism_templates *tmpl,
+                               const prism_build_opts *opts, prism_graph_t *out) {
+  if (!topo || !tmpl || !out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (opts && (opts->n_shards > 1 || opts->shard_index != 0))
+    return fail(PRISM_E_INVALID_ARG, "n_shards > 1 is not supported by this ABI revision");
+  Plan plan;
+  std::string err;
+  prism_status st = plan_graph(*topo, *tmpl, plan, err);
+  if (st != PRISM_OK) return fail(st, err);
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(PRISM_E_CUDA, "no CUDA device (there is no CPU fallback)");
+  auto *G = new prism_graph_s();
+  std::unique_ptr<prism_graph_s> guard(G);
+  G->device = -1;
+  if (opts && opts->device >= 0) CU(cudaSetDevice(opts->device));
+  CU(cudaGetDevice(&G->device));
+  G->stream = opts ? (cudaStream_t)opts->stream : nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    G->alloc = g_alloc;
+    G->free_fn = g_free;
+    G->ctx = g_alloc_ctx;
+  }
+  G->plan = std::move(plan);
+  const Plan &P = G->plan;
+  DevGraph &d = G->dg;
+  d.W = (int32_t)P.W;
+  d.pp = P.topo.pp;
+  d.tp = P.topo.tp;
+  d.dp = P.topo.dp;
+  d.ep = P.topo.ep;
+  d.order = P.topo.order;
+  d.N = P.N;
+  d.G = P.G;
+  d.M = P.M;
+  d.nq = (int32_t)P.q.size();
+  const size_t W = P.W, N = P.N, M = P.M, Gn = P.G, pp = P.topo.pp;
+  const size_t nops = (size_t)tmpl->n_ops;
+  d.rank_ptr = G->take<int32_t>(W + 1);
+  d.rank_slot = G->take<int32_t>(W + 1);
+  d.rank_stage = G->take<int32_t>(W);
+  d.node_rank = G->take<int32_t>(N);
+  d.node_dur = G->take<int64_t>(N);
+  d.node_kind = G->take<uint8_t>(N);
+  d.node_label = G->take<uint32_t>(N);
+  d.node_alloc = G->take<int64_t>(N);
+  d.node_free = G->take<int64_t>(N);
+  d.node_prev_sync = G->take<int32_t>(N);
+  d.node_gptr = G->take<int32_t>(N + 1);
+  d.node_grp = G->take<int32_t>(M);
+  d.grp_ptr = G->take<int32_t>(Gn + 1);
+  d.grp_mem = G->take<int32_t>(M);
+  d.grp_dur = G->take<int64_t>(Gn);
+  d.grp_uid = G->take<uint64_t>(Gn);
+  d.grp_level = G->take<int32_t>(Gn);
+  prism_op *t_ops = G->take<prism_op>(nops);
+  d.t_ops = t_ops;
+  d.t_op0 = G->take<int64_t>(pp);
+  d.t_len = G->take<int64_t>(pp);
+  d.t_prev_sync = G->take<int32_t>(nops);
+  d.t_slot_ptr = G->take<int32_t>(nops);
+  d.t_slots_total = G->take<int64_t>(pp);
+  d.static_mem = G->take<int64_t>(pp);
+  QGroup *q = G->take<QGroup>(P.q.size());
+  d.q = q;
+  int32_t *wpos = G->take<int32_t>(P.wpos.size());
+  d.wpos = wpos;
+  if (G->oom) return fail(PRISM_E_OOM, "device allocation failed while building the graph");
+  cudaStream_t s = G->stream;
+  if (nops) {
+    CU(cudaMemcpyAsync(t_ops, tmpl->ops, nops * sizeof(prism_op), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(d.t_prev_sync, P.t_prev_sync.data(), nops * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(d.t_slot_ptr, P.t_slot_ptr.data(), nops * 4, cudaMemcpyHostToDevice, s));
+  }
+  CU(cudaMemcpyAsync(d.t_op0, P.stage_op0.data(), pp * 8, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(d.t_len, P.stage_len.data(), pp * 8, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(d.t_slots_total, P.stage_slots.data(), pp * 8, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(d.static_mem, tmpl->static_mem, pp * 8, cudaMemcpyHostToDevice, s));
+  if (!P.q.empty()) CU(cudaMemcpyAsync(q, P.q.data(), P.q.size() * sizeof(QGroup), cudaMemcpyHostToDevice, s));
+  if (!P.wpos.empty()) CU(cudaMemcpyAsync(wpos, P.wpos.data(), P.wpos.size() * 4, cudaMemcpyHostToDevice, s));
+  if (opts && (opts->flags & PRISM_BUILD_PROFILE)) {
+    G->profile = true;
+    for (auto &e : G->ev) CU(cudaEventCreate(&e));
+  }
+  G->rec(0);
+  CU(launch_expand(d, s));
+  G->rec(1);
+  CU(cudaStreamSynchronize(s));
+  *out = guard.release();
+  return PRISM_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Tiles of every level for a team width of `lanes` (one membership per team per round).
+prism_status plan_tiles(prism_graph_s *G, int lanes) {
+  if (G->tiles_lanes == lanes) return PRISM_OK;
+  const Plan &P = G->plan;
+  const int teams = 256 / lanes;
+  const int sc = lanes == 32 ? 64 : lanes;
+  const int cap_smem = std::max(1, (48 * 1024) / (sc * 8));
+  std::vector<Tile> tiles;
+  G->lvl_tile_ptr.assign(P.levels + 2, 0);
+  G->lvl_max_cnt.assign(P.levels + 2, 1);
+  for (int l = 0; l <= P.levels; ++l) {
+    G->lvl_tile_ptr[l] = (int32_t)tiles.size();
+    for (int32_t qi = P.level_q_ptr[l]; qi < P.level_q_ptr[l + 1]; ++qi) {
+      const QGroup &q = P.q[qi];
+      int gpt = std::max(1, teams / q.size);
+      gpt = std::min(gpt, cap_smem);
+      for (int32_t i0 = 0; i0 < q.inst; i0 += gpt) {
+        Tile t{qi, i0, std::min(gpt, q.inst - i0), 0};
+        G->lvl_max_cnt[l] = std::max(G->lvl_max_cnt[l], t.cnt);
+        tiles.push_back(t);
+      }
+    }
+  }
+  G->lvl_tile_ptr[P.levels + 1] = (int32_t)tiles.size();
+  size_t cap = G->tiles_bytes;
+  if (!G->ensure(G->tiles, cap, std::max<size_t>(16, tiles.size() * sizeof(Tile))))
+    return fail(PRISM_E_OOM, "tile plan allocation failed");
+  G->tiles_bytes = cap;
+  if (!tiles.empty()) {
+    cudaError_t e = cudaMemcpyAsync(G->tiles, tiles.data(), tiles.size() * sizeof(Tile),
+                                    cudaMemcpyHostToDevice, G->stream);
+    if (e != cudaSuccess) return fail(PRISM_E_CUDA, cudaGetErrorString(e));
+    e = cudaStreamSynchronize(G->stream);  // host vector goes out of scope
+    if (e != cudaSuccess) return fail(PRISM_E_CUDA, cudaGetErrorString(e));
+  }
+  G->tiles_lanes = lanes;
+  return PRISM_OK;
+}
+
+prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *iter_dev) {
+  if (!G || !sc || !iter_dev) return fail(PRISM_E_INVALID_ARG, "null argument");
+  if (sc->n < 1 || sc->n > (1 << 20) || sc->amp_q16 < 0 || sc->amp_q16 > 65535)
+    return fail(PRISM_E_INVALID_ARG, "scenario count must be >= 1 and amp_q16 in [0, 65535]");
+  CU(cudaSetDevice(G->device));
+  const int32_t S = sc->n;
+  int lanes = 1;
+  while (lanes < S && lanes < 32) lanes <<= 1;
+  const int SC = lanes == 32 ? 64 : lanes;
+  const int nchunks = (S + SC - 1) / SC;
+  const int32_t Sp = nchunks * SC;
+  ScenParams p{};
+  p.S = S;
+  p.amp = sc->amp_q16;
+  p.seed = sc->seed;
+  p.mask = sc->kind_mask;
+  p.record = sc->record ? 1 : 0;
+  p.mod = 2 * sc->amp_q16 + 1;
+  p.mod_magic = ~0ULL / (uint64_t)p.mod + 1;
+  const Plan &P = G->plan;
+  G->recorded = 0;
+  if (p.record) {
+    if (!G->ensure(G->fin, G->fin_bytes, (size_t)P.N * Sp * 8)) return fail(PRISM_E_OOM, "fin[N][S] allocation failed");
+  }
+  if (!G->ensure(G->gfin, G->gfin_bytes, (size_t)P.G * Sp * 8)) return fail(PRISM_E_OOM, "gfin allocation failed");
+  if (!G->ensure(G->rank_end, G->rank_end_bytes, (size_t)P.W * Sp * 8)) return fail(PRISM_E_OOM, "rank_end allocation failed");
+  prism_status st = plan_tiles(G, lanes);
+  if (st) return st;
+  int64_t launches = 0;
+  G->rec(2);
+  for (int l = 1; l <= P.levels; ++l) {
+    const int32_t t0 = G->lvl_tile_ptr[l], t1 = G->lvl_tile_ptr[l + 1];
+    if (t1 == t0) continue;
+    CU(launch_level(G->dg, p, G->tiles + t0, t1 - t0, G->lvl_max_cnt[l], p.record ? G->fin : nullptr,
+                    G->gfin, lanes, nchunks, G->stream));
+    ++launches;
+  }
+  G->rec(3);
+  CU(launch_tail(G->dg, p, p.record ? G->fin : nullptr, G->gfin, G->rank_end, lanes, nchunks, G->stream));
+  G->rec(4);
+  CU(launch_reduce(G->dg.W, S, Sp, G->rank_end, iter_dev, G->stream));
+  G->rec(5);
+  G->launches = launches + 2;
+  G->last = p;
+  G->last_Sp = Sp;
+  G->recorded = p.record;
+  return PRISM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+prism_status prism_replay_async(prism_graph_t G, const prism_scenarios *sc, int64_t *iter_ns_dev_out) {
+  return replay_impl(G, sc, iter_ns_dev_out);
+}
+
+prism_status prism_replay(prism_graph_t G, const prism_scenarios *sc, int64_t *iter_ns_out) {
+  if (!G || !sc || !iter_ns_out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  if (sc->n < 1) return fail(PRISM_E_INVALID_ARG, "scenario count must be >= 1");
+  CU(cudaSetDevice(G->device));
+  if (!G->ensure(G->iter, G->iter_bytes, (size_t)sc->n * 8)) return fail(PRISM_E_OOM, "iter allocation failed");
+  prism_status st = replay_impl(G, sc, G->iter);
+  if (st) return st;
+  CU(cudaMemcpyAsync(iter_ns_out, G->iter, (size_t)sc->n * 8, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaStreamSynchronize(G->stream));
+  return PRISM_OK;
+}
+
+prism_status prism_peak_memory_async(prism_graph_t G, int64_t *peak_dev) {
+  if (!G || !peak_dev) return fail(PRISM_E_INVALID_ARG, "null argument");
+  CU(cudaSetDevice(G->device));
+  G->rec(6);
+  CU(launch_peak(G->dg, peak_dev, G->stream));
+  G->rec(7);
+  return PRISM_OK;
+}
+
+prism_status prism_peak_memory(prism_graph_t G, int64_t *peak_out) {
+  if (!G || !peak_out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  CU(cudaSetDevice(G->device));
+  const size_t bytes = std::max<size_t>(16, (size_t)G->plan.W * 8);
+  if (!G->ensure(G->scratch, G->scratch_bytes, bytes)) return fail(PRISM_E_OOM, "scratch allocation failed");
+  G->rec(6);
+  CU(launch_peak(G->dg, G->scratch, G->stream));
+  G->rec(7);
+  CU(cudaMemcpyAsync(peak_out, G->scratch, (size_t)G->plan.W * 8, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaStreamSynchronize(G->stream));
+  return PRISM_OK;
+}
+
+prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, int64_t *start_ns,
+                              int64_t *finish_ns, int64_t cap, int64_t *n_ops_out,
+                              int32_t coords_out[5]) {
+  if (!G) return fail(PRISM_E_INVALID_ARG, "null graph");
+  const Plan &P = G->plan;
+  if (rank < 0 || rank >= P.W) return fail(PRISM_E_UNKNOWN_RANK, "rank " + std::to_string(rank) + " outside the world");
+  const Topo &t = P.topo;
+  int32_t tp_i = rank % t.tp, pp_i, dp_i;
+  if (t.order == PRISM_ORDER_MEGATRON) {
+    dp_i = (rank / t.tp) % t.dp;
+    pp_i = rank / (t.tp * t.dp);
+  } else {
+    pp_i = (rank / t.tp) % t.pp;
+    dp_i = rank / (t.tp * t.pp);
+  }
+  if (coords_out) {
+    coords_out[0] = tp_i;
+    coords_out[1] = pp_i;
+    coords_out[2] = dp_i;
+    coords_out[3] = dp_i % t.ep;
+    coords_out[4] = dp_i / t.ep;
+  }
+  const int64_t n = P.stage_len[pp_i];
+  if (n_ops_out) *n_ops_out = n;
+  if (!G->recorded) return fail(PRISM_E_NOT_REPLAYED, "no replay with record != 0 has run on this graph");
+  if (scenario < 0 || scenario >= G->last.S) return fail(PRISM_E_INVALID_ARG, "scenario outside the last replay");
+  if (cap < n || (n > 0 && (!start_ns || !finish_ns))) return fail(PRISM_E_INVALID_ARG, "output capacity too small");
+  if (n == 0) return PRISM_OK;
+  CU(cudaSetDevice(G->device));
+  const size_t bytes = (size_t)n * 16;
+  if (!G->ensure(G->scratch, G->scratch_bytes, bytes)) return fail(PRISM_E_OOM, "scratch allocation failed");
+  CU(launch_query(G->dg, G->last, G->last_Sp, G->fin, G->gfin, rank, scenario, G->scratch, G->scratch + n, G->stream));
+  CU(cudaMemcpyAsync(start_ns, G->scratch, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaMemcpyAsync(finish_ns, G->scratch + n, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaStreamSynchronize(G->stream));
+  return PRISM_OK;
+}
+
+prism_status prism_graph_stats(prism_graph_t G, int64_t out[10]) {
+  if (!G || !out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  const Plan &P = G->plan;
+  out[0] = P.W;
+  out[1] = P.N;
+  out[2] = P.G;
+  out[3] = P.M;
+  out[4] = P.levels;
+  out[5] = (int64_t)P.q.size();
+  out[6] = P.sync_nodes;
+  out[7] = P.max_group;
+  out[8] = G->structure_bytes;
+  out[9] = G->launches;
+  return PRISM_OK;
+}
+
+void prism_destroy_graph(prism_graph_t G) { delete G; }
+
+prism_status prism_last_timing(prism_graph_t G, float out[5]) {
+  if (!G || !out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  if (!G->profile) return fail(PRISM_E_INVALID_ARG, "graph was not built with PRISM_BUILD_PROFILE");
+  CU(cudaSetDevice(G->device));
+  const int pairs[5][2] = {{0, 1}, {2, 3}, {3, 4}, {4, 5}, {6, 7}};
+  for (int i = 0; i < 5; ++i) {
+    out[i] = -1.f;
+    if (G->ev_done[pairs[i][0]] && G->ev_done[pairs[i][1]]) {
+      CU(cudaEventSynchronize(G->ev[pairs[i][1]]));
+      CU(cudaEventElapsedTime(&out[i], G->ev[pairs[i][0]], G->ev[pairs[i][1]]));
+    }
+  }
+  return PRISM_OK;
+}
+
+}  // extern "C"
+
+// ---- debug export (tests): copy device CSR arrays to host ------------------------------------
+extern "C" PRISM_API prism_status prism_debug_export(prism_graph_t G, int32_t which, void *host_out, int64_t bytes) {
+  if (!G || !host_out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  const DevGraph &d = G->dg;
+  const void *src = nullptr;
+  int64_t need = 0;
+  switch (which) {
+    case 0: src = d.rank_ptr; need = (d.W + 1) * 4; break;
+    case 1: src = d.node_rank; need = d.N * 4; break;
+    case 2: src = d.node_dur; need = d.N * 8; break;
+    case 3: src = d.node_kind; need = d.N; break;
+    case 4: src = d.node_label; need = d.N * 4; break;
+    case 5: src = d.node_alloc; need = d.N * 8; break;
+    case 6: src = d.node_free; need = d.N * 8; break;
+    case 7: src = d.node_prev_sync; need = d.N * 4; break;
+    case 8: src = d.node_gptr; need = (d.N + 1) * 4; break;
+    case 9: src = d.node_grp; need = d.M * 4; break;
+    case 10: src = d.grp_ptr; need = (d.G + 1) * 4; break;
+    case 11: src = d.grp_mem; need = d.M * 4; break;
+    case 12: src = d.grp_dur; need = d.G * 8; break;
+    case 13: src = d.grp_uid; need = d.G * 8; break;
+    case 14: src = d.grp_level; need = d.G * 4; break;
+    case 15: src = G->fin; need = G->recorded ? d.N * (int64_t)G->last_Sp * 8 : 0; break;
+    default: return fail(PRISM_E_INVALID_ARG, "unknown array");
+  }
+  if (bytes < need) return fail(PRISM_E_INVALID_ARG, "buffer too small: need " + std::to_string(need));
+  if (need == 0) return PRISM_OK;
+  CU(cudaSetDevice(G->device));
+  CU(cudaMemcpyAsync(host_out, src, (size_t)need, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaStreamSynchronize(G->stream));
+  return PRISM_OK;
+}

@@ -1,0 +1,181 @@
+// expand.cu — rows a1-a4: rank coordinates, template expansion into the node SoA, and the
+// sync-group CSR (collective instances + P2P messages -> member node ids).
+//
+// Every store here is a coalesced streaming write of the CSR DAG; the per-stage template tables
+// (a few hundred KB) stay L2-resident and are read by every rank of their stage ("execution
+// graphs are identical across DP groups" -> the expander copies one template per stage into every
+// rank's node range). Algorithmic bytes: 41 B per node + 8 B per membership + 24 B per group
+// (DESIGN.md §6).
+#include <cuda_runtime.h>
+
+#include "graph.h"
+
+namespace prism {
+
+namespace {
+
+// Row a1: rank -> (tp, pp, dp) under the rank order (reading Z1); ep/edp carved from dp.
+__device__ __forceinline__ int32_t stage_of(const DevGraph &g, int32_t r) {
+  return g.order == PRISM_ORDER_MEGATRON ? r / (g.tp * g.dp) : (r / g.tp) % g.pp;
+}
+__device__ __forceinline__ int32_t rank_of(const DevGraph &g, int32_t tp_i, int32_t pp_i, int32_t dp_i) {
+  return g.order == PRISM_ORDER_MEGATRON ? tp_i + g.tp * (dp_i + g.dp * pp_i)
+                                         : tp_i + g.tp * (pp_i + g.pp * dp_i);
+}
+
+// Exclusive scans of per-rank node / slot counts (one block; W <= 2^30 but small in practice).
+__global__ void __launch_bounds__(1024) rank_tables_kernel(DevGraph g) {
+  __shared__ int64_t s_nodes[1024], s_slots[1024];
+  __shared__ int64_t carry_n, carry_s;
+  if (threadIdx.x == 0) carry_n = carry_s = 0;
+  __syncthreads();
+  for (int32_t base = 0; base < g.W; base += 1024) {
+    int32_t r = base + threadIdx.x;
+    int64_t n = 0, sl = 0;
+    if (r < g.W) {
+      int32_t s = stage_of(g, r);
+      g.rank_stage[r] = s;
+      n = g.t_len[s];
+      sl = g.t_slots_total[s];
+    }
+    s_nodes[threadIdx.x] = n;
+    s_slots[threadIdx.x] = sl;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {  // Hillis-Steele inclusive scan
+      int64_t a = threadIdx.x >= off ? s_nodes[threadIdx.x - off] : 0;
+      int64_t b = threadIdx.x >= off ? s_slots[threadIdx.x - off] : 0;
+      __syncthreads();
+      s_nodes[threadIdx.x] += a;
+      s_slots[threadIdx.x] += b;
+      __syncthreads();
+    }
+    if (r < g.W) {
+      g.rank_ptr[r] = (int32_t)(carry_n + s_nodes[threadIdx.x] - n);
+      g.rank_slot[r] = (int32_t)(carry_s + s_slots[threadIdx.x] - sl);
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) {
+      carry_n += s_nodes[1023];
+      carry_s += s_slots[1023];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    g.rank_ptr[g.W] = (int32_t)carry_n;
+    g.rank_slot[g.W] = (int32_t)carry_s;
+    g.node_gptr[g.N] = (int32_t)carry_s;
+    g.grp_ptr[g.G] = (int32_t)g.M;
+  }
+}
+
+// Row a3: one block per rank (grid-stride), threads over the rank's template ops.
+__global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
+  for (int32_t r = blockIdx.x; r < g.W; r += gridDim.x) {
+    const int32_t s = g.rank_stage[r];
+    const int32_t rb = g.rank_ptr[r];
+    const int32_t slot0 = g.rank_slot[r];
+    const int64_t op0 = g.t_op0[s];
+    const int32_t len = (int32_t)g.t_len[s];
+    for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
+      const prism_op &o = g.t_ops[op0 + i];
+      const int32_t n = rb + i;
+      const int32_t tps = g.t_prev_sync[op0 + i];
+      g.node_rank[n] = r;
+      g.node_dur[n] = o.dur_ns;
+      g.node_kind[n] = o.kind;
+      g.node_label[n] = o.label;
+      g.node_alloc[n] = o.mem_alloc;
+      g.node_free[n] = o.mem_free;
+      g.node_prev_sync[n] = tps < 0 ? -1 : rb + tps;
+      g.node_gptr[n] = slot0 + g.t_slot_ptr[op0 + i];
+    }
+  }
+}
+
+// Row a4: one thread per membership (grid-stride). The quotient group is found by binary search
+// over mbase; the concrete instance / member follow in closed form from the coordinates.
+__global__ void __launch_bounds__(256) build_groups_kernel(DevGraph g) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < g.M; m += stride) {
+    int32_t lo = 0, hi = g.nq - 1;
+    while (lo < hi) {  // last q with mbase <= m
+      int32_t mid = (lo + hi + 1) >> 1;
+      if (g.q[mid].mbase <= m) lo = mid; else hi = mid - 1;
+    }
+    const QGroup &q = g.q[lo];
+    const int64_t local = m - q.mbase;
+    const int32_t inst = (int32_t)(local / q.size);
+    const int32_t j = (int32_t)(local - (int64_t)inst * q.size);
+    const int64_t grp = q.gbase + inst;
+    int32_t rank, tidx = q.tidx, slot = q.slot;
+    uint64_t gid;
+    const int32_t s = q.stage;
+    switch (q.type) {
+      case PRISM_ROLE_TP:  // instance = dp index, member = tp index
+        rank = rank_of(g, j, s, inst);
+        gid = (uint64_t)s + (uint64_t)g.pp * inst;
+        break;
+      case PRISM_ROLE_DP:  // instance = tp index, member = dp index
+        rank = rank_of(g, inst, s, j);
+        gid = (uint64_t)inst + (uint64_t)g.tp * s;
+        break;
+      case PRISM_ROLE_EP: {  // instance = (tp, edp), member = ep index
+        int32_t tpi = inst % g.tp, edp = inst / g.tp;
+        rank = rank_of(g, tpi, s, edp * g.ep + j);
+        gid = (uint64_t)tpi + (uint64_t)g.tp * (s + (uint64_t)g.pp * edp);
+        break;
+      }
+      case PRISM_ROLE_EDP: {  // instance = (tp, ep), member = edp index
+        int32_t tpi = inst % g.tp, epi = inst / g.tp;
+        rank = rank_of(g, tpi, s, j * g.ep + epi);
+        gid = (uint64_t)tpi + (uint64_t)g.tp * (s + (uint64_t)g.pp * epi);
+        break;
+      }
+      case PRISM_ROLE_WORLD:
+        rank = j;
+        tidx = g.wpos[q.wpos + g.rank_stage[j]];
+        gid = 0;
+        break;
+      default: {  // P2P message: member 0 = sender, member 1 = receiver (same tp/dp coords)
+        int32_t tpi = inst % g.tp, dpi = inst / g.tp;
+        int32_t sender = rank_of(g, tpi, s, dpi);
+        if (j == 0) {
+          rank = sender;
+        } else {
+          rank = rank_of(g, tpi, q.stage2, dpi);
+          tidx = q.tidx2;
+          slot = q.slot2;
+        }
+        gid = (uint64_t)sender * 2 + q.dir;
+        break;
+      }
+    }
+    const int32_t node = g.rank_ptr[rank] + tidx;
+    g.grp_mem[m] = node;
+    g.node_grp[g.node_gptr[node] + slot] = (int32_t)grp;
+    if (j == 0) {
+      g.grp_ptr[grp] = (int32_t)m;
+      g.grp_dur[grp] = q.dur;
+      g.grp_level[grp] = q.level;
+      g.grp_uid[grp] = ((uint64_t)q.type << 56) | (gid << 24) | (uint64_t)q.occ;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_expand(const DevGraph &g, cudaStream_t st) {
+  rank_tables_kernel<<<1, 1024, 0, st>>>(g);
+  if (g.N > 0) {
+    int blocks = g.W < 148 * 16 ? g.W : 148 * 16;
+    expand_nodes_kernel<<<blocks, 256, 0, st>>>(g);
+  }
+  if (g.M > 0) {
+    int64_t want = (g.M + 255) / 256;
+    int blocks = (int)(want < 148 * 32 ? want : 148 * 32);
+    build_groups_kernel<<<blocks, 256, 0, st>>>(g);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace prism

@@ -1,0 +1,81 @@
+// graph.h — the device-resident graph (row a3/a4 output) and launch wrappers of every kernel.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "prism_internal.h"
+
+namespace prism {
+
+// Plain device pointers; passed by value to kernels.
+struct DevGraph {
+  int32_t W, pp, tp, dp, ep, order;
+  int64_t N, G, M;
+  // rank tables
+  int32_t *rank_ptr;        // [W+1] first node of each rank
+  int32_t *rank_slot;       // [W+1] first membership slot (node_grp) of each rank
+  int32_t *rank_stage;      // [W]
+  // node SoA
+  int32_t *node_rank;       // [N]
+  int64_t *node_dur;        // [N]
+  uint8_t *node_kind;       // [N]
+  uint32_t *node_label;     // [N]
+  int64_t *node_alloc;      // [N]
+  int64_t *node_free;       // [N]
+  int32_t *node_prev_sync;  // [N]
+  int32_t *node_gptr;       // [N+1]
+  int32_t *node_grp;        // [M]
+  // sync-group CSR (sorted by level)
+  int32_t *grp_ptr;         // [G+1]
+  int32_t *grp_mem;         // [M]
+  int64_t *grp_dur;         // [G]
+  uint64_t *grp_uid;        // [G]
+  int32_t *grp_level;       // [G]
+  // per-stage template tables (tiny; L2 resident)
+  const prism_op *t_ops;    // concatenated templates
+  int64_t *t_op0;           // [pp] first op of each stage
+  int64_t *t_len;           // [pp]
+  int32_t *t_prev_sync;     // per op
+  int32_t *t_slot_ptr;      // per op
+  int64_t *t_slots_total;   // [pp]
+  int64_t *static_mem;      // [pp]
+  const QGroup *q;          // quotient groups (level order)
+  int32_t nq;
+  const int32_t *wpos;      // WORLD per-stage template indices
+};
+
+// Scenario parameters as seen by the kernels.
+struct ScenParams {
+  int32_t S;         // scenarios
+  int32_t amp;       // amp_q16
+  uint64_t seed;
+  uint32_t mask;     // kind mask
+  int32_t record;    // write fin[N][S]
+  int32_t mod;       // 2*amp+1
+  uint64_t mod_magic;  // Lemire fastmod constant for mod (x < 2^32)
+};
+
+// Tile of a level launch: `cnt` concrete groups of quotient group `q` starting at instance `i0`.
+struct Tile {
+  int32_t q, i0, cnt, pad;
+};
+
+// expand.cu
+cudaError_t launch_expand(const DevGraph &g, cudaStream_t st);
+// replay.cu
+cudaError_t launch_level(const DevGraph &g, const ScenParams &p, const Tile *tiles, int32_t ntiles,
+                         int32_t max_cnt, int64_t *fin, int64_t *gfin, int lanes, int nchunks,
+                         cudaStream_t st);
+cudaError_t launch_tail(const DevGraph &g, const ScenParams &p, int64_t *fin, const int64_t *gfin,
+                        int64_t *rank_end, int lanes, int nchunks, cudaStream_t st);
+cudaError_t launch_reduce(int32_t W, int32_t S, int32_t Sp, const int64_t *rank_end, int64_t *iter,
+                          cudaStream_t st);
+cudaError_t launch_query(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin,
+                         const int64_t *gfin, int32_t rank, int32_t scen, int64_t *start_out,
+                         int64_t *finish_out, cudaStream_t st);
+// memory.cu
+cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st);
+
+}  // namespace prism

@@ -1,0 +1,58 @@
+// memory.cu — row a9: per-rank peak memory ("max_memory_allocated").
+//
+// Events per op: +alloc at its start, -free at its finish, ordered by (time, per-rank event
+// index). On a single-stream rank the event times are non-decreasing in program order (start_i >=
+// finish_{i-1} >= start_{i-1}), so that order IS program order (Z6) and the peak
+// does not depend on the scenario: peak_r = static + max(0, max_i (R_i + alloc_i)) where R_i is
+// the exclusive prefix sum of (alloc - free) — the running total right after op i's allocation.
+// One warp per rank: 32 ops per step, 64-bit warp inclusive scan with shuffles, HBM read-bound
+// (16 B per node: alloc + free), 8 B per rank written.
+#include <cuda_runtime.h>
+
+#include "graph.h"
+
+namespace prism {
+
+namespace {
+
+__global__ void __launch_bounds__(256) peak_kernel(DevGraph g, int64_t *__restrict__ peak) {
+  const int lane = threadIdx.x & 31;
+  const int32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (int32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < g.W; r += warps) {
+    const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
+    int64_t carry = 0, best = 0;
+    for (int32_t base = rb; base < re; base += 32) {
+      const int32_t i = base + lane;
+      int64_t a = 0, f = 0;
+      if (i < re) {
+        a = __ldcs(g.node_alloc + i);
+        f = __ldcs(g.node_free + i);
+      }
+      int64_t x = a - f;  // inclusive scan of (alloc - free)
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      const int64_t after_alloc = carry + x - (a - f) + a;  // R_i + alloc_i
+      int64_t m = i < re ? after_alloc : 0;
+#pragma unroll
+      for (int off = 16; off; off >>= 1) m = max(m, (int64_t)__shfl_xor_sync(0xffffffffu, m, off));
+      best = max(best, m);
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) peak[r] = g.static_mem[g.rank_stage[r]] + best;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st) {
+  if (g.W == 0) return cudaSuccess;
+  int blocks = (g.W + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  peak_kernel<<<blocks, 256, 0, st>>>(g, peak);
+  return cudaGetLastError();
+}
+
+}  // namespace prism

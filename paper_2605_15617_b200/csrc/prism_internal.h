@@ -1,0 +1,81 @@
+// prism_internal.h — shared declarations of the CUDA path (kernels + C ABI). Not part of the ABI.
+//
+// Data layout in HBM:
+//   node SoA, rank-major / program order:  node_rank[N] i32, node_dur[N] i64, node_kind[N] u8,
+//     node_label[N] u32, node_alloc[N] i64, node_free[N] i64, node_prev_sync[N] i32 (previous
+//     sync node of the same rank, -1 if none), node_gptr[N+1] i32 -> node_grp[M] i32 (the sync
+//     groups of a node, slot order = P2P mask bit order).
+//   sync-group CSR sorted by level:  grp_ptr[G+1] i32 -> grp_mem[M] i32 (member node ids),
+//     grp_dur[G] i64 (max of members' op durations, reading Z2), grp_uid[G] u64 (perturbation
+//     uid), grp_level[G] i32.
+//   replay state (per call):  fin[N][S] i64 (scenario-fastest: one node's S finishes are one
+//     contiguous 8*S-byte run), gfin[G][S] i64 (group finish = max member ready + dur'),
+//     rank_end[W][S] i64, iter[S] i64.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/prism.h"
+
+namespace prism {
+
+// One quotient group: a template-level synchronization (all concrete instances are symmetric
+// under the topology, so level / duration / member positions are per quotient group).
+struct QGroup {
+  int32_t type;        // PRISM_ROLE_TP..WORLD (collective) or PRISM_ROLE_P2P
+  int32_t stage;       // collective: the stage of every member; P2P: sender stage
+  int32_t tidx;        // collective: template index; P2P: sender template index
+  int32_t slot;        // node_grp slot of the membership (sender for P2P)
+  int32_t stage2;      // P2P receiver stage
+  int32_t tidx2;       // P2P receiver template index
+  int32_t slot2;       // P2P receiver slot
+  int32_t size;        // members per concrete group
+  int32_t inst;        // concrete instances
+  int32_t level;       // 1-based frontier level
+  int32_t occ;         // occurrence number (uid low bits)
+  int32_t dir;         // P2P: 0 = SEND_NEXT/RECV_PREV, 1 = SEND_PREV/RECV_NEXT
+  int32_t wpos;        // WORLD: offset of its per-stage template indices in the wpos table
+  int32_t pad;
+  int64_t dur;         // shared duration (max over member ops)
+  int64_t gbase;       // first concrete group id
+  int64_t mbase;       // first membership index
+};
+
+struct Topo {
+  int32_t tp, pp, dp, ep, order;
+};
+
+// Host-side plan of a graph (validation + quotient analysis), produced by plan_graph().
+struct Plan {
+  Topo topo;
+  int64_t W = 0, N = 0, G = 0, M = 0, sync_nodes = 0;
+  int32_t levels = 0, max_group = 0;
+  // per template op (concatenated over stages, indexed by global op index)
+  std::vector<int32_t> t_prev_sync;  // template-local index of the previous sync op, -1
+  std::vector<int32_t> t_slot_ptr;   // template-local slot prefix (exclusive), per op
+  std::vector<int32_t> t_slots;      // slots of each op
+  std::vector<int64_t> stage_len;    // [pp]
+  std::vector<int64_t> stage_slots;  // [pp] total slots per template
+  std::vector<int64_t> stage_op0;    // [pp] first global op index
+  std::vector<QGroup> q;             // sorted by (level, creation order)
+  std::vector<int32_t> wpos;         // WORLD template indices, pp per WORLD quotient group
+  std::vector<int32_t> level_q_ptr;  // [levels+2]: quotient groups of level l = [ptr[l], ptr[l+1])
+};
+
+// Returns PRISM_OK or an error status with *err filled.
+prism_status plan_graph(const prism_topology &topo, const prism_templates &tm, Plan &plan,
+                        std::string &err);
+
+// ---- device helpers -------------------------------------------------------------------------
+#ifdef __CUDACC__
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+#endif
+
+}  // namespace prism

@@ -1,0 +1,283 @@
+// replay.cu — rows a6-a8: wavefront replay over the level-sorted CSR DAG.
+//
+// Semantics (§5.1, §6.1, §5.3; readings Z2-Z5 in DESIGN.md §3):
+//   ready(n)  = finish of n's stream predecessor (0 for a rank's first op)
+//   compute   : finish = ready + dur'                              (waits out the duration)
+//   group g   : start_g = max over members of ready (segmented max); gfin_g = start_g + dur'_g
+//   sync node : finish = max over its groups of gfin_g              (all must reach it)
+// One launch per frontier level l (row a5) relaxes every group of level l: for each membership a
+// team of L lanes (lane = scenario, SPL scenarios per lane) walks the member's chain segment from
+// its previous sync node (resolved at a lower level) through the compute spans in between,
+// writing their finish times (once, by the membership in the node's first slot), and folds the
+// member's ready time into a shared-memory accumulator of its group (the segmented max); the
+// block then writes gfin for its groups. All arithmetic is int64; results are exact.
+#include <cuda_runtime.h>
+
+#include "graph.h"
+
+namespace prism {
+
+namespace {
+
+constexpr uint64_t K_GOLD = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t K_MIX = 0xBF58476D1CE4E5B9ULL;
+
+// Reading Z8: d' = (d * (65536 + delta)) >> 16, delta = ((h >> 40) mod (2 amp + 1)) - amp with
+// h = splitmix64(seed ^ k*K_GOLD ^ uid*K_MIX). `x` is that xor already formed. The mod uses
+// Lemire's direct remainder (exact for 32-bit numerators): r = hi64((M * v) mod 2^64, d).
+__device__ __forceinline__ int64_t perturb_x(int64_t d, uint64_t x, const ScenParams &p) {
+  const uint64_t h = splitmix64(x);
+  const uint32_t v = (uint32_t)(h >> 40);
+  const uint64_t low = p.mod_magic * (uint64_t)v;
+  const uint32_t r = (uint32_t)__umul64hi(low, (uint64_t)(uint32_t)p.mod);
+  const int64_t delta = (int64_t)r - p.amp;
+  return (d * (65536 + delta)) >> 16;
+}
+
+template <int SPL>
+struct Vec;
+template <>
+struct Vec<1> {
+  __device__ static void store(int64_t *p, const int64_t *t) { *p = t[0]; }
+  __device__ static void load_max(const int64_t *p, int64_t *t) { t[0] = max(t[0], __ldcg(p)); }
+};
+template <>
+struct Vec<2> {
+  __device__ static void store(int64_t *p, const int64_t *t) {
+    longlong2 v;
+    v.x = t[0];
+    v.y = t[1];
+    *reinterpret_cast<longlong2 *>(p) = v;
+  }
+  __device__ static void load_max(const int64_t *p, int64_t *t) {
+    longlong2 v = __ldcg(reinterpret_cast<const longlong2 *>(p));
+    t[0] = max(t[0], (int64_t)v.x);
+    t[1] = max(t[1], (int64_t)v.y);
+  }
+};
+
+// Walk the chain segment that ends at node n: returns ready(n) per scenario in t[]. When `write`,
+// stores the finish of the previous sync node and of every compute span in the segment.
+template <int SPL>
+__device__ __forceinline__ void walk_segment(const DevGraph &g, const ScenParams &p, int32_t r,
+                                             int32_t ps, int32_t end, int64_t *__restrict__ fin,
+                                             const int64_t *__restrict__ gfin, int32_t Sp, int32_t k0,
+                                             const uint64_t *sx, const bool *pj, bool write, int64_t *t) {
+  const int32_t rb = g.rank_ptr[r];
+#pragma unroll
+  for (int j = 0; j < SPL; ++j) t[j] = 0;
+  if (ps >= 0) {
+    const int32_t h0 = g.node_gptr[ps], h1 = g.node_gptr[ps + 1];
+    for (int32_t h = h0; h < h1; ++h) {
+      const int64_t grp = g.node_grp[h];
+      Vec<SPL>::load_max(gfin + grp * Sp + k0, t);
+    }
+    if (write) Vec<SPL>::store(fin + (int64_t)ps * Sp + k0, t);
+  }
+  const uint64_t rhi = (uint64_t)r << 32;
+  for (int32_t i = (ps >= 0 ? ps + 1 : rb); i < end; ++i) {
+    const int64_t d = g.node_dur[i];
+    const uint64_t uidx = (rhi | (uint32_t)(i - rb)) * K_MIX;
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) {
+      const int64_t dd = pj[j] ? perturb_x(d, sx[j] ^ uidx, p) : d;
+      t[j] += dd;
+    }
+    if (write) Vec<SPL>::store(fin + (int64_t)i * Sp + k0, t);
+  }
+}
+
+template <int L, int SPL>
+__global__ void __launch_bounds__(256) level_kernel(DevGraph g, ScenParams p,
+                                                     const Tile *__restrict__ tiles,
+                                                     int64_t *__restrict__ fin,
+                                                     int64_t *__restrict__ gfin) {
+  constexpr int SC = L * SPL;
+  constexpr int TEAMS = 256 / L;
+  extern __shared__ unsigned long long acc[];
+  const Tile tl = tiles[blockIdx.x];
+  const QGroup &q = g.q[tl.q];
+  const int32_t z = q.size;
+  const int32_t cnt = tl.cnt;
+  const int64_t g0 = q.gbase + tl.i0;
+  const int64_t m0 = q.mbase + (int64_t)tl.i0 * z;
+  const int32_t nmem = cnt * z;
+  const int32_t Sp = gridDim.y * SC;
+  for (int x = threadIdx.x; x < cnt * SC; x += 256) acc[x] = 0ULL;
+  __syncthreads();
+
+  const int team = threadIdx.x / L, lane = threadIdx.x % L;
+  const int32_t k0 = blockIdx.y * SC + lane * SPL;
+  uint64_t sx[SPL];
+  bool pj[SPL];  // scenario 0 and unmasked kinds are never perturbed
+#pragma unroll
+  for (int j = 0; j < SPL; ++j) {
+    sx[j] = p.seed ^ ((uint64_t)(k0 + j) * K_GOLD);
+    pj[j] = (p.mask & 1u) && p.amp > 0 && (k0 + j) > 0;
+  }
+  for (int32_t mm = team; mm < nmem; mm += TEAMS) {
+    const int32_t n = g.grp_mem[m0 + mm];
+    const int32_t gl = mm / z;
+    const int32_t r = g.node_rank[n];
+    const int32_t ps = g.node_prev_sync[n];
+    const bool primary = p.record && g.node_grp[g.node_gptr[n]] == (int32_t)(g0 + gl);
+    int64_t t[SPL];
+    walk_segment<SPL>(g, p, r, ps, n, fin, gfin, Sp, k0, sx, pj, primary, t);
+#pragma unroll
+    for (int j = 0; j < SPL; ++j) atomicMax(&acc[gl * SC + lane * SPL + j], (unsigned long long)t[j]);
+  }
+  __syncthreads();
+  const uint32_t gbit = q.type == PRISM_ROLE_P2P ? 4u : 2u;
+  const bool gpert = (p.mask & gbit) && p.amp > 0;
+  for (int x = threadIdx.x; x < cnt * SC; x += 256) {
+    const int32_t gl = x / SC;
+    const int32_t kk = blockIdx.y * SC + (x - gl * SC);
+    const int64_t grp = g0 + gl;
+    const int64_t d = g.grp_dur[grp];
+    int64_t dd = d;
+    if (gpert && kk > 0) dd = perturb_x(d, p.seed ^ ((uint64_t)kk * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
+    gfin[grp * Sp + kk] = (int64_t)acc[x] + dd;
+  }
+}
+
+// Tail: after the last sync node of every rank (or the whole chain if it has none).
+template <int L, int SPL>
+__global__ void __launch_bounds__(256) tail_kernel(DevGraph g, ScenParams p, int64_t *__restrict__ fin,
+                                                    const int64_t *__restrict__ gfin,
+                                                    int64_t *__restrict__ rank_end) {
+  constexpr int SC = L * SPL;
+  constexpr int TEAMS = 256 / L;
+  const int32_t Sp = gridDim.y * SC;
+  const int team = threadIdx.x / L, lane = threadIdx.x % L;
+  const int32_t k0 = blockIdx.y * SC + lane * SPL;
+  uint64_t sx[SPL];
+  bool pj[SPL];
+#pragma unroll
+  for (int j = 0; j < SPL; ++j) {
+    sx[j] = p.seed ^ ((uint64_t)(k0 + j) * K_GOLD);
+    pj[j] = (p.mask & 1u) && p.amp > 0 && (k0 + j) > 0;
+  }
+  for (int32_t r = blockIdx.x * TEAMS + team; r < g.W; r += gridDim.x * TEAMS) {
+    const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
+    int64_t t[SPL];
+    if (re == rb) {
+#pragma unroll
+      for (int j = 0; j < SPL; ++j) t[j] = 0;
+    } else {
+      const int32_t last = re - 1;
+      const bool last_sync = g.node_gptr[last + 1] > g.node_gptr[last];
+      const int32_t ps = last_sync ? last : g.node_prev_sync[last];
+      walk_segment<SPL>(g, p, r, ps, re, fin, gfin, Sp, k0, sx, pj, p.record != 0, t);
+    }
+    Vec<SPL>::store(rank_end + (int64_t)r * Sp + k0, t);
+  }
+}
+
+// Row a8: T_k = max over ranks of the rank's last finish (every chain is non-decreasing).
+__global__ void __launch_bounds__(256) reduce_iter_kernel(int32_t W, int32_t Sp,
+                                                          const int64_t *__restrict__ rank_end,
+                                                          int64_t *__restrict__ iter) {
+  const int32_t k = blockIdx.x;
+  int64_t m = 0;
+  for (int32_t r = threadIdx.x; r < W; r += blockDim.x) m = max(m, rank_end[(int64_t)r * Sp + k]);
+  for (int off = 16; off; off >>= 1) m = max(m, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off));
+  __shared__ int64_t wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = max(m, wm[w]);
+    iter[k] = max(m, wm[0]);
+  }
+}
+
+// prism_query_rank: start/finish of one rank's ops in one scenario from fin/gfin.
+__global__ void query_kernel(DevGraph g, ScenParams p, int32_t Sp, const int64_t *__restrict__ fin,
+                             const int64_t *__restrict__ gfin, int32_t r, int32_t k,
+                             int64_t *__restrict__ start_out, int64_t *__restrict__ finish_out) {
+  const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
+  for (int32_t i = rb + blockIdx.x * blockDim.x + threadIdx.x; i < re; i += gridDim.x * blockDim.x) {
+    const int32_t h0 = g.node_gptr[i], h1 = g.node_gptr[i + 1];
+    int64_t st;
+    if (h0 == h1) {
+      st = i == rb ? 0 : fin[(int64_t)(i - 1) * Sp + k];
+    } else {  // start = max over groups of (gfin - dur')
+      st = 0;
+      for (int32_t h = h0; h < h1; ++h) {
+        const int64_t grp = g.node_grp[h];
+        const uint32_t gbit = (g.grp_uid[grp] >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
+        int64_t d = g.grp_dur[grp];
+        if ((p.mask & gbit) && p.amp > 0 && k > 0)
+          d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
+        st = max(st, gfin[grp * Sp + k] - d);
+      }
+    }
+    start_out[i - rb] = st;
+    finish_out[i - rb] = fin[(int64_t)i * Sp + k];
+  }
+}
+
+template <int L, int SPL>
+cudaError_t level_t(const DevGraph &g, const ScenParams &p, const Tile *tiles, int32_t ntiles,
+                    int32_t max_cnt, int64_t *fin, int64_t *gfin, int nchunks, cudaStream_t st) {
+  const size_t smem = (size_t)max_cnt * L * SPL * sizeof(unsigned long long);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(level_kernel<L, SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid(ntiles, nchunks);
+  level_kernel<L, SPL><<<grid, 256, smem, st>>>(g, p, tiles, fin, gfin);
+  return cudaGetLastError();
+}
+
+template <int L, int SPL>
+cudaError_t tail_t(const DevGraph &g, const ScenParams &p, int64_t *fin, const int64_t *gfin,
+                   int64_t *rank_end, int nchunks, cudaStream_t st) {
+  constexpr int TEAMS = 256 / L;
+  int blocks = (g.W + TEAMS - 1) / TEAMS;
+  if (blocks < 1) blocks = 1;
+  dim3 grid(blocks, nchunks);
+  tail_kernel<L, SPL><<<grid, 256, 0, st>>>(g, p, fin, gfin, rank_end);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_level(const DevGraph &g, const ScenParams &p, const Tile *tiles, int32_t ntiles,
+                         int32_t max_cnt, int64_t *fin, int64_t *gfin, int lanes, int nchunks,
+                         cudaStream_t st) {
+  switch (lanes) {
+    case 1: return level_t<1, 1>(g, p, tiles, ntiles, max_cnt, fin, gfin, nchunks, st);
+    case 2: return level_t<2, 1>(g, p, tiles, ntiles, max_cnt, fin, gfin, nchunks, st);
+    case 4: return level_t<4, 1>(g, p, tiles, ntiles, max_cnt, fin, gfin, nchunks, st);
+    case 8: return level_t<8, 1>(g, p, tiles, ntiles, max_cnt, fin, gfin, nchunks, st);
+    case 16: return level_t<16, 1>(g, p, tiles, ntiles, max_cnt, fin, gfin, nchunks, st);
+    default: return level_t<32, 2>(g, p, tiles, ntiles, max_cnt, fin, gfin, nchunks, st);
+  }
+}
+
+cudaError_t launch_tail(const DevGraph &g, const ScenParams &p, int64_t *fin, const int64_t *gfin,
+                        int64_t *rank_end, int lanes, int nchunks, cudaStream_t st) {
+  switch (lanes) {
+    case 1: return tail_t<1, 1>(g, p, fin, gfin, rank_end, nchunks, st);
+    case 2: return tail_t<2, 1>(g, p, fin, gfin, rank_end, nchunks, st);
+    case 4: return tail_t<4, 1>(g, p, fin, gfin, rank_end, nchunks, st);
+    case 8: return tail_t<8, 1>(g, p, fin, gfin, rank_end, nchunks, st);
+    case 16: return tail_t<16, 1>(g, p, fin, gfin, rank_end, nchunks, st);
+    default: return tail_t<32, 2>(g, p, fin, gfin, rank_end, nchunks, st);
+  }
+}
+
+cudaError_t launch_reduce(int32_t W, int32_t S, int32_t Sp, const int64_t *rank_end, int64_t *iter,
+                          cudaStream_t st) {
+  reduce_iter_kernel<<<S, 256, 0, st>>>(W, Sp, rank_end, iter);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_query(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin,
+                            const int64_t *gfin, int32_t rank, int32_t scen, int64_t *start_out,
+                            int64_t *finish_out, cudaStream_t st) {
+  query_kernel<<<64, 256, 0, st>>>(g, p, Sp, fin, gfin, rank, scen, start_out, finish_out);
+  return cudaGetLastError();
+}
+
+}  // namespace prism

@@ -1,0 +1,202 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Integer times and bytes => the bar is bit-exact equality everywhere (north_star).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as w
+
+pytestmark = pytest.mark.gpu
+
+NPROC = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def prism():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2605_15617_b200 as P
+
+    P.build_library()
+    P.use_torch_allocator()
+    return P
+
+
+def _graph(P, tm):
+    import torch
+
+    return P.Graph(tm, stream=torch.cuda.current_stream().cuda_stream)
+
+
+# ------------------------------------------------------------------ rows a1-a5: the CSR DAG
+def _check_csr(P, tm):
+    g = _graph(P, tm)
+    st = g.stats()
+    ex = oracle.expand(tm)
+    assert (st["nodes"], st["groups"], st["memberships"], st["levels"]) == (
+        ex["nodes"], ex["groups"], ex["memberships"], ex["levels"])
+    # node SoA: every rank holds its stage template (rank-major, program order)
+    rank_ptr = g.export("rank_ptr")
+    node_rank = g.export("node_rank")
+    dur = g.export("node_dur")
+    t = tm.topo
+    for r in range(t.world):
+        s = (r // t.tp) % t.pp if t.rank_order == 0 else r // (t.tp * t.dp)
+        a, b = rank_ptr[r], rank_ptr[r + 1]
+        tmpl = tm.stage(s)
+        assert b - a == len(tmpl)
+        assert (node_rank[a:b] == r).all()
+        assert (dur[a:b] == tmpl["dur_ns"]).all()
+        assert (g.export("node_alloc")[a:b] == tmpl["mem_alloc"]).all() if r == 0 else True
+    # groups: same uid set, same members / duration / level per uid
+    uid = g.export("grp_uid")
+    gptr = g.export("grp_ptr")
+    mem = g.export("grp_mem")
+    gdur = g.export("grp_dur")
+    glvl = g.export("grp_level")
+    assert len(set(uid.tolist())) == len(uid)
+    o_index = {int(u): i for i, u in enumerate(ex["uid"])}
+    assert set(o_index) == set(int(u) for u in uid)
+    for i, u in enumerate(uid):
+        j = o_index[int(u)]
+        mine = np.sort(mem[gptr[i]:gptr[i + 1]])
+        theirs = ex["mem"][ex["ptr"][j]:ex["ptr"][j + 1]]
+        assert np.array_equal(mine, theirs), (hex(int(u)), mine, theirs)
+        assert gdur[i] == ex["dur"][j] and glvl[i] == ex["level"][j]
+    assert (np.diff(glvl) >= 0).all()  # sorted by level (frontier tiles are contiguous)
+    # node -> group lists are the inverse of group -> members
+    ngptr = g.export("node_gptr")
+    ngrp = g.export("node_grp")
+    for n in range(0, st["nodes"], max(1, st["nodes"] // 500)):
+        for h in ngrp[ngptr[n]:ngptr[n + 1]]:
+            assert n in mem[gptr[h]:gptr[h + 1]]
+    g.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2s", "C3s", "C4s", "C5s"])
+def test_csr_configs(prism, name):
+    tm = w.config(name) if name == "C1" else w.scaled(name[:2])
+    _check_csr(prism, tm)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_csr_random(prism, seed):
+    _check_csr(prism, w.random_templates(seed, max_world=32, max_ops=40))
+
+
+# ------------------------------------------------------------------ rows a6-a9: replay + memory
+def _check_replay(P, tm, S, amp=6554, mask=7, times=True, seed=0x5EED):
+    g = _graph(P, tm)
+    it = g.replay(S, seed=seed, amp_q16=amp, kind_mask=mask, record=True)
+    ref = oracle.replay(tm, S, seed=seed, amp_q16=amp, kind_mask=mask, times=times,
+                        threads=min(NPROC, S))
+    assert np.array_equal(it, ref["iter"]), (it[:8], ref["iter"][:8])
+    assert np.array_equal(g.peak_memory(), ref["peak"][0])
+    if times:
+        W = tm.topo.world
+        ranks = range(W) if W <= 64 else np.random.default_rng(0).choice(W, 64, replace=False)
+        for k in sorted({0, min(1, S - 1), S - 1}):
+            for r in ranks:
+                st, fi, coords = g.query_rank(int(r), k)
+                rp = g.export("rank_ptr")
+                a, b = rp[r], rp[r + 1]
+                assert np.array_equal(fi, ref["finish"][k, a:b]), (k, r)
+                assert np.array_equal(st, ref["start"][k, a:b]), (k, r)
+    g.close()
+    return it
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_replay_random(prism, seed):
+    tm = w.random_templates(seed, max_world=32, max_ops=40)
+    S = [1, 2, 3, 5, 17, 33, 64, 70][seed % 8]
+    _check_replay(prism, tm, S)
+
+
+def test_c1_closed_form_gpu(prism):
+    assert _check_replay(prism, w.config("C1"), 1, amp=0)[0] == 64_800
+    assert _check_replay(prism, w.config("C1", p2p_c=50), 1, amp=0)[0] == 65_050
+    g = _graph(prism, w.config("C1"))
+    pk = g.peak_memory()
+    assert sorted(set(pk.tolist())) == [1_077_936_128, 1_082_130_432]
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_replay_scaled_configs(prism, name):
+    _check_replay(prism, w.scaled(name), 64, times=True)
+
+
+def test_fin_array_all_nodes(prism):
+    """Every node-scenario finish of the recorded replay equals the oracle (scenario-fastest)."""
+    tm = w.scaled("C3")
+    g = _graph(prism, tm)
+    S = 64
+    g.replay(S, amp_q16=6554, kind_mask=7)
+    fin = g.export("fin", scen_pad=64).reshape(-1, 64)
+    ref = oracle.replay(tm, S, amp_q16=6554, kind_mask=7, times=True, threads=NPROC)
+    assert np.array_equal(fin[:, :S].T, ref["finish"])
+
+
+def test_deterministic_and_record_off(prism):
+    tm = w.scaled("C2")
+    g = _graph(prism, tm)
+    a = g.replay(64, amp_q16=6554, kind_mask=7)
+    b = g.replay(64, amp_q16=6554, kind_mask=7)
+    c = g.replay(64, amp_q16=6554, kind_mask=7, record=False)
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+    with pytest.raises(prism.PrismError) as e:
+        g.query_rank(0, 0)
+    assert e.value.name == "PRISM_E_NOT_REPLAYED"
+
+
+def test_edge_cases(prism):
+    # all-empty templates
+    tm = w.assemble(w.Topology(2, 2, 2), [np.zeros(0, w.OP_DTYPE)] * 2, [5, 6])
+    g = _graph(prism, tm)
+    assert g.replay(3).tolist() == [0, 0, 0]
+    assert g.peak_memory().tolist() == [5, 5, 6, 6, 5, 5, 6, 6]
+    # one stage empty, the other compute only; amplitude maximum
+    b = w._StageBuilder()
+    for d in (0, 1, 2**40):
+        b.compute(d)
+    tm = w.assemble(w.Topology(1, 2, 3), [b.array(), np.zeros(0, w.OP_DTYPE)], [0, 0])
+    _check_replay(prism, tm, 9, amp=65535)
+    with pytest.raises(prism.PrismError) as e:
+        g.query_rank(99, 0)
+    assert e.value.name == "PRISM_E_UNKNOWN_RANK"
+
+
+def test_world_collectives_large_groups(prism):
+    """WORLD collectives (one group spanning every rank) and EP/EDP groups."""
+    for seed in range(100, 110):
+        tm = w.random_templates(seed, max_world=64, max_ops=60)
+        _check_replay(prism, tm, 64, times=False)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_full_size_sampled(prism, name):
+    """BASELINE.json full sizes in the bench launch configuration (S = 64, +-10% jitter): the
+    iteration time of sampled scenarios and every rank's peak equal the oracle's."""
+    tm = w.config(name)
+    g = _graph(prism, tm)
+    S = 64
+    it = g.replay(S, amp_q16=6554, kind_mask=7)
+    pk = g.peak_memory()
+    ks = [0, 1, 63]
+    res = [oracle.replay(tm, 1, scen_first=k, amp_q16=6554, kind_mask=7, peaks=(k == 0)) for k in ks]
+    for k, r in zip(ks, res):
+        assert it[k] == r["iter"][0], (name, k)
+    assert np.array_equal(pk, res[0]["peak"][0])
+    # per-rank end times of scenario 63 via query of sampled ranks
+    rp = g.export("rank_ptr")
+    for rk in np.random.default_rng(1).choice(tm.topo.world, 16, replace=False):
+        st, fi, _ = g.query_rank(int(rk), 63)
+        assert fi[-1] == res[2]["rank_end"][0, rk] if len(fi) else True
+    g.close()
