@@ -123,7 +123,7 @@ def run_prism(args):
     sh = stream.cuda_stream
     tm = w.config(args.config)
     S = args.scenarios
-    kw = dict(amp_q16=args.amp, kind_mask=7, seed=0x5EED)
+    kw = dict(amp_q16=args.amp, kind_mask=7, seed=0x5EED, algo=args.algo)
     iter_dev = torch.zeros(S, dtype=torch.int64, device="cuda")
     peak_dev = torch.zeros(tm.topo.world, dtype=torch.int64, device="cuda")
 
@@ -181,6 +181,7 @@ def run_prism(args):
         for k in ("levels", "tail", "reduce", "peak"):
             prof[k].append(t[k])
     prof["expand"].append(gp.last_timing()["expand"])
+    schedule = gp.last_algo()
     gp.close()
     med = {k: sorted(v)[len(v) // 2] for k, v in prof.items()}
     ab = algorithmic_bytes(st, S)
@@ -237,7 +238,7 @@ def run_prism(args):
             "workload": f"{args.config}: {w.CONFIG_DESCRIPTIONS[args.config]}",
             "ranks": tm.topo.world, "nodes": st["nodes"], "sync_groups": st["groups"],
             "memberships": st["memberships"], "levels": st["levels"], "scenarios": S,
-            "amp_q16": args.amp, "record_times": True,
+            "amp_q16": args.amp, "record_times": True, "schedule": schedule,
             "parallelism": f"replicas{ws}" if ws > 1 else "single-gpu",
             "l2": "working set (fin[N][S] = %.1f GB) > 126 MB L2; no flush needed" % (st["nodes"] * S * 8 / 1e9),
         },
@@ -248,7 +249,9 @@ def run_prism(args):
         },
         "roofline": {
             "bound": "hbm",
-            "kernel": "replay (level_kernel x levels + tail_kernel + reduce_iter_kernel)",
+            "kernel": ("replay: cell_kernel (one cooperative launch) + reduce_iter_kernel"
+                       if schedule == "cells" else
+                       "replay: level_kernel x levels + tail_kernel + reduce_iter_kernel"),
             "achieved": round(achieved, 1),
             "peak": peak_bw,
             "peak_source": peak_src,
@@ -339,6 +342,7 @@ def main():
     ap.add_argument("--scenarios", type=int, default=64)
     ap.add_argument("--amp", type=int, default=6554)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--algo", default="auto", choices=["auto", "levels", "cells"])
     args = ap.parse_args()
     args.config = args.config.upper()
     if args.warmup < 3 and args.impl == "prism":

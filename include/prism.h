@@ -151,7 +151,11 @@ typedef struct {
   uint64_t seed;
   uint32_t kind_mask; /* bit (1<<PRISM_KIND_*) = perturb that kind                             */
   int32_t record;     /* nonzero: keep every node's finish time for prism_query_rank           */
+  int32_t algo;       /* PRISM_ALGO_AUTO (cells when they fit on the device, else levels),
+                         PRISM_ALGO_LEVELS (one launch per frontier level), PRISM_ALGO_CELLS   */
 } prism_scenarios;
+
+enum { PRISM_ALGO_AUTO = 0, PRISM_ALGO_LEVELS = 1, PRISM_ALGO_CELLS = 2 };
 
 /* ---- entry points ------------------------------------------------------------------------ */
 
@@ -214,6 +218,9 @@ PRISM_API prism_status prism_query_rank(prism_graph_t g, int32_t rank, int32_t s
 PRISM_API prism_status prism_graph_stats(prism_graph_t g, int64_t out[10]);
 
 PRISM_API void prism_destroy_graph(prism_graph_t g);
+
+/* Schedule used by the last replay: PRISM_ALGO_LEVELS or PRISM_ALGO_CELLS (0 before any). */
+PRISM_API prism_status prism_last_algo(prism_graph_t g, int32_t *algo_out);
 
 /* Device time (ms, CUDA events on the graph's stream) of the last call of each kernel group of a
  * graph built with PRISM_BUILD_PROFILE: out[0] expand (a1-a4, last build), out[1] level loop of the

@@ -17,13 +17,13 @@ import numpy as np
 __all__ = ["lib", "Graph", "plan", "PrismError", "build_library", "LIB_PATH", "EXPORTED_SYMBOLS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libprism_b200.so")
+LIB_PATH = os.environ.get("PRISM_LIB") or os.path.join(_HERE, "libprism_b200.so")  # PRISM_LIB: dev experiments
 
 EXPORTED_SYMBOLS = [
     "prism_status_string", "prism_last_error", "prism_abi_version", "prism_set_allocator",
     "prism_build_graph", "prism_replay", "prism_replay_async", "prism_peak_memory",
     "prism_peak_memory_async", "prism_query_rank", "prism_graph_stats", "prism_destroy_graph",
-    "prism_debug_export", "prism_plan", "prism_last_timing",
+    "prism_debug_export", "prism_plan", "prism_last_timing", "prism_last_algo",
 ]
 
 STATUS_NAMES = {
@@ -58,7 +58,7 @@ class _BuildOpts(ctypes.Structure):
 
 class _Scenarios(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("amp_q16", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("kind_mask", ctypes.c_uint32), ("record", ctypes.c_int32)]
+                ("kind_mask", ctypes.c_uint32), ("record", ctypes.c_int32), ("algo", ctypes.c_int32)]
 
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -100,10 +100,11 @@ def lib():
         L.prism_debug_export.argtypes = [P, ctypes.c_int32, P, ctypes.c_int64]
         L.prism_plan.argtypes = [P, P, P]
         L.prism_last_timing.argtypes = [P, P]
+        L.prism_last_algo.argtypes = [P, P]
         for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
                      "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
                      "prism_graph_stats", "prism_debug_export", "prism_plan",
-                     "prism_last_timing"):
+                     "prism_last_timing", "prism_last_algo"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
     return _lib
@@ -215,23 +216,31 @@ class Graph:
         _check(lib().prism_last_timing(self._h, _ptr(out)))
         return dict(zip(["expand", "levels", "tail", "reduce", "peak"], (float(x) for x in out)))
 
-    @staticmethod
-    def _scen(n, seed, amp_q16, kind_mask, record):
-        return _Scenarios(int(n), int(amp_q16), int(seed) & (2**64 - 1), int(kind_mask), int(bool(record)))
+    ALGOS = {"auto": 0, "levels": 1, "cells": 2}
+
+    @classmethod
+    def _scen(cls, n, seed, amp_q16, kind_mask, record, algo):
+        return _Scenarios(int(n), int(amp_q16), int(seed) & (2**64 - 1), int(kind_mask), int(bool(record)),
+                          cls.ALGOS[algo])
 
     def replay(self, n: int = 1, *, seed: int = 0x5EED, amp_q16: int = 0, kind_mask: int = 0,
-               record: bool = True) -> np.ndarray:
+               record: bool = True, algo: str = "auto") -> np.ndarray:
         """Iteration time (ns) of each of n scenarios (host result, synchronizing)."""
         out = np.zeros(n, np.int64)
-        sc = self._scen(n, seed, amp_q16, kind_mask, record)
+        sc = self._scen(n, seed, amp_q16, kind_mask, record, algo)
         _check(lib().prism_replay(self._h, ctypes.byref(sc), _ptr(out)))
         return out
 
     def replay_async(self, iter_dev_ptr: int, n: int = 1, *, seed: int = 0x5EED, amp_q16: int = 0,
-                     kind_mask: int = 0, record: bool = True) -> None:
+                     kind_mask: int = 0, record: bool = True, algo: str = "auto") -> None:
         """Asynchronous replay writing n int64 iteration times to a DEVICE pointer."""
-        sc = self._scen(n, seed, amp_q16, kind_mask, record)
+        sc = self._scen(n, seed, amp_q16, kind_mask, record, algo)
         _check(lib().prism_replay_async(self._h, ctypes.byref(sc), ctypes.c_void_p(iter_dev_ptr)))
+
+    def last_algo(self) -> str:
+        v = ctypes.c_int32(0)
+        _check(lib().prism_last_algo(self._h, ctypes.byref(v)))
+        return {0: "none", 1: "levels", 2: "cells"}[v.value]
 
     def peak_memory(self) -> np.ndarray:
         out = np.zeros(self.topo.tp * self.topo.pp * self.topo.dp, np.int64)

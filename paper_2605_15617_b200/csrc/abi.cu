@@ -62,6 +62,18 @@ struct prism_graph_s {
   size_t iter_bytes = 0;
   int64_t *scratch = nullptr;
   size_t scratch_bytes = 0;
+  // cell-kernel state
+  int64_t *rslot = nullptr;   // ready slots; parity-encoded, see replay_cells.cu
+  size_t rslot_bytes = 0;
+  int parity = 0;             // encoding of the next replay
+  bool rslot_dirty = true;    // needs a reset (new allocation / aborted replay / new stride)
+  int32_t rslot_Sp = 0;
+  int64_t *acc = nullptr;     // large-group accumulators [G_large][Sp]
+  size_t acc_bytes = 0;
+  uint32_t *sync_words = nullptr;  // arrive[G_large], status[4]
+  size_t sync_bytes = 0;
+  uint32_t *h_status = nullptr;    // pinned copy of the status word
+  int last_algo = 0;
   int recorded = 0;
   ScenParams last{};
   int32_t last_Sp = 0;
@@ -125,6 +137,10 @@ struct prism_graph_s {
     dfree(iter);
     dfree(scratch);
     dfree(tiles);
+    dfree(rslot);
+    dfree(acc);
+    dfree(sync_words);
+    if (h_status) cudaFreeHost(h_status);
     for (auto &b : blocks) dfree(b.first);
     cudaStreamSynchronize(stream);
     for (auto &e : ev)
@@ -241,6 +257,14 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.grp_dur = G->take<int64_t>(Gn);
   d.grp_uid = G->take<uint64_t>(Gn);
   d.grp_level = G->take<int32_t>(Gn);
+  d.node_mslot = G->take<int32_t>(M);
+  d.node_cls = G->take<uint8_t>(N);
+  d.node_sdur = G->take<int64_t>(N);
+  d.node_uid = G->take<uint64_t>(N);
+  d.grp_xbase = G->take<int64_t>(Gn);
+  d.grp_lidx = G->take<int32_t>(Gn);
+  d.M_cross = P.M_cross;
+  d.G_large = P.G_large;
   prism_op *t_ops = G->take<prism_op>(nops);
   d.t_ops = t_ops;
   d.t_op0 = G->take<int64_t>(pp);
@@ -325,11 +349,24 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   if (!G || !sc || !iter_dev) return fail(PRISM_E_INVALID_ARG, "null argument");
   if (sc->n < 1 || sc->n > (1 << 20) || sc->amp_q16 < 0 || sc->amp_q16 > 65535)
     return fail(PRISM_E_INVALID_ARG, "scenario count must be >= 1 and amp_q16 in [0, 65535]");
+  if (sc->algo < PRISM_ALGO_AUTO || sc->algo > PRISM_ALGO_CELLS) return fail(PRISM_E_INVALID_ARG, "unknown algo");
   CU(cudaSetDevice(G->device));
   const int32_t S = sc->n;
-  int lanes = 1;
-  while (lanes < S && lanes < 32) lanes <<= 1;
-  const int SC = lanes == 32 ? 64 : lanes;
+  const Plan &P = G->plan;
+  // schedule: the cell kernel (64-scenario chunks, one cooperative launch each) when every cell
+  // CTA of a chunk can be co-resident, else one launch per frontier level
+  const int cell_sc = cells_chunk_scenarios();
+  const int cell_chunks = (S + cell_sc - 1) / cell_sc;
+  bool cells = false;
+  if (sc->algo != PRISM_ALGO_LEVELS) {
+    cells = cells_fit(G->dg, cell_chunks);
+    if (!cells && sc->algo == PRISM_ALGO_CELLS)
+      return fail(PRISM_E_INVALID_ARG, "PRISM_ALGO_CELLS: the cells of this graph do not fit co-resident on the device");
+  }
+  int lanes = 32;
+  if (!cells)
+    for (lanes = 1; lanes < S && lanes < 32;) lanes <<= 1;
+  const int SC = cells ? cell_sc : (lanes == 32 ? 64 : lanes);
   const int nchunks = (S + SC - 1) / SC;
   const int32_t Sp = nchunks * SC;
   ScenParams p{};
@@ -340,33 +377,75 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   p.record = sc->record ? 1 : 0;
   p.mod = 2 * sc->amp_q16 + 1;
   p.mod_magic = ~0ULL / (uint64_t)p.mod + 1;
-  const Plan &P = G->plan;
   G->recorded = 0;
   if (p.record) {
     if (!G->ensure(G->fin, G->fin_bytes, (size_t)P.N * Sp * 8)) return fail(PRISM_E_OOM, "fin[N][S] allocation failed");
   }
   if (!G->ensure(G->gfin, G->gfin_bytes, (size_t)P.G * Sp * 8)) return fail(PRISM_E_OOM, "gfin allocation failed");
   if (!G->ensure(G->rank_end, G->rank_end_bytes, (size_t)P.W * Sp * 8)) return fail(PRISM_E_OOM, "rank_end allocation failed");
-  prism_status st = plan_tiles(G, lanes);
-  if (st) return st;
   int64_t launches = 0;
-  G->rec(2);
-  for (int l = 1; l <= P.levels; ++l) {
-    const int32_t t0 = G->lvl_tile_ptr[l], t1 = G->lvl_tile_ptr[l + 1];
-    if (t1 == t0) continue;
-    CU(launch_level(G->dg, p, G->tiles + t0, t1 - t0, G->lvl_max_cnt[l], p.record ? G->fin : nullptr,
-                    G->gfin, lanes, nchunks, G->stream));
+  if (cells) {
+    const size_t rs_bytes = std::max<size_t>(16, (size_t)P.M_cross * Sp * 8);
+    if (G->rslot_bytes < rs_bytes || G->rslot_Sp != Sp) G->rslot_dirty = true;
+    G->rslot_Sp = Sp;
+    if (!G->ensure(G->rslot, G->rslot_bytes, rs_bytes)) return fail(PRISM_E_OOM, "ready-slot allocation failed");
+    if (!G->ensure(G->acc, G->acc_bytes, std::max<size_t>(16, (size_t)P.G_large * Sp * 8)))
+      return fail(PRISM_E_OOM, "accumulator allocation failed");
+    const size_t nwords = (size_t)P.G_large + 4;
+    if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
+    if (!G->h_status) CU(cudaHostAlloc((void **)&G->h_status, 16, cudaHostAllocDefault));
+    if (G->rslot_dirty) {  // all slots read "not yet" under parity 0
+      CU(cudaMemsetAsync(G->rslot, 0xFF, G->rslot_bytes, G->stream));
+      G->parity = 0;
+      G->rslot_dirty = false;
+    }
+    CU(cudaMemsetAsync(G->acc, 0, (size_t)P.G_large * Sp * 8, G->stream));
+    CU(cudaMemsetAsync(G->sync_words, 0, nwords * 4, G->stream));
+    G->rec(2);
+    for (int ch = 0; ch < nchunks; ++ch) {
+      CU(launch_cells(G->dg, p, G->rslot, G->acc, G->sync_words, G->sync_words + P.G_large, G->parity,
+                      p.record ? G->fin : nullptr, G->gfin, G->rank_end, ch, Sp, G->stream));
+      ++launches;
+    }
+    G->parity ^= 1;
+    CU(cudaMemcpyAsync(G->h_status, G->sync_words + P.G_large, 4, cudaMemcpyDeviceToHost, G->stream));
+    G->rec(3);
+    G->rec(4);
+  } else {
+    prism_status st = plan_tiles(G, lanes);
+    if (st) return st;
+    G->rec(2);
+    for (int l = 1; l <= P.levels; ++l) {
+      const int32_t t0 = G->lvl_tile_ptr[l], t1 = G->lvl_tile_ptr[l + 1];
+      if (t1 == t0) continue;
+      CU(launch_level(G->dg, p, G->tiles + t0, t1 - t0, G->lvl_max_cnt[l], p.record ? G->fin : nullptr,
+                      G->gfin, lanes, nchunks, G->stream));
+      ++launches;
+    }
+    G->rec(3);
+    CU(launch_tail(G->dg, p, p.record ? G->fin : nullptr, G->gfin, G->rank_end, lanes, nchunks, G->stream));
+    G->rec(4);
     ++launches;
   }
-  G->rec(3);
-  CU(launch_tail(G->dg, p, p.record ? G->fin : nullptr, G->gfin, G->rank_end, lanes, nchunks, G->stream));
-  G->rec(4);
   CU(launch_reduce(G->dg.W, S, Sp, G->rank_end, iter_dev, G->stream));
   G->rec(5);
-  G->launches = launches + 2;
+  G->launches = launches + 1;
   G->last = p;
   G->last_Sp = Sp;
   G->recorded = p.record;
+  G->last_algo = cells ? PRISM_ALGO_CELLS : PRISM_ALGO_LEVELS;
+  return PRISM_OK;
+}
+
+// Abort status of the last cell-kernel replay (valid once the stream has passed it).
+prism_status check_status(prism_graph_t G) {
+  if (G->last_algo == PRISM_ALGO_CELLS && G->h_status && *G->h_status != 0) {
+    const uint32_t s = *G->h_status;
+    *G->h_status = 0;
+    G->recorded = 0;
+    G->rslot_dirty = true;
+    return fail((prism_status)s, "replay aborted by the device watchdog (no progress for 10 s)");
+  }
   return PRISM_OK;
 }
 
@@ -387,7 +466,7 @@ prism_status prism_replay(prism_graph_t G, const prism_scenarios *sc, int64_t *i
   if (st) return st;
   CU(cudaMemcpyAsync(iter_ns_out, G->iter, (size_t)sc->n * 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaStreamSynchronize(G->stream));
-  return PRISM_OK;
+  return check_status(G);
 }
 
 prism_status prism_peak_memory_async(prism_graph_t G, int64_t *peak_dev) {
@@ -447,7 +526,7 @@ prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, i
   CU(cudaMemcpyAsync(start_ns, G->scratch, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaMemcpyAsync(finish_ns, G->scratch + n, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaStreamSynchronize(G->stream));
-  return PRISM_OK;
+  return check_status(G);
 }
 
 prism_status prism_graph_stats(prism_graph_t G, int64_t out[10]) {
@@ -463,6 +542,12 @@ prism_status prism_graph_stats(prism_graph_t G, int64_t out[10]) {
   out[7] = P.max_group;
   out[8] = G->structure_bytes;
   out[9] = G->launches;
+  return PRISM_OK;
+}
+
+prism_status prism_last_algo(prism_graph_t G, int32_t *algo_out) {
+  if (!G || !algo_out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  *algo_out = G->last_algo;
   return PRISM_OK;
 }
 

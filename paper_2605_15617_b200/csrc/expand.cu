@@ -88,6 +88,11 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
       g.node_free[n] = o.mem_free;
       g.node_prev_sync[n] = tps < 0 ? -1 : rb + tps;
       g.node_gptr[n] = slot0 + g.t_slot_ptr[op0 + i];
+      if (o.kind == PRISM_KIND_COMPUTE) {  // sync nodes are filled in by build_groups_kernel
+        g.node_cls[n] = 0;
+        g.node_sdur[n] = o.dur_ns;
+        g.node_uid[n] = ((uint64_t)r << 32) | (uint32_t)i;
+      }
     }
   }
 }
@@ -153,11 +158,20 @@ __global__ void __launch_bounds__(256) build_groups_kernel(DevGraph g) {
     const int32_t node = g.rank_ptr[rank] + tidx;
     g.grp_mem[m] = node;
     g.node_grp[g.node_gptr[node] + slot] = (int32_t)grp;
+    g.node_mslot[g.node_gptr[node] + slot] = (int32_t)m;
+    const uint64_t uid = ((uint64_t)q.type << 56) | (gid << 24) | (uint64_t)q.occ;
+    if (slot == 0) {  // the node's first group provides its replay record
+      g.node_cls[node] = q.type == PRISM_ROLE_TP ? 1 : 2;
+      g.node_sdur[node] = q.dur;
+      g.node_uid[node] = uid;
+    }
     if (j == 0) {
+      g.grp_xbase[grp] = q.xbase < 0 ? -1 : q.xbase + (int64_t)inst * q.size;
+      g.grp_lidx[grp] = q.lbase < 0 ? -1 : (int32_t)(q.lbase + inst);
       g.grp_ptr[grp] = (int32_t)m;
       g.grp_dur[grp] = q.dur;
       g.grp_level[grp] = q.level;
-      g.grp_uid[grp] = ((uint64_t)q.type << 56) | (gid << 24) | (uint64_t)q.occ;
+      g.grp_uid[grp] = uid;
     }
   }
 }

@@ -33,6 +33,15 @@ struct DevGraph {
   int64_t *grp_dur;         // [G]
   uint64_t *grp_uid;        // [G]
   int32_t *grp_level;       // [G]
+  // replay v2 (cell kernel) support
+  int32_t *node_mslot;      // [M] membership index of each node slot (parallel to node_grp)
+  // per-node replay record (written by the expander): what the chain walk needs, coalesced
+  uint8_t *node_cls;        // [N] 0 compute span, 1 in-cell (TP) collective, 2 cross-cell sync
+  int64_t *node_sdur;       // [N] compute: own duration; single-group sync: the group's duration
+  uint64_t *node_uid;       // [N] perturbation uid: (rank<<32)|tidx, or the (first) group's uid
+  int64_t *grp_xbase;       // [G] first ready slot (small cross-cell group), else -1
+  int32_t *grp_lidx;        // [G] accumulator index (large cross-cell group), else -1
+  int64_t M_cross, G_large;
   // per-stage template tables (tiny; L2 resident)
   const prism_op *t_ops;    // concatenated templates
   int64_t *t_op0;           // [pp] first op of each stage
@@ -75,6 +84,12 @@ cudaError_t launch_reduce(int32_t W, int32_t S, int32_t Sp, const int64_t *rank_
 cudaError_t launch_query(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin,
                          const int64_t *gfin, int32_t rank, int32_t scen, int64_t *start_out,
                          int64_t *finish_out, cudaStream_t st);
+// replay_cells.cu (cell kernel); cudaErrorCooperativeLaunchTooLarge = does not fit, use levels
+bool cells_fit(const DevGraph &g, int nchunks);
+int cells_chunk_scenarios();
+cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc,
+                         uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t *gfin,
+                         int64_t *rank_end, int chunk, int Sp, cudaStream_t st);
 // memory.cu
 cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st);
 

@@ -293,12 +293,25 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
   std::iota(ord.begin(), ord.end(), 0);
   std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return Q[a].level < Q[b].level; });
   P.q.resize(Q.size());
-  int64_t G = 0, M = 0;
+  int64_t G = 0, M = 0, X = 0, LG = 0;
   int32_t levels = 0, maxg = 0;
   for (size_t i = 0; i < ord.size(); ++i) {
     QGroup g = Q[ord[i]];
     g.gbase = G;
     g.mbase = M;
+    // replay v2 cells are TP groups: a TP collective is resolved inside its cell's CTA; every
+    // other group exchanges ready times through global ready slots
+    g.xbase = -1;
+    g.lbase = -1;
+    if (g.type != PRISM_ROLE_TP) {
+      if (g.size <= kSmallGroup) {
+        g.xbase = X;
+        X += (int64_t)g.inst * g.size;
+      } else {
+        g.lbase = LG;
+        LG += g.inst;
+      }
+    }
     G += g.inst;
     M += (int64_t)g.inst * g.size;
     levels = std::max(levels, g.level);
@@ -312,6 +325,8 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
   P.max_group = maxg;
   P.G = G;
   P.M = M;
+  P.M_cross = X;
+  P.G_large = LG;
   int64_t N = 0, sync_nodes = 0;
   for (int s = 0; s < pp; ++s) {
     N += P.stage_len[s] * t.tp * t.dp;

@@ -21,6 +21,10 @@
 
 namespace prism {
 
+// Cross-cell groups with at most this many members use the value-as-flag protocol of the cell
+// kernel (ready slots); larger ones use max-accumulators + arrival counters.
+constexpr int32_t kSmallGroup = 8;
+
 // One quotient group: a template-level synchronization (all concrete instances are symmetric
 // under the topology, so level / duration / member positions are per quotient group).
 struct QGroup {
@@ -41,6 +45,8 @@ struct QGroup {
   int64_t dur;         // shared duration (max over member ops)
   int64_t gbase;       // first concrete group id
   int64_t mbase;       // first membership index
+  int64_t xbase;       // first ready slot (cell kernel, small cross-cell groups); -1 otherwise
+  int64_t lbase;       // first accumulator index (cell kernel, large groups); -1 otherwise
 };
 
 struct Topo {
@@ -51,6 +57,8 @@ struct Topo {
 struct Plan {
   Topo topo;
   int64_t W = 0, N = 0, G = 0, M = 0, sync_nodes = 0;
+  int64_t M_cross = 0;  // memberships of small cross-cell groups (cell-kernel ready slots)
+  int64_t G_large = 0;  // cross-cell groups larger than kSmallGroup (cell-kernel accumulators)
   int32_t levels = 0, max_group = 0;
   // per template op (concatenated over stages, indexed by global op index)
   std::vector<int32_t> t_prev_sync;  // template-local index of the previous sync op, -1

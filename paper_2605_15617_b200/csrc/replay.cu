@@ -200,6 +200,13 @@ __global__ void query_kernel(DevGraph g, ScenParams p, int32_t Sp, const int64_t
     int64_t st;
     if (h0 == h1) {
       st = i == rb ? 0 : fin[(int64_t)(i - 1) * Sp + k];
+    } else if (h1 - h0 == 1) {  // one group: the node spans exactly the group occurrence
+      const int64_t grp = g.node_grp[h0];
+      const uint32_t gbit = (g.grp_uid[grp] >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
+      int64_t d = g.grp_dur[grp];
+      if ((p.mask & gbit) && p.amp > 0 && k > 0)
+        d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
+      st = fin[(int64_t)i * Sp + k] - d;
     } else {  // start = max over groups of (gfin - dur')
       st = 0;
       for (int32_t h = h0; h < h1; ++h) {

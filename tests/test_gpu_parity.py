@@ -91,9 +91,11 @@ def test_csr_random(prism, seed):
 
 
 # ------------------------------------------------------------------ rows a6-a9: replay + memory
-def _check_replay(P, tm, S, amp=6554, mask=7, times=True, seed=0x5EED):
+def _check_replay(P, tm, S, amp=6554, mask=7, times=True, seed=0x5EED, algo="auto"):
     g = _graph(P, tm)
-    it = g.replay(S, seed=seed, amp_q16=amp, kind_mask=mask, record=True)
+    it = g.replay(S, seed=seed, amp_q16=amp, kind_mask=mask, record=True, algo=algo)
+    if algo != "auto":
+        assert g.last_algo() == algo
     ref = oracle.replay(tm, S, seed=seed, amp_q16=amp, kind_mask=mask, times=times,
                         threads=min(NPROC, S))
     assert np.array_equal(it, ref["iter"]), (it[:8], ref["iter"][:8])
@@ -112,11 +114,14 @@ def _check_replay(P, tm, S, amp=6554, mask=7, times=True, seed=0x5EED):
     return it
 
 
+@pytest.mark.parametrize("algo", ["levels", "cells"])
 @pytest.mark.parametrize("seed", range(40))
-def test_replay_random(prism, seed):
+def test_replay_random(prism, seed, algo):
     tm = w.random_templates(seed, max_world=32, max_ops=40)
     S = [1, 2, 3, 5, 17, 33, 64, 70][seed % 8]
-    _check_replay(prism, tm, S)
+    if algo == "cells" and tm.topo.tp > 8:
+        pytest.skip("cells need tp <= 8")
+    _check_replay(prism, tm, S, algo=algo)
 
 
 def test_c1_closed_form_gpu(prism):
@@ -127,17 +132,19 @@ def test_c1_closed_form_gpu(prism):
     assert sorted(set(pk.tolist())) == [1_077_936_128, 1_082_130_432]
 
 
+@pytest.mark.parametrize("algo", ["levels", "cells"])
 @pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
-def test_replay_scaled_configs(prism, name):
-    _check_replay(prism, w.scaled(name), 64, times=True)
+def test_replay_scaled_configs(prism, name, algo):
+    _check_replay(prism, w.scaled(name), 64, times=True, algo=algo)
 
 
-def test_fin_array_all_nodes(prism):
+@pytest.mark.parametrize("algo", ["levels", "cells"])
+def test_fin_array_all_nodes(prism, algo):
     """Every node-scenario finish of the recorded replay equals the oracle (scenario-fastest)."""
     tm = w.scaled("C3")
     g = _graph(prism, tm)
     S = 64
-    g.replay(S, amp_q16=6554, kind_mask=7)
+    g.replay(S, amp_q16=6554, kind_mask=7, algo=algo)
     fin = g.export("fin", scen_pad=64).reshape(-1, 64)
     ref = oracle.replay(tm, S, amp_q16=6554, kind_mask=7, times=True, threads=NPROC)
     assert np.array_equal(fin[:, :S].T, ref["finish"])
@@ -149,7 +156,11 @@ def test_deterministic_and_record_off(prism):
     a = g.replay(64, amp_q16=6554, kind_mask=7)
     b = g.replay(64, amp_q16=6554, kind_mask=7)
     c = g.replay(64, amp_q16=6554, kind_mask=7, record=False)
-    assert np.array_equal(a, b) and np.array_equal(a, c)
+    d = g.replay(64, amp_q16=6554, kind_mask=7, record=False, algo="levels")
+    e = g.replay(130, amp_q16=6554, kind_mask=7, algo="cells")  # 3 scenario chunks
+    assert np.array_equal(a, b) and np.array_equal(a, c) and np.array_equal(a, d)
+    assert np.array_equal(e[:64], a)
+    g.replay(64, amp_q16=6554, kind_mask=7, record=False)
     with pytest.raises(prism.PrismError) as e:
         g.query_rank(0, 0)
     assert e.value.name == "PRISM_E_NOT_REPLAYED"
@@ -172,16 +183,18 @@ def test_edge_cases(prism):
     assert e.value.name == "PRISM_E_UNKNOWN_RANK"
 
 
-def test_world_collectives_large_groups(prism):
+@pytest.mark.parametrize("algo", ["levels", "cells"])
+def test_world_collectives_large_groups(prism, algo):
     """WORLD collectives (one group spanning every rank) and EP/EDP groups."""
     for seed in range(100, 110):
         tm = w.random_templates(seed, max_world=64, max_ops=60)
-        _check_replay(prism, tm, 64, times=False)
+        _check_replay(prism, tm, 64, times=False, algo=algo if tm.topo.tp <= 8 else "auto")
 
 
 @pytest.mark.slow
 @pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
 def test_full_size_sampled(prism, name):
+    """(auto schedule = the cell kernel at these sizes, as bench.py runs it)"""
     """BASELINE.json full sizes in the bench launch configuration (S = 64, +-10% jitter): the
     iteration time of sampled scenarios and every rank's peak equal the oracle's."""
     tm = w.config(name)
