@@ -21,6 +21,33 @@ using namespace prism;
 namespace {
 
 thread_local std::string t_err;
+
+// Pinned host words for the cell kernel's abort status, shared by all graphs (cudaHostAlloc /
+// cudaFreeHost per graph would synchronize the device on every build/destroy).
+std::mutex g_pin_mu;
+uint32_t *g_pin = nullptr;
+std::vector<int> g_pin_free;
+constexpr int kPinWords = 4096;
+uint32_t *pin_take() {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  if (!g_pin) {
+    if (cudaHostAlloc((void **)&g_pin, kPinWords * 4, cudaHostAllocDefault) != cudaSuccess) {
+      g_pin = nullptr;
+      return nullptr;
+    }
+    for (int i = kPinWords - 1; i >= 0; --i) g_pin_free.push_back(i);
+  }
+  if (g_pin_free.empty()) return nullptr;
+  const int i = g_pin_free.back();
+  g_pin_free.pop_back();
+  g_pin[i] = 0;
+  return g_pin + i;
+}
+void pin_give(uint32_t *p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back((int)(p - g_pin));
+}
 std::mutex g_alloc_mu;
 prism_alloc_fn g_alloc = nullptr;
 prism_free_fn g_free = nullptr;
@@ -140,7 +167,7 @@ struct prism_graph_s {
     dfree(rslot);
     dfree(acc);
     dfree(sync_words);
-    if (h_status) cudaFreeHost(h_status);
+    pin_give(h_status);
     for (auto &b : blocks) dfree(b.first);
     cudaStreamSynchronize(stream);
     for (auto &e : ev)
@@ -393,7 +420,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
       return fail(PRISM_E_OOM, "accumulator allocation failed");
     const size_t nwords = (size_t)P.G_large + 4;
     if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
-    if (!G->h_status) CU(cudaHostAlloc((void **)&G->h_status, 16, cudaHostAllocDefault));
+    if (!G->h_status && !(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status word unavailable");
     if (G->rslot_dirty) {  // all slots read "not yet" under parity 0
       CU(cudaMemsetAsync(G->rslot, 0xFF, G->rslot_bytes, G->stream));
       G->parity = 0;

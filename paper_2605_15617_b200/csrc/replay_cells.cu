@@ -162,8 +162,9 @@ __device__ __forceinline__ bool cross_sync(const DevGraph &g, const ScenParams &
         for (int q = 0; q < SPL; ++q) m[q] = max(m[q], a.parity ? ~v[q] : v[q]);
       }
     } else {
+      // chunks run as successive launches and every chunk adds `size` arrivals
       const uint32_t *cnt = a.arrive + g.grp_lidx[gg];
-      while (ld_relaxed(cnt) < (uint32_t)size) {
+      while (ld_relaxed(cnt) < (uint32_t)size * (uint32_t)(k0 / SC + 1)) {
         if (wait_tick(a, spins, tw)) return false;
       }
       fence_acq_rel();
