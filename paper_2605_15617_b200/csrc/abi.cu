@@ -290,6 +290,10 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.node_uid = G->take<uint64_t>(N);
   d.grp_xbase = G->take<int64_t>(Gn);
   d.grp_lidx = G->take<int32_t>(Gn);
+  d.h_base = G->take<int32_t>(M);
+  d.h_meta = G->take<uint32_t>(M);
+  d.h_dur = G->take<int64_t>(M);
+  d.h_uid = G->take<uint64_t>(M);
   d.M_cross = P.M_cross;
   d.G_large = P.G_large;
   prism_op *t_ops = G->take<prism_op>(nops);
@@ -418,7 +422,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     if (!G->ensure(G->rslot, G->rslot_bytes, rs_bytes)) return fail(PRISM_E_OOM, "ready-slot allocation failed");
     if (!G->ensure(G->acc, G->acc_bytes, std::max<size_t>(16, (size_t)P.G_large * Sp * 8)))
       return fail(PRISM_E_OOM, "accumulator allocation failed");
-    const size_t nwords = (size_t)P.G_large + 4;
+    const size_t nwords = (size_t)P.G_large * nchunks + 4;
     if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
     if (!G->h_status && !(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status word unavailable");
     if (G->rslot_dirty) {  // all slots read "not yet" under parity 0
@@ -429,13 +433,16 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     CU(cudaMemsetAsync(G->acc, 0, (size_t)P.G_large * Sp * 8, G->stream));
     CU(cudaMemsetAsync(G->sync_words, 0, nwords * 4, G->stream));
     G->rec(2);
-    for (int ch = 0; ch < nchunks; ++ch) {
-      CU(launch_cells(G->dg, p, G->rslot, G->acc, G->sync_words, G->sync_words + P.G_large, G->parity,
-                      p.record ? G->fin : nullptr, G->gfin, G->rank_end, ch, Sp, G->stream));
+    uint32_t *status = G->sync_words + (size_t)P.G_large * nchunks;
+    const int per_launch = cells_chunks_per_launch(G->dg, nchunks);
+    for (int ch = 0; ch < nchunks; ch += per_launch) {
+      CU(launch_cells(G->dg, p, G->rslot, G->acc, G->sync_words, status, G->parity,
+                      p.record ? G->fin : nullptr, G->gfin, G->rank_end, ch, std::min(per_launch, nchunks - ch),
+                      Sp, G->stream));
       ++launches;
     }
     G->parity ^= 1;
-    CU(cudaMemcpyAsync(G->h_status, G->sync_words + P.G_large, 4, cudaMemcpyDeviceToHost, G->stream));
+    CU(cudaMemcpyAsync(G->h_status, status, 4, cudaMemcpyDeviceToHost, G->stream));
     G->rec(3);
     G->rec(4);
   } else {

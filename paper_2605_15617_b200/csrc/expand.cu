@@ -160,6 +160,14 @@ __global__ void __launch_bounds__(256) build_groups_kernel(DevGraph g) {
     g.node_grp[g.node_gptr[node] + slot] = (int32_t)grp;
     g.node_mslot[g.node_gptr[node] + slot] = (int32_t)m;
     const uint64_t uid = ((uint64_t)q.type << 56) | (gid << 24) | (uint64_t)q.occ;
+    {
+      const int32_t h = g.node_gptr[node] + slot;
+      const bool large = q.xbase < 0 && q.lbase >= 0;
+      g.h_base[h] = large ? (int32_t)(q.lbase + inst) : (q.xbase < 0 ? -1 : (int32_t)(q.xbase + (int64_t)inst * q.size));
+      g.h_meta[h] = (uint32_t)min(q.size, 0xFFFF) | ((uint32_t)min(j, 0x7FFF) << 16) | (large ? 0x80000000u : 0u);
+      g.h_dur[h] = q.dur;
+      g.h_uid[h] = uid;
+    }
     if (slot == 0) {  // the node's first group provides its replay record
       g.node_cls[node] = q.type == PRISM_ROLE_TP ? 1 : 2;
       g.node_sdur[node] = q.dur;

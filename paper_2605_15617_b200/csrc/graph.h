@@ -41,6 +41,11 @@ struct DevGraph {
   uint64_t *node_uid;       // [N] perturbation uid: (rank<<32)|tidx, or the (first) group's uid
   int64_t *grp_xbase;       // [G] first ready slot (small cross-cell group), else -1
   int32_t *grp_lidx;        // [G] accumulator index (large cross-cell group), else -1
+  // per membership slot h (parallel to node_grp): flat sync record for the cell kernel
+  int32_t *h_base;          // small group: first ready slot of the group; large: accumulator index
+  uint32_t *h_meta;         // size (bits 0-15) | own member offset (16-30) | large (bit 31)
+  int64_t *h_dur;           // the group's duration
+  uint64_t *h_uid;          // the group's perturbation uid
   int64_t M_cross, G_large;
   // per-stage template tables (tiny; L2 resident)
   const prism_op *t_ops;    // concatenated templates
@@ -87,9 +92,10 @@ cudaError_t launch_query(const DevGraph &g, const ScenParams &p, int32_t Sp, con
 // replay_cells.cu (cell kernel); cudaErrorCooperativeLaunchTooLarge = does not fit, use levels
 bool cells_fit(const DevGraph &g, int nchunks);
 int cells_chunk_scenarios();
+int cells_chunks_per_launch(const DevGraph &g, int nchunks);
 cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc,
                          uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t *gfin,
-                         int64_t *rank_end, int chunk, int Sp, cudaStream_t st);
+                         int64_t *rank_end, int chunk0, int nchunks_launch, int Sp, cudaStream_t st);
 // memory.cu
 cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st);
 

@@ -1,28 +1,29 @@
-// replay_cells.cu — replay v2: one persistent cooperative launch for the whole replay (rows a6-a8).
+// replay_cells.cu — the cell kernel: one persistent cooperative launch replays every rank (rows
+// a6-a8).
 //
 // Same semantics as replay.cu (readings Z2-Z5), different
 // schedule. A *cell* is one TP group: the tp ranks of a (stage, dp) pair. They run the same stage
-// template, so they walk it in lockstep, and every TP collective's members are exactly
-// the cell. One CTA owns one (cell, 64-scenario chunk): ceil(tp/2) warps, each warp = two of
-// the cell's ranks (half-warps), each lane = 4 scenarios of its rank (warp-cooperative per-rank op
-// chains, 4 independent hash chains per lane). Per op:
-//   compute span      : t += dur'                               (registers only)
-//   TP collective     : segmented max over the cell's ranks through shared memory (one
-//                       __syncthreads, double-buffered slots), t = max + dur'_g
-//   small cross-cell  : (P2P message, EP/EDP group of <= 8) every member stores its ready times
-//   group               into its global ready slot (reset to -1 before the launch) and polls the
-//                       other members' slots until they are valid: an aligned 8-byte store is
-//                       single-copy atomic, so the value is its own flag and no fence is needed
-//   large cross-cell  : (DP, WORLD, big EP) red.max of the ready times into the group's
-//   group               accumulator, fence, arrive on its counter; members poll the counter and
-//                       read the accumulator (segmented max done by the L2 atomics)
-// and a node finishes at the max over its groups' (start + dur'_g) (reading Z3).
-// Scheduling: every CTA of a 64-scenario chunk is co-resident (cudaLaunchCooperativeKernel refuses
+// template, so they walk it in lockstep, and every TP collective's members are exactly the
+// cell. One warp owns one (cell, 32-scenario chunk): lane = scenario, and the lane keeps the chain
+// state t[r] of all tp ranks of the cell in registers. Per template op:
+//   compute span      : t[r] += dur'(rank r)            tp independent hash chains per lane (ILP)
+//   TP collective     : t[r] = max_r t[r] + dur'_g      the segmented max is register-local
+//   small cross-cell  : (P2P message, EP/EDP groups of <= 8) every member stores its ready time into
+//   group               its global ready slot and polls the other members' slots until they are
+//                       valid: an aligned 8-byte store is single-copy atomic, so the value is its own
+//                       flag (parity-encoded per replay, see CellArgs) and no fence is needed
+//   large cross-cell  : (DP, WORLD, big EP) red.max of the ready times into the group's accumulator,
+//   group               fence, arrive on its counter; members poll the counter, then read the
+//                       accumulator (the segmented max is done by the L2 atomics)
+// and a node finishes at the max over its groups' (start + dur'_g) (reading Z3). fin stores are
+// 256-byte coalesced rows (32 scenarios of one node).
+//
+// Scheduling: every warp of the launch is co-resident (cudaLaunchCooperativeKernel refuses
 // otherwise and the caller falls back to the level-by-level path), so a waiting warp cannot starve
-// the producer it waits for; chunks run as successive launches. The build already proved the sync
-// structure acyclic (plan.cpp) and the lockstep walk is deadlock-free because a cell's ranks are
-// symmetric; a %globaltimer watchdog still turns any unexpected stall into
-// PRISM_E_DEADLOCK instead of a hung GPU.
+// the producer it waits for. The build already proved the sync structure acyclic (plan.cpp) and the
+// lockstep walk is deadlock-free because a cell's ranks are symmetric; a
+// %globaltimer watchdog still turns any unexpected stall into PRISM_E_DEADLOCK instead of a hung
+// GPU.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,23 +34,23 @@ namespace prism {
 
 namespace {
 
-#ifndef PRISM_CELL_MINB
-#define PRISM_CELL_MINB 7
-#endif
 constexpr uint64_t K_GOLD = 0x9E3779B97F4A7C15ULL;
 constexpr uint64_t K_MIX = 0xBF58476D1CE4E5B9ULL;
-constexpr int SPL = 4;        // scenarios per lane
-constexpr int SC = 16 * SPL;  // scenarios per unit (a half-warp covers one rank)
-constexpr int MAX_TP = 8;     // CTA = ceil(tp/2) warps <= 128 threads
-constexpr int SMALL = kSmallGroup;  // groups up to this size use the value-as-flag protocol
+constexpr int SC = 32;          // scenarios per unit (one warp, lane = scenario)
+constexpr int WARPS = 1;        // units per CTA (1: warps spread evenly over the SMs)
+constexpr int MAX_TP = 8;       // tp of the instantiated cell kernels
+constexpr int SMALL = kSmallGroup;
 
 __device__ __forceinline__ int64_t perturb_x(int64_t d, uint64_t x, const ScenParams &p) {
-  const uint64_t h = splitmix64(x);
-  const uint32_t v = (uint32_t)(h >> 40);
+  // splitmix64(x) >> 40 (reading Z8): the finaliser's last step z ^ (z >> 31) leaves bits 40..63
+  // unchanged (z >> 31 >> 40 == 0), so it is skipped
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  const uint32_t v = (uint32_t)(z >> 40);
   const uint64_t low = p.mod_magic * (uint64_t)v;
   const uint32_t r = (uint32_t)__umul64hi(low, (uint64_t)(uint32_t)p.mod);
-  const int64_t delta = (int64_t)r - p.amp;
-  return (d * (65536 + delta)) >> 16;
+  return (d * (int64_t)(r + (uint32_t)(65536 - p.amp))) >> 16;
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -62,18 +63,30 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void ld_relaxed4(const int64_t *p, int64_t *v) {
-  asm volatile("ld.relaxed.gpu.global.v2.s64 {%0, %1}, [%2];" : "=l"(v[0]), "=l"(v[1]) : "l"(p) : "memory");
-  asm volatile("ld.relaxed.gpu.global.v2.s64 {%0, %1}, [%2];" : "=l"(v[2]), "=l"(v[3]) : "l"(p + 2) : "memory");
+__device__ __forceinline__ int64_t ld_relaxed64(const int64_t *p) {
+  int64_t v;
+  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// Deposit of a ready time: a strong (relaxed, gpu-scope) store goes to L2 right away; a weak store
+// may linger in the SM for tens of microseconds (measured), which the pipeline pays per handoff.
+__device__ __forceinline__ void st_relaxed64(int64_t *p, int64_t v) {
+  asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-__device__ __forceinline__ void st4(int64_t *p, const int64_t *t) {
-  *reinterpret_cast<longlong2 *>(p) = make_longlong2(t[0], t[1]);
-  *reinterpret_cast<longlong2 *>(p + 2) = make_longlong2(t[2], t[3]);
-}
 __device__ __forceinline__ void red_max(int64_t *p, int64_t v) {
   asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"((uint64_t)v) : "memory");
 }
+
+#ifdef PRISM_CELL_STATS
+__device__ unsigned long long g_dep_time[1 << 22];     // deposit globaltimer per ready slot (chunk 0)
+__device__ unsigned long long g_lat[4];                // sum latency, sum skew, count, max latency
+__device__ unsigned long long g_wait_hist[16 * 4096];  // [stage][template op] wait cycles (stage < 16)
+__device__ unsigned long long g_cell_stats[16384 * 8];  // per warp: total, cross, -, polls, start, end
+#define STAT_ADD(i, v) g_cell_stats[(size_t)(blockIdx.x * WARPS + (threadIdx.x >> 5)) * 8 + (i)] += (v)
+#else
+#define STAT_ADD(i, v)
+#endif
 
 struct CellArgs {
   int64_t *rslot;      // [M_cross][Sp] ready slots of small-group memberships
@@ -84,6 +97,10 @@ struct CellArgs {
   int32_t parity;      // ready-slot encoding of this replay: 0 -> t (valid >= 0), 1 -> ~t (valid < 0);
                        // every slot is written once per replay, so the previous replay's values
                        // read as "not yet" and no reset pass is needed
+  int32_t n_units;     // cells x chunks of this launch
+  int32_t Sp;          // scenario stride (all chunks x 32)
+  int32_t chunk0;      // first chunk of this launch
+  int32_t nchunks;     // chunks of the whole replay (arrival counters are per chunk)
 };
 
 __device__ __forceinline__ int32_t rank_of(const DevGraph &g, int32_t tp_i, int32_t pp_i, int32_t dp_i) {
@@ -94,8 +111,9 @@ __device__ __forceinline__ int32_t rank_of(const DevGraph &g, int32_t tp_i, int3
 // Backoff + watchdog for a waiting lane; returns true when the replay was aborted.
 __device__ __forceinline__ bool wait_tick(const CellArgs &a, uint32_t &spins, uint64_t &t0) {
   ++spins;
-  __nanosleep(spins < 8 ? 20u * spins : 200u);
-  if ((spins & 255) == 0) {
+  if ((threadIdx.x & 31) == 0) STAT_ADD(3, 1);
+  __nanosleep(spins < 12 ? 32u : 256u);  // short: handoff latency is amplified by the pipeline
+  if ((spins & 63) == 0) {
     if (ld_relaxed(a.status) != 0) return true;
     if (t0 == 0) t0 = globaltimer();
     if (globaltimer() - t0 > a.timeout_ns) {
@@ -106,212 +124,333 @@ __device__ __forceinline__ bool wait_tick(const CellArgs &a, uint32_t &spins, ui
   return false;
 }
 
-// Cross-cell synchronization of node n for this lane's 4 scenarios (t = ready on entry, finish on
-// exit). Returns false when the watchdog aborted the replay.
-__device__ __forceinline__ bool cross_sync(const DevGraph &g, const ScenParams &p, const CellArgs &a,
-                                           int64_t *__restrict__ gfin, int32_t n, int32_t k0, int32_t Sp,
-                                           bool active, bool lead, int64_t *t) {
-  const int32_t h0 = g.node_gptr[n], h1 = g.node_gptr[n + 1];
-  // 1. arrive on every group of the node
+// Cross-cell node at template index i for all C ranks of the cell (rare: a few % of ops; kept
+// rolled and out of the unrolled per-rank register code so the kernel fits the instruction cache).
+// ts[r * 32 + lane] holds rank r's ready time on entry and its finish on exit (shared memory);
+// hs0 = membership slot of rank 0's node, rs0 = rank 0's first slot, rsh[r] = rank r's first slot;
+// ns = slots of the op. Deposit / arrive for every rank first, then wait (a group may contain
+// several ranks of the cell, e.g. WORLD).
+__device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p, const CellArgs &a,
+                                       int64_t *__restrict__ gfin, int64_t *ts, const int32_t *rsh, int C,
+                                       int32_t hoff, int32_t ns, int32_t k) {
+  const int lane = threadIdx.x & 31;
+  const int32_t Sp = a.Sp;
+  const int32_t ck = k / SC;
   bool large_any = false;
-  for (int32_t h = h0; h < h1; ++h) {
-    const int32_t gg = g.node_grp[h];
-    const int32_t mb = g.grp_ptr[gg], size = g.grp_ptr[gg + 1] - mb;
-    if (size <= SMALL) {
-      if (active) {
-        int64_t v[SPL];
-#pragma unroll
-        for (int q = 0; q < SPL; ++q) v[q] = a.parity ? ~t[q] : t[q];
-        st4(a.rslot + (g.grp_xbase[gg] + (g.node_mslot[h] - mb)) * Sp + k0, v);
+  for (int r = 0; r < C; ++r) {
+    const int64_t tr = ts[r * 32 + lane];
+    for (int32_t q = 0; q < ns; ++q) {
+      const int32_t h = rsh[r] + hoff + q;
+      const uint32_t meta = g.h_meta[h];
+      const int32_t base = g.h_base[h];
+      if (!(meta & 0x80000000u)) {
+#ifdef PRISM_CELL_STATS
+        if (k == 0 && base + (int32_t)((meta >> 16) & 0x7FFF) < (1 << 22)) {
+          g_dep_time[base + (int32_t)((meta >> 16) & 0x7FFF)] = globaltimer();
+          __threadfence();
+        }
+#endif
+        st_relaxed64(a.rslot + (int64_t)(base + (int32_t)((meta >> 16) & 0x7FFF)) * Sp + k, a.parity ? ~tr : tr);
+      } else {
+        large_any = true;
+        red_max(a.acc + (int64_t)base * Sp + k, tr);
       }
-    } else {
-      large_any = true;
-      if (active)
-        for (int q = 0; q < SPL; ++q) red_max(a.acc + (int64_t)g.grp_lidx[gg] * Sp + k0 + q, t[q]);
     }
   }
   if (large_any) {
     __threadfence();  // the accumulations are performed before the arrival is counted
     __syncwarp();
-    if (lead)
-      for (int32_t h = h0; h < h1; ++h) {
-        const int32_t gg = g.node_grp[h];
-        if (g.grp_ptr[gg + 1] - g.grp_ptr[gg] > SMALL) atomicAdd(a.arrive + g.grp_lidx[gg], 1u);
-      }
+    if (lane == 0)
+      for (int r = 0; r < C; ++r)
+        for (int32_t q = 0; q < ns; ++q) {
+          const int32_t h = rsh[r] + hoff + q;
+          if (g.h_meta[h] & 0x80000000u) atomicAdd(a.arrive + (int64_t)g.h_base[h] * a.nchunks + ck, 1u);
+        }
   }
-  // 2. wait for every group, finish = max over groups of (max ready + dur')
-  int64_t f[SPL] = {0, 0, 0, 0};
-  const uint64_t sx = p.seed;
+  // Wait: each pass issues every poll of every rank / group / member as an independent load (one
+  // L2 round trip per pass); the own slot is not read back. Then fold per rank.
   uint32_t spins = 0;
   uint64_t tw = 0;
-  for (int32_t h = h0; h < h1; ++h) {
-    const int32_t gg = g.node_grp[h];
-    const int32_t mb = g.grp_ptr[gg], size = g.grp_ptr[gg + 1] - mb;
-    int64_t m[SPL] = {0, 0, 0, 0};
-    if (size <= SMALL) {
-      const int64_t xb = g.grp_xbase[gg];
-      for (int32_t mm = 0; mm < size; ++mm) {
-        int64_t v[SPL];
-        const int64_t *src = a.rslot + (xb + mm) * Sp + k0;
-        while (true) {
-          ld_relaxed4(src, v);
-          const int64_t all = a.parity ? (v[0] & v[1] & v[2] & v[3]) : (v[0] | v[1] | v[2] | v[3]);
-          if ((a.parity ? all < 0 : all >= 0) || !active) break;
-          if (wait_tick(a, spins, tw)) return false;
+  while (true) {
+    bool ok = true;
+    for (int r = 0; r < C; ++r)
+      for (int32_t q = 0; q < ns; ++q) {
+        const int32_t h = rsh[r] + hoff + q;
+        const uint32_t meta = g.h_meta[h];
+        const int32_t base = g.h_base[h];
+        const int32_t size = (int32_t)(meta & 0xFFFF);
+        if (!(meta & 0x80000000u)) {
+          const int32_t own = (int32_t)((meta >> 16) & 0x7FFF);
+          const int64_t *src = a.rslot + (int64_t)base * Sp + k;
+          for (int32_t mm = 0; mm < size; ++mm, src += Sp) {
+            if (mm == own) continue;
+            const int64_t v = ld_relaxed64(src);
+            ok &= a.parity ? v < 0 : v >= 0;
+          }
+        } else {
+          ok &= ld_relaxed(a.arrive + (int64_t)base * a.nchunks + ck) >= (uint32_t)size;
         }
-        for (int q = 0; q < SPL; ++q) m[q] = max(m[q], a.parity ? ~v[q] : v[q]);
       }
-    } else {
-      // chunks run as successive launches and every chunk adds `size` arrivals
-      const uint32_t *cnt = a.arrive + g.grp_lidx[gg];
-      while (ld_relaxed(cnt) < (uint32_t)size * (uint32_t)(k0 / SC + 1)) {
-        if (wait_tick(a, spins, tw)) return false;
-      }
-      fence_acq_rel();
-      const int64_t *src = a.acc + (int64_t)g.grp_lidx[gg] * Sp + k0;
-      for (int q = 0; q < SPL; ++q) m[q] = __ldcg(src + q);
-    }
-    const int64_t gd = g.grp_dur[gg];
-    const uint64_t uid = g.grp_uid[gg];
-    const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
-    const bool gp = (p.mask & gb) && p.amp > 0;
-    const uint64_t gx = uid * K_MIX;
-    int64_t e[SPL];
-#pragma unroll
-    for (int q = 0; q < SPL; ++q) {
-      const int32_t k = k0 + q;
-      e[q] = (gp && k > 0) ? perturb_x(gd, sx ^ ((uint64_t)k * K_GOLD) ^ gx, p) : gd;
-      m[q] += e[q];
-      f[q] = max(f[q], m[q]);
-    }
-    // the group's finish is kept for queries of multi-group (P2P batch) nodes; every member
-    // computes the same value, so a node with several groups stores its own groups' finishes
-    if (active && h1 - h0 > 1) st4(gfin + (int64_t)gg * Sp + k0, m);
+    if (__all_sync(0xffffffffu, ok)) break;
+    ++spins;
+    if (spins > 6 && wait_tick(a, spins, tw)) return false;
   }
-#pragma unroll
-  for (int q = 0; q < SPL; ++q) t[q] = f[q];
+  if (large_any) fence_acq_rel();
+  for (int r = 0; r < C; ++r) {
+    const int64_t tr = ts[r * 32 + lane];
+    int64_t fr = 0;
+    for (int32_t q = 0; q < ns; ++q) {
+      const int32_t h = rsh[r] + hoff + q;
+      const uint32_t meta = g.h_meta[h];
+      int64_t m = tr;
+      if (!(meta & 0x80000000u)) {
+        const int32_t own = (int32_t)((meta >> 16) & 0x7FFF);
+        const int64_t *src = a.rslot + (int64_t)g.h_base[h] * Sp + k;
+        for (int32_t mm = 0; mm < (int32_t)(meta & 0xFFFF); ++mm, src += Sp) {
+          if (mm == own) continue;
+          const int64_t v = ld_relaxed64(src);
+          m = max(m, a.parity ? ~v : v);
+        }
+      } else {
+        m = __ldcg(a.acc + (int64_t)g.h_base[h] * Sp + k);
+      }
+      const int64_t gd = g.h_dur[h];
+      const uint64_t uid = g.h_uid[h];
+      const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
+      if ((p.mask & gb) && p.amp > 0 && k > 0) m += perturb_x(gd, p.seed ^ ((uint64_t)k * K_GOLD) ^ (uid * K_MIX), p);
+      else m += gd;
+      fr = max(fr, m);
+      if (ns > 1) gfin[(int64_t)g.node_grp[h] * Sp + k] = m;  // P2P-batch group finishes, for queries
+    }
+    ts[r * 32 + lane] = fr;
+  }
   return true;
 }
 
-__global__ void __launch_bounds__(128, PRISM_CELL_MINB) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
-                                                                   int32_t chunk, int32_t Sp,
-                                                                   int64_t *__restrict__ fin,
-                                                                   int64_t *__restrict__ gfin,
-                                                                   int64_t *__restrict__ rank_end) {
-  __shared__ __align__(16) int64_t slot[2][MAX_TP][16][SPL];
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int half = lane >> 4, l16 = lane & 15;
-  const int32_t tpi = 2 * w + half;
-  const bool active = tpi < g.tp;
-  const int32_t cell = blockIdx.x;
+template <int C>
+__global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
+                                                         int64_t *__restrict__ fin,
+                                                         int64_t *__restrict__ gfin,
+                                                         int64_t *__restrict__ rank_end) {
+  const int lane = threadIdx.x & 31;
+  const int32_t unit = blockIdx.x * WARPS + (threadIdx.x >> 5);
+  if (unit >= a.n_units) return;
+  const int32_t cells = g.pp * g.dp;
+  const int32_t cell = unit % cells, chunk = a.chunk0 + unit / cells;
   const int32_t s = cell % g.pp, dpi = cell / g.pp;
-  const int32_t r = rank_of(g, active ? tpi : 0, s, dpi);
-  const int32_t rb = g.rank_ptr[r];
-  const int32_t len = g.rank_ptr[r + 1] - rb;
-  const int32_t k0 = chunk * SC + l16 * SPL;
-  const bool lead = l16 == 0 && active;
-  const bool cpert = (p.mask & 1u) && p.amp > 0;
-  const bool gpert = (p.mask & 2u) && p.amp > 0;
-  uint64_t sx[SPL];
-  bool pj[SPL];
+  const int32_t Sp = a.Sp;
+  const int32_t k = chunk * SC + lane;
+  __shared__ int64_t ts[MAX_TP * 32];  // chain state of the cross-cell path (rolled over ranks)
+  __shared__ int32_t rsh[MAX_TP];       // first membership slot of each rank
+  int32_t rb[C];
+  int32_t rs[C];   // first membership slot of each rank (node_gptr of its first node)
+  uint64_t rk[C];  // (rank << 32) * K_MIX: a compute span's uid mix is rk + tidx * K_MIX
 #pragma unroll
-  for (int q = 0; q < SPL; ++q) {
-    sx[q] = p.seed ^ ((uint64_t)(k0 + q) * K_GOLD);
-    pj[q] = k0 + q > 0;
+  for (int r = 0; r < C; ++r) {
+    const int32_t rr = rank_of(g, r, s, dpi);
+    rb[r] = g.rank_ptr[rr];
+    rs[r] = g.node_gptr[rb[r]];
+    rk[r] = ((uint64_t)rr << 32) * K_MIX;
+    if (lane == 0) rsh[r] = rs[r];
   }
-  int64_t t[SPL] = {0, 0, 0, 0};
-  int buf = 0;
-  for (int32_t base = 0; base < len; base += 16) {
-    // one coalesced round trip for the next 16 ops of each of the warp's two ranks
-    const int32_t cnt = min(16, len - base);
-    uint32_t cls = 2;
-    int64_t dl = 0;
-    uint64_t uxl = 0;
-    if (l16 < cnt) {
-      const int32_t n = rb + base + l16;
-      cls = g.node_cls[n];
-      dl = g.node_sdur[n];
-      uxl = g.node_uid[n] * K_MIX;
+  __syncwarp();
+  const int32_t len = g.rank_ptr[rank_of(g, 0, s, dpi) + 1] - rb[0];
+  const uint64_t sx = p.seed ^ ((uint64_t)k * K_GOLD);
+  const bool cpert = (p.mask & 1u) && p.amp > 0 && k > 0;
+  const bool gpert = (p.mask & 2u) && p.amp > 0 && k > 0;
+  int64_t t[C];
+#pragma unroll
+  for (int r = 0; r < C; ++r) t[r] = 0;
+#ifdef PRISM_CELL_STATS
+  const long long k_start = clock64();
+  if (lane == 0) STAT_ADD(4, globaltimer());
+#endif
+  // op records of the cell's first rank (the template is shared; the per-rank part of a compute
+  // span's uid is rk[r]), 32 ops per coalesced round trip, next batch in flight
+  uint32_t ncls = 2;
+  int64_t nd = 0;
+  uint64_t nux = 0;
+  if (lane < len) {
+    ncls = g.node_cls[rb[0] + lane];
+    nd = g.node_sdur[rb[0] + lane];
+    nux = g.node_uid[rb[0] + lane];
+  }
+  for (int32_t base = 0; base < len; base += 32) {
+    const int32_t cnt = min(32, len - base);
+    const uint32_t bcls = ncls;
+    const int64_t bd = nd;
+    const uint64_t bux = nux;
+    if (base + 32 + lane < len) {
+      const int32_t n = rb[0] + base + 32 + lane;
+      ncls = g.node_cls[n];
+      nd = g.node_sdur[n];
+      nux = g.node_uid[n];
     }
     for (int32_t j = 0; j < cnt; ++j) {
-      const int src = (half << 4) | j;
-      const uint32_t c = __shfl_sync(0xffffffffu, cls, src);
-      const int64_t d = __shfl_sync(0xffffffffu, dl, src);
-      const uint64_t ux = __shfl_sync(0xffffffffu, uxl, src);
-      const int32_t n = rb + base + j;
-      if (c == 0) {  // compute span: wait out the (perturbed) duration
+      const uint32_t c = __shfl_sync(0xffffffffu, bcls, j);
+      const int64_t d = __shfl_sync(0xffffffffu, bd, j);
+      const int32_t i = base + j;
+      if (c == 0) {  // compute span: every rank waits out its own perturbed duration
         if (cpert) {
+          const uint64_t ix = (uint64_t)i * K_MIX;
 #pragma unroll
-          for (int q = 0; q < SPL; ++q) t[q] += pj[q] ? perturb_x(d, sx[q] ^ ux, p) : d;
+          for (int r = 0; r < C; ++r) t[r] += perturb_x(d, sx ^ (rk[r] + ix), p);
         } else {
 #pragma unroll
-          for (int q = 0; q < SPL; ++q) t[q] += d;
+          for (int r = 0; r < C; ++r) t[r] += d;
         }
-      } else if (c == 1) {  // in-cell TP collective: segmented max over the cell's ranks
-        int64_t e[SPL];
+      } else if (c == 1) {  // in-cell TP collective: register-local segmented max
+        const uint64_t ux = __shfl_sync(0xffffffffu, bux, j);
+        int64_t m = t[0];
 #pragma unroll
-        for (int q = 0; q < SPL; ++q) e[q] = (gpert && pj[q]) ? perturb_x(d, sx[q] ^ ux, p) : d;
-        if (active) {
-          *reinterpret_cast<longlong2 *>(&slot[buf][tpi][l16][0]) = make_longlong2(t[0], t[1]);
-          *reinterpret_cast<longlong2 *>(&slot[buf][tpi][l16][2]) = make_longlong2(t[2], t[3]);
-        }
-        __syncthreads();
-        int64_t m[SPL] = {0, 0, 0, 0};
-        for (int qq = 0; qq < g.tp; ++qq) {
-          const longlong2 v0 = *reinterpret_cast<const longlong2 *>(&slot[buf][qq][l16][0]);
-          const longlong2 v1 = *reinterpret_cast<const longlong2 *>(&slot[buf][qq][l16][2]);
-          m[0] = max(m[0], (int64_t)v0.x);
-          m[1] = max(m[1], (int64_t)v0.y);
-          m[2] = max(m[2], (int64_t)v1.x);
-          m[3] = max(m[3], (int64_t)v1.y);
-        }
-        buf ^= 1;
+        for (int r = 1; r < C; ++r) m = max(m, t[r]);
+        m += gpert ? perturb_x(d, sx ^ (ux * K_MIX), p) : d;
 #pragma unroll
-        for (int q = 0; q < SPL; ++q) t[q] = m[q] + e[q];
-      } else {  // cross-cell synchronization
-        if (!cross_sync(g, p, a, gfin, n, k0, Sp, active, lead, t)) return;
+        for (int r = 0; r < C; ++r) t[r] = m;
+      } else {  // cross-cell synchronization, rank by rank (deposit all first: no self-wait)
+#ifdef PRISM_CELL_STATS
+        const long long c0 = clock64();
+#endif
+        // rank r's slots of this op: rs[r] + (template slot offset), identical templates
+        const int32_t h0 = g.node_gptr[rb[0] + i];
+        const int32_t ns = g.node_gptr[rb[0] + i + 1] - h0;
+#pragma unroll
+        for (int r = 0; r < C; ++r) ts[r * 32 + lane] = t[r];
+        __syncwarp();
+        const bool ok = cross_all(g, p, a, gfin, ts, rsh, C, h0 - rs[0], ns, k);
+        __syncwarp();
+        if (!ok) return;
+#pragma unroll
+        for (int r = 0; r < C; ++r) t[r] = ts[r * 32 + lane];
+#ifdef PRISM_CELL_STATS
+        if (lane == 0) {
+          const long long dc = clock64() - c0;
+          STAT_ADD(1, dc);
+          if (s < 16 && i < 4096) atomicAdd(&g_wait_hist[s * 4096 + i], (unsigned long long)dc);
+        }
+#endif
       }
-      if (p.record && active) st4(fin + (int64_t)n * Sp + k0, t);
+      if (p.record) {
+#pragma unroll
+        for (int r = 0; r < C; ++r) fin[(int64_t)(rb[r] + i) * Sp + k] = t[r];
+      }
     }
   }
-  if (active) st4(rank_end + (int64_t)r * Sp + k0, t);
+#pragma unroll
+  for (int r = 0; r < C; ++r) rank_end[(int64_t)rank_of(g, r, s, dpi) * Sp + k] = t[r];
+#ifdef PRISM_CELL_STATS
+  if (lane == 0) {
+    STAT_ADD(0, clock64() - k_start);
+    STAT_ADD(5, globaltimer());
+  }
+#endif
 }
 
-bool cell_fit(const DevGraph &g) {
-  if (g.tp > MAX_TP) return false;
-  const int threads = ((g.tp + 1) / 2) * 32;
+typedef void (*cell_fn)(DevGraph, ScenParams, CellArgs, int64_t *, int64_t *, int64_t *);
+
+cell_fn cell_kernel_for(int tp) {
+  switch (tp) {
+    case 1: return cell_kernel<1>;
+    case 2: return cell_kernel<2>;
+    case 3: return cell_kernel<3>;
+    case 4: return cell_kernel<4>;
+    case 5: return cell_kernel<5>;
+    case 6: return cell_kernel<6>;
+    case 7: return cell_kernel<7>;
+    case 8: return cell_kernel<8>;
+    default: return nullptr;
+  }
+}
+
+// CTAs needed for `units` warps, if they can all be co-resident.
+bool cell_fit_units(const DevGraph &g, int64_t units, int *ctas) {
+  cell_fn fn = cell_kernel_for(g.tp);
+  if (!fn) return false;
   int dev = 0, sms = 0, coop = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
   if (!coop) return false;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cell_kernel, threads, 0) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, 0) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return (int64_t)per_sm * sms >= (int64_t)g.pp * g.dp;
+  const int64_t need = (units + WARPS - 1) / WARPS;
+  if (ctas) *ctas = (int)need;
+  return need >= 1 && (int64_t)per_sm * sms >= need;
 }
 
 }  // namespace
 
+// Chunks of 32 scenarios per unit; every chunk of a replay runs in one launch when they all fit,
+// else the caller launches one chunk at a time (chunk groups of 1).
 bool cells_fit(const DevGraph &g, int nchunks) {
-  (void)nchunks;  // chunks run as successive launches
-  return cell_fit(g);
+  return cell_fit_units(g, (int64_t)g.pp * g.dp, nullptr) && nchunks >= 1;
 }
 
 int cells_chunk_scenarios() { return SC; }
 
+int cells_chunks_per_launch(const DevGraph &g, int nchunks) {
+  for (int c = nchunks; c > 1; --c)
+    if (nchunks % c == 0 && cell_fit_units(g, (int64_t)g.pp * g.dp * c, nullptr)) return c;
+  return 1;
+}
+
 cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc,
                          uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t *gfin,
-                         int64_t *rank_end, int chunk, int Sp, cudaStream_t st) {
-  if (!cell_fit(g)) return cudaErrorCooperativeLaunchTooLarge;
-  CellArgs a{rslot, acc, arrive, status, 10ull * 1000 * 1000 * 1000, parity};
+                         int64_t *rank_end, int chunk0, int nchunks_launch, int Sp, cudaStream_t st) {
+  const int64_t units = (int64_t)g.pp * g.dp * nchunks_launch;
+  int ctas = 0;
+  if (!cell_fit_units(g, units, &ctas)) return cudaErrorCooperativeLaunchTooLarge;
+  // the launch covers chunks [chunk0, chunk0 + nchunks_launch) of the replay's Sp / 32 chunks
+  CellArgs a{rslot, acc, arrive, status, 10ull * 1000 * 1000 * 1000, parity, (int32_t)units, Sp, chunk0,
+             Sp / SC};
   DevGraph gg = g;
   ScenParams pp = p;
-  int32_t ch = chunk, sp = Sp;
-  void *args[] = {&gg, &pp, &a, &ch, &sp, &fin, &gfin, &rank_end};
-  return cudaLaunchCooperativeKernel((const void *)cell_kernel, dim3(g.pp * g.dp), dim3(((g.tp + 1) / 2) * 32),
+  void *args[] = {&gg, &pp, &a, &fin, &gfin, &rank_end};
+  return cudaLaunchCooperativeKernel((const void *)cell_kernel_for(g.tp), dim3(ctas), dim3(WARPS * 32),
                                      args, 0, st);
+}
+
+// Debug statistics of the last cell-kernel launch (PRISM_CELL_STATS builds only).
+extern "C" PRISM_API int prism_debug_lat(unsigned long long *out) {
+#ifdef PRISM_CELL_STATS
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_lat, sizeof(unsigned long long) * 4);
+  unsigned long long z[4] = {0, 0, 0, 0};
+  cudaMemcpyToSymbol(g_lat, z, sizeof z);
+  return 0;
+#else
+  (void)out;
+  return -2;
+#endif
+}
+
+extern "C" PRISM_API int prism_debug_wait_hist(unsigned long long *out) {
+#ifdef PRISM_CELL_STATS
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, g_wait_hist, sizeof(unsigned long long) * 16 * 4096) != cudaSuccess) return -1;
+  static unsigned long long zeros[16 * 4096];
+  cudaMemcpyToSymbol(g_wait_hist, zeros, sizeof zeros);
+  return 0;
+#else
+  (void)out;
+  return -2;
+#endif
+}
+
+extern "C" PRISM_API int prism_debug_cell_stats(unsigned long long *out, int n) {
+#ifdef PRISM_CELL_STATS
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, g_cell_stats, sizeof(unsigned long long) * (size_t)n) != cudaSuccess) return -1;
+  static unsigned long long zeros[16384 * 8];
+  cudaMemcpyToSymbol(g_cell_stats, zeros, sizeof zeros);
+  return 0;
+#else
+  (void)out;
+  (void)n;
+  return -2;
+#endif
 }
 
 }  // namespace prism
