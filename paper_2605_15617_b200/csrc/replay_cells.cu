@@ -124,106 +124,110 @@ __device__ __forceinline__ bool wait_tick(const CellArgs &a, uint32_t &spins, ui
   return false;
 }
 
+// Per-warp shared scratch of the cross-cell path.
+struct CrossScratch {
+  uint32_t meta[MAX_TP * 4];   // (rank, slot) pair x = r * ns + q: sync record of rank r's q-th group
+  int32_t base[MAX_TP * 4];
+  int32_t grp[MAX_TP * 4];
+  int64_t dur[MAX_TP * 4];
+  uint64_t uid[MAX_TP * 4];
+  int64_t vmax[MAX_TP * 4][32];  // per pair, per lane: max ready time over the group's members
+};
+
 // Cross-cell node at template index i for all C ranks of the cell (rare: a few % of ops; kept
 // rolled and out of the unrolled per-rank register code so the kernel fits the instruction cache).
 // ts[r * 32 + lane] holds rank r's ready time on entry and its finish on exit (shared memory);
-// hs0 = membership slot of rank 0's node, rs0 = rank 0's first slot, rsh[r] = rank r's first slot;
-// ns = slots of the op. Deposit / arrive for every rank first, then wait (a group may contain
-// several ranks of the cell, e.g. WORLD).
+// rsh[r] = rank r's first membership slot, hoff = the op's slot offset in the template, ns = slots
+// of the op. The op's C x ns sync records are staged in shared memory by one lane-parallel load;
+// deposit / arrive for every rank first, then poll (every poll of a pass is an independent load,
+// folded on the fly, the own slot is not read back), then finish = max over groups + dur'.
 __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p, const CellArgs &a,
-                                       int64_t *__restrict__ gfin, int64_t *ts, const int32_t *rsh, int C,
-                                       int32_t hoff, int32_t ns, int32_t k) {
+                                          int64_t *__restrict__ gfin, int64_t *ts, const int32_t *rsh, int C,
+                                          int32_t hoff, int32_t ns, int32_t k, CrossScratch &cs) {
   const int lane = threadIdx.x & 31;
   const int32_t Sp = a.Sp;
   const int32_t ck = k / SC;
+  const int np = C * ns;  // <= 32
+  if (lane < np) {
+    const int r = lane / ns, q = lane - (lane / ns) * ns;
+    const int32_t h = rsh[r] + hoff + q;
+    cs.meta[lane] = g.h_meta[h];
+    cs.base[lane] = g.h_base[h];
+    cs.dur[lane] = g.h_dur[h];
+    cs.uid[lane] = g.h_uid[h];
+    cs.grp[lane] = ns > 1 ? g.node_grp[h] : 0;
+  }
+  __syncwarp();
   bool large_any = false;
-  for (int r = 0; r < C; ++r) {
-    const int64_t tr = ts[r * 32 + lane];
-    for (int32_t q = 0; q < ns; ++q) {
-      const int32_t h = rsh[r] + hoff + q;
-      const uint32_t meta = g.h_meta[h];
-      const int32_t base = g.h_base[h];
-      if (!(meta & 0x80000000u)) {
+  for (int x = 0; x < np; ++x) {
+    const int64_t tr = ts[(x / ns) * 32 + lane];
+    const uint32_t meta = cs.meta[x];
+    const int32_t base = cs.base[x];
+    if (!(meta & 0x80000000u)) {
 #ifdef PRISM_CELL_STATS
-        if (k == 0 && base + (int32_t)((meta >> 16) & 0x7FFF) < (1 << 22)) {
-          g_dep_time[base + (int32_t)((meta >> 16) & 0x7FFF)] = globaltimer();
-          __threadfence();
-        }
-#endif
-        st_relaxed64(a.rslot + (int64_t)(base + (int32_t)((meta >> 16) & 0x7FFF)) * Sp + k, a.parity ? ~tr : tr);
-      } else {
-        large_any = true;
-        red_max(a.acc + (int64_t)base * Sp + k, tr);
+      if (k == 0 && base + (int32_t)((meta >> 16) & 0x7FFF) < (1 << 22)) {
+        g_dep_time[base + (int32_t)((meta >> 16) & 0x7FFF)] = globaltimer();
+        __threadfence();
       }
+#endif
+      st_relaxed64(a.rslot + (int64_t)(base + (int32_t)((meta >> 16) & 0x7FFF)) * Sp + k, a.parity ? ~tr : tr);
+    } else {
+      large_any = true;
+      red_max(a.acc + (int64_t)base * Sp + k, tr);
     }
   }
   if (large_any) {
     __threadfence();  // the accumulations are performed before the arrival is counted
     __syncwarp();
     if (lane == 0)
-      for (int r = 0; r < C; ++r)
-        for (int32_t q = 0; q < ns; ++q) {
-          const int32_t h = rsh[r] + hoff + q;
-          if (g.h_meta[h] & 0x80000000u) atomicAdd(a.arrive + (int64_t)g.h_base[h] * a.nchunks + ck, 1u);
-        }
+      for (int x = 0; x < np; ++x)
+        if (cs.meta[x] & 0x80000000u) atomicAdd(a.arrive + (int64_t)cs.base[x] * a.nchunks + ck, 1u);
   }
-  // Wait: each pass issues every poll of every rank / group / member as an independent load (one
-  // L2 round trip per pass); the own slot is not read back. Then fold per rank.
   uint32_t spins = 0;
   uint64_t tw = 0;
   while (true) {
     bool ok = true;
-    for (int r = 0; r < C; ++r)
-      for (int32_t q = 0; q < ns; ++q) {
-        const int32_t h = rsh[r] + hoff + q;
-        const uint32_t meta = g.h_meta[h];
-        const int32_t base = g.h_base[h];
-        const int32_t size = (int32_t)(meta & 0xFFFF);
-        if (!(meta & 0x80000000u)) {
-          const int32_t own = (int32_t)((meta >> 16) & 0x7FFF);
-          const int64_t *src = a.rslot + (int64_t)base * Sp + k;
-          for (int32_t mm = 0; mm < size; ++mm, src += Sp) {
-            if (mm == own) continue;
-            const int64_t v = ld_relaxed64(src);
-            ok &= a.parity ? v < 0 : v >= 0;
-          }
-        } else {
-          ok &= ld_relaxed(a.arrive + (int64_t)base * a.nchunks + ck) >= (uint32_t)size;
+#pragma unroll 4
+    for (int x = 0; x < np; ++x) {
+      const uint32_t meta = cs.meta[x];
+      const int32_t base = cs.base[x];
+      const int32_t size = (int32_t)(meta & 0xFFFF);
+      if (!(meta & 0x80000000u)) {
+        const int32_t own = (int32_t)((meta >> 16) & 0x7FFF);
+        int64_t m = ts[(x / ns) * 32 + lane];
+        const int64_t *src = a.rslot + (int64_t)base * Sp + k;
+        for (int32_t mm = 0; mm < size; ++mm, src += Sp) {
+          if (mm == own) continue;
+          const int64_t v = ld_relaxed64(src);
+          ok &= a.parity ? v < 0 : v >= 0;
+          m = max(m, a.parity ? ~v : v);
         }
+        cs.vmax[x][lane] = m;
+      } else {
+        ok &= ld_relaxed(a.arrive + (int64_t)base * a.nchunks + ck) >= (uint32_t)size;
       }
+    }
     if (__all_sync(0xffffffffu, ok)) break;
     ++spins;
     if (spins > 6 && wait_tick(a, spins, tw)) return false;
   }
   if (large_any) fence_acq_rel();
   for (int r = 0; r < C; ++r) {
-    const int64_t tr = ts[r * 32 + lane];
     int64_t fr = 0;
     for (int32_t q = 0; q < ns; ++q) {
-      const int32_t h = rsh[r] + hoff + q;
-      const uint32_t meta = g.h_meta[h];
-      int64_t m = tr;
-      if (!(meta & 0x80000000u)) {
-        const int32_t own = (int32_t)((meta >> 16) & 0x7FFF);
-        const int64_t *src = a.rslot + (int64_t)g.h_base[h] * Sp + k;
-        for (int32_t mm = 0; mm < (int32_t)(meta & 0xFFFF); ++mm, src += Sp) {
-          if (mm == own) continue;
-          const int64_t v = ld_relaxed64(src);
-          m = max(m, a.parity ? ~v : v);
-        }
-      } else {
-        m = __ldcg(a.acc + (int64_t)g.h_base[h] * Sp + k);
-      }
-      const int64_t gd = g.h_dur[h];
-      const uint64_t uid = g.h_uid[h];
+      const int x = r * ns + q;
+      int64_t m = (cs.meta[x] & 0x80000000u) ? __ldcg(a.acc + (int64_t)cs.base[x] * Sp + k) : cs.vmax[x][lane];
+      const int64_t gd = cs.dur[x];
+      const uint64_t uid = cs.uid[x];
       const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
       if ((p.mask & gb) && p.amp > 0 && k > 0) m += perturb_x(gd, p.seed ^ ((uint64_t)k * K_GOLD) ^ (uid * K_MIX), p);
       else m += gd;
       fr = max(fr, m);
-      if (ns > 1) gfin[(int64_t)g.node_grp[h] * Sp + k] = m;  // P2P-batch group finishes, for queries
+      if (ns > 1) gfin[(int64_t)cs.grp[x] * Sp + k] = m;  // P2P-batch group finishes, for queries
     }
     ts[r * 32 + lane] = fr;
   }
+  __syncwarp();
   return true;
 }
 
@@ -241,6 +245,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   const int32_t Sp = a.Sp;
   const int32_t k = chunk * SC + lane;
   __shared__ int64_t ts[MAX_TP * 32];  // chain state of the cross-cell path (rolled over ranks)
+  __shared__ CrossScratch cs;
   __shared__ int32_t rsh[MAX_TP];       // first membership slot of each rank
   int32_t rb[C];
   int32_t rs[C];   // first membership slot of each rank (node_gptr of its first node)
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
 #pragma unroll
         for (int r = 0; r < C; ++r) ts[r * 32 + lane] = t[r];
         __syncwarp();
-        const bool ok = cross_all(g, p, a, gfin, ts, rsh, C, h0 - rs[0], ns, k);
+        const bool ok = cross_all(g, p, a, gfin, ts, rsh, C, h0 - rs[0], ns, k, cs);
         __syncwarp();
         if (!ok) return;
 #pragma unroll
