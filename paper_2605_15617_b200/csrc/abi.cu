@@ -6,6 +6,8 @@
 // (a9). No CPU fallback: every compute entry point fails with PRISM_E_CUDA without a device.
 #include <cuda_runtime.h>
 
+#include <malloc.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -68,6 +70,18 @@ prism_status fail(prism_status s, const std::string &m) {
 
 }  // namespace
 
+namespace {
+// The host plan allocates a few MB of short-lived tables per build; with glibc's default mmap
+// threshold every build page-faults them in afresh (~0.9 ms of a ~2.3 ms plan for C5). Keep
+// such blocks in the heap so repeated builds reuse warm pages.
+struct MallocTuning {
+  MallocTuning() {
+    mallopt(M_MMAP_THRESHOLD, 64 << 20);
+    mallopt(M_TRIM_THRESHOLD, 256 << 20);
+  }
+} g_malloc_tuning;
+}  // namespace
+
 struct prism_graph_s {
   Plan plan;
   DevGraph dg{};
@@ -111,6 +125,7 @@ struct prism_graph_s {
   std::vector<int32_t> lvl_tile_ptr, lvl_max_cnt;
   int64_t launches = 0;
   bool oom = false;
+  std::vector<unsigned char> staging;  // packed host tables of the build upload
   // profiling events: 0/1 expand, 2/3 levels, 4 tail end, 5 reduce end, 6/7 peak
   bool profile = false;
   cudaEvent_t ev[8] = {};
@@ -267,60 +282,108 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.nq = (int32_t)P.q.size();
   const size_t W = P.W, N = P.N, M = P.M, Gn = P.G, pp = P.topo.pp;
   const size_t nops = (size_t)tmpl->n_ops;
-  d.rank_ptr = G->take<int32_t>(W + 1);
-  d.rank_slot = G->take<int32_t>(W + 1);
-  d.rank_stage = G->take<int32_t>(W);
-  d.node_rank = G->take<int32_t>(N);
-  d.node_dur = G->take<int64_t>(N);
-  d.node_kind = G->take<uint8_t>(N);
-  d.node_label = G->take<uint32_t>(N);
-  d.node_alloc = G->take<int64_t>(N);
-  d.node_free = G->take<int64_t>(N);
-  d.node_prev_sync = G->take<int32_t>(N);
-  d.node_gptr = G->take<int32_t>(N + 1);
-  d.node_grp = G->take<int32_t>(M);
-  d.grp_ptr = G->take<int32_t>(Gn + 1);
-  d.grp_mem = G->take<int32_t>(M);
-  d.grp_dur = G->take<int64_t>(Gn);
-  d.grp_uid = G->take<uint64_t>(Gn);
-  d.grp_level = G->take<int32_t>(Gn);
-  d.node_mslot = G->take<int32_t>(M);
-  d.node_cls = G->take<uint8_t>(N);
-  d.node_sdur = G->take<int64_t>(N);
-  d.node_uid = G->take<uint64_t>(N);
-  d.grp_xbase = G->take<int64_t>(Gn);
-  d.grp_lidx = G->take<int32_t>(Gn);
-  d.h_base = G->take<int32_t>(M);
-  d.h_meta = G->take<uint32_t>(M);
-  d.h_dur = G->take<int64_t>(M);
-  d.h_uid = G->take<uint64_t>(M);
+  // One device allocation for the whole graph (a Python allocator hook costs ~tens of us per
+  // call), carved into 256-byte aligned arrays; the host-made tables live in one section that is
+  // uploaded with a single copy from a packed host buffer.
+  const size_t nslot = P.slot_q.size(), nch = P.chunk_q.size();
+  size_t off = 0;
+  auto carve = [&off](size_t bytes) {
+    off = (off + 255) & ~(size_t)255;
+    const size_t o = off;
+    off += std::max<size_t>(bytes, 1);
+    return o;
+  };
+  // tables (uploaded)
+  const size_t o_ops = carve(nops * sizeof(prism_op)), o_tps = carve(nops * 4), o_tsp = carve(nops * 4);
+  const size_t o_op0 = carve(pp * 8), o_len = carve(pp * 8), o_slt = carve(pp * 8), o_stat = carve(pp * 8);
+  const size_t o_q = carve(P.q.size() * sizeof(QGroup)), o_wpos = carve(P.wpos.size() * 4);
+  const size_t o_ss0 = carve(P.stage_slot0.size() * 8), o_slq = carve(nslot * 4), o_sltd = carve(nslot * 4);
+  const size_t o_slr = carve(nslot), o_slf = carve(nslot), o_chq = carve(nch * 4), o_chm = carve(nch * 8);
+  const size_t table_bytes = off;
+  // graph arrays (written by the expand kernels)
+  const size_t o_rp = carve((W + 1) * 4), o_rs = carve((W + 1) * 4), o_rst = carve(W * 4);
+  const size_t o_nrank = carve(N * 4), o_ndur = carve(N * 8), o_nkind = carve(N), o_nlab = carve(N * 4);
+  const size_t o_nal = carve(N * 8), o_nfr = carve(N * 8), o_nps = carve(N * 4), o_ngp = carve((N + 1) * 4);
+  const size_t o_ngrp = carve(M * 4), o_gptr = carve((Gn + 1) * 4), o_gmem = carve(M * 4), o_gdur = carve(Gn * 8);
+  const size_t o_guid = carve(Gn * 8), o_glvl = carve(Gn * 4), o_nms = carve(M * 4), o_ncls = carve(N);
+  const size_t o_nsd = carve(N * 8), o_nuid = carve(N * 8), o_gxb = carve(Gn * 8), o_gli = carve(Gn * 4);
+  const size_t o_hb = carve(M * 4), o_hm = carve(M * 4), o_hd = carve(M * 8), o_hu = carve(M * 8);
+  const size_t total = off;
+  unsigned char *base = G->take<unsigned char>(total);
+  if (G->oom || !base) return fail(PRISM_E_OOM, "device allocation failed while building the graph");
+  auto at = [base](size_t o) { return (void *)(base + o); };
+  prism_op *t_ops = (prism_op *)at(o_ops);
+  d.t_ops = t_ops;
+  d.t_prev_sync = (int32_t *)at(o_tps);
+  d.t_slot_ptr = (int32_t *)at(o_tsp);
+  d.t_op0 = (int64_t *)at(o_op0);
+  d.t_len = (int64_t *)at(o_len);
+  d.t_slots_total = (int64_t *)at(o_slt);
+  d.static_mem = (int64_t *)at(o_stat);
+  d.q = (const QGroup *)at(o_q);
+  d.wpos = (const int32_t *)at(o_wpos);
+  d.stage_slot0 = (const int64_t *)at(o_ss0);
+  d.slot_q = (const int32_t *)at(o_slq);
+  d.slot_tidx = (const int32_t *)at(o_sltd);
+  d.slot_role = (const uint8_t *)at(o_slr);
+  d.slot_first = (const uint8_t *)at(o_slf);
+  d.chunk_q = (const int32_t *)at(o_chq);
+  d.chunk_m = (const int64_t *)at(o_chm);
+  d.nchunk = (int32_t)nch;
+  d.rank_ptr = (int32_t *)at(o_rp);
+  d.rank_slot = (int32_t *)at(o_rs);
+  d.rank_stage = (int32_t *)at(o_rst);
+  d.node_rank = (int32_t *)at(o_nrank);
+  d.node_dur = (int64_t *)at(o_ndur);
+  d.node_kind = (uint8_t *)at(o_nkind);
+  d.node_label = (uint32_t *)at(o_nlab);
+  d.node_alloc = (int64_t *)at(o_nal);
+  d.node_free = (int64_t *)at(o_nfr);
+  d.node_prev_sync = (int32_t *)at(o_nps);
+  d.node_gptr = (int32_t *)at(o_ngp);
+  d.node_grp = (int32_t *)at(o_ngrp);
+  d.grp_ptr = (int32_t *)at(o_gptr);
+  d.grp_mem = (int32_t *)at(o_gmem);
+  d.grp_dur = (int64_t *)at(o_gdur);
+  d.grp_uid = (uint64_t *)at(o_guid);
+  d.grp_level = (int32_t *)at(o_glvl);
+  d.node_mslot = (int32_t *)at(o_nms);
+  d.node_cls = (uint8_t *)at(o_ncls);
+  d.node_sdur = (int64_t *)at(o_nsd);
+  d.node_uid = (uint64_t *)at(o_nuid);
+  d.grp_xbase = (int64_t *)at(o_gxb);
+  d.grp_lidx = (int32_t *)at(o_gli);
+  d.h_base = (int32_t *)at(o_hb);
+  d.h_meta = (uint32_t *)at(o_hm);
+  d.h_dur = (int64_t *)at(o_hd);
+  d.h_uid = (uint64_t *)at(o_hu);
   d.M_cross = P.M_cross;
   d.G_large = P.G_large;
-  prism_op *t_ops = G->take<prism_op>(nops);
-  d.t_ops = t_ops;
-  d.t_op0 = G->take<int64_t>(pp);
-  d.t_len = G->take<int64_t>(pp);
-  d.t_prev_sync = G->take<int32_t>(nops);
-  d.t_slot_ptr = G->take<int32_t>(nops);
-  d.t_slots_total = G->take<int64_t>(pp);
-  d.static_mem = G->take<int64_t>(pp);
-  QGroup *q = G->take<QGroup>(P.q.size());
-  d.q = q;
-  int32_t *wpos = G->take<int32_t>(P.wpos.size());
-  d.wpos = wpos;
-  if (G->oom) return fail(PRISM_E_OOM, "device allocation failed while building the graph");
   cudaStream_t s = G->stream;
-  if (nops) {
-    CU(cudaMemcpyAsync(t_ops, tmpl->ops, nops * sizeof(prism_op), cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(d.t_prev_sync, P.t_prev_sync.data(), nops * 4, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(d.t_slot_ptr, P.t_slot_ptr.data(), nops * 4, cudaMemcpyHostToDevice, s));
+  {  // packed upload of the host tables
+    std::vector<unsigned char> &h = G->staging;
+    h.assign(table_bytes, 0);
+    auto put = [&h](size_t o, const void *src, size_t bytes) {
+      if (bytes) std::memcpy(h.data() + o, src, bytes);
+    };
+    put(o_ops, tmpl->ops, nops * sizeof(prism_op));
+    put(o_tps, P.t_prev_sync.data(), nops * 4);
+    put(o_tsp, P.t_slot_ptr.data(), nops * 4);
+    put(o_op0, P.stage_op0.data(), pp * 8);
+    put(o_len, P.stage_len.data(), pp * 8);
+    put(o_slt, P.stage_slots.data(), pp * 8);
+    put(o_stat, tmpl->static_mem, pp * 8);
+    put(o_q, P.q.data(), P.q.size() * sizeof(QGroup));
+    put(o_wpos, P.wpos.data(), P.wpos.size() * 4);
+    put(o_ss0, P.stage_slot0.data(), P.stage_slot0.size() * 8);
+    put(o_slq, P.slot_q.data(), nslot * 4);
+    put(o_sltd, P.slot_tidx.data(), nslot * 4);
+    put(o_slr, P.slot_role.data(), nslot);
+    put(o_slf, P.slot_first.data(), nslot);
+    put(o_chq, P.chunk_q.data(), nch * 4);
+    put(o_chm, P.chunk_m.data(), nch * 8);
+    CU(cudaMemcpyAsync(base, h.data(), table_bytes, cudaMemcpyHostToDevice, s));
   }
-  CU(cudaMemcpyAsync(d.t_op0, P.stage_op0.data(), pp * 8, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(d.t_len, P.stage_len.data(), pp * 8, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(d.t_slots_total, P.stage_slots.data(), pp * 8, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync(d.static_mem, tmpl->static_mem, pp * 8, cudaMemcpyHostToDevice, s));
-  if (!P.q.empty()) CU(cudaMemcpyAsync(q, P.q.data(), P.q.size() * sizeof(QGroup), cudaMemcpyHostToDevice, s));
-  if (!P.wpos.empty()) CU(cudaMemcpyAsync(wpos, P.wpos.data(), P.wpos.size() * 4, cudaMemcpyHostToDevice, s));
   if (opts && (opts->flags & PRISM_BUILD_PROFILE)) {
     G->profile = true;
     for (auto &e : G->ev) CU(cudaEventCreate(&e));

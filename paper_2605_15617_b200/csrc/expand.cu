@@ -68,7 +68,31 @@ __global__ void __launch_bounds__(1024) rank_tables_kernel(DevGraph g) {
   }
 }
 
-// Row a3: one block per rank (grid-stride), threads over the rank's template ops.
+// Concrete group id (uid field) of instance `inst` of quotient group q (closed form, a2).
+__device__ __forceinline__ uint64_t group_gid(const DevGraph &g, const QGroup &q, int32_t inst) {
+  const int32_t s = q.stage;
+  switch (q.type) {
+    case PRISM_ROLE_TP: return (uint64_t)s + (uint64_t)g.pp * inst;                    // inst = dp
+    case PRISM_ROLE_DP: return (uint64_t)inst + (uint64_t)g.tp * s;                    // inst = tp
+    case PRISM_ROLE_EP:                                                                  // (tp, edp)
+      return (uint64_t)(inst % g.tp) + (uint64_t)g.tp * (s + (uint64_t)g.pp * (inst / g.tp));
+    case PRISM_ROLE_EDP:                                                                 // (tp, ep)
+      return (uint64_t)(inst % g.tp) + (uint64_t)g.tp * (s + (uint64_t)g.pp * (inst / g.tp));
+    case PRISM_ROLE_WORLD: return 0;
+    default: {  // P2P message: sender rank * 2 + direction
+      const int32_t sender = rank_of(g, inst % g.tp, s, inst / g.tp);
+      return (uint64_t)sender * 2 + q.dir;
+    }
+  }
+}
+__device__ __forceinline__ uint64_t group_uid(const DevGraph &g, const QGroup &q, int32_t inst) {
+  return ((uint64_t)q.type << 56) | (group_gid(g, q, inst) << 24) | (uint64_t)q.occ;
+}
+
+// Rows a3 + a4 (node side): one block per rank (grid-stride), threads over the rank's template
+// ops, then over its template slots; every write is a coalesced run along the rank's nodes /
+// membership slots. A slot's group instance and member index follow in closed form from the
+// rank's coordinates (the same enumeration as the group side below).
 __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
   for (int32_t r = blockIdx.x; r < g.W; r += gridDim.x) {
     const int32_t s = g.rank_stage[r];
@@ -88,98 +112,91 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
       g.node_free[n] = o.mem_free;
       g.node_prev_sync[n] = tps < 0 ? -1 : rb + tps;
       g.node_gptr[n] = slot0 + g.t_slot_ptr[op0 + i];
-      if (o.kind == PRISM_KIND_COMPUTE) {  // sync nodes are filled in by build_groups_kernel
+      if (o.kind == PRISM_KIND_COMPUTE) {  // sync nodes get their record from their first slot
         g.node_cls[n] = 0;
         g.node_sdur[n] = o.dur_ns;
         g.node_uid[n] = ((uint64_t)r << 32) | (uint32_t)i;
       }
     }
-  }
-}
-
-// Row a4: one thread per membership (grid-stride). The quotient group is found by binary search
-// over mbase; the concrete instance / member follow in closed form from the coordinates.
-__global__ void __launch_bounds__(256) build_groups_kernel(DevGraph g) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < g.M; m += stride) {
-    int32_t lo = 0, hi = g.nq - 1;
-    while (lo < hi) {  // last q with mbase <= m
-      int32_t mid = (lo + hi + 1) >> 1;
-      if (g.q[mid].mbase <= m) lo = mid; else hi = mid - 1;
-    }
-    const QGroup &q = g.q[lo];
-    const int64_t local = m - q.mbase;
-    const int32_t inst = (int32_t)(local / q.size);
-    const int32_t j = (int32_t)(local - (int64_t)inst * q.size);
-    const int64_t grp = q.gbase + inst;
-    int32_t rank, tidx = q.tidx, slot = q.slot;
-    uint64_t gid;
-    const int32_t s = q.stage;
-    switch (q.type) {
-      case PRISM_ROLE_TP:  // instance = dp index, member = tp index
-        rank = rank_of(g, j, s, inst);
-        gid = (uint64_t)s + (uint64_t)g.pp * inst;
-        break;
-      case PRISM_ROLE_DP:  // instance = tp index, member = dp index
-        rank = rank_of(g, inst, s, j);
-        gid = (uint64_t)inst + (uint64_t)g.tp * s;
-        break;
-      case PRISM_ROLE_EP: {  // instance = (tp, edp), member = ep index
-        int32_t tpi = inst % g.tp, edp = inst / g.tp;
-        rank = rank_of(g, tpi, s, edp * g.ep + j);
-        gid = (uint64_t)tpi + (uint64_t)g.tp * (s + (uint64_t)g.pp * edp);
-        break;
+    // coordinates of r
+    const int32_t tpi = r % g.tp;
+    const int32_t dpi = g.order == PRISM_ORDER_MEGATRON ? (r / g.tp) % g.dp : r / (g.tp * g.pp);
+    const int32_t epi = dpi % g.ep, edpi = dpi / g.ep;
+    const int64_t u0 = g.stage_slot0[s];
+    const int32_t nsl = (int32_t)(g.stage_slot0[s + 1] - u0);
+    for (int32_t u = threadIdx.x; u < nsl; u += blockDim.x) {
+      const QGroup &q = g.q[g.slot_q[u0 + u]];
+      int32_t inst, j;
+      switch (q.type) {
+        case PRISM_ROLE_TP: inst = dpi; j = tpi; break;
+        case PRISM_ROLE_DP: inst = tpi; j = dpi; break;
+        case PRISM_ROLE_EP: inst = tpi + g.tp * edpi; j = epi; break;
+        case PRISM_ROLE_EDP: inst = tpi + g.tp * epi; j = edpi; break;
+        case PRISM_ROLE_WORLD: inst = 0; j = r; break;
+        default: inst = tpi + g.tp * dpi; j = g.slot_role[u0 + u]; break;
       }
-      case PRISM_ROLE_EDP: {  // instance = (tp, ep), member = edp index
-        int32_t tpi = inst % g.tp, epi = inst / g.tp;
-        rank = rank_of(g, tpi, s, j * g.ep + epi);
-        gid = (uint64_t)tpi + (uint64_t)g.tp * (s + (uint64_t)g.pp * epi);
-        break;
-      }
-      case PRISM_ROLE_WORLD:
-        rank = j;
-        tidx = g.wpos[q.wpos + g.rank_stage[j]];
-        gid = 0;
-        break;
-      default: {  // P2P message: member 0 = sender, member 1 = receiver (same tp/dp coords)
-        int32_t tpi = inst % g.tp, dpi = inst / g.tp;
-        int32_t sender = rank_of(g, tpi, s, dpi);
-        if (j == 0) {
-          rank = sender;
-        } else {
-          rank = rank_of(g, tpi, q.stage2, dpi);
-          tidx = q.tidx2;
-          slot = q.slot2;
-        }
-        gid = (uint64_t)sender * 2 + q.dir;
-        break;
-      }
-    }
-    const int32_t node = g.rank_ptr[rank] + tidx;
-    g.grp_mem[m] = node;
-    g.node_grp[g.node_gptr[node] + slot] = (int32_t)grp;
-    g.node_mslot[g.node_gptr[node] + slot] = (int32_t)m;
-    const uint64_t uid = ((uint64_t)q.type << 56) | (gid << 24) | (uint64_t)q.occ;
-    {
-      const int32_t h = g.node_gptr[node] + slot;
+      const int32_t h = slot0 + u;
+      const int64_t grp = q.gbase + inst;
+      const uint64_t uid = group_uid(g, q, inst);
       const bool large = q.xbase < 0 && q.lbase >= 0;
+      g.node_grp[h] = (int32_t)grp;
+      g.node_mslot[h] = (int32_t)(q.mbase + (int64_t)inst * q.size + j);
       g.h_base[h] = large ? (int32_t)(q.lbase + inst) : (q.xbase < 0 ? -1 : (int32_t)(q.xbase + (int64_t)inst * q.size));
       g.h_meta[h] = (uint32_t)min(q.size, 0xFFFF) | ((uint32_t)min(j, 0x7FFF) << 16) | (large ? 0x80000000u : 0u);
       g.h_dur[h] = q.dur;
       g.h_uid[h] = uid;
+      if (g.slot_first[u0 + u]) {  // the node's first group provides its replay record
+        const int32_t n = rb + g.slot_tidx[u0 + u];
+        g.node_cls[n] = q.type == PRISM_ROLE_TP ? 1 : 2;
+        g.node_sdur[n] = q.dur;
+        g.node_uid[n] = uid;
+      }
     }
-    if (slot == 0) {  // the node's first group provides its replay record
-      g.node_cls[node] = q.type == PRISM_ROLE_TP ? 1 : 2;
-      g.node_sdur[node] = q.dur;
-      g.node_uid[node] = uid;
-    }
-    if (j == 0) {
-      g.grp_xbase[grp] = q.xbase < 0 ? -1 : q.xbase + (int64_t)inst * q.size;
-      g.grp_lidx[grp] = q.lbase < 0 ? -1 : (int32_t)(q.lbase + inst);
-      g.grp_ptr[grp] = (int32_t)m;
-      g.grp_dur[grp] = q.dur;
-      g.grp_level[grp] = q.level;
-      g.grp_uid[grp] = uid;
+  }
+}
+
+// Row a4 (group side): one block per chunk of 2048 memberships of one quotient group (host-made
+// chunk table, no search); member node ids by closed form from the coordinates; coalesced writes
+// of grp_mem and of the per-group arrays.
+__global__ void __launch_bounds__(256) build_groups_kernel(DevGraph g) {
+  for (int32_t c = blockIdx.x; c < g.nchunk; c += gridDim.x) {
+    const QGroup &q = g.q[g.chunk_q[c]];
+    const int64_t mq = (int64_t)q.inst * q.size;
+    const int64_t m_end = min(mq, g.chunk_m[c] + 2048);
+    const int32_t s = q.stage;
+    for (int64_t local = g.chunk_m[c] + threadIdx.x; local < m_end; local += blockDim.x) {
+      const int32_t inst = (int32_t)(local / q.size);
+      const int32_t j = (int32_t)(local - (int64_t)inst * q.size);
+      const int64_t m = q.mbase + local;
+      const int64_t grp = q.gbase + inst;
+      int32_t rank, tidx = q.tidx;
+      switch (q.type) {
+        case PRISM_ROLE_TP: rank = rank_of(g, j, s, inst); break;
+        case PRISM_ROLE_DP: rank = rank_of(g, inst, s, j); break;
+        case PRISM_ROLE_EP: rank = rank_of(g, inst % g.tp, s, (inst / g.tp) * g.ep + j); break;
+        case PRISM_ROLE_EDP: rank = rank_of(g, inst % g.tp, s, j * g.ep + inst / g.tp); break;
+        case PRISM_ROLE_WORLD:
+          rank = j;
+          tidx = g.wpos[q.wpos + g.rank_stage[j]];
+          break;
+        default:  // P2P message: member 0 = sender, member 1 = receiver (same tp/dp coords)
+          if (j == 0) {
+            rank = rank_of(g, inst % g.tp, s, inst / g.tp);
+          } else {
+            rank = rank_of(g, inst % g.tp, q.stage2, inst / g.tp);
+            tidx = q.tidx2;
+          }
+          break;
+      }
+      g.grp_mem[m] = g.rank_ptr[rank] + tidx;
+      if (j == 0) {
+        g.grp_ptr[grp] = (int32_t)m;
+        g.grp_dur[grp] = q.dur;
+        g.grp_level[grp] = q.level;
+        g.grp_uid[grp] = group_uid(g, q, inst);
+        g.grp_xbase[grp] = q.xbase < 0 ? -1 : q.xbase + (int64_t)inst * q.size;
+        g.grp_lidx[grp] = q.lbase < 0 ? -1 : (int32_t)(q.lbase + inst);
+      }
     }
   }
 }
@@ -192,11 +209,7 @@ cudaError_t launch_expand(const DevGraph &g, cudaStream_t st) {
     int blocks = g.W < 148 * 16 ? g.W : 148 * 16;
     expand_nodes_kernel<<<blocks, 256, 0, st>>>(g);
   }
-  if (g.M > 0) {
-    int64_t want = (g.M + 255) / 256;
-    int blocks = (int)(want < 148 * 32 ? want : 148 * 32);
-    build_groups_kernel<<<blocks, 256, 0, st>>>(g);
-  }
+  if (g.M > 0 && g.nchunk > 0) build_groups_kernel<<<g.nchunk, 256, 0, st>>>(g);
   return cudaGetLastError();
 }
 

@@ -57,6 +57,15 @@ struct DevGraph {
   int64_t *static_mem;      // [pp]
   const QGroup *q;          // quotient groups (level order)
   int32_t nq;
+  // per template slot (stage-major, stage s at stage_slot0[s]) and group-side build chunks
+  const int64_t *stage_slot0;
+  const int32_t *slot_q;
+  const int32_t *slot_tidx;
+  const uint8_t *slot_role;
+  const uint8_t *slot_first;
+  const int32_t *chunk_q;
+  const int64_t *chunk_m;
+  int32_t nchunk;
   const int32_t *wpos;      // WORLD per-stage template indices
 };
 

@@ -25,6 +25,14 @@
 
 #include "prism_internal.h"
 
+#ifdef PLAN_TIMING
+#include <chrono>
+#define TMARK(name) do { auto _n = std::chrono::high_resolution_clock::now(); \
+  std::fprintf(stderr, "  %-12s %.3f ms\n", name, std::chrono::duration<double, std::milli>(_n - _t).count()); _t = _n; } while (0)
+#else
+#define TMARK(name)
+#endif
+
 namespace prism {
 
 namespace {
@@ -66,6 +74,9 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     err = "tmpl_ptr must start at 0 and end at n_ops";
     return PRISM_E_INVALID_ARG;
   }
+#ifdef PLAN_TIMING
+  auto _t = std::chrono::high_resolution_clock::now();
+#endif
   P = Plan();
   P.topo = t;
   P.W = W;
@@ -127,8 +138,15 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     P.stage_slots[s] = slots;
   }
 
+  TMARK("scan");
   // ---- quotient groups --------------------------------------------------------------------
   std::vector<QGroup> Q;
+  {
+    size_t est = 0;
+    for (auto &v : role_ops) est += v.size();
+    for (auto &v : bit_ops) est += v.size();
+    Q.reserve(est);
+  }
   auto base_q = [](int type) {
     QGroup g{};
     g.type = type;
@@ -152,6 +170,7 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
       }
     }
   }
+  TMARK("q-coll");
   {  // WORLD: the k-th WORLD op of every stage
     size_t K = role_ops[0 * 6 + PRISM_ROLE_WORLD].size();
     for (int s = 1; s < pp; ++s)
@@ -184,6 +203,7 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
       Q.push_back(g);
     }
   }
+  TMARK("q-world");
   // intra-stage collective types agree trivially (one template op per quotient group)
   for (int s = 0; s < pp && pp > 1; ++s) {
     for (int dir = 0; dir < 2; ++dir) {
@@ -217,34 +237,44 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
   for (auto &g : Q)
     if (g.occ >= (1 << 24)) { err = "more than 2^24 occurrences of one group"; return PRISM_E_INVALID_ARG; }
 
+  TMARK("quotient");
   // ---- levels: structural replay on the quotient graph ------------------------------------
   // positions = (stage, template index) of sync ops; pos_q lists the quotient groups of each.
   std::vector<int64_t> pos_base(pp + 1, 0);
   for (int s = 0; s < pp; ++s) pos_base[s + 1] = pos_base[s] + P.stage_len[s];
-  std::vector<std::vector<int32_t>> pos_q(pos_base[pp]);
-  std::vector<int32_t> npos(Q.size());
-  for (size_t qi = 0; qi < Q.size(); ++qi) {
+  // pos_q: quotient groups of each position, as a CSR (positions x <= 4 groups)
+  const int64_t npos_all = pos_base[pp];
+  std::vector<int32_t> pq_ptr(npos_all + 1, 0), npos(Q.size());
+  auto for_positions = [&](size_t qi, auto &&fn) {
     const QGroup &g = Q[qi];
     if (g.type == PRISM_ROLE_WORLD) {
-      for (int s = 0; s < pp; ++s) pos_q[pos_base[s] + P.wpos[g.wpos + s]].push_back((int32_t)qi);
-      npos[qi] = pp;
+      for (int s = 0; s < pp; ++s) fn(pos_base[s] + P.wpos[g.wpos + s]);
     } else if (g.type == PRISM_ROLE_P2P) {
-      pos_q[pos_base[g.stage] + g.tidx].push_back((int32_t)qi);
-      pos_q[pos_base[g.stage2] + g.tidx2].push_back((int32_t)qi);
-      npos[qi] = 2;
+      fn(pos_base[g.stage] + g.tidx);
+      fn(pos_base[g.stage2] + g.tidx2);
     } else {
-      pos_q[pos_base[g.stage] + g.tidx].push_back((int32_t)qi);
-      npos[qi] = 1;
+      fn(pos_base[g.stage] + g.tidx);
     }
+  };
+  for (size_t qi = 0; qi < Q.size(); ++qi) {
+    int32_t c = 0;
+    for_positions(qi, [&](int64_t x) { ++pq_ptr[x + 1]; ++c; });
+    npos[qi] = c;
+  }
+  for (int64_t x = 0; x < npos_all; ++x) pq_ptr[x + 1] += pq_ptr[x];
+  std::vector<int32_t> pq(pq_ptr[npos_all]);
+  {
+    std::vector<int32_t> fill(pq_ptr.begin(), pq_ptr.end() - 1);
+    for (size_t qi = 0; qi < Q.size(); ++qi) for_positions(qi, [&](int64_t x) { pq[fill[x]++] = (int32_t)qi; });
   }
   std::vector<int32_t> arrived(Q.size(), 0), qlvl(Q.size(), 0), rdy(Q.size(), 0);
-  std::vector<int32_t> pend(pos_base[pp], 0), poslvl(pos_base[pp], 0);
-  for (int64_t i = 0; i < pos_base[pp]; ++i) pend[i] = (int32_t)pos_q[i].size();
+  std::vector<int32_t> pend(npos_all, 0), poslvl(npos_all, 0);
+  for (int64_t i = 0; i < npos_all; ++i) pend[i] = pq_ptr[i + 1] - pq_ptr[i];
   std::vector<int64_t> cursor(pp, 0);
   std::vector<int32_t> curlvl(pp, 0);
   std::vector<int> work;
   auto next_sync = [&](int s, int64_t from) {
-    while (from < P.stage_len[s] && pos_q[pos_base[s] + from].empty()) ++from;
+    while (from < P.stage_len[s] && pq_ptr[pos_base[s] + from + 1] == pq_ptr[pos_base[s] + from]) ++from;
     return from;
   };
   for (int s = 0; s < pp; ++s) {
@@ -255,8 +285,9 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     int s = work.back();
     work.pop_back();
     if (cursor[s] >= P.stage_len[s]) continue;
-    int64_t pos = pos_base[s] + cursor[s];
-    for (int32_t qi : pos_q[pos]) {
+    const int64_t pos = pos_base[s] + cursor[s];
+    for (int32_t e = pq_ptr[pos]; e < pq_ptr[pos + 1]; ++e) {
+      const int32_t qi = pq[e];
       rdy[qi] = std::max(rdy[qi], curlvl[s]);
       if (++arrived[qi] == npos[qi]) {
         qlvl[qi] = rdy[qi] + 1;
@@ -288,11 +319,20 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     }
   for (size_t qi = 0; qi < Q.size(); ++qi) Q[qi].level = qlvl[qi];
 
+  TMARK("levels");
   // ---- order by level, assign concrete group ids / membership ranges ----------------------
   std::vector<int32_t> ord(Q.size());
-  std::iota(ord.begin(), ord.end(), 0);
-  std::stable_sort(ord.begin(), ord.end(), [&](int32_t a, int32_t b) { return Q[a].level < Q[b].level; });
+  {  // stable counting sort by level
+    int32_t maxl = 0;
+    for (auto &g : Q) maxl = std::max(maxl, g.level);
+    std::vector<int32_t> cnt(maxl + 2, 0);
+    for (auto &g : Q) ++cnt[g.level + 1];
+    for (int32_t l = 0; l <= maxl; ++l) cnt[l + 1] += cnt[l];
+    for (size_t qi = 0; qi < Q.size(); ++qi) ord[cnt[Q[qi].level]++] = (int32_t)qi;
+  }
   P.q.resize(Q.size());
+  std::vector<int32_t> new_index(Q.size());
+  for (size_t i = 0; i < ord.size(); ++i) new_index[ord[i]] = (int32_t)i;
   int64_t G = 0, M = 0, X = 0, LG = 0;
   int32_t levels = 0, maxg = 0;
   for (size_t i = 0; i < ord.size(); ++i) {
@@ -318,6 +358,52 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     maxg = std::max(maxg, g.size);
     P.q[i] = g;
   }
+  TMARK("order");
+  // per template slot tables (node-side expansion) and group-side chunks
+  P.stage_slot0.assign(pp + 1, 0);
+  for (int s = 0; s < pp; ++s) P.stage_slot0[s + 1] = P.stage_slot0[s] + P.stage_slots[s];
+  const int64_t nslots = P.stage_slot0[pp];
+  P.slot_q.assign(nslots, -1);
+  P.slot_tidx.assign(nslots, 0);
+  P.slot_role.assign(nslots, 0);
+  P.slot_first.assign(nslots, 0);
+  for (int s = 0; s < pp; ++s)
+    for (int64_t i = 0; i < P.stage_len[s]; ++i) {
+      const int64_t op = P.stage_op0[s] + i;
+      for (int32_t u = 0; u < P.t_slots[op]; ++u) {
+        const int64_t x = P.stage_slot0[s] + P.t_slot_ptr[op] + u;
+        P.slot_tidx[x] = (int32_t)i;
+        P.slot_first[x] = u == 0;
+      }
+    }
+  auto put = [&](int s, int32_t tidx, int32_t slot, int32_t qnew, uint8_t role) {
+    const int64_t op = P.stage_op0[s] + tidx;
+    const int64_t x = P.stage_slot0[s] + P.t_slot_ptr[op] + slot;
+    P.slot_q[x] = qnew;
+    P.slot_role[x] = role;
+  };
+  for (size_t qi = 0; qi < Q.size(); ++qi) {
+    const QGroup &g = Q[qi];
+    const int32_t qn = new_index[qi];
+    if (g.type == PRISM_ROLE_WORLD) {
+      for (int s = 0; s < pp; ++s) put(s, P.wpos[g.wpos + s], 0, qn, 0);
+    } else if (g.type == PRISM_ROLE_P2P) {
+      put(g.stage, g.tidx, g.slot, qn, 0);
+      put(g.stage2, g.tidx2, g.slot2, qn, 1);
+    } else {
+      put(g.stage, g.tidx, 0, qn, 0);
+    }
+  }
+  for (int64_t x = 0; x < nslots; ++x)
+    if (P.slot_q[x] < 0) { err = "internal: template slot without a group"; return PRISM_E_INVALID_ARG; }
+  for (size_t i = 0; i < P.q.size(); ++i) {
+    const int64_t mq = (int64_t)P.q[i].inst * P.q[i].size;
+    for (int64_t off = 0; off < mq; off += 2048) {
+      P.chunk_q.push_back((int32_t)i);
+      P.chunk_m.push_back(off);
+    }
+  }
+  TMARK("slots");
   P.level_q_ptr.assign(levels + 2, 0);
   for (const auto &g : P.q) P.level_q_ptr[g.level + 1]++;
   for (int l = 0; l <= levels; ++l) P.level_q_ptr[l + 1] += P.level_q_ptr[l];

@@ -70,6 +70,15 @@ struct Plan {
   std::vector<QGroup> q;             // sorted by (level, creation order)
   std::vector<int32_t> wpos;         // WORLD template indices, pp per WORLD quotient group
   std::vector<int32_t> level_q_ptr;  // [levels+2]: quotient groups of level l = [ptr[l], ptr[l+1])
+  // per template slot (stage-major; stage s's slots start at stage_slot0[s]): the quotient group
+  // it joins (index into q), its template op, its member role in a P2P message (0 sender,
+  // 1 receiver) and whether it is its op's first slot
+  std::vector<int64_t> stage_slot0;  // [pp+1]
+  std::vector<int32_t> slot_q, slot_tidx;
+  std::vector<uint8_t> slot_role, slot_first;
+  // group-side build chunks: (quotient group, first local membership), 2048 memberships each
+  std::vector<int32_t> chunk_q;
+  std::vector<int64_t> chunk_m;
 };
 
 // Returns PRISM_OK or an error status with *err filled.
