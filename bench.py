@@ -286,13 +286,19 @@ def cpu_baseline(args, sample_dp: int = 8):
     cores = os.cpu_count() or 1
     S = max(1, min(args.scenarios, cores))
     oracle.build()
-    t0 = time.perf_counter()
-    r = oracle.replay(tm, S, amp_q16=args.amp, kind_mask=7, peaks=True, threads=S)
-    dt = time.perf_counter() - t0
-    return {"value": round(tm.n_nodes * S / dt, 1), "unit": "node-scenarios/s", "cores": min(S, cores),
+    # repeat the sample until ~10 s of CPU work (the contract's 10-30 s bounded sample)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.replay(tm, S, amp_q16=args.amp, kind_mask=7, peaks=True, threads=S)
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt >= args.cpu_seconds or reps >= 200:
+            break
+    return {"value": round(reps * tm.n_nodes * S / dt, 1), "unit": "node-scenarios/s", "cores": min(S, cores),
             "kind": "oracle", "seconds": round(dt, 2),
             "sample": f"{args.config} templates at dp={dp} ({tm.topo.world} of {t.world} ranks, "
-                      f"{tm.n_nodes} nodes), {S} scenarios, one thread each, expansion + DES + peak"}
+                      f"{tm.n_nodes} nodes), {S} scenarios, one thread each, expansion + DES + peak, "
+                      f"repeated {reps}x"}
 
 
 def run_reference(args):
@@ -342,6 +348,7 @@ def main():
     ap.add_argument("--scenarios", type=int, default=64)
     ap.add_argument("--amp", type=int, default=6554)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU work of the cpu_baseline sample")
     ap.add_argument("--algo", default="auto", choices=["auto", "levels", "cells"])
     args = ap.parse_args()
     args.config = args.config.upper()
