@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PRISM_ABI_VERSION 1
+#define PRISM_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define PRISM_API __attribute__((visibility("default")))
@@ -132,8 +132,10 @@ typedef struct {
   void *stream;           /* cudaStream_t all device work of this graph is issued on (NULL = legacy
                              default stream)                                                  */
   int32_t device;         /* CUDA device ordinal, -1 = current                                 */
-  int32_t n_shards;       /* 1 (multi-GPU sharding is reserved for a later ABI revision)        */
-  int32_t shard_index;    /* 0                                                                */
+  int32_t n_shards;       /* >= 1: the replay is sharded over n_shards GPUs (row e; see the
+                             "multi-GPU" section below); dp % n_shards == 0, n_shards <= 16   */
+  int32_t shard_index;    /* 0 .. n_shards-1: this shard replays the ranks with
+                             dp_i in [shard_index*dp/n_shards, (shard_index+1)*dp/n_shards)  */
   int32_t flags;          /* PRISM_BUILD_PROFILE: record CUDA events around every kernel group */
 } prism_build_opts;
 
@@ -204,6 +206,42 @@ PRISM_API prism_status prism_replay_async(prism_graph_t g, const prism_scenarios
  * the scenario and no replay is required. Writes world entries to peak_bytes_out (host). */
 PRISM_API prism_status prism_peak_memory(prism_graph_t g, int64_t *peak_bytes_out);
 PRISM_API prism_status prism_peak_memory_async(prism_graph_t g, int64_t *peak_bytes_dev_out);
+
+/* ---- multi-GPU (row e): rank sharding with a fused peer-memory exchange ---------------------
+ *
+ * The ranks are partitioned by DP block: shard i owns every rank whose dp coordinate lies in
+ * [i*dp/n, (i+1)*dp/n) (north_star: "Ranks are sharded across the 8 B200s of one box"). TP groups
+ * and P2P messages never cross a DP block, so only DP / EP / EDP / WORLD collectives span shards.
+ * Every shard holds the whole (replicated, O(N)) graph structure and replays only its own cells;
+ * the cell kernel pushes the ready time of a member of a cross-shard group straight into the
+ * exchange buffer of every shard holding a member of that group (NVLink peer stores and red.max
+ * atomics at system scope) and polls its local copy, so the segmented max over a group's members
+ * ("all participating nodes must reach the operation before any can proceed") is done by the
+ * replay kernel itself, tile by tile, instead of by a separate collective between launches. The
+ * iteration time is the max over shards of each shard's partial max, exchanged the same way by the
+ * final reduce kernel, so every shard returns the same T_k. Results are bit-identical to n = 1.
+ *
+ * Protocol (SPMD, every shard calls the same functions in the same order):
+ *   1. prism_build_graph with opts.n_shards = n, opts.shard_index = i on the shard's device;
+ *   2. prism_shard_prepare(g, S, handle): allocates the shard's exchange buffer for replays of
+ *      exactly S scenarios and writes its CUDA IPC handle (PRISM_SHARD_HANDLE_BYTES bytes);
+ *   3. all-gather the n handles (the Python binding uses torch.distributed), then
+ *      prism_shard_connect(g, handles[n]) opens the peers' buffers; or, when all shards live in
+ *      one process, prism_shard_connect_local(g, graphs[n]);
+ *   4. prism_replay / prism_replay_async with n == S on every shard. The replays of all shards
+ *      must run concurrently (one process per GPU, or independent streams of one process), since
+ *      a shard's kernel waits for its peers' ready times; a shard that never arrives is reported
+ *      by the device watchdog as PRISM_E_DEADLOCK after 10 s instead of hanging the GPU.
+ * prism_peak_memory returns all world peaks on every shard (the structure is replicated);
+ * prism_query_rank answers for the shard's own ranks (PRISM_E_INVALID_ARG names the owner
+ * otherwise). Replaying a sharded graph before connect, or with n != S, is PRISM_E_INVALID_ARG.
+ * The exchange buffer is released with the graph; peers must destroy their graphs only after the
+ * last replay of every shard has completed. */
+#define PRISM_SHARD_HANDLE_BYTES 64
+
+PRISM_API prism_status prism_shard_prepare(prism_graph_t g, int32_t n_scenarios, void *handle_out);
+PRISM_API prism_status prism_shard_connect(prism_graph_t g, const void *handles);
+PRISM_API prism_status prism_shard_connect_local(prism_graph_t g, const prism_graph_t *shards);
 
 /* Per-op start and finish times of one rank in one scenario of the last recorded replay, in
  * program order, plus the rank's coordinates (tp, pp, dp, ep, edp). If cap < the rank's op count

@@ -24,7 +24,9 @@ EXPORTED_SYMBOLS = [
     "prism_build_graph", "prism_replay", "prism_replay_async", "prism_peak_memory",
     "prism_peak_memory_async", "prism_query_rank", "prism_graph_stats", "prism_destroy_graph",
     "prism_debug_export", "prism_plan", "prism_last_timing", "prism_last_algo",
+    "prism_shard_prepare", "prism_shard_connect", "prism_shard_connect_local",
 ]
+SHARD_HANDLE_BYTES = 64
 
 STATUS_NAMES = {
     0: "PRISM_OK", 1: "PRISM_E_INVALID_ARG", 2: "PRISM_E_INVALID_SPEC", 3: "PRISM_E_GA_TOO_SMALL",
@@ -101,10 +103,14 @@ def lib():
         L.prism_plan.argtypes = [P, P, P]
         L.prism_last_timing.argtypes = [P, P]
         L.prism_last_algo.argtypes = [P, P]
+        L.prism_shard_prepare.argtypes = [P, ctypes.c_int32, P]
+        L.prism_shard_connect.argtypes = [P, P]
+        L.prism_shard_connect_local.argtypes = [P, P]
         for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
                      "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
                      "prism_graph_stats", "prism_debug_export", "prism_plan",
-                     "prism_last_timing", "prism_last_algo"):
+                     "prism_last_timing", "prism_last_algo", "prism_shard_prepare",
+                     "prism_shard_connect", "prism_shard_connect_local"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
     return _lib
@@ -172,11 +178,12 @@ class Graph:
     """An expanded execution graph resident on one GPU (prism_build_graph)."""
 
     def __init__(self, templates, *, stream: Optional[int] = None, device: int = -1,
-                 profile: bool = False):
+                 profile: bool = False, n_shards: int = 1, shard_index: int = 0):
         L = lib()
         self.topo = templates.topo
+        self.n_shards, self.shard_index = int(n_shards), int(shard_index)
         self._topo, self._tm, self._keep = _marshal(templates)
-        self._opts = _BuildOpts(stream or 0, device, 1, 0, 1 if profile else 0)
+        self._opts = _BuildOpts(stream or 0, device, self.n_shards, self.shard_index, 1 if profile else 0)
         h = ctypes.c_void_p()
         self._h = None
         _check(L.prism_build_graph(ctypes.byref(self._topo), ctypes.byref(self._tm),
@@ -262,6 +269,32 @@ class Graph:
         _check(lib().prism_query_rank(self._h, rank, scenario, _ptr(start), _ptr(fin), n.value, None, None))
         return start[: n.value], fin[: n.value], tuple(int(c) for c in coords)
 
+    # ---------------------------------------------------------------- row e: sharding
+    def shard_prepare(self, n_scenarios: int) -> bytes:
+        """Allocate this shard's exchange buffer for replays of n_scenarios; returns its IPC handle."""
+        h = ctypes.create_string_buffer(SHARD_HANDLE_BYTES)
+        _check(lib().prism_shard_prepare(self._h, int(n_scenarios), h))
+        return h.raw
+
+    def shard_connect(self, handles) -> None:
+        """Open the peers' exchange buffers (handles[m] = shard m's shard_prepare result)."""
+        if len(handles) != self.n_shards:
+            raise ValueError("need one handle per shard")
+        buf = ctypes.create_string_buffer(b"".join(bytes(h) for h in handles), SHARD_HANDLE_BYTES * self.n_shards)
+        _check(lib().prism_shard_connect(self._h, buf))
+
+    def shard_connect_local(self, graphs) -> None:
+        """Connect to the other shards of the same process (graphs[m] = shard m)."""
+        arr = (ctypes.c_void_p * len(graphs))(*[g._h.value for g in graphs])
+        _check(lib().prism_shard_connect_local(self._h, arr))
+
+    def shard_connect_dist(self, n_scenarios: int, group=None) -> None:
+        """SPMD helper: prepare, all-gather the handles over torch.distributed, connect."""
+        import torch.distributed as dist
+
+        mine = self.shard_prepare(n_scenarios)
+        self.shard_connect(gather_handles(mine, self.n_shards, self.shard_index, group))
+
     def export(self, name: str, scen_pad: int = 0) -> np.ndarray:
         """Copy one device CSR array to the host (tests)."""
         st = self.stats()
@@ -277,3 +310,38 @@ class Graph:
         out = np.zeros(max(1, count), dt)
         _check(lib().prism_debug_export(self._h, which, _ptr(out), out.nbytes))
         return out[:count]
+
+
+def gather_handles(mine: bytes, n_shards: int, shard_index: int, group=None):
+    """All-gather every shard's exchange-buffer handle over torch.distributed, ordered by shard."""
+    import torch.distributed as dist
+
+    if dist.get_world_size(group) != n_shards:
+        raise ValueError("the process group must hold exactly one process per shard")
+    allh = [None] * n_shards
+    dist.all_gather_object(allh, (shard_index, bytes(mine)), group=group)
+    idx = [i for i, _ in allh]
+    if sorted(idx) != list(range(n_shards)):
+        raise ValueError(f"shard indices {idx} are not a permutation of 0..{n_shards - 1}")
+    return [h for _, h in sorted(allh)]
+
+
+def shard_dp_block(dp: int, n_shards: int, shard_index: int):
+    """Row e host logic: the DP coordinates [d0, d1) replayed by one shard (DP-block sharding,
+    include/prism.h "multi-GPU"); dp must be a multiple of n_shards."""
+    if n_shards < 1 or dp % n_shards or not 0 <= shard_index < n_shards:
+        raise ValueError("dp must be a multiple of n_shards and shard_index in [0, n_shards)")
+    b = dp // n_shards
+    return b * shard_index, b * (shard_index + 1)
+
+
+def shard_ranks(topo, n_shards: int, shard_index: int):
+    """The global ranks a shard owns (every (tp, pp) coordinate of its DP block, reading Z1)."""
+    d0, d1 = shard_dp_block(topo.dp, n_shards, shard_index)
+    out = []
+    for dpi in range(d0, d1):
+        for s in range(topo.pp):
+            for t in range(topo.tp):
+                out.append(t + topo.tp * (s + topo.pp * dpi) if getattr(topo, "rank_order", 0) == 0
+                           else t + topo.tp * (dpi + topo.dp * s))
+    return sorted(out)

@@ -9,7 +9,9 @@
 #include <malloc.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -54,6 +56,15 @@ std::mutex g_alloc_mu;
 prism_alloc_fn g_alloc = nullptr;
 prism_free_fn g_free = nullptr;
 void *g_alloc_ctx = nullptr;
+
+// PRISM_TRACE=1: host timestamps of the launch sequence (diagnostics of blocking API calls).
+void trace(const char *what) {
+  static const bool on = std::getenv("PRISM_TRACE") != nullptr;
+  if (!on) return;
+  static const auto t0 = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[prism %9.3f ms] %s\n",
+               std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(), what);
+}
 
 prism_status fail(prism_status s, const std::string &m) {
   t_err = m;
@@ -116,6 +127,18 @@ struct prism_graph_s {
   uint32_t *h_status = nullptr;    // pinned copy of the status word
   int last_algo = 0;
   int recorded = 0;
+  // fin keeps rows [fin_node0, fin_node0 + fin_rows) (all nodes unless sharded)
+  int64_t fin_node0 = 0, fin_rows = 0;
+  // row e: sharding (n_shards > 1)
+  int n_shards = 1, shard = 0;
+  unsigned char *ex = nullptr;          // exchange buffer (cudaMalloc: IPC-exportable)
+  size_t ex_bytes = 0;
+  int32_t ex_S = 0, ex_Sp = 0;
+  ShardLink link{};
+  bool connected = false;
+  std::vector<void *> ipc_open;         // peer buffers opened with cudaIpcOpenMemHandle
+  int64_t *part = nullptr;              // [S] local partial iteration times
+  size_t part_bytes = 0;
   ScenParams last{};
   int32_t last_Sp = 0;
   // tile plan cache (depends on lanes)
@@ -182,9 +205,12 @@ struct prism_graph_s {
     dfree(rslot);
     dfree(acc);
     dfree(sync_words);
+    dfree(part);
     pin_give(h_status);
     for (auto &b : blocks) dfree(b.first);
     cudaStreamSynchronize(stream);
+    for (void *p : ipc_open) cudaIpcCloseMemHandle(p);
+    if (ex) cudaFree(ex);
     for (auto &e : ev)
       if (e) cudaEventDestroy(e);
   }
@@ -245,8 +271,12 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
                                const prism_build_opts *opts, prism_graph_t *out) {
   if (!topo || !tmpl || !out) return fail(PRISM_E_INVALID_ARG, "null argument");
   *out = nullptr;
-  if (opts && (opts->n_shards > 1 || opts->shard_index != 0))
-    return fail(PRISM_E_INVALID_ARG, "n_shards > 1 is not supported by this ABI revision");
+  const int n_shards = opts ? std::max(1, opts->n_shards) : 1;
+  const int shard = opts ? opts->shard_index : 0;
+  if (n_shards > kMaxShards || shard < 0 || shard >= n_shards)
+    return fail(PRISM_E_INVALID_ARG, "n_shards must be in [1, 16] and shard_index in [0, n_shards)");
+  if (topo->dp < 1 || topo->dp % n_shards != 0)
+    return fail(PRISM_E_INVALID_SPEC, "dp must be a multiple of n_shards (ranks are sharded by DP block)");
   Plan plan;
   std::string err;
   prism_status st = plan_graph(*topo, *tmpl, plan, err);
@@ -280,6 +310,23 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.G = P.G;
   d.M = P.M;
   d.nq = (int32_t)P.q.size();
+  d.n_shards = n_shards;
+  d.shard = shard;
+  d.d0 = P.topo.dp / n_shards * shard;
+  d.d1 = P.topo.dp / n_shards * (shard + 1);
+  G->n_shards = n_shards;
+  G->shard = shard;
+  {  // fin rows kept by this graph: its DP block is one contiguous node range under TP_PP_DP
+    int64_t per_replica = 0;
+    for (int s2 = 0; s2 < P.topo.pp; ++s2) per_replica += P.stage_len[s2] * P.topo.tp;
+    if (n_shards > 1 && P.topo.order == PRISM_ORDER_TP_PP_DP) {
+      G->fin_node0 = per_replica * d.d0;
+      G->fin_rows = per_replica * (d.d1 - d.d0);
+    } else {
+      G->fin_node0 = 0;
+      G->fin_rows = P.N;
+    }
+  }
   const size_t W = P.W, N = P.N, M = P.M, Gn = P.G, pp = P.topo.pp;
   const size_t nops = (size_t)tmpl->n_ops;
   // One device allocation for the whole graph (a Python allocator hook costs ~tens of us per
@@ -308,6 +355,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t o_guid = carve(Gn * 8), o_glvl = carve(Gn * 4), o_nms = carve(M * 4), o_ncls = carve(N);
   const size_t o_nsd = carve(N * 8), o_nuid = carve(N * 8), o_gxb = carve(Gn * 8), o_gli = carve(Gn * 4);
   const size_t o_hb = carve(M * 4), o_hm = carve(M * 4), o_hd = carve(M * 8), o_hu = carve(M * 8);
+  const size_t o_hs = n_shards > 1 ? carve(M * 4) : 0;
   const size_t total = off;
   unsigned char *base = G->take<unsigned char>(total);
   if (G->oom || !base) return fail(PRISM_E_OOM, "device allocation failed while building the graph");
@@ -357,6 +405,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.h_meta = (uint32_t *)at(o_hm);
   d.h_dur = (int64_t *)at(o_hd);
   d.h_uid = (uint64_t *)at(o_hu);
+  d.h_smask = n_shards > 1 ? (uint32_t *)at(o_hs) : nullptr;
   d.M_cross = P.M_cross;
   d.G_large = P.G_large;
   cudaStream_t s = G->stream;
@@ -387,6 +436,17 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   if (opts && (opts->flags & PRISM_BUILD_PROFILE)) {
     G->profile = true;
     for (auto &e : G->ev) CU(cudaEventCreate(&e));
+  }
+  {  // once per device and process: load every kernel a replay may launch (see replay.cu)
+    static std::mutex mu;
+    static std::vector<int> loaded;
+    std::lock_guard<std::mutex> lk(mu);
+    if (std::find(loaded.begin(), loaded.end(), G->device) == loaded.end()) {
+      CU(preload_replay_kernels());
+      CU(preload_cells());
+      CU(preload_peak_kernel());
+      loaded.push_back(G->device);
+    }
   }
   G->rec(0);
   CU(launch_expand(d, s));
@@ -452,6 +512,13 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   const int cell_sc = cells_chunk_scenarios();
   const int cell_chunks = (S + cell_sc - 1) / cell_sc;
   bool cells = false;
+  const bool sharded = G->n_shards > 1;
+  if (sharded) {
+    if (!G->connected) return fail(PRISM_E_INVALID_ARG, "sharded graph: call prism_shard_prepare and prism_shard_connect first");
+    if (S != G->ex_S) return fail(PRISM_E_INVALID_ARG, "sharded graph: the replay's scenario count must equal prism_shard_prepare's");
+    if (sc->algo == PRISM_ALGO_LEVELS) return fail(PRISM_E_INVALID_ARG, "sharded replays run on the cell kernel only");
+    if (!cells_fit(G->dg, cell_chunks)) return fail(PRISM_E_INVALID_ARG, "sharded replay: the shard's cells do not fit co-resident on the device");
+  }
   if (sc->algo != PRISM_ALGO_LEVELS) {
     cells = cells_fit(G->dg, cell_chunks);
     if (!cells && sc->algo == PRISM_ALGO_CELLS)
@@ -472,13 +539,50 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   p.mod = 2 * sc->amp_q16 + 1;
   p.mod_magic = ~0ULL / (uint64_t)p.mod + 1;
   G->recorded = 0;
+  trace("replay: begin");
   if (p.record) {
-    if (!G->ensure(G->fin, G->fin_bytes, (size_t)P.N * Sp * 8)) return fail(PRISM_E_OOM, "fin[N][S] allocation failed");
+    if (!G->ensure(G->fin, G->fin_bytes, (size_t)std::max<int64_t>(1, G->fin_rows) * Sp * 8))
+      return fail(PRISM_E_OOM, "fin[N][S] allocation failed");
   }
   if (!G->ensure(G->gfin, G->gfin_bytes, (size_t)P.G * Sp * 8)) return fail(PRISM_E_OOM, "gfin allocation failed");
   if (!G->ensure(G->rank_end, G->rank_end_bytes, (size_t)P.W * Sp * 8)) return fail(PRISM_E_OOM, "rank_end allocation failed");
   int64_t launches = 0;
-  if (cells) {
+  trace("replay: buffers ready");
+  if (sharded) {
+    // row e: ready slots / accumulators / counters live in the peer-mapped exchange buffer; they
+    // were reset at prepare, and the accumulators and counters are reset again right after the
+    // cell kernel, before this shard publishes its partial (the peers' next pushes wait for it)
+    const size_t nwords = 4;
+    if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
+    if (!G->h_status && !(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status word unavailable");
+    if (!G->ensure(G->part, G->part_bytes, (size_t)Sp * 8)) return fail(PRISM_E_OOM, "partial allocation failed");
+    CU(cudaMemsetAsync(G->sync_words, 0, nwords * 4, G->stream));
+    G->link.epoch += 1;
+    uint32_t *status = G->sync_words;
+    int64_t *rslot = (int64_t *)(G->ex + G->link.o_rslot);
+    int64_t *acc = (int64_t *)(G->ex + G->link.o_acc);
+    uint32_t *arrive = (uint32_t *)(G->ex + G->link.o_arrive);
+    G->rec(2);
+    trace("shard: launch cells");
+    const int per_launch = cells_chunks_per_launch(G->dg, nchunks);
+    for (int ch = 0; ch < nchunks; ch += per_launch) {
+      CU(launch_cells(G->dg, p, rslot, acc, arrive, status, G->parity, p.record ? G->fin : nullptr, G->fin_node0,
+                      G->gfin, G->rank_end, ch, std::min(per_launch, nchunks - ch), Sp, &G->link, G->stream));
+      ++launches;
+    }
+    trace("shard: cells launched");
+    G->parity ^= 1;
+    CU(cudaMemsetAsync(acc, 0, (size_t)P.G_large * Sp * 8, G->stream));
+    CU(cudaMemsetAsync(arrive, 0, (size_t)P.G_large * nchunks * 4, G->stream));
+    trace("shard: memsets");
+    G->rec(3);
+    G->rec(4);
+    CU(launch_shard_reduce(G->dg, G->link, S, Sp, G->rank_end, G->part, iter_dev, status, G->stream));
+    trace("shard: reduce launched");
+    CU(cudaMemcpyAsync(G->h_status, status, 4, cudaMemcpyDeviceToHost, G->stream));
+    trace("shard: status copy");
+    launches += 2;
+  } else if (cells) {
     const size_t rs_bytes = std::max<size_t>(16, (size_t)P.M_cross * Sp * 8);
     if (G->rslot_bytes < rs_bytes || G->rslot_Sp != Sp) G->rslot_dirty = true;
     G->rslot_Sp = Sp;
@@ -500,8 +604,8 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     const int per_launch = cells_chunks_per_launch(G->dg, nchunks);
     for (int ch = 0; ch < nchunks; ch += per_launch) {
       CU(launch_cells(G->dg, p, G->rslot, G->acc, G->sync_words, status, G->parity,
-                      p.record ? G->fin : nullptr, G->gfin, G->rank_end, ch, std::min(per_launch, nchunks - ch),
-                      Sp, G->stream));
+                      p.record ? G->fin : nullptr, 0, G->gfin, G->rank_end, ch,
+                      std::min(per_launch, nchunks - ch), Sp, nullptr, G->stream));
       ++launches;
     }
     G->parity ^= 1;
@@ -524,9 +628,12 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     G->rec(4);
     ++launches;
   }
-  CU(launch_reduce(G->dg.W, S, Sp, G->rank_end, iter_dev, G->stream));
+  if (!sharded) {
+    CU(launch_reduce(G->dg.W, S, Sp, G->rank_end, iter_dev, G->stream));
+    ++launches;
+  }
   G->rec(5);
-  G->launches = launches + 1;
+  G->launches = launches;
   G->last = p;
   G->last_Sp = Sp;
   G->recorded = p.record;
@@ -541,6 +648,7 @@ prism_status check_status(prism_graph_t G) {
     *G->h_status = 0;
     G->recorded = 0;
     G->rslot_dirty = true;
+    G->connected = false;  // a sharded graph must be re-prepared after an aborted replay
     return fail((prism_status)s, "replay aborted by the device watchdog (no progress for 10 s)");
   }
   return PRISM_OK;
@@ -612,6 +720,9 @@ prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, i
   }
   const int64_t n = P.stage_len[pp_i];
   if (n_ops_out) *n_ops_out = n;
+  if (G->n_shards > 1 && (dp_i < G->dg.d0 || dp_i >= G->dg.d1) && start_ns)
+    return fail(PRISM_E_INVALID_ARG, "rank " + std::to_string(rank) + " is replayed by shard " +
+                                         std::to_string(dp_i / (t.dp / G->n_shards)));
   if (!G->recorded) return fail(PRISM_E_NOT_REPLAYED, "no replay with record != 0 has run on this graph");
   if (scenario < 0 || scenario >= G->last.S) return fail(PRISM_E_INVALID_ARG, "scenario outside the last replay");
   if (cap < n || (n > 0 && (!start_ns || !finish_ns))) return fail(PRISM_E_INVALID_ARG, "output capacity too small");
@@ -619,11 +730,109 @@ prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, i
   CU(cudaSetDevice(G->device));
   const size_t bytes = (size_t)n * 16;
   if (!G->ensure(G->scratch, G->scratch_bytes, bytes)) return fail(PRISM_E_OOM, "scratch allocation failed");
-  CU(launch_query(G->dg, G->last, G->last_Sp, G->fin, G->gfin, rank, scenario, G->scratch, G->scratch + n, G->stream));
+  CU(launch_query(G->dg, G->last, G->last_Sp, G->fin, G->fin_node0, G->gfin, rank, scenario, G->scratch,
+                  G->scratch + n, G->stream));
   CU(cudaMemcpyAsync(start_ns, G->scratch, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaMemcpyAsync(finish_ns, G->scratch + n, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaStreamSynchronize(G->stream));
   return check_status(G);
+}
+
+// ---- row e: sharding ---------------------------------------------------------------------
+
+prism_status prism_shard_prepare(prism_graph_t G, int32_t n_scenarios, void *handle_out) {
+  if (!G || !handle_out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  if (G->n_shards < 2) return fail(PRISM_E_INVALID_ARG, "graph was not built with n_shards > 1");
+  if (n_scenarios < 1 || n_scenarios > (1 << 20)) return fail(PRISM_E_INVALID_ARG, "scenario count out of range");
+  CU(cudaSetDevice(G->device));
+  CU(cudaStreamSynchronize(G->stream));
+  const Plan &P = G->plan;
+  const int SCn = cells_chunk_scenarios();
+  const int nchunks = (n_scenarios + SCn - 1) / SCn;
+  const int64_t Sp = (int64_t)nchunks * SCn;
+  size_t off = 0;
+  auto carve = [&off](size_t bytes) {
+    off = (off + 255) & ~(size_t)255;
+    const size_t o = off;
+    off += std::max<size_t>(bytes, 8);
+    return o;
+  };
+  ShardLink L{};
+  L.n = G->n_shards;
+  L.self = G->shard;
+  L.o_rslot = (int64_t)carve((size_t)P.M_cross * Sp * 8);
+  L.o_acc = (int64_t)carve((size_t)P.G_large * Sp * 8);
+  L.o_arrive = (int64_t)carve((size_t)P.G_large * nchunks * 4);
+  L.o_part = (int64_t)carve((size_t)2 * G->n_shards * Sp * 8);
+  L.o_flag = (int64_t)carve((size_t)G->n_shards * 4);
+  const size_t bytes = off;
+  for (void *p : G->ipc_open) cudaIpcCloseMemHandle(p);
+  G->ipc_open.clear();
+  if (G->ex) cudaFree(G->ex);
+  G->ex = nullptr;
+  G->connected = false;
+  CU(cudaMalloc((void **)&G->ex, bytes));
+  G->ex_bytes = bytes;
+  CU(cudaMemset(G->ex, 0, bytes));
+  CU(cudaMemset(G->ex + L.o_rslot, 0xFF, (size_t)P.M_cross * Sp * 8));  // "not yet" under parity 0
+  CU(cudaDeviceSynchronize());
+  G->parity = 0;
+  G->ex_S = n_scenarios;
+  G->ex_Sp = (int32_t)Sp;
+  G->link = L;
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(cudaIpcMemHandle_t) <= PRISM_SHARD_HANDLE_BYTES, "IPC handle size");
+  std::memset(handle_out, 0, PRISM_SHARD_HANDLE_BYTES);
+  if (cudaIpcGetMemHandle(&h, G->ex) == cudaSuccess) std::memcpy(handle_out, &h, sizeof h);
+  else cudaGetLastError();  // IPC unavailable: only prism_shard_connect_local can be used
+  return PRISM_OK;
+}
+
+prism_status prism_shard_connect(prism_graph_t G, const void *handles) {
+  if (!G || !handles) return fail(PRISM_E_INVALID_ARG, "null argument");
+  if (!G->ex) return fail(PRISM_E_INVALID_ARG, "call prism_shard_prepare first");
+  CU(cudaSetDevice(G->device));
+  const unsigned char *hb = (const unsigned char *)handles;
+  for (int m = 0; m < G->n_shards; ++m) {
+    if (m == G->shard) {
+      G->link.base[m] = G->ex;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hb + (size_t)m * PRISM_SHARD_HANDLE_BYTES, sizeof h);
+    void *p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(PRISM_E_CUDA, "cudaIpcOpenMemHandle of shard " + std::to_string(m) + ": " + cudaGetErrorString(e));
+    }
+    G->ipc_open.push_back(p);
+    G->link.base[m] = (unsigned char *)p;
+  }
+  G->connected = true;
+  return PRISM_OK;
+}
+
+prism_status prism_shard_connect_local(prism_graph_t G, const prism_graph_t *shards) {
+  if (!G || !shards) return fail(PRISM_E_INVALID_ARG, "null argument");
+  if (!G->ex) return fail(PRISM_E_INVALID_ARG, "call prism_shard_prepare first");
+  CU(cudaSetDevice(G->device));
+  for (int m = 0; m < G->n_shards; ++m) {
+    const prism_graph_s *o = shards[m];
+    if (!o || !o->ex || o->n_shards != G->n_shards || o->shard != m || o->ex_bytes != G->ex_bytes)
+      return fail(PRISM_E_INVALID_ARG, "shard " + std::to_string(m) + " is not a prepared peer of this graph");
+    if (o->device != G->device) {
+      int can = 0;
+      CU(cudaDeviceCanAccessPeer(&can, G->device, o->device));
+      if (!can) return fail(PRISM_E_CUDA, "no peer access between devices");
+      cudaError_t e = cudaDeviceEnablePeerAccess(o->device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return fail(PRISM_E_CUDA, cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+    G->link.base[m] = o->ex;
+  }
+  G->connected = true;
+  return PRISM_OK;
 }
 
 prism_status prism_graph_stats(prism_graph_t G, int64_t out[10]) {
@@ -689,7 +898,7 @@ extern "C" PRISM_API prism_status prism_debug_export(prism_graph_t G, int32_t wh
     case 12: src = d.grp_dur; need = d.G * 8; break;
     case 13: src = d.grp_uid; need = d.G * 8; break;
     case 14: src = d.grp_level; need = d.G * 4; break;
-    case 15: src = G->fin; need = G->recorded ? d.N * (int64_t)G->last_Sp * 8 : 0; break;
+    case 15: src = G->fin; need = G->recorded ? G->fin_rows * (int64_t)G->last_Sp * 8 : 0; break;
     default: return fail(PRISM_E_INVALID_ARG, "unknown array");
   }
   if (bytes < need) return fail(PRISM_E_INVALID_ARG, "buffer too small: need " + std::to_string(need));

@@ -89,6 +89,30 @@ __device__ __forceinline__ uint64_t group_uid(const DevGraph &g, const QGroup &q
   return ((uint64_t)q.type << 56) | (group_gid(g, q, inst) << 24) | (uint64_t)q.occ;
 }
 
+// Row e: the shards holding a member of the group of a rank with DP coordinates (dpi, epi, edpi)
+// under the DP-block sharding (shard of dp_i = dp_i / (dp / n_shards)); TP groups and P2P
+// messages stay inside one DP coordinate, hence inside one shard.
+__device__ __forceinline__ uint32_t shard_mask(const DevGraph &g, int32_t type, int32_t dpi, int32_t epi,
+                                               int32_t edpi) {
+  const int32_t B = g.dp / g.n_shards;
+  switch (type) {
+    case PRISM_ROLE_DP:
+    case PRISM_ROLE_WORLD: return g.n_shards >= 32 ? 0xFFFFFFFFu : (1u << g.n_shards) - 1u;
+    case PRISM_ROLE_EP: {  // members dp = edpi*ep + j, j < ep: a contiguous block
+      const int32_t a = (edpi * g.ep) / B, b = (edpi * g.ep + g.ep - 1) / B;
+      uint32_t m = 0;
+      for (int32_t x = a; x <= b; ++x) m |= 1u << x;
+      return m;
+    }
+    case PRISM_ROLE_EDP: {  // members dp = j*ep + epi, j < dp/ep
+      uint32_t m = 0;
+      for (int32_t j = 0; j < g.dp / g.ep; ++j) m |= 1u << ((j * g.ep + epi) / B);
+      return m;
+    }
+    default: return 1u << (dpi / B);
+  }
+}
+
 // Rows a3 + a4 (node side): one block per rank (grid-stride), threads over the rank's template
 // ops, then over its template slots; every write is a coalesced run along the rank's nodes /
 // membership slots. A slot's group instance and member index follow in closed form from the
@@ -145,6 +169,7 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
       g.h_meta[h] = (uint32_t)min(q.size, 0xFFFF) | ((uint32_t)min(j, 0x7FFF) << 16) | (large ? 0x80000000u : 0u);
       g.h_dur[h] = q.dur;
       g.h_uid[h] = uid;
+      if (g.h_smask) g.h_smask[h] = shard_mask(g, q.type, dpi, epi, edpi);
       if (g.slot_first[u0 + u]) {  // the node's first group provides its replay record
         const int32_t n = rb + g.slot_tidx[u0 + u];
         g.node_cls[n] = q.type == PRISM_ROLE_TP ? 1 : 2;

@@ -12,6 +12,8 @@ namespace prism {
 // Plain device pointers; passed by value to kernels.
 struct DevGraph {
   int32_t W, pp, tp, dp, ep, order;
+  // row e: this shard replays the ranks with dp_i in [d0, d1) (d0 = 0, d1 = dp unsharded)
+  int32_t n_shards, shard, d0, d1;
   int64_t N, G, M;
   // rank tables
   int32_t *rank_ptr;        // [W+1] first node of each rank
@@ -46,6 +48,7 @@ struct DevGraph {
   uint32_t *h_meta;         // size (bits 0-15) | own member offset (16-30) | large (bit 31)
   int64_t *h_dur;           // the group's duration
   uint64_t *h_uid;          // the group's perturbation uid
+  uint32_t *h_smask;        // sharded graphs: bit m = shard m holds a member of the slot's group
   int64_t M_cross, G_large;
   // per-stage template tables (tiny; L2 resident)
   const prism_op *t_ops;    // concatenated templates
@@ -80,6 +83,17 @@ struct ScenParams {
   uint64_t mod_magic;  // Lemire fastmod constant for mod (x < 2^32)
 };
 
+// Row e: the peer-memory exchange of a sharded replay. Every shard's exchange buffer has the
+// same layout (same plan, same S), so one set of byte offsets addresses all of them.
+constexpr int kMaxShards = 16;
+struct ShardLink {
+  int32_t n, self;                 // shards, this shard (n = 0: unsharded)
+  uint32_t epoch;                  // replays since prepare, 1-based (flags of this replay)
+  int32_t pad;
+  unsigned char *base[kMaxShards];  // exchange buffer of every shard (peer-mapped), own included
+  int64_t o_rslot, o_acc, o_arrive, o_part, o_flag;  // byte offsets inside a buffer
+};
+
 // Tile of a level launch: `cnt` concrete groups of quotient group `q` starting at instance `i0`.
 struct Tile {
   int32_t q, i0, cnt, pad;
@@ -96,16 +110,25 @@ cudaError_t launch_tail(const DevGraph &g, const ScenParams &p, int64_t *fin, co
 cudaError_t launch_reduce(int32_t W, int32_t S, int32_t Sp, const int64_t *rank_end, int64_t *iter,
                           cudaStream_t st);
 cudaError_t launch_query(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin,
-                         const int64_t *gfin, int32_t rank, int32_t scen, int64_t *start_out,
+                         int64_t node0, const int64_t *gfin, int32_t rank, int32_t scen, int64_t *start_out,
                          int64_t *finish_out, cudaStream_t st);
 // replay_cells.cu (cell kernel); cudaErrorCooperativeLaunchTooLarge = does not fit, use levels
 bool cells_fit(const DevGraph &g, int nchunks);
 int cells_chunk_scenarios();
 int cells_chunks_per_launch(const DevGraph &g, int nchunks);
 cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc,
-                         uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t *gfin,
-                         int64_t *rank_end, int chunk0, int nchunks_launch, int Sp, cudaStream_t st);
+                         uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t node0,
+                         int64_t *gfin, int64_t *rank_end, int chunk0, int nchunks_launch, int Sp,
+                         const ShardLink *link, cudaStream_t st);
+// row e: iteration times of a sharded replay (local partial max, peer exchange, global max)
+cudaError_t launch_shard_reduce(const DevGraph &g, const ShardLink &link, int32_t S, int32_t Sp,
+                                const int64_t *rank_end, int64_t *part_local, int64_t *iter,
+                                uint32_t *status, cudaStream_t st);
 // memory.cu
 cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st);
+// eager loading of the kernels that can be launched behind a running (waiting) replay
+cudaError_t preload_replay_kernels();
+cudaError_t preload_cells();
+cudaError_t preload_peak_kernel();
 
 }  // namespace prism

@@ -190,11 +190,91 @@ __global__ void __launch_bounds__(256) reduce_iter_kernel(int32_t W, int32_t Sp,
   }
 }
 
+// Row e, sharded replay: partial iteration time of this shard's ranks (one block per scenario).
+__global__ void __launch_bounds__(256) shard_partial_kernel(DevGraph g, int32_t Sp,
+                                                            const int64_t *__restrict__ rank_end,
+                                                            int64_t *__restrict__ part) {
+  const int32_t k = blockIdx.x;
+  const int32_t nloc = g.tp * g.pp * (g.d1 - g.d0);
+  int64_t m = 0;
+  for (int32_t x = threadIdx.x; x < nloc; x += blockDim.x) {
+    const int32_t tpi = x % g.tp, s = (x / g.tp) % g.pp, dpi = g.d0 + x / (g.tp * g.pp);
+    const int32_t r = g.order == PRISM_ORDER_MEGATRON ? tpi + g.tp * (dpi + g.dp * s)
+                                                      : tpi + g.tp * (s + g.pp * dpi);
+    m = max(m, rank_end[(int64_t)r * Sp + k]);
+  }
+  for (int off = 16; off; off >>= 1) m = max(m, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off));
+  __shared__ int64_t wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = max(m, wm[w]);
+    part[k] = max(m, wm[0]);
+  }
+}
+
+// Row e: exchange of the partials over peer memory, then T_k = max over shards. One block: store
+// this shard's S partials into slot [epoch & 1][self] of every shard's buffer, fence (system
+// scope), publish flag[self] = epoch at every shard, wait for every shard's flag, reduce. The two
+// part buffers alternate by epoch: a shard can only reach replay e+2's exchange after every shard
+// finished reading replay e's.
+__global__ void __launch_bounds__(1024) shard_exchange_kernel(ShardLink L, int32_t S, int32_t Sp,
+                                                              const int64_t *__restrict__ part,
+                                                              int64_t *__restrict__ iter,
+                                                              uint32_t *status) {
+  const int64_t slab = (int64_t)L.n * Sp;  // int64 per epoch-parity buffer
+  const int64_t po = (int64_t)(L.epoch & 1) * slab + (int64_t)L.self * Sp;
+  for (int m = 0; m < L.n; ++m) {
+    int64_t *dst = (int64_t *)(L.base[m] + L.o_part) + po;
+    for (int32_t k = threadIdx.x; k < S; k += blockDim.x) dst[k] = part[k];
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x < L.n) {
+    uint32_t *f = (uint32_t *)(L.base[threadIdx.x] + L.o_flag) + L.self;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(L.epoch) : "memory");
+  }
+  __shared__ int aborted;
+  if (threadIdx.x == 0) aborted = 0;
+  __syncthreads();
+  if (threadIdx.x < L.n) {
+    const uint32_t *f = (const uint32_t *)(L.base[L.self] + L.o_flag) + threadIdx.x;
+    uint64_t t0 = 0;
+    uint32_t spins = 0;
+    while (true) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if ((int32_t)(v - L.epoch) >= 0) break;
+      __nanosleep(200);
+      if ((++spins & 255) == 0) {
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        if (now - t0 > 10ull * 1000 * 1000 * 1000) {
+          atomicCAS(status, 0u, (uint32_t)PRISM_E_DEADLOCK);
+          aborted = 1;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (aborted) return;
+  const int64_t *mine = (const int64_t *)(L.base[L.self] + L.o_part) + (int64_t)(L.epoch & 1) * slab;
+  for (int32_t k = threadIdx.x; k < S; k += blockDim.x) {
+    int64_t m = 0;
+    for (int s = 0; s < L.n; ++s) m = max(m, __ldcv(mine + (int64_t)s * Sp + k));
+    iter[k] = m;
+  }
+}
+
 // prism_query_rank: start/finish of one rank's ops in one scenario from fin/gfin.
-__global__ void query_kernel(DevGraph g, ScenParams p, int32_t Sp, const int64_t *__restrict__ fin,
-                             const int64_t *__restrict__ gfin, int32_t r, int32_t k,
+// fin rows start at node node0 (a sharded replay keeps only its own ranks' rows).
+__global__ void query_kernel(DevGraph g, ScenParams p, int32_t Sp, const int64_t *__restrict__ fin0,
+                             int64_t node0, const int64_t *__restrict__ gfin, int32_t r, int32_t k,
                              int64_t *__restrict__ start_out, int64_t *__restrict__ finish_out) {
   const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
+  const int64_t *fin = fin0 - node0 * Sp;
   for (int32_t i = rb + blockIdx.x * blockDim.x + threadIdx.x; i < re; i += gridDim.x * blockDim.x) {
     const int32_t h0 = g.node_gptr[i], h1 = g.node_gptr[i + 1];
     int64_t st;
@@ -280,10 +360,33 @@ cudaError_t launch_reduce(int32_t W, int32_t S, int32_t Sp, const int64_t *rank_
   return cudaGetLastError();
 }
 
+// With lazy module loading (CUDA 12 default) the first launch of a kernel loads it, and loading
+// waits for the work already running on the device; a sharded replay launches its reduce kernels
+// while its cell kernel is still waiting for peers, so every kernel that can be launched behind a
+// running replay is loaded up front (prism_build_graph calls this once per device).
+cudaError_t preload_replay_kernels() {
+  cudaFuncAttributes a;
+  const void *fns[] = {(const void *)reduce_iter_kernel, (const void *)shard_partial_kernel,
+                       (const void *)shard_exchange_kernel, (const void *)query_kernel};
+  for (const void *f : fns) {
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_shard_reduce(const DevGraph &g, const ShardLink &link, int32_t S, int32_t Sp,
+                                const int64_t *rank_end, int64_t *part_local, int64_t *iter,
+                                uint32_t *status, cudaStream_t st) {
+  shard_partial_kernel<<<S, 256, 0, st>>>(g, Sp, rank_end, part_local);
+  shard_exchange_kernel<<<1, 1024, 0, st>>>(link, S, Sp, part_local, iter, status);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_query(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin,
-                            const int64_t *gfin, int32_t rank, int32_t scen, int64_t *start_out,
-                            int64_t *finish_out, cudaStream_t st) {
-  query_kernel<<<64, 256, 0, st>>>(g, p, Sp, fin, gfin, rank, scen, start_out, finish_out);
+                         int64_t node0, const int64_t *gfin, int32_t rank, int32_t scen,
+                         int64_t *start_out, int64_t *finish_out, cudaStream_t st) {
+  query_kernel<<<64, 256, 0, st>>>(g, p, Sp, fin, node0, gfin, rank, scen, start_out, finish_out);
   return cudaGetLastError();
 }
 

@@ -77,6 +77,33 @@ __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gp
 __device__ __forceinline__ void red_max(int64_t *p, int64_t v) {
   asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"((uint64_t)v) : "memory");
 }
+// System-scope variants for the sharded replay (row e): the other party is a thread on a peer GPU
+// reaching this memory over NVLink, so the strong operations must be scoped .sys.
+__device__ __forceinline__ uint32_t ld_relaxed_sys(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int64_t ld_relaxed_sys64(const int64_t *p) {
+  int64_t v;
+  asm volatile("ld.relaxed.sys.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys64(int64_t *p, int64_t v) {
+  asm volatile("st.relaxed.sys.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_max_sys(int64_t *p, int64_t v) {
+  asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" ::"l"(p), "l"((uint64_t)v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+template <bool SH>
+__device__ __forceinline__ int64_t poll64(const int64_t *p) {
+  return SH ? ld_relaxed_sys64(p) : ld_relaxed64(p);
+}
+template <bool SH>
+__device__ __forceinline__ uint32_t poll32(const uint32_t *p) {
+  return SH ? ld_relaxed_sys(p) : ld_relaxed(p);
+}
 
 #ifdef PRISM_CELL_STATS
 __device__ unsigned long long g_dep_time[1 << 22];     // deposit globaltimer per ready slot (chunk 0)
@@ -101,7 +128,17 @@ struct CellArgs {
   int32_t Sp;          // scenario stride (all chunks x 32)
   int32_t chunk0;      // first chunk of this launch
   int32_t nchunks;     // chunks of the whole replay (arrival counters are per chunk)
+  ShardLink L;         // row e: peer exchange buffers (sharded kernels only)
 };
+
+// Row e: a cross-shard deposit goes to the copy of every shard holding a member of the group
+// (mask bit m = shard m, own shard included); the layout of all copies is identical.
+__device__ __forceinline__ int64_t *peer64(const ShardLink &L, int m, int64_t off_bytes) {
+  return (int64_t *)(L.base[m] + off_bytes);
+}
+__device__ __forceinline__ uint32_t *peer32(const ShardLink &L, int m, int64_t off_bytes) {
+  return (uint32_t *)(L.base[m] + off_bytes);
+}
 
 __device__ __forceinline__ int32_t rank_of(const DevGraph &g, int32_t tp_i, int32_t pp_i, int32_t dp_i) {
   return g.order == PRISM_ORDER_MEGATRON ? tp_i + g.tp * (dp_i + g.dp * pp_i)
@@ -131,6 +168,7 @@ struct CrossScratch {
   int32_t grp[MAX_TP * 4];
   int64_t dur[MAX_TP * 4];
   uint64_t uid[MAX_TP * 4];
+  uint32_t smask[MAX_TP * 4];  // row e: shards holding members of the pair's group
   int64_t vmax[MAX_TP * 4][32];  // per pair, per lane: max ready time over the group's members
 };
 
@@ -141,6 +179,7 @@ struct CrossScratch {
 // of the op. The op's C x ns sync records are staged in shared memory by one lane-parallel load;
 // deposit / arrive for every rank first, then poll (every poll of a pass is an independent load,
 // folded on the fly, the own slot is not read back), then finish = max over groups + dur'.
+template <bool SH>
 __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p, const CellArgs &a,
                                           int64_t *__restrict__ gfin, int64_t *ts, const int32_t *rsh, int C,
                                           int32_t hoff, int32_t ns, int32_t k, CrossScratch &cs) {
@@ -156,6 +195,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
     cs.dur[lane] = g.h_dur[h];
     cs.uid[lane] = g.h_uid[h];
     cs.grp[lane] = ns > 1 ? g.node_grp[h] : 0;
+    if (SH) cs.smask[lane] = g.h_smask[h];
   }
   __syncwarp();
   bool large_any = false;
@@ -170,18 +210,40 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
         __threadfence();
       }
 #endif
-      st_relaxed64(a.rslot + (int64_t)(base + (int32_t)((meta >> 16) & 0x7FFF)) * Sp + k, a.parity ? ~tr : tr);
+      const int64_t off = (int64_t)(base + (int32_t)((meta >> 16) & 0x7FFF)) * Sp + k;
+      const int64_t enc = a.parity ? ~tr : tr;
+      if (!SH) {
+        st_relaxed64(a.rslot + off, enc);
+      } else {
+        for (uint32_t m = cs.smask[x]; m; m &= m - 1)
+          st_relaxed_sys64(peer64(a.L, __ffs(m) - 1, a.L.o_rslot) + off, enc);
+      }
     } else {
       large_any = true;
-      red_max(a.acc + (int64_t)base * Sp + k, tr);
+      const int64_t off = (int64_t)base * Sp + k;
+      if (!SH) {
+        red_max(a.acc + off, tr);
+      } else {
+        for (uint32_t m = cs.smask[x]; m; m &= m - 1) red_max_sys(peer64(a.L, __ffs(m) - 1, a.L.o_acc) + off, tr);
+      }
     }
   }
   if (large_any) {
-    __threadfence();  // the accumulations are performed before the arrival is counted
+    // the accumulations are performed before the arrival is counted
+    if (SH) __threadfence_system();
+    else __threadfence();
     __syncwarp();
     if (lane == 0)
       for (int x = 0; x < np; ++x)
-        if (cs.meta[x] & 0x80000000u) atomicAdd(a.arrive + (int64_t)cs.base[x] * a.nchunks + ck, 1u);
+        if (cs.meta[x] & 0x80000000u) {
+          const int64_t ai = (int64_t)cs.base[x] * a.nchunks + ck;
+          if (!SH) {
+            atomicAdd(a.arrive + ai, 1u);
+          } else {
+            for (uint32_t m = cs.smask[x]; m; m &= m - 1)
+              atomicAdd_system(peer32(a.L, __ffs(m) - 1, a.L.o_arrive) + ai, 1u);
+          }
+        }
   }
   uint32_t spins = 0;
   uint64_t tw = 0;
@@ -198,20 +260,23 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
         const int64_t *src = a.rslot + (int64_t)base * Sp + k;
         for (int32_t mm = 0; mm < size; ++mm, src += Sp) {
           if (mm == own) continue;
-          const int64_t v = ld_relaxed64(src);
+          const int64_t v = poll64<SH>(src);
           ok &= a.parity ? v < 0 : v >= 0;
           m = max(m, a.parity ? ~v : v);
         }
         cs.vmax[x][lane] = m;
       } else {
-        ok &= ld_relaxed(a.arrive + (int64_t)base * a.nchunks + ck) >= (uint32_t)size;
+        ok &= poll32<SH>(a.arrive + (int64_t)base * a.nchunks + ck) >= (uint32_t)size;
       }
     }
     if (__all_sync(0xffffffffu, ok)) break;
     ++spins;
     if (spins > 6 && wait_tick(a, spins, tw)) return false;
   }
-  if (large_any) fence_acq_rel();
+  if (large_any) {
+    if (SH) fence_acq_rel_sys();
+    else fence_acq_rel();
+  }
   for (int r = 0; r < C; ++r) {
     int64_t fr = 0;
     for (int32_t q = 0; q < ns; ++q) {
@@ -231,7 +296,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
   return true;
 }
 
-template <int C>
+template <int C, bool SH>
 __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
                                                          int64_t *__restrict__ fin,
                                                          int64_t *__restrict__ gfin,
@@ -239,9 +304,9 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   const int lane = threadIdx.x & 31;
   const int32_t unit = blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (unit >= a.n_units) return;
-  const int32_t cells = g.pp * g.dp;
+  const int32_t cells = g.pp * (g.d1 - g.d0);  // this shard's cells (all of them unsharded)
   const int32_t cell = unit % cells, chunk = a.chunk0 + unit / cells;
-  const int32_t s = cell % g.pp, dpi = cell / g.pp;
+  const int32_t s = cell % g.pp, dpi = g.d0 + cell / g.pp;
   const int32_t Sp = a.Sp;
   const int32_t k = chunk * SC + lane;
   __shared__ int64_t ts[MAX_TP * 32];  // chain state of the cross-cell path (rolled over ranks)
@@ -322,7 +387,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
 #pragma unroll
         for (int r = 0; r < C; ++r) ts[r * 32 + lane] = t[r];
         __syncwarp();
-        const bool ok = cross_all(g, p, a, gfin, ts, rsh, C, h0 - rs[0], ns, k, cs);
+        const bool ok = cross_all<SH>(g, p, a, gfin, ts, rsh, C, h0 - rs[0], ns, k, cs);
         __syncwarp();
         if (!ok) return;
 #pragma unroll
@@ -353,23 +418,37 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
 
 typedef void (*cell_fn)(DevGraph, ScenParams, CellArgs, int64_t *, int64_t *, int64_t *);
 
-cell_fn cell_kernel_for(int tp) {
+template <bool SH>
+cell_fn cell_kernel_t(int tp) {
   switch (tp) {
-    case 1: return cell_kernel<1>;
-    case 2: return cell_kernel<2>;
-    case 3: return cell_kernel<3>;
-    case 4: return cell_kernel<4>;
-    case 5: return cell_kernel<5>;
-    case 6: return cell_kernel<6>;
-    case 7: return cell_kernel<7>;
-    case 8: return cell_kernel<8>;
+    case 1: return cell_kernel<1, SH>;
+    case 2: return cell_kernel<2, SH>;
+    case 3: return cell_kernel<3, SH>;
+    case 4: return cell_kernel<4, SH>;
+    case 5: return cell_kernel<5, SH>;
+    case 6: return cell_kernel<6, SH>;
+    case 7: return cell_kernel<7, SH>;
+    case 8: return cell_kernel<8, SH>;
     default: return nullptr;
   }
+}
+cell_fn cell_kernel_for(const DevGraph &g) {
+  return g.n_shards > 1 ? cell_kernel_t<true>(g.tp) : cell_kernel_t<false>(g.tp);
+}
+
+cudaError_t preload_cell_kernels() {
+  cudaFuncAttributes a;
+  for (int tp = 1; tp <= MAX_TP; ++tp) {
+    cudaError_t e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<false>(tp));
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<true>(tp));
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 // CTAs needed for `units` warps, if they can all be co-resident.
 bool cell_fit_units(const DevGraph &g, int64_t units, int *ctas) {
-  cell_fn fn = cell_kernel_for(g.tp);
+  cell_fn fn = cell_kernel_for(g);
   if (!fn) return false;
   int dev = 0, sms = 0, coop = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
@@ -387,34 +466,40 @@ bool cell_fit_units(const DevGraph &g, int64_t units, int *ctas) {
 
 }  // namespace
 
+cudaError_t preload_cells() { return preload_cell_kernels(); }
+
 // Chunks of 32 scenarios per unit; every chunk of a replay runs in one launch when they all fit,
 // else the caller launches one chunk at a time (chunk groups of 1).
 bool cells_fit(const DevGraph &g, int nchunks) {
-  return cell_fit_units(g, (int64_t)g.pp * g.dp, nullptr) && nchunks >= 1;
+  return cell_fit_units(g, (int64_t)g.pp * (g.d1 - g.d0), nullptr) && nchunks >= 1;
 }
 
 int cells_chunk_scenarios() { return SC; }
 
 int cells_chunks_per_launch(const DevGraph &g, int nchunks) {
   for (int c = nchunks; c > 1; --c)
-    if (nchunks % c == 0 && cell_fit_units(g, (int64_t)g.pp * g.dp * c, nullptr)) return c;
+    if (nchunks % c == 0 && cell_fit_units(g, (int64_t)g.pp * (g.d1 - g.d0) * c, nullptr)) return c;
   return 1;
 }
 
 cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc,
-                         uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t *gfin,
-                         int64_t *rank_end, int chunk0, int nchunks_launch, int Sp, cudaStream_t st) {
-  const int64_t units = (int64_t)g.pp * g.dp * nchunks_launch;
+                         uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t node0,
+                         int64_t *gfin, int64_t *rank_end, int chunk0, int nchunks_launch, int Sp,
+                         const ShardLink *link, cudaStream_t st) {
+  const int64_t units = (int64_t)g.pp * (g.d1 - g.d0) * nchunks_launch;
   int ctas = 0;
   if (!cell_fit_units(g, units, &ctas)) return cudaErrorCooperativeLaunchTooLarge;
   // the launch covers chunks [chunk0, chunk0 + nchunks_launch) of the replay's Sp / 32 chunks
   CellArgs a{rslot, acc, arrive, status, 10ull * 1000 * 1000 * 1000, parity, (int32_t)units, Sp, chunk0,
-             Sp / SC};
+             Sp / SC, ShardLink{}};
+  if (link) a.L = *link;
   DevGraph gg = g;
   ScenParams pp = p;
-  void *args[] = {&gg, &pp, &a, &fin, &gfin, &rank_end};
-  return cudaLaunchCooperativeKernel((const void *)cell_kernel_for(g.tp), dim3(ctas), dim3(WARPS * 32),
-                                     args, 0, st);
+  // fin keeps only rows [node0, ...) (a sharded replay stores its own ranks' rows): rebase the
+  // pointer so the kernel indexes it by global node id
+  int64_t *fin_g = fin ? (int64_t *)((uintptr_t)fin - (uintptr_t)(node0 * Sp * 8)) : nullptr;
+  void *args[] = {&gg, &pp, &a, &fin_g, &gfin, &rank_end};
+  return cudaLaunchCooperativeKernel((const void *)cell_kernel_for(g), dim3(ctas), dim3(WARPS * 32), args, 0, st);
 }
 
 // Debug statistics of the last cell-kernel launch (PRISM_CELL_STATS builds only).

@@ -1,0 +1,121 @@
+"""Row e on the GPU: the rank-sharded replay (DP blocks, peer-memory exchange inside the cell
+kernel) against the CPU oracle, bit-exact. All shards of a test live in one process on cuda:0,
+each with its own stream, connected with prism_shard_connect_local; the multi-process path differs
+only in how the exchange buffers are mapped (CUDA IPC, prism_shard_connect)."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads as w
+
+pytestmark = pytest.mark.gpu
+NPROC = os.cpu_count() or 1
+
+
+@pytest.fixture(scope="module")
+def prism():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2605_15617_b200 as P
+
+    P.build_library()
+    P.use_torch_allocator()
+    return P
+
+
+def _sharded(P, tm, n, S):
+    import torch
+
+    streams = [torch.cuda.Stream() for _ in range(n)]
+    gs = [P.Graph(tm, stream=streams[i].cuda_stream, n_shards=n, shard_index=i) for i in range(n)]
+    for g in gs:
+        g.shard_prepare(S)
+    for g in gs:
+        g.shard_connect_local(gs)
+    return gs, streams
+
+
+def _replay_all(gs, S, **kw):
+    import torch
+
+    outs = [torch.full((S,), -1, dtype=torch.int64, device="cuda") for _ in gs]
+    for g, o in zip(gs, outs):
+        g.replay_async(o.data_ptr(), S, **kw)
+    torch.cuda.synchronize()
+    return [o.cpu().numpy() for o in outs]
+
+
+def _check(P, tm, n, S, reps=2, times=True):
+    gs, _ = _sharded(P, tm, n, S)
+    ref = oracle.replay(tm, S, amp_q16=6554, kind_mask=7, times=times, threads=min(NPROC, S))
+    for rep in range(reps):  # repeated replays: exchange reset, parity flip, epoch flags
+        outs = _replay_all(gs, S, amp_q16=6554, kind_mask=7)
+        for i, o in enumerate(outs):
+            assert np.array_equal(o, ref["iter"]), (rep, i, o[:4], ref["iter"][:4])
+    for i, g in enumerate(gs):
+        assert np.array_equal(g.peak_memory(), ref["peak"][0])
+        assert g.last_algo() == "cells"
+    if times:
+        rng = np.random.default_rng(n)
+        W = tm.topo.world
+        rp = P.Graph(tm).export("rank_ptr")
+        for i, g in enumerate(gs):
+            own = P.shard_ranks(tm.topo, n, i)
+            for r in rng.choice(own, min(8, len(own)), replace=False):
+                for k in (0, S - 1):
+                    st, fi, c = g.query_rank(int(r), k)
+                    a, b = rp[r], rp[r + 1]
+                    assert np.array_equal(fi, ref["finish"][k, a:b]) and np.array_equal(st, ref["start"][k, a:b])
+            other = [r for r in range(W) if r not in set(own)]
+            if other:
+                with pytest.raises(P.PrismError):
+                    g.query_rank(int(other[0]), 0)
+    for g in gs:
+        g.close()
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C5"])
+def test_sharded_scaled_dense(prism, name):
+    _check(prism, w.scaled(name), 2, 64)
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_sharded_moe_ep_edp(prism, n):
+    """C4-shaped MoE (dp 8, ep 4): EP all-to-alls and EDP groups span shards for n >= 2."""
+    _check(prism, w.scaled("C4"), n, 33)
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_sharded_dense_dp4(prism, n):
+    tm = w.build_training_templates(w.TrainSetup(w.LLAMA3_70B, w.Topology(8, 4, 4), 8, [20] * 4), "dp4")
+    _check(prism, tm, n, 64)
+
+
+@pytest.mark.parametrize("seed", range(200, 230))
+def test_sharded_random(prism, seed):
+    tm = w.random_templates(seed, max_world=32, max_ops=40)
+    if tm.topo.dp % 2 or tm.topo.tp > 8:
+        pytest.skip("needs an even dp and tp <= 8")
+    _check(prism, tm, 2, [1, 5, 32, 40][seed % 4], times=True)
+
+
+def test_sharded_megatron_order(prism):
+    tm = w.scaled("C2")
+    tm = w.Templates(w.Topology(8, 8, 2, 1, 1, 1), tm.ops, tm.tmpl_ptr, tm.static_mem)
+    _check(prism, tm, 2, 32)
+
+
+def test_shard_errors(prism):
+    tm = w.scaled("C2")
+    with pytest.raises(prism.PrismError) as e:
+        prism.Graph(tm, n_shards=3, shard_index=0)  # dp = 2
+    assert e.value.name == "PRISM_E_INVALID_SPEC"
+    g = prism.Graph(tm, n_shards=2, shard_index=0)
+    with pytest.raises(prism.PrismError) as e:
+        g.replay(4)
+    assert e.value.name == "PRISM_E_INVALID_ARG"  # not connected
+    g.close()
