@@ -9,9 +9,11 @@ perturbed what-if scenarios (a6-a8) and prism_peak_memory (a9), all through the 
   python bench.py --impl reference ...   (the CPU oracle on a bounded sample of the workload)
 
 Prints ONE JSON line on rank 0. Metric: replayed graph ops/s = nodes x scenarios / step time
-(plus emulated iterations/s = scenarios / step time in "extra"). Multi-GPU: one process per GPU
-(torchrun); every rank replays its own replica of the workload (row e sharding is not used by
-this bench yet: "replicas", weak scaling); time = max over ranks of the device-timed region.
+(plus emulated iterations/s = scenarios / step time in "extra"). Multi-GPU (row e): one process
+per GPU (torchrun); by default the 8192 ranks are sharded over the N GPUs by DP block with the
+cross-shard segmented max fused into the replay kernel over NVLink peer memory, and the scenario
+batch grows with N (N x 64: weak scaling, per-GPU node-scenarios fixed); `--shard replicas` runs N
+independent replicas instead. Time = max over ranks of the device-timed region.
 """
 from __future__ import annotations
 
@@ -122,28 +124,38 @@ def run_prism(args):
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
     tm = w.config(args.config)
-    S = args.scenarios
+    sharded = ws > 1 and args.shard == "ranks"
+    S = args.scenarios * (ws if sharded else 1)  # sharded: N x 64 scenarios over N GPUs (weak)
     kw = dict(amp_q16=args.amp, kind_mask=7, seed=0x5EED, algo=args.algo)
     iter_dev = torch.zeros(S, dtype=torch.int64, device="cuda")
     peak_dev = torch.zeros(tm.topo.world, dtype=torch.int64, device="cuda")
+    comm = [None]  # sharded: the graph currently holding the connected exchange buffer
+
+    def new_graph(profile=False):
+        if not sharded:
+            return prism.Graph(tm, stream=sh, profile=profile)
+        g = prism.Graph(tm, stream=sh, profile=profile, n_shards=ws, shard_index=rank)
+        if comm[0] is None:
+            g.shard_connect_dist(S)  # once: exchange-buffer IPC handles over torch.distributed
+        else:
+            g.shard_adopt(comm[0])   # a rebuilt graph keeps the connected buffer
+        comm[0] = g
+        return g
 
     graphs = []
 
     def step():
-        # the previous step's graph is released first (its buffers return to the caching
-        # allocator and are reused by this build); the last one survives the timed region
+        # build first (a sharded build adopts the previous graph's exchange buffer), then release
+        # the previous step's graph; the last one survives the timed region
+        g = new_graph()
         while graphs:
             graphs.pop().close()
-        g = prism.Graph(tm, stream=sh)
         g.replay_async(iter_dev.data_ptr(), S, record=True, **kw)
         g.peak_memory_async(peak_dev.data_ptr())
         graphs.append(g)
 
     for _ in range(args.warmup):
         step()
-        for g in graphs:
-            g.close()
-        graphs.clear()
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
@@ -160,19 +172,19 @@ def run_prism(args):
     iters = iter_dev.cpu().numpy().copy()
     st = graphs[0].stats()
     launches_per_step = st["replay_launches"] + 3 + 1  # expand: rank tables, nodes, groups; peak
-    for g in graphs:
-        g.close()
-    graphs.clear()
     if ws > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    units = st["nodes"] * S
-    value = ws * units / (ms_step / 1e3)
+    units = st["nodes"] * S * (1 if sharded else ws)  # node-scenarios of the whole job per step
+    value = units / (ms_step / 1e3)
 
     # ---- per-kernel-group device times (profiled graph, CUDA events on the launching stream)
-    gp = prism.Graph(tm, stream=sh, profile=True)
+    gp = new_graph(profile=True)
+    for g in graphs:
+        g.close()
+    graphs.clear()
     prof = {"expand": [], "levels": [], "tail": [], "reduce": [], "peak": []}
     for i in range(3):
         gp.replay_async(iter_dev.data_ptr(), S, record=True, **kw)
@@ -182,9 +194,10 @@ def run_prism(args):
             prof[k].append(t[k])
     prof["expand"].append(gp.last_timing()["expand"])
     schedule = gp.last_algo()
-    gp.close()
     med = {k: sorted(v)[len(v) // 2] for k, v in prof.items()}
     ab = algorithmic_bytes(st, S)
+    if sharded:  # this GPU replays 1/ws of the ranks: its share of the algorithmic bytes
+        ab = {k: v // ws for k, v in ab.items()}
     replay_ms = med["levels"] + med["tail"] + med["reduce"]
     peak_bw, peak_src = _peaks()
     achieved = ab["replay"] / (replay_ms / 1e3) / 1e9
@@ -197,11 +210,14 @@ def run_prism(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         reps = max(1, min(args.steps, 3))
+        prev = gp
         for _ in range(reps):
-            g = prism.Graph(tm, stream=sh)
+            g = new_graph()
+            prev.close()
             it_host = g.replay(S, record=True, **kw)
             pk_host = g.peak_memory()
-            g.close()
+            prev = g
+        prev.close()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / reps
         assert (it_host == iters).all()
     if ws > 1:
@@ -239,11 +255,13 @@ def run_prism(args):
             "ranks": tm.topo.world, "nodes": st["nodes"], "sync_groups": st["groups"],
             "memberships": st["memberships"], "levels": st["levels"], "scenarios": S,
             "amp_q16": args.amp, "record_times": True, "schedule": schedule,
-            "parallelism": f"replicas{ws}" if ws > 1 else "single-gpu",
+            "parallelism": ("single-gpu" if ws == 1 else
+                            f"ranks sharded over {ws} GPUs by DP block, exchange fused in the replay kernel "
+                            f"(NVLink peer memory)" if sharded else f"replicas{ws}"),
             "l2": "working set (fin[N][S] = %.1f GB) > 126 MB L2; no flush needed" % (st["nodes"] * S * 8 / 1e9),
         },
         "extra": {
-            "emulated_iterations_per_s": round(ws * S / (ms_step / 1e3), 2),
+            "emulated_iterations_per_s": round(S * (1 if sharded else ws) / (ms_step / 1e3), 2),
             "iteration_time_ns_scenario0": int(iters[0]),
             "device_ms": {k: round(v, 4) for k, v in med.items()},
         },
@@ -260,7 +278,7 @@ def run_prism(args):
             "alg_bytes_per_call": ab["replay"],
             "traffic": traffic,
         },
-        "e2e": {"value": round(ws * units / (e2e_ms / 1e3), 1), "unit": "node-scenarios/s",
+        "e2e": {"value": round(units / (e2e_ms / 1e3), 1), "unit": "node-scenarios/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
@@ -350,6 +368,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU work of the cpu_baseline sample")
     ap.add_argument("--algo", default="auto", choices=["auto", "levels", "cells"])
+    ap.add_argument("--shard", default="ranks", choices=["ranks", "replicas"],
+                    help="N>1: shard the ranks over the GPUs (row e) or run independent replicas")
     args = ap.parse_args()
     args.config = args.config.upper()
     if args.warmup < 3 and args.impl == "prism":

@@ -242,6 +242,11 @@ PRISM_API prism_status prism_peak_memory_async(prism_graph_t g, int64_t *peak_by
 PRISM_API prism_status prism_shard_prepare(prism_graph_t g, int32_t n_scenarios, void *handle_out);
 PRISM_API prism_status prism_shard_connect(prism_graph_t g, const void *handles);
 PRISM_API prism_status prism_shard_connect_local(prism_graph_t g, const prism_graph_t *shards);
+/* Move the connected exchange buffer (and the peers' mapping of it) of `from` to a newly built
+ * graph g of the same plan and shard (a rebuilt graph keeps its communicator; SPMD: every shard
+ * adopts at the same point of its call sequence). Waits for `from`'s stream unless both graphs
+ * use the same stream (then stream order suffices); `from` is left unconnected. PRISM_E_INVALID_ARG if the plans' exchange layouts or the shards differ. */
+PRISM_API prism_status prism_shard_adopt(prism_graph_t g, prism_graph_t from);
 
 /* Per-op start and finish times of one rank in one scenario of the last recorded replay, in
  * program order, plus the rank's coordinates (tp, pp, dp, ep, edp). If cap < the rank's op count

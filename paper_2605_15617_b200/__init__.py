@@ -24,7 +24,7 @@ EXPORTED_SYMBOLS = [
     "prism_build_graph", "prism_replay", "prism_replay_async", "prism_peak_memory",
     "prism_peak_memory_async", "prism_query_rank", "prism_graph_stats", "prism_destroy_graph",
     "prism_debug_export", "prism_plan", "prism_last_timing", "prism_last_algo",
-    "prism_shard_prepare", "prism_shard_connect", "prism_shard_connect_local",
+    "prism_shard_prepare", "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
 ]
 SHARD_HANDLE_BYTES = 64
 
@@ -106,11 +106,12 @@ def lib():
         L.prism_shard_prepare.argtypes = [P, ctypes.c_int32, P]
         L.prism_shard_connect.argtypes = [P, P]
         L.prism_shard_connect_local.argtypes = [P, P]
+        L.prism_shard_adopt.argtypes = [P, P]
         for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
                      "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
                      "prism_graph_stats", "prism_debug_export", "prism_plan",
                      "prism_last_timing", "prism_last_algo", "prism_shard_prepare",
-                     "prism_shard_connect", "prism_shard_connect_local"):
+                     "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
     return _lib
@@ -287,6 +288,10 @@ class Graph:
         """Connect to the other shards of the same process (graphs[m] = shard m)."""
         arr = (ctypes.c_void_p * len(graphs))(*[g._h.value for g in graphs])
         _check(lib().prism_shard_connect_local(self._h, arr))
+
+    def shard_adopt(self, other: "Graph") -> None:
+        """Take over the connected exchange buffer of `other` (same plan and shard)."""
+        _check(lib().prism_shard_adopt(self._h, other._h))
 
     def shard_connect_dist(self, n_scenarios: int, group=None) -> None:
         """SPMD helper: prepare, all-gather the handles over torch.distributed, connect."""

@@ -835,6 +835,31 @@ prism_status prism_shard_connect_local(prism_graph_t G, const prism_graph_t *sha
   return PRISM_OK;
 }
 
+prism_status prism_shard_adopt(prism_graph_t G, prism_graph_t from) {
+  if (!G || !from) return fail(PRISM_E_INVALID_ARG, "null argument");
+  if (G == from) return PRISM_OK;
+  const Plan &a = G->plan, &b = from->plan;
+  if (!from->ex || !from->connected || G->n_shards != from->n_shards || G->shard != from->shard ||
+      G->device != from->device || a.M_cross != b.M_cross || a.G_large != b.G_large || a.W != b.W)
+    return fail(PRISM_E_INVALID_ARG, "adopt: `from` must be a connected shard graph of the same plan and shard");
+  CU(cudaSetDevice(G->device));
+  if (from->stream != G->stream) CU(cudaStreamSynchronize(from->stream));  // same stream: ordered
+  for (void *p : G->ipc_open) cudaIpcCloseMemHandle(p);
+  if (G->ex) cudaFree(G->ex);
+  G->ex = from->ex;
+  G->ex_bytes = from->ex_bytes;
+  G->ex_S = from->ex_S;
+  G->ex_Sp = from->ex_Sp;
+  G->link = from->link;
+  G->parity = from->parity;
+  G->ipc_open = std::move(from->ipc_open);
+  G->connected = true;
+  from->ex = nullptr;
+  from->ipc_open.clear();
+  from->connected = false;
+  return PRISM_OK;
+}
+
 prism_status prism_graph_stats(prism_graph_t G, int64_t out[10]) {
   if (!G || !out) return fail(PRISM_E_INVALID_ARG, "null argument");
   const Plan &P = G->plan;

@@ -119,3 +119,25 @@ def test_shard_errors(prism):
         g.replay(4)
     assert e.value.name == "PRISM_E_INVALID_ARG"  # not connected
     g.close()
+
+
+def test_multiprocess_ipc(prism, tmp_path):
+    """The multi-process path: 2 processes (torchrun, gloo for the handle all-gather) share cuda:0,
+    map each other's exchange buffers with CUDA IPC (prism_shard_connect) and replay 3 times."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SHARD_DEVICE="0")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29517",
+                        os.path.join(root, "tests", "shard_mp_worker.py"), "C2"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l.split() for l in r.stdout.splitlines() if " rep " in l]
+    ref = [l for l in r.stdout.splitlines() if l.startswith("ref")][0]
+    want = ref[len("ref "):]
+    assert len(lines) == 6
+    for l in r.stdout.splitlines():
+        if " rep " in l:
+            assert " ok " in l and want in l, l
