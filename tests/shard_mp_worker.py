@@ -1,5 +1,5 @@
 """Multi-process sharded replay on ONE GPU (2 processes, CUDA IPC exchange) — experiment of the
-prism_shard_connect path; run: torchrun --nproc-per-node 2 tools/shard_mp.py [config]."""
+prism_shard_connect path; run by tests/test_gpu_shards.py::test_multiprocess_ipc under torchrun."""
 import os, sys, time
 import numpy as np
 import torch
