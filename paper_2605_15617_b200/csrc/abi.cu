@@ -346,6 +346,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t o_q = carve(P.q.size() * sizeof(QGroup)), o_wpos = carve(P.wpos.size() * 4);
   const size_t o_ss0 = carve(P.stage_slot0.size() * 8), o_slq = carve(nslot * 4), o_sltd = carve(nslot * 4);
   const size_t o_slr = carve(nslot), o_slf = carve(nslot), o_chq = carve(nch * 4), o_chm = carve(nch * 8);
+  const size_t o_tcls = carve(nops), o_xptr = carve((pp + 1) * 4), o_xops = carve(P.x_ops.size() * sizeof(XOp));
   const size_t table_bytes = off;
   // graph arrays (written by the expand kernels)
   const size_t o_rp = carve((W + 1) * 4), o_rs = carve((W + 1) * 4), o_rst = carve(W * 4);
@@ -378,6 +379,9 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.chunk_q = (const int32_t *)at(o_chq);
   d.chunk_m = (const int64_t *)at(o_chm);
   d.nchunk = (int32_t)nch;
+  d.t_cls = (const uint8_t *)at(o_tcls);
+  d.x_ptr = (const int32_t *)at(o_xptr);
+  d.x_ops = (const XOp *)at(o_xops);
   d.rank_ptr = (int32_t *)at(o_rp);
   d.rank_slot = (int32_t *)at(o_rs);
   d.rank_stage = (int32_t *)at(o_rst);
@@ -431,6 +435,9 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     put(o_slf, P.slot_first.data(), nslot);
     put(o_chq, P.chunk_q.data(), nch * 4);
     put(o_chm, P.chunk_m.data(), nch * 8);
+    put(o_tcls, P.t_cls.data(), nops);
+    put(o_xptr, P.x_ptr.data(), (pp + 1) * 4);
+    put(o_xops, P.x_ops.data(), P.x_ops.size() * sizeof(XOp));
     CU(cudaMemcpyAsync(base, h.data(), table_bytes, cudaMemcpyHostToDevice, s));
   }
   if (opts && (opts->flags & PRISM_BUILD_PROFILE)) {

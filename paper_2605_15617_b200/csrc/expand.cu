@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
       if (g.h_smask) g.h_smask[h] = shard_mask(g, q.type, dpi, epi, edpi);
       if (g.slot_first[u0 + u]) {  // the node's first group provides its replay record
         const int32_t n = rb + g.slot_tidx[u0 + u];
-        g.node_cls[n] = q.type == PRISM_ROLE_TP ? 1 : 2;
+        g.node_cls[n] = g.t_cls[op0 + g.slot_tidx[u0 + u]];
         g.node_sdur[n] = q.dur;
         g.node_uid[n] = uid;
       }

@@ -70,6 +70,9 @@ struct DevGraph {
   const int64_t *chunk_m;
   int32_t nchunk;
   const int32_t *wpos;      // WORLD per-stage template indices
+  const uint8_t *t_cls;     // replay class per template op (Plan::t_cls)
+  const int32_t *x_ptr;     // [pp+1] cross-op list of each stage
+  const XOp *x_ops;
 };
 
 // Scenario parameters as seen by the kernels.

@@ -138,6 +138,52 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     P.stage_slots[s] = slots;
   }
 
+  // replay classes (cell kernel) and per-stage cross-op lists
+  P.t_cls.assign(tm.n_ops, 0);
+  {
+    // WORLD op k chains only if, on every stage, the op right before it is WORLD op k-1
+    std::vector<int32_t> wk(pp, 0);
+    std::vector<uint8_t> wchain;
+    for (int s = 0; s < pp; ++s) {
+      const int64_t a = tm.tmpl_ptr[s], b = tm.tmpl_ptr[s + 1];
+      int32_t k = 0;
+      for (int64_t i = a; i < b; ++i) {
+        const prism_op &o = tm.ops[i];
+        if (o.kind == PRISM_KIND_COLLECTIVE && o.role == PRISM_ROLE_WORLD) {
+          const bool prev_world = i > a && tm.ops[i - 1].kind == PRISM_KIND_COLLECTIVE &&
+                                  tm.ops[i - 1].role == PRISM_ROLE_WORLD;
+          if ((int32_t)wchain.size() <= k) wchain.push_back(1);
+          wchain[k] &= prev_world ? 1 : 0;
+          ++k;
+        }
+      }
+    }
+    P.x_ptr.assign(pp + 1, 0);
+    for (int s = 0; s < pp; ++s) {
+      const int64_t a = tm.tmpl_ptr[s], b = tm.tmpl_ptr[s + 1];
+      int32_t k = 0;
+      for (int64_t i = a; i < b; ++i) {
+        const prism_op &o = tm.ops[i];
+        uint8_t c = 0;
+        if (o.kind == PRISM_KIND_COLLECTIVE) {
+          if (o.role == PRISM_ROLE_TP) {
+            c = 1;
+          } else if (o.role == PRISM_ROLE_WORLD) {
+            c = (k < (int32_t)wchain.size() && wchain[k]) ? 3 : 2;
+            ++k;
+          } else {
+            const bool same = i > a && tm.ops[i - 1].kind == PRISM_KIND_COLLECTIVE && tm.ops[i - 1].role == o.role;
+            c = same ? 3 : 2;
+          }
+        } else if (o.kind == PRISM_KIND_P2P) {
+          c = 2;
+        }
+        P.t_cls[i] = c;
+        if (c == 2) P.x_ops.push_back(XOp{(int32_t)(i - a), P.t_slot_ptr[i], P.t_slots[i], 0});
+      }
+      P.x_ptr[s + 1] = (int32_t)P.x_ops.size();
+    }
+  }
   TMARK("scan");
   // ---- quotient groups --------------------------------------------------------------------
   std::vector<QGroup> Q;

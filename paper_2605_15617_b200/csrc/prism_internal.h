@@ -49,6 +49,11 @@ struct QGroup {
   int64_t lbase;       // first accumulator index (cell kernel, large groups); -1 otherwise
 };
 
+// A cross-cell op of a stage template: its template index, first slot offset and slot count.
+struct XOp {
+  int32_t tidx, hoff, ns, pad;
+};
+
 struct Topo {
   int32_t tp, pp, dp, ep, order;
 };
@@ -66,6 +71,14 @@ struct Plan {
   std::vector<int32_t> t_slots;      // slots of each op
   std::vector<int64_t> stage_len;    // [pp]
   std::vector<int64_t> stage_slots;  // [pp] total slots per template
+  // replay class of every template op (cell kernel): 0 compute span, 1 TP collective (the cell's
+  // own group), 2 cross-cell synchronization, 3 chained collective: a DP/EP/EDP/WORLD collective
+  // that immediately follows a collective of the same group, so every member is ready exactly at
+  // that group's shared finish and start = own ready time (exact)
+  std::vector<uint8_t> t_cls;
+  // per stage, the cross-cell ops (class 2) in template order: x_ptr[pp+1] -> XOp
+  std::vector<int32_t> x_ptr;
+  std::vector<XOp> x_ops;
   std::vector<int64_t> stage_op0;    // [pp] first global op index
   std::vector<QGroup> q;             // sorted by (level, creation order)
   std::vector<int32_t> wpos;         // WORLD template indices, pp per WORLD quotient group

@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "graph.h"
 
@@ -128,6 +130,9 @@ struct CellArgs {
   int32_t Sp;          // scenario stride (all chunks x 32)
   int32_t chunk0;      // first chunk of this launch
   int32_t nchunks;     // chunks of the whole replay (arrival counters are per chunk)
+  uint32_t poll_spin;      // polls before the first sleep
+  uint32_t poll_sleep0;    // first sleep (ns), doubled per further poll ...
+  uint32_t poll_sleep_max; // ... up to this
   ShardLink L;         // row e: peer exchange buffers (sharded kernels only)
 };
 
@@ -145,11 +150,15 @@ __device__ __forceinline__ int32_t rank_of(const DevGraph &g, int32_t tp_i, int3
                                          : tp_i + g.tp * (pp_i + g.pp * dp_i);
 }
 
-// Backoff + watchdog for a waiting lane; returns true when the replay was aborted.
+// Backoff + watchdog of a waiting warp; returns true when the replay was aborted. The sleep grows
+// geometrically from poll_sleep0 to poll_sleep_max ns: a short wait costs one short handoff, a long
+// wait (a pipeline stage idling through the 1F1B warm-up) stops stealing issue slots from the
+// computing warps of its SM.
 __device__ __forceinline__ bool wait_tick(const CellArgs &a, uint32_t &spins, uint64_t &t0) {
   ++spins;
   if ((threadIdx.x & 31) == 0) STAT_ADD(3, 1);
-  __nanosleep(spins < 12 ? 32u : 256u);  // short: handoff latency is amplified by the pipeline
+  const uint32_t sh = min(spins, 16u);
+  __nanosleep(min(a.poll_sleep_max, a.poll_sleep0 << sh));
   if ((spins & 63) == 0) {
     if (ld_relaxed(a.status) != 0) return true;
     if (t0 == 0) t0 = globaltimer();
@@ -159,6 +168,33 @@ __device__ __forceinline__ bool wait_tick(const CellArgs &a, uint32_t &spins, ui
     }
   }
   return false;
+}
+
+// Sync records of the next cross-cell op, one (rank, slot) pair per lane, loaded right after the
+// previous cross op so that their latency overlaps the compute spans in between (the handoff path
+// of a rendezvous then starts with no dependent global load).
+struct PreRec {
+  uint32_t meta, smask;
+  int32_t base, grp;
+  int64_t dur;
+  uint64_t uid;
+};
+
+template <bool SH>
+__device__ __forceinline__ void prefetch_cross(const DevGraph &g, const XOp &xo, const int32_t *rsh, int C,
+                                               PreRec &pre) {
+  const int lane = threadIdx.x & 31;
+  const int ns = xo.ns;
+  if (ns > 0 && lane < C * ns) {
+    const int r = lane / ns, q = lane - r * ns;
+    const int32_t h = rsh[r] + xo.hoff + q;
+    pre.meta = g.h_meta[h];
+    pre.base = g.h_base[h];
+    pre.dur = g.h_dur[h];
+    pre.uid = g.h_uid[h];
+    pre.grp = ns > 1 ? g.node_grp[h] : 0;
+    pre.smask = SH ? g.h_smask[h] : 0u;
+  }
 }
 
 // Per-warp shared scratch of the cross-cell path.
@@ -181,21 +217,19 @@ struct CrossScratch {
 // folded on the fly, the own slot is not read back), then finish = max over groups + dur'.
 template <bool SH>
 __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p, const CellArgs &a,
-                                          int64_t *__restrict__ gfin, int64_t *ts, const int32_t *rsh, int C,
-                                          int32_t hoff, int32_t ns, int32_t k, CrossScratch &cs) {
+                                          int64_t *__restrict__ gfin, int64_t *ts, int C, int32_t ns,
+                                          int32_t k, CrossScratch &cs, const PreRec &pre) {
   const int lane = threadIdx.x & 31;
   const int32_t Sp = a.Sp;
   const int32_t ck = k / SC;
   const int np = C * ns;  // <= 32
-  if (lane < np) {
-    const int r = lane / ns, q = lane - (lane / ns) * ns;
-    const int32_t h = rsh[r] + hoff + q;
-    cs.meta[lane] = g.h_meta[h];
-    cs.base[lane] = g.h_base[h];
-    cs.dur[lane] = g.h_dur[h];
-    cs.uid[lane] = g.h_uid[h];
-    cs.grp[lane] = ns > 1 ? g.node_grp[h] : 0;
-    if (SH) cs.smask[lane] = g.h_smask[h];
+  if (lane < np) {  // the op's sync records, prefetched into registers one cross op ahead
+    cs.meta[lane] = pre.meta;
+    cs.base[lane] = pre.base;
+    cs.dur[lane] = pre.dur;
+    cs.uid[lane] = pre.uid;
+    cs.grp[lane] = pre.grp;
+    if (SH) cs.smask[lane] = pre.smask;
   }
   __syncwarp();
   bool large_any = false;
@@ -245,33 +279,38 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
           }
         }
   }
+  // poll until every (rank, group) pair of the op is resolved; a pair resolved for this lane is
+  // not polled again. Slot values are parity-encoded: v ^ pm is the ready time when >= 0.
+  const int64_t pm = a.parity ? -1 : 0;
+  uint32_t pending = np >= 32 ? 0xFFFFFFFFu : ((1u << np) - 1u);
   uint32_t spins = 0;
   uint64_t tw = 0;
   while (true) {
-    bool ok = true;
-#pragma unroll 4
-    for (int x = 0; x < np; ++x) {
+    for (uint32_t left = pending; left; left &= left - 1) {
+      const int x = __ffs(left) - 1;
       const uint32_t meta = cs.meta[x];
       const int32_t base = cs.base[x];
       const int32_t size = (int32_t)(meta & 0xFFFF);
+      bool okx;
       if (!(meta & 0x80000000u)) {
         const int32_t own = (int32_t)((meta >> 16) & 0x7FFF);
         int64_t m = ts[(x / ns) * 32 + lane];
+        okx = true;
         const int64_t *src = a.rslot + (int64_t)base * Sp + k;
         for (int32_t mm = 0; mm < size; ++mm, src += Sp) {
           if (mm == own) continue;
-          const int64_t v = poll64<SH>(src);
-          ok &= a.parity ? v < 0 : v >= 0;
-          m = max(m, a.parity ? ~v : v);
+          const int64_t v = poll64<SH>(src) ^ pm;
+          okx &= v >= 0;
+          m = max(m, v);
         }
-        cs.vmax[x][lane] = m;
+        if (okx) cs.vmax[x][lane] = m;
       } else {
-        ok &= poll32<SH>(a.arrive + (int64_t)base * a.nchunks + ck) >= (uint32_t)size;
+        okx = poll32<SH>(a.arrive + (int64_t)base * a.nchunks + ck) >= (uint32_t)size;
       }
+      if (okx) pending &= ~(1u << x);
     }
-    if (__all_sync(0xffffffffu, ok)) break;
-    ++spins;
-    if (spins > 6 && wait_tick(a, spins, tw)) return false;
+    if (__all_sync(0xffffffffu, pending == 0)) break;
+    if (++spins > a.poll_spin && wait_tick(a, spins, tw)) return false;
   }
   if (large_any) {
     if (SH) fence_acq_rel_sys();
@@ -335,6 +374,15 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   const long long k_start = clock64();
   if (lane == 0) STAT_ADD(4, globaltimer());
 #endif
+  // cross-op cursor of the stage template and the prefetched records of the next cross op
+  int32_t xk = g.x_ptr[s];
+  const int32_t xend = g.x_ptr[s + 1];
+  XOp xo{len, 0, 0, 0};
+  PreRec pre{0u, 0u, 0, 0, 0, 0};
+  if (xk < xend) {
+    xo = g.x_ops[xk];
+    prefetch_cross<SH>(g, xo, rsh, C, pre);
+  }
   // op records of the cell's first rank (the template is shared; the per-rank part of a compute
   // span's uid is rk[r]), 32 ops per coalesced round trip, next batch in flight
   uint32_t ncls = 2;
@@ -377,21 +425,35 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
         m += gpert ? perturb_x(d, sx ^ (ux * K_MIX), p) : d;
 #pragma unroll
         for (int r = 0; r < C; ++r) t[r] = m;
+      } else if (c == 3) {  // chained collective: every member is ready at the previous
+                            // occurrence's shared finish, so start = own ready time (exact)
+        const uint64_t ux = __shfl_sync(0xffffffffu, bux, j);
+        if (gpert) {
+          // rank r's group uid = ux + r * 2^24 (gid = tp_i + ...), WORLD: one group
+          const uint64_t um = ux * K_MIX;
+          const uint64_t stepm = ((ux >> 56) == PRISM_ROLE_WORLD ? 0ull : (1ull << 24)) * K_MIX;
+#pragma unroll
+          for (int r = 0; r < C; ++r) t[r] += perturb_x(d, sx ^ (um + (uint64_t)r * stepm), p);
+        } else {
+#pragma unroll
+          for (int r = 0; r < C; ++r) t[r] += d;
+        }
       } else {  // cross-cell synchronization, rank by rank (deposit all first: no self-wait)
 #ifdef PRISM_CELL_STATS
         const long long c0 = clock64();
 #endif
-        // rank r's slots of this op: rs[r] + (template slot offset), identical templates
-        const int32_t h0 = g.node_gptr[rb[0] + i];
-        const int32_t ns = g.node_gptr[rb[0] + i + 1] - h0;
 #pragma unroll
         for (int r = 0; r < C; ++r) ts[r * 32 + lane] = t[r];
         __syncwarp();
-        const bool ok = cross_all<SH>(g, p, a, gfin, ts, rsh, C, h0 - rs[0], ns, k, cs);
+        const bool ok = cross_all<SH>(g, p, a, gfin, ts, C, xo.ns, k, cs, pre);
         __syncwarp();
         if (!ok) return;
 #pragma unroll
         for (int r = 0; r < C; ++r) t[r] = ts[r * 32 + lane];
+        if (++xk < xend) {  // next cross op: its records load while the compute spans run
+          xo = g.x_ops[xk];
+          prefetch_cross<SH>(g, xo, rsh, C, pre);
+        }
 #ifdef PRISM_CELL_STATS
         if (lane == 0) {
           const long long dc = clock64() - c0;
@@ -468,6 +530,20 @@ bool cell_fit_units(const DevGraph &g, int64_t units, int *ctas) {
 
 cudaError_t preload_cells() { return preload_cell_kernels(); }
 
+// Poll/backoff policy of the waiting warps; PRISM_POLL="spin,sleep0,sleep_max" overrides it
+// (tuning experiments, tools/poll_sweep.py).
+struct PollPolicy {
+  uint32_t spin, sleep0, sleep_max;
+};
+PollPolicy poll_policy() {
+  PollPolicy p{2, 32, 1024};
+  if (const char *e = std::getenv("PRISM_POLL")) {
+    unsigned a = 0, b = 0, c = 0;
+    if (std::sscanf(e, "%u,%u,%u", &a, &b, &c) == 3) p = {a, b, c};
+  }
+  return p;
+}
+
 // Chunks of 32 scenarios per unit; every chunk of a replay runs in one launch when they all fit,
 // else the caller launches one chunk at a time (chunk groups of 1).
 bool cells_fit(const DevGraph &g, int nchunks) {
@@ -490,8 +566,9 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
   int ctas = 0;
   if (!cell_fit_units(g, units, &ctas)) return cudaErrorCooperativeLaunchTooLarge;
   // the launch covers chunks [chunk0, chunk0 + nchunks_launch) of the replay's Sp / 32 chunks
+  static const PollPolicy pol = poll_policy();
   CellArgs a{rslot, acc, arrive, status, 10ull * 1000 * 1000 * 1000, parity, (int32_t)units, Sp, chunk0,
-             Sp / SC, ShardLink{}};
+             Sp / SC, pol.spin, pol.sleep0, pol.sleep_max, ShardLink{}};
   if (link) a.L = *link;
   DevGraph gg = g;
   ScenParams pp = p;
