@@ -42,6 +42,7 @@ constexpr int SC = 32;          // scenarios per unit (one warp, lane = scenario
 constexpr int WARPS = 1;        // units per CTA (1: warps spread evenly over the SMs)
 constexpr int MAX_TP = 8;       // tp of the instantiated cell kernels
 constexpr int SMALL = kSmallGroup;
+constexpr int kPollList = MAX_TP * 4 * (kSmallGroup - 1);  // <= 32 pairs x 7 other members
 
 __device__ __forceinline__ int64_t perturb_x(int64_t d, uint64_t x, const ScenParams &p) {
   // splitmix64(x) >> 40 (reading Z8): the finaliser's last step z ^ (z >> 31) leaves bits 40..63
@@ -206,6 +207,10 @@ struct CrossScratch {
   uint64_t uid[MAX_TP * 4];
   uint32_t smask[MAX_TP * 4];  // row e: shards holding members of the pair's group
   int64_t vmax[MAX_TP * 4][32];  // per pair, per lane: max ready time over the group's members
+  // poll list: one entry per (pair, other member) of a small group (ready-slot index) or per large
+  // group (arrival-counter index), so a poll round issues every load before folding any of them
+  int32_t lidx[kPollList];
+  uint8_t lpair[kPollList];      // pair index | 0x80 for a large group's counter
 };
 
 // Cross-cell node at template index i for all C ranks of the cell (rare: a few % of ops; kept
@@ -279,36 +284,106 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
           }
         }
   }
-  // poll until every (rank, group) pair of the op is resolved; a pair resolved for this lane is
-  // not polled again. Slot values are parity-encoded: v ^ pm is the ready time when >= 0.
+  // poll until every (rank, group) pair of the op is resolved. The (pair, member) loads of a
+  // round are flattened into one list and issued 8 at a time before any is folded (a loop with a
+  // load-dependent branch per pair would serialise one L2 round trip per pair); a pair resolved
+  // for this lane is not polled again. Slot values are parity-encoded: v ^ pm is the ready time
+  // when >= 0; a large group is resolved when its arrival counter reaches its size.
   const int64_t pm = a.parity ? -1 : 0;
+#ifdef PRISM_CELL_STATS
+  const unsigned long long t_enter = globaltimer();
+#endif
+  int32_t nl;
+  {
+    int32_t cnt = 0;
+    uint32_t meta = 0;
+    if (lane < np) {
+      meta = cs.meta[lane];
+      cnt = (meta & 0x80000000u) ? 1 : (int32_t)(meta & 0xFFFF) - 1;
+    }
+    int32_t incl = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    nl = __shfl_sync(0xffffffffu, incl, 31);
+    if (lane < np) {
+      int32_t o = incl - cnt;
+      const int32_t base = cs.base[lane];
+      if (meta & 0x80000000u) {
+        cs.lidx[o] = base;
+        cs.lpair[o] = (uint8_t)(lane | 0x80);
+      } else {
+        const int32_t size = (int32_t)(meta & 0xFFFF), own = (int32_t)((meta >> 16) & 0x7FFF);
+        for (int32_t mm = 0; mm < size; ++mm)
+          if (mm != own) {
+            cs.lidx[o] = base + mm;
+            cs.lpair[o] = (uint8_t)lane;
+            ++o;
+          }
+      }
+    }
+    for (int x = 0; x < np; ++x) cs.vmax[x][lane] = ts[(x / ns) * 32 + lane];
+    __syncwarp();
+  }
   uint32_t pending = np >= 32 ? 0xFFFFFFFFu : ((1u << np) - 1u);
   uint32_t spins = 0;
   uint64_t tw = 0;
   while (true) {
-    for (uint32_t left = pending; left; left &= left - 1) {
-      const int x = __ffs(left) - 1;
-      const uint32_t meta = cs.meta[x];
-      const int32_t base = cs.base[x];
-      const int32_t size = (int32_t)(meta & 0xFFFF);
-      bool okx;
-      if (!(meta & 0x80000000u)) {
-        const int32_t own = (int32_t)((meta >> 16) & 0x7FFF);
-        int64_t m = ts[(x / ns) * 32 + lane];
-        okx = true;
-        const int64_t *src = a.rslot + (int64_t)base * Sp + k;
-        for (int32_t mm = 0; mm < size; ++mm, src += Sp) {
-          if (mm == own) continue;
-          const int64_t v = poll64<SH>(src) ^ pm;
-          okx &= v >= 0;
-          m = max(m, v);
+    uint32_t bad = 0;
+    for (int32_t j0 = 0; j0 < nl; j0 += 8) {
+      int64_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int32_t j = j0 + u;
+        v[u] = 0;
+        if (j < nl) {
+          const uint32_t pr = cs.lpair[j];
+          if ((pending >> (pr & 31)) & 1u) {
+            const int32_t idx = cs.lidx[j];
+            if (pr & 0x80)
+              v[u] = (int64_t)poll32<SH>(a.arrive + (int64_t)idx * a.nchunks + ck) -
+                     (int64_t)(cs.meta[pr & 31] & 0xFFFF);
+            else
+              v[u] = poll64<SH>(a.rslot + (int64_t)idx * Sp + k) ^ pm;
+          }
         }
-        if (okx) cs.vmax[x][lane] = m;
-      } else {
-        okx = poll32<SH>(a.arrive + (int64_t)base * a.nchunks + ck) >= (uint32_t)size;
       }
-      if (okx) pending &= ~(1u << x);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int32_t j = j0 + u;
+        if (j < nl) {
+          const uint32_t pr = cs.lpair[j];
+          const int x = pr & 31;
+          if ((pending >> x) & 1u) {
+            if (v[u] < 0) bad |= 1u << x;
+            else if (!(pr & 0x80)) cs.vmax[x][lane] = max(cs.vmax[x][lane], v[u]);
+          }
+        }
+      }
     }
+#ifdef PRISM_CELL_STATS
+    if (k == 0) {
+      const unsigned long long now = globaltimer();  // before the (slow) timestamp loads below
+      for (uint32_t done = pending & ~bad; done; done &= done - 1) {
+        const int x = __ffs(done) - 1;
+        const uint32_t meta = cs.meta[x];
+        if (meta & 0x80000000u) continue;
+        const int32_t base = cs.base[x], size = (int32_t)(meta & 0xFFFF), own = (int32_t)((meta >> 16) & 0x7FFF);
+        unsigned long long dep = 0;
+        for (int32_t mm = 0; mm < size; ++mm)
+          if (mm != own && base + mm < (1 << 22)) dep = max(dep, *(volatile unsigned long long *)&g_dep_time[base + mm]);
+        if (dep && now > dep && dep > t_enter) {  // the consumer was already waiting
+          atomicAdd(&g_lat[0], now - dep);
+          atomicAdd(&g_lat[1], dep - t_enter);
+          atomicAdd(&g_lat[2], 1ull);
+          atomicMax(&g_lat[3], now - dep);
+        }
+      }
+    }
+#endif
+    pending &= bad;
     if (__all_sync(0xffffffffu, pending == 0)) break;
     if (++spins > a.poll_spin && wait_tick(a, spins, tw)) return false;
   }

@@ -8,15 +8,17 @@ tm = w.config(sys.argv[1] if len(sys.argv) > 1 else "C5")
 g = prism.Graph(tm, stream=torch.cuda.current_stream().cuda_stream, profile=True)
 L = prism.lib()
 buf = (ctypes.c_ulonglong * (16 * 4096))()
-g.replay(64, amp_q16=6554, kind_mask=7, algo="cells"); L.prism_debug_wait_hist(buf)
-g.replay(64, amp_q16=6554, kind_mask=7, algo="cells"); L.prism_debug_wait_hist(buf)
+REC = os.environ.get("REC", "1") == "1"
+AMP = int(os.environ.get("AMP", "6554"))
+g.replay(64, amp_q16=AMP, kind_mask=7, algo="cells", record=REC); L.prism_debug_wait_hist(buf)
+g.replay(64, amp_q16=AMP, kind_mask=7, algo="cells", record=REC); L.prism_debug_wait_hist(buf)
 lat = (ctypes.c_ulonglong * 4)()
 L.prism_debug_lat(lat)
-g.replay(64, amp_q16=6554, kind_mask=7, algo="cells"); L.prism_debug_wait_hist(buf)
+g.replay(64, amp_q16=AMP, kind_mask=7, algo="cells", record=REC); L.prism_debug_wait_hist(buf)
 L.prism_debug_lat(lat)
 print("kernel ms", g.last_timing()["levels"])
 n = max(1, lat[2])
-print(f"P2P rendezvous (chunk 0, {lat[2]} samples): detection latency mean {lat[0]/n/1e3:.2f} us max {lat[3]/1e3:.1f} us; partner lateness mean {lat[1]/n/1e3:.2f} us")
+print(f"P2P rendezvous (chunk 0, {lat[2]} samples): handoff (consumer already waiting) latency mean {lat[0]/n/1e3:.2f} us max {lat[3]/1e3:.1f} us; partner lateness mean {lat[1]/n/1e3:.2f} us")
 h = np.frombuffer(buf, dtype=np.uint64).reshape(16, 4096).astype(np.float64)
 ncell = tm.topo.dp * 2  # warps per stage (2 chunks)
 for s in (0, 1, 7, 14, 15):
