@@ -113,6 +113,7 @@ __device__ unsigned long long g_dep_time[1 << 22];     // deposit globaltimer pe
 __device__ unsigned long long g_lat[4];                // sum latency, sum skew, count, max latency
 __device__ unsigned long long g_wait_hist[16 * 4096];  // [stage][template op] wait cycles (stage < 16)
 __device__ unsigned long long g_cell_stats[16384 * 8];  // per warp: total, cross, -, polls, start, end
+__device__ unsigned long long g_tl[16 * 128 * 4];  // dp 0, chunk 0: [stage][cross op] enter, deposited, detected, exit
 #define STAT_ADD(i, v) g_cell_stats[(size_t)(blockIdx.x * WARPS + (threadIdx.x >> 5)) * 8 + (i)] += (v)
 #else
 #define STAT_ADD(i, v)
@@ -223,7 +224,7 @@ struct CrossScratch {
 template <bool SH>
 __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p, const CellArgs &a,
                                           int64_t *__restrict__ gfin, int64_t *ts, int C, int32_t ns,
-                                          int32_t k, CrossScratch &cs, const PreRec &pre) {
+                                          int32_t k, CrossScratch &cs, const PreRec &pre, int tl) {
   const int lane = threadIdx.x & 31;
   const int32_t Sp = a.Sp;
   const int32_t ck = k / SC;
@@ -243,12 +244,6 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
     const uint32_t meta = cs.meta[x];
     const int32_t base = cs.base[x];
     if (!(meta & 0x80000000u)) {
-#ifdef PRISM_CELL_STATS
-      if (k == 0 && base + (int32_t)((meta >> 16) & 0x7FFF) < (1 << 22)) {
-        g_dep_time[base + (int32_t)((meta >> 16) & 0x7FFF)] = globaltimer();
-        __threadfence();
-      }
-#endif
       const int64_t off = (int64_t)(base + (int32_t)((meta >> 16) & 0x7FFF)) * Sp + k;
       const int64_t enc = a.parity ? ~tr : tr;
       if (!SH) {
@@ -284,15 +279,15 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
           }
         }
   }
+#ifdef PRISM_CELL_STATS
+  if (tl >= 0 && lane == 0) g_tl[tl * 4 + 1] = globaltimer();
+#endif
   // poll until every (rank, group) pair of the op is resolved. The (pair, member) loads of a
   // round are flattened into one list and issued 8 at a time before any is folded (a loop with a
   // load-dependent branch per pair would serialise one L2 round trip per pair); a pair resolved
   // for this lane is not polled again. Slot values are parity-encoded: v ^ pm is the ready time
   // when >= 0; a large group is resolved when its arrival counter reaches its size.
   const int64_t pm = a.parity ? -1 : 0;
-#ifdef PRISM_CELL_STATS
-  const unsigned long long t_enter = globaltimer();
-#endif
   int32_t nl;
   {
     int32_t cnt = 0;
@@ -363,30 +358,13 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
         }
       }
     }
-#ifdef PRISM_CELL_STATS
-    if (k == 0) {
-      const unsigned long long now = globaltimer();  // before the (slow) timestamp loads below
-      for (uint32_t done = pending & ~bad; done; done &= done - 1) {
-        const int x = __ffs(done) - 1;
-        const uint32_t meta = cs.meta[x];
-        if (meta & 0x80000000u) continue;
-        const int32_t base = cs.base[x], size = (int32_t)(meta & 0xFFFF), own = (int32_t)((meta >> 16) & 0x7FFF);
-        unsigned long long dep = 0;
-        for (int32_t mm = 0; mm < size; ++mm)
-          if (mm != own && base + mm < (1 << 22)) dep = max(dep, *(volatile unsigned long long *)&g_dep_time[base + mm]);
-        if (dep && now > dep && dep > t_enter) {  // the consumer was already waiting
-          atomicAdd(&g_lat[0], now - dep);
-          atomicAdd(&g_lat[1], dep - t_enter);
-          atomicAdd(&g_lat[2], 1ull);
-          atomicMax(&g_lat[3], now - dep);
-        }
-      }
-    }
-#endif
     pending &= bad;
     if (__all_sync(0xffffffffu, pending == 0)) break;
     if (++spins > a.poll_spin && wait_tick(a, spins, tw)) return false;
   }
+#ifdef PRISM_CELL_STATS
+  if (tl >= 0 && lane == 0) g_tl[tl * 4 + 2] = globaltimer();
+#endif
   if (large_any) {
     if (SH) fence_acq_rel_sys();
     else fence_acq_rel();
@@ -440,8 +418,12 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   __syncwarp();
   const int32_t len = g.rank_ptr[rank_of(g, 0, s, dpi) + 1] - rb[0];
   const uint64_t sx = p.seed ^ ((uint64_t)k * K_GOLD);
-  const bool cpert = (p.mask & 1u) && p.amp > 0 && k > 0;
-  const bool gpert = (p.mask & 2u) && p.amp > 0 && k > 0;
+  // per-warp flags pinned in a register (an asm output cannot be rematerialised from the kernel
+  // parameters, which the compiler otherwise reloads on every op)
+  uint32_t fl = (((p.mask & 1u) && p.amp > 0 && k > 0) ? 1u : 0u) | (((p.mask & 2u) && p.amp > 0 && k > 0) ? 2u : 0u) |
+                (p.record ? 4u : 0u);
+  asm volatile("" : "+r"(fl));
+  const bool cpert = fl & 1u, gpert = fl & 2u, record = fl & 4u;
   int64_t t[C];
 #pragma unroll
   for (int r = 0; r < C; ++r) t[r] = 0;
@@ -479,10 +461,16 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
       nd = g.node_sdur[n];
       nux = g.node_uid[n];
     }
+    // op j's class / duration were fetched during op j-1 (software pipelined: the dispatch
+    // branch of an op does not wait on its shuffles)
+    uint32_t c_n = __shfl_sync(0xffffffffu, bcls, 0);
+    int64_t d_n = __shfl_sync(0xffffffffu, bd, 0);
     for (int32_t j = 0; j < cnt; ++j) {
-      const uint32_t c = __shfl_sync(0xffffffffu, bcls, j);
-      const int64_t d = __shfl_sync(0xffffffffu, bd, j);
+      const uint32_t c = c_n;
+      const int64_t d = d_n;
       const int32_t i = base + j;
+      c_n = __shfl_sync(0xffffffffu, bcls, (j + 1) & 31);
+      d_n = __shfl_sync(0xffffffffu, bd, (j + 1) & 31);
       if (c == 0) {  // compute span: every rank waits out its own perturbed duration
         if (cpert) {
           const uint64_t ix = (uint64_t)i * K_MIX;
@@ -517,14 +505,22 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
 #ifdef PRISM_CELL_STATS
         const long long c0 = clock64();
 #endif
+        int tl = -1;
+#ifdef PRISM_CELL_STATS
+        if (k < 32 && dpi == 0 && s < 16 && xk - g.x_ptr[s] < 128) tl = s * 128 + (xk - g.x_ptr[s]);
+        if (tl >= 0 && lane == 0) g_tl[tl * 4 + 0] = globaltimer();
+#endif
 #pragma unroll
         for (int r = 0; r < C; ++r) ts[r * 32 + lane] = t[r];
         __syncwarp();
-        const bool ok = cross_all<SH>(g, p, a, gfin, ts, C, xo.ns, k, cs, pre);
+        const bool ok = cross_all<SH>(g, p, a, gfin, ts, C, xo.ns, k, cs, pre, tl);
         __syncwarp();
-        if (!ok) return;
 #pragma unroll
         for (int r = 0; r < C; ++r) t[r] = ts[r * 32 + lane];
+#ifdef PRISM_CELL_STATS
+        if (tl >= 0 && lane == 0) g_tl[tl * 4 + 3] = globaltimer();
+#endif
+        if (!ok) return;
         if (++xk < xend) {  // next cross op: its records load while the compute spans run
           xo = g.x_ops[xk];
           prefetch_cross<SH>(g, xo, rsh, C, pre);
@@ -537,7 +533,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
         }
 #endif
       }
-      if (p.record) {
+      if (record) {
 #pragma unroll
         for (int r = 0; r < C; ++r) fin[(int64_t)(rb[r] + i) * Sp + k] = t[r];
       }
@@ -662,6 +658,16 @@ extern "C" PRISM_API int prism_debug_lat(unsigned long long *out) {
   unsigned long long z[4] = {0, 0, 0, 0};
   cudaMemcpyToSymbol(g_lat, z, sizeof z);
   return 0;
+#else
+  (void)out;
+  return -2;
+#endif
+}
+
+extern "C" PRISM_API int prism_debug_timeline(unsigned long long *out) {
+#ifdef PRISM_CELL_STATS
+  cudaDeviceSynchronize();
+  return cudaMemcpyFromSymbol(out, g_tl, sizeof(unsigned long long) * 16 * 128 * 4) == cudaSuccess ? 0 : -1;
 #else
   (void)out;
   return -2;
