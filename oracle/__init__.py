@@ -59,6 +59,15 @@ def _load():
                                           ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32, P, P, P,
                                           P, P, ctypes.c_int32, ctypes.c_char_p, ctypes.c_int]
             lib.oracle_replay.restype = ctypes.c_int
+            lib.oracle_replay_ov.argtypes = [P, P, ctypes.c_int64, P, P, P, P, P, ctypes.c_int32,
+                                             ctypes.c_int32, ctypes.c_uint64, ctypes.c_int32,
+                                             ctypes.c_uint32, P, P, P, P, P, ctypes.c_int32,
+                                             ctypes.c_char_p, ctypes.c_int]
+            lib.oracle_replay_ov.restype = ctypes.c_int
+            lib.oracle_critical_path.argtypes = [P, P, ctypes.c_int64, P, P, P, ctypes.c_int32,
+                                                 ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32, P,
+                                                 ctypes.c_int64, P, P, ctypes.c_char_p, ctypes.c_int]
+            lib.oracle_critical_path.restype = ctypes.c_int
             lib.oracle_splitmix64.argtypes = [ctypes.c_uint64]
             lib.oracle_splitmix64.restype = ctypes.c_uint64
             lib.oracle_perturb.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32,
@@ -109,10 +118,22 @@ def expand(tm) -> Dict[str, np.ndarray]:
             "levels": int(stats[4]), "sync_nodes": int(stats[5]), "max_group": int(stats[6])}
 
 
+def _opt64(a, n):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    if a.shape != (n,):
+        raise ValueError(f"per-node override must have shape ({n},)")
+    return a
+
+
 def replay(tm, n_scen: int = 1, *, seed: int = 0x5EED, amp_q16: int = 0, kind_mask: int = 0,
-           scen_first: int = 0, times: bool = False, peaks: bool = True, threads: int = 1):
+           scen_first: int = 0, times: bool = False, peaks: bool = True, threads: int = 1,
+           node_dur=None, node_alloc=None, node_free=None):
     """Replay scenarios scen_first .. scen_first+n_scen-1. Returns a dict with
-    iter [S], rank_end [S, W], peak [S, W] (if peaks), start/finish [S, N] (if times)."""
+    iter [S], rank_end [S, W], peak [S, W] (if peaks), start/finish [S, N] (if times).
+    node_dur / node_alloc / node_free: optional per-node overrides (rows f1/f3/f4), node order =
+    rank-major program order; a sync group lasts the max of its members' durations (Z2)."""
     lib = _load()
     topo = _topo_buf(tm.topo)
     ops, ptr, st = _inputs(tm)
@@ -124,9 +145,10 @@ def replay(tm, n_scen: int = 1, *, seed: int = 0x5EED, amp_q16: int = 0, kind_ma
     s0 = np.zeros((n_scen, N), np.int64) if times else None
     f0 = np.zeros((n_scen, N), np.int64) if times else None
     err = ctypes.create_string_buffer(512)
-    s = lib.oracle_replay(_ptr(topo), _ptr(ops), len(ops), _ptr(ptr), _ptr(st), scen_first, n_scen,
-                          seed, amp_q16, kind_mask, _ptr(it), _ptr(re), _ptr(pk), _ptr(s0), _ptr(f0),
-                          threads, err, 512)
+    nd, na, nf = _opt64(node_dur, N), _opt64(node_alloc, N), _opt64(node_free, N)
+    s = lib.oracle_replay_ov(_ptr(topo), _ptr(ops), len(ops), _ptr(ptr), _ptr(st), _ptr(nd), _ptr(na),
+                             _ptr(nf), scen_first, n_scen, seed, amp_q16, kind_mask, _ptr(it), _ptr(re),
+                             _ptr(pk), _ptr(s0), _ptr(f0), threads, err, 512)
     if s:
         raise OracleError(s, err.value.decode())
     out = {"iter": it, "rank_end": re}
@@ -144,3 +166,84 @@ def splitmix64(x: int) -> int:
 
 def perturb(d: int, uid: int, k: int, seed: int, amp: int) -> int:
     return int(_load().oracle_perturb(d, uid & (2**64 - 1), k, seed & (2**64 - 1), amp))
+
+
+def critical_path(tm, k: int = 0, *, seed: int = 0x5EED, amp_q16: int = 0, kind_mask: int = 0,
+                  node_dur=None):
+    """Row f3: (path [nodes, last first], T) of scenario k (walk and tie rules: prism_oracle.cpp
+    oracle_critical_path)."""
+    lib = _load()
+    topo = _topo_buf(tm.topo)
+    ops, ptr, st = _inputs(tm)
+    N = tm.n_nodes
+    nd = _opt64(node_dur, N)
+    cap = N + 1
+    path = np.zeros(cap, np.int32)
+    n = ctypes.c_int64(0)
+    T = ctypes.c_int64(0)
+    err = ctypes.create_string_buffer(512)
+    s = lib.oracle_critical_path(_ptr(topo), _ptr(ops), len(ops), _ptr(ptr), _ptr(st), _ptr(nd), k, seed,
+                                 amp_q16, kind_mask, _ptr(path), cap, ctypes.byref(n), ctypes.byref(T), err, 512)
+    if s:
+        raise OracleError(s, err.value.decode())
+    return path[: n.value].copy(), int(T.value)
+
+
+def node_table(tm) -> Dict[str, np.ndarray]:
+    """Per-node (rank-major program order) rank, template index, kind, label and template duration,
+    expanded with plain loops from the templates (every rank of stage s runs template s)."""
+    t = tm.topo
+    rank, tidx, kind, label, dur = [], [], [], [], []
+    for r in range(t.world):
+        s = (r // t.tp) % t.pp if t.rank_order == 0 else r // (t.tp * t.dp)
+        T = tm.stage(s)
+        n = len(T)
+        rank.append(np.full(n, r, np.int32))
+        tidx.append(np.arange(n, dtype=np.int32))
+        kind.append(T["kind"].astype(np.uint8))
+        label.append(T["label"].astype(np.uint32))
+        dur.append(T["dur_ns"].astype(np.int64))
+    cat = (lambda xs, dt: np.concatenate(xs) if xs else np.zeros(0, dt))
+    return {"rank": cat(rank, np.int32), "tidx": cat(tidx, np.int32), "kind": cat(kind, np.uint8),
+            "label": cat(label, np.uint32), "dur": cat(dur, np.int64)}
+
+
+class UnknownLabel(OracleError):
+    def __init__(self, label):
+        RuntimeError.__init__(self, f"UNKNOWN_LABEL: no node carries label {label:#x}")
+        self.status, self.name = 8, "UNKNOWN_LABEL"
+
+
+def whatif_durations(tm, *, node_dur=None, label_dur=None, rank_factor_q16=None) -> np.ndarray:
+    """Row f3 (SPEC S:488-505 what_if / fault_inject): per-node durations after
+    (1) the base (node_dur, else the template durations), (2) label overrides: every node whose
+    label is a key of label_dur lasts label_dur[label] (UnknownLabel if no node carries it),
+    (3) fault injection: every COMPUTE node of rank r lasts (d * rank_factor_q16[r]) >> 16."""
+    nt = node_table(tm)
+    d = (np.array(node_dur, dtype=np.int64) if node_dur is not None else nt["dur"].copy())
+    for lab, v in (label_dur or {}).items():
+        hit = nt["label"] == np.uint32(lab)
+        if not hit.any():
+            raise UnknownLabel(int(lab))
+        d[hit] = int(v)
+    if rank_factor_q16 is not None:
+        f = np.asarray(rank_factor_q16, dtype=np.int64)
+        comp = nt["kind"] == 0
+        for i in np.nonzero(comp)[0]:  # plain loop: the definition, element by element
+            d[i] = (int(d[i]) * int(f[nt["rank"][i]])) >> 16
+    return d
+
+
+def slice_local_finish(tm, node_dur, slices) -> np.ndarray:
+    """Row f1, the UNcalibrated timing (reading R5): each slice's real ranks are timed
+    in a run where every other rank is a virtual rank replaying the bare graph, i.e. with zero
+    durations; a node's slice-local finish is taken from the run of its own rank's
+    slice. Concatenating them is what inter-slice calibration corrects."""
+    nt = node_table(tm)
+    d = np.asarray(node_dur, dtype=np.int64)
+    out = np.zeros(len(d), np.int64)
+    for ranks in slices:
+        sel = np.isin(nt["rank"], np.asarray(list(ranks), dtype=np.int32))
+        r = replay(tm, 1, node_dur=np.where(sel, d, 0), times=True, peaks=False)
+        out[sel] = r["finish"][0][sel]
+    return out

@@ -37,8 +37,9 @@ def _rank(topo, tp, pp, dp):
     return tp + topo.tp * (pp + topo.pp * dp)
 
 
-def expand(tm):
-    """Returns (nodes, groups): nodes[n] = (rank, tidx, op); groups: key -> list of (node, dur)."""
+def expand(tm, node_dur=None):
+    """Returns (nodes, groups): nodes[n] = (rank, tidx, op); groups: key -> list of (node, dur).
+    node_dur (optional, per node): durations replacing the template's (rows f1/f3/f4)."""
     topo = tm.topo
     W = topo.tp * topo.pp * topo.dp
     nodes: List[Tuple[int, int, object]] = []
@@ -58,7 +59,7 @@ def expand(tm):
                 gid = {1: (s, dpi), 2: (tpi, s), 3: (tpi, s, edpi), 4: (tpi, s, epi), 5: ()}[role]
                 k = occ.get(role, 0)
                 occ[role] = k + 1
-                groups.setdefault(("C", role, gid, k), []).append((n, int(op["dur_ns"])))
+                groups.setdefault(("C", role, gid, k), []).append((n, _d(op, n, node_dur)))
             elif op["kind"] == 2:
                 prev = _rank(topo, tpi, (s - 1) % topo.pp, dpi)
                 nxt = _rank(topo, tpi, (s + 1) % topo.pp, dpi)
@@ -66,14 +67,18 @@ def expand(tm):
                     if int(op["p2p_mask"]) & bit:
                         k = occ.get(("b", bit), 0)
                         occ[("b", bit)] = k + 1
-                        groups.setdefault(("P", sender, d, k), []).append((n, int(op["dur_ns"])))
+                        groups.setdefault(("P", sender, d, k), []).append((n, _d(op, n, node_dur)))
         rank_nodes.append(mine)
     return nodes, rank_nodes, groups
 
 
-def iteration_time(tm) -> Tuple[int, List[int]]:
+def _d(op, n, node_dur):
+    return int(op["dur_ns"]) if node_dur is None else int(node_dur[n])
+
+
+def iteration_time(tm, node_dur=None) -> Tuple[int, List[int]]:
     """(T, finish per node) by exhaustive path enumeration."""
-    nodes, rank_nodes, groups = expand(tm)
+    nodes, rank_nodes, groups = expand(tm, node_dur)
     # vertices: ("n", node) for every node; ("g", key) for groups
     weight: Dict[tuple, int] = {}
     preds: Dict[tuple, List[tuple]] = {}
@@ -90,7 +95,7 @@ def iteration_time(tm) -> Tuple[int, List[int]]:
                 for key in node_groups[n]:
                     preds[v].append(("g", key))
             else:
-                weight[v] = int(nodes[n][2]["dur_ns"])
+                weight[v] = _d(nodes[n][2], n, node_dur)
                 if j > 0:
                     preds[v].append(("n", mine[j - 1]))
     for key, mem in groups.items():

@@ -132,8 +132,31 @@ struct Graph {
   std::vector<std::vector<int32_t>> node_groups;  // group indices per node (in insertion order)
   std::vector<Group> groups;
   std::vector<int64_t> static_of_rank;
+  // rows f1/f3/f4: optional per-node overrides of the template durations / memory deltas
+  const int64_t *nd_ov = nullptr, *alloc_ov = nullptr, *free_ov = nullptr;
   std::string err;
 };
+
+// Rows f1/f3/f4 (P:1170-1179 calibration, P:1767-1773 what-if, P:1745-1748 MoE imbalance): node n
+// lasts node_dur[n] instead of its template duration; a synchronization group lasts the max of its
+// members' durations (reading Z2, unchanged); memory deltas likewise per node.
+int apply_overrides(Graph &g, const int64_t *node_dur, const int64_t *node_alloc, const int64_t *node_free) {
+  g.nd_ov = node_dur;
+  g.alloc_ov = node_alloc;
+  g.free_ov = node_free;
+  if (node_dur) {
+    for (int64_t n = 0; n < g.N; ++n)
+      if (node_dur[n] < 0 || node_dur[n] > (1LL << 40)) { g.err = "node duration out of range"; return E_INVALID_ARG; }
+    for (auto &G : g.groups) {
+      G.dur = 0;
+      for (int32_t m : G.members) G.dur = std::max(G.dur, node_dur[m]);
+    }
+  }
+  if (node_alloc || node_free)
+    for (int64_t n = 0; n < g.N; ++n)
+      if ((node_alloc && node_alloc[n] < 0) || (node_free && node_free[n] < 0)) { g.err = "negative memory delta"; return E_INVALID_ARG; }
+  return OK;
+}
 
 int expand(const Topo &t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
            const int64_t *static_mem, Graph &g) {
@@ -249,11 +272,11 @@ int expand(const Topo &t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
   return OK;
 }
 
-int64_t node_dur(const Graph &g, int32_t n, int k, uint64_t seed, int amp, uint32_t mask) {
-  const Op *o = g.node_op[n];
-  if (!(mask & 1u)) return o->dur;
+int64_t node_duration(const Graph &g, int32_t n, int k, uint64_t seed, int amp, uint32_t mask) {
+  const int64_t d = g.nd_ov ? g.nd_ov[n] : g.node_op[n]->dur;
+  if (!(mask & 1u)) return d;
   uint64_t uid = ((uint64_t)g.node_rank[n] << 32) | (uint64_t)(uint32_t)g.node_tidx[n];
-  return perturb(o->dur, uid, k, seed, amp);
+  return perturb(d, uid, k, seed, amp);
 }
 
 int64_t group_dur(const Group &G, int k, uint64_t seed, int amp, uint32_t mask) {
@@ -331,8 +354,8 @@ int peak_memory(const Graph &g, const std::vector<int64_t> &start, const std::ve
     std::vector<std::tuple<int64_t, int64_t, int64_t>> ev;
     for (int64_t n = g.rank_base[r]; n < g.rank_base[r + 1]; ++n) {
       int64_t i = n - g.rank_base[r];
-      ev.emplace_back(start[n], 2 * i, g.node_op[n]->alloc);
-      ev.emplace_back(finish[n], 2 * i + 1, -g.node_op[n]->free_);
+      ev.emplace_back(start[n], 2 * i, g.alloc_ov ? g.alloc_ov[n] : g.node_op[n]->alloc);
+      ev.emplace_back(finish[n], 2 * i + 1, -(g.free_ov ? g.free_ov[n] : g.node_op[n]->free_));
     }
     std::sort(ev.begin(), ev.end());
     int64_t run = 0, best = 0;
@@ -415,17 +438,23 @@ int oracle_expand(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tm
 // Replays n_scen scenarios (scenario indices k = scen_first .. scen_first+n_scen-1).
 // iter_out[n_scen] (required); rank_end_out[n_scen][W], peak_out[n_scen][W],
 // start_out/finish_out[n_scen][N] optional (NULL = not written). n_threads >= 1.
-int oracle_replay(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
-                  const int64_t *static_mem, int32_t scen_first, int32_t n_scen, uint64_t seed,
-                  int32_t amp, uint32_t kind_mask, int64_t *iter_out, int64_t *rank_end_out,
-                  int64_t *peak_out, int64_t *start_out, int64_t *finish_out, int32_t n_threads,
-                  char *err, int errlen) {
+// Overrides (rows f1/f3/f4, optional, [N] in the oracle's node order = rank-major program order):
+// node_dur replaces the template durations (groups last the max of their members'), node_alloc /
+// node_free the memory deltas.
+int oracle_replay_ov(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
+                     const int64_t *static_mem, const int64_t *node_dur, const int64_t *node_alloc,
+                     const int64_t *node_free, int32_t scen_first, int32_t n_scen, uint64_t seed,
+                     int32_t amp, uint32_t kind_mask, int64_t *iter_out, int64_t *rank_end_out,
+                     int64_t *peak_out, int64_t *start_out, int64_t *finish_out, int32_t n_threads,
+                     char *err, int errlen) {
   if (n_scen < 0 || amp < 0 || amp > 65535 || n_threads < 1 || !iter_out) {
     put_err(err, errlen, "bad arguments");
     return E_INVALID_ARG;
   }
   Graph g;
   int st = expand(*t, ops, n_ops, tmpl_ptr, static_mem, g);
+  if (st) { put_err(err, errlen, g.err); return st; }
+  st = apply_overrides(g, node_dur, node_alloc, node_free);
   if (st) { put_err(err, errlen, g.err); return st; }
   std::vector<int> status(n_scen, OK);
   std::vector<std::string> msgs(n_scen);
@@ -434,7 +463,7 @@ int oracle_replay(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tm
     for (int j = tid; j < n_scen; j += n_threads) {
       int k = scen_first + j;
       for (size_t gi = 0; gi < g.groups.size(); ++gi) gd[gi] = group_dur(g.groups[gi], k, seed, amp, kind_mask);
-      auto nd = [&](int32_t n) { return node_dur(g, n, k, seed, amp, kind_mask); };
+      auto nd = [&](int32_t n) { return node_duration(g, n, k, seed, amp, kind_mask); };
       int s2 = replay(g, nd, gd, start, finish, msgs[j]);
       if (s2) { status[j] = s2; continue; }
       int64_t T = 0;
@@ -461,6 +490,75 @@ int oracle_replay(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tm
   }
   for (int j = 0; j < n_scen; ++j)
     if (status[j]) { put_err(err, errlen, msgs[j]); return status[j]; }
+  return OK;
+}
+
+int oracle_replay(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
+                  const int64_t *static_mem, int32_t scen_first, int32_t n_scen, uint64_t seed,
+                  int32_t amp, uint32_t kind_mask, int64_t *iter_out, int64_t *rank_end_out,
+                  int64_t *peak_out, int64_t *start_out, int64_t *finish_out, int32_t n_threads,
+                  char *err, int errlen) {
+  return oracle_replay_ov(t, ops, n_ops, tmpl_ptr, static_mem, nullptr, nullptr, nullptr, scen_first, n_scen,
+                          seed, amp, kind_mask, iter_out, rank_end_out, peak_out, start_out, finish_out,
+                          n_threads, err, errlen);
+}
+
+// Row f3 (what-if attribution): the critical path of scenario k, walked back from the
+// node that finishes last (T; lowest node id on ties). A compute node was started by its stream
+// predecessor. A synchronization node finished with the group reaching the max (start + dur') over
+// its groups (lowest uid on ties); that group started when its latest member became ready (max
+// ready = finish of the member's stream predecessor; lowest member id on ties), so the walk
+// continues at that member's predecessor; it stops at a node whose start is 0 with no predecessor
+// edge. path_out receives the visited nodes, last first (n_out = count; capacity cap).
+int oracle_critical_path(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
+                         const int64_t *static_mem, const int64_t *node_dur, int32_t k, uint64_t seed,
+                         int32_t amp, uint32_t kind_mask, int32_t *path_out, int64_t cap, int64_t *n_out,
+                         int64_t *T_out, char *err, int errlen) {
+  Graph g;
+  int st = expand(*t, ops, n_ops, tmpl_ptr, static_mem, g);
+  if (st) { put_err(err, errlen, g.err); return st; }
+  st = apply_overrides(g, node_dur, nullptr, nullptr);
+  if (st) { put_err(err, errlen, g.err); return st; }
+  std::vector<int64_t> gd(g.groups.size()), start, finish;
+  for (size_t gi = 0; gi < g.groups.size(); ++gi) gd[gi] = group_dur(g.groups[gi], k, seed, amp, kind_mask);
+  std::string e2;
+  st = replay(g, [&](int32_t n) { return node_duration(g, n, k, seed, amp, kind_mask); }, gd, start, finish, e2);
+  if (st) { put_err(err, errlen, e2); return st; }
+  int64_t T = 0;
+  int32_t cur = -1;
+  for (int64_t n = 0; n < g.N; ++n)
+    if (finish[n] > T || cur < 0) {
+      if (cur < 0 || finish[n] > T) { T = finish[n]; cur = (int32_t)n; }
+    }
+  if (T_out) *T_out = T;
+  int64_t len = 0;
+  auto first_of_rank = [&](int32_t n) { return n == g.rank_base[g.node_rank[n]]; };
+  auto ready = [&](int32_t m) { return first_of_rank(m) ? (int64_t)0 : finish[m - 1]; };
+  while (cur >= 0) {
+    if (len < cap && path_out) path_out[len] = cur;
+    ++len;
+    int32_t next = -1;
+    if (g.node_groups[cur].empty()) {
+      if (!first_of_rank(cur)) next = cur - 1;
+    } else {
+      int32_t best = -1;
+      int64_t bf = -1;
+      for (int32_t gi : g.node_groups[cur]) {
+        int64_t gs = 0;
+        for (int32_t m : g.groups[gi].members) gs = std::max(gs, ready(m));
+        const int64_t f = gs + gd[gi];
+        if (f > bf || (f == bf && g.groups[gi].uid < g.groups[best].uid)) { bf = f; best = gi; }
+      }
+      const Group &G = g.groups[best];
+      int32_t mstar = -1;
+      int64_t mr = -1;
+      for (int32_t m : G.members)  // members sorted by id: the first max is the lowest id
+        if (ready(m) > mr) { mr = ready(m); mstar = m; }
+      if (!first_of_rank(mstar)) next = mstar - 1;
+    }
+    cur = next;
+  }
+  if (n_out) *n_out = len;
   return OK;
 }
 
