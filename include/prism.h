@@ -248,6 +248,49 @@ PRISM_API prism_status prism_shard_connect_local(prism_graph_t g, const prism_gr
  * use the same stream (then stream order suffices); `from` is left unconnected. PRISM_E_INVALID_ARG if the plans' exchange layouts or the shards differ. */
 PRISM_API prism_status prism_shard_adopt(prism_graph_t g, prism_graph_t from);
 
+/* ---- rows f1 / f3 / f4: per-node durations, memory deltas, critical path -------------------
+ *
+ * f1, inter-slice calibration (§5.3): "timing within each slice is locally accurate
+ * but not globally aligned"; the timed graph (one measured duration per node, each rank measured
+ * in the slice where it ran as a real rank) is re-timed by the same ASAP replay, which shifts a
+ * receive after its send and propagates (node_dur).
+ * f3, what-if attribution ("a fake GPU kernel that spins for the desired and
+ * optimized duration"): label overrides, per-rank compute slowdown (fault
+ * injection) and the critical path (prism_critical_path).
+ * f4, MoE imbalance (P:1745-1748 mock router): per-(stage, ep rank) durations and activation
+ * sizes enter as node_dur / node_alloc / node_free.
+ * Effective duration of node n (node order = rank-major, program order, as prism_query_rank):
+ *   d = node_dur ? node_dur[n] : template dur_ns;  d = label_dur[i] if label(n) == labels[i];
+ *   d = (d * rank_slow_q16[rank(n)]) >> 16 if node n is a compute span.
+ * A synchronization group lasts the max of its members' effective durations (reading Z2), and
+ * scenario perturbation (prism_scenarios) applies on top. Arrays are host, copied. Applies to all
+ * later replays / peak scans until reset with d == NULL (or all fields empty); invalidates the
+ * recorded replay. Errors: PRISM_E_INVALID_ARG (duration outside [0, 2^40], factor outside
+ * [0, 2^20], duplicate label), PRISM_E_UNKNOWN_LABEL (no node carries a label),
+ * PRISM_E_NEGATIVE_MEMORY (a rank's running allocation would drop below zero). */
+typedef struct {
+  const int64_t *node_dur;       /* [N] or NULL                                                  */
+  const uint32_t *labels;        /* [n_labels] label overrides ...                               */
+  const int64_t *label_dur;      /* [n_labels] ... and their durations                           */
+  int32_t n_labels;
+  int32_t pad;
+  const int32_t *rank_slow_q16;  /* [world] or NULL: compute-span factor, Q16 (65536 = 1.0)      */
+  const int64_t *node_alloc;     /* [N] or NULL: bytes allocated at the node's start             */
+  const int64_t *node_free;      /* [N] or NULL: bytes freed at the node's finish                */
+} prism_durations;
+
+PRISM_API prism_status prism_set_durations(prism_graph_t g, const prism_durations *d);
+
+/* Row f3: the critical path of scenario `scenario` of the last recorded replay, walked back from
+ * the lowest-numbered node finishing at T: a compute span continues at its stream predecessor; a
+ * synchronization node at the group with the max (start + duration') among its groups (lowest uid
+ * on ties), then at the stream predecessor of that group's latest-ready member (lowest node id on
+ * ties); the walk ends at a node with no predecessor edge. path_out[0..n) = the nodes, last first;
+ * *T_out = T. If cap < n: *n_out = n and PRISM_E_INVALID_ARG. PRISM_E_NOT_REPLAYED without a
+ * recorded replay; sharded graphs are not supported (PRISM_E_INVALID_ARG). */
+PRISM_API prism_status prism_critical_path(prism_graph_t g, int32_t scenario, int32_t *path_out, int64_t cap,
+                                           int64_t *n_out, int64_t *T_out);
+
 /* Per-op start and finish times of one rank in one scenario of the last recorded replay, in
  * program order, plus the rank's coordinates (tp, pp, dp, ep, edp). If cap < the rank's op count
  * the call writes the count to *n_ops_out and returns PRISM_E_INVALID_ARG.

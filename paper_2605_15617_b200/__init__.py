@@ -25,6 +25,7 @@ EXPORTED_SYMBOLS = [
     "prism_peak_memory_async", "prism_query_rank", "prism_graph_stats", "prism_destroy_graph",
     "prism_debug_export", "prism_plan", "prism_last_timing", "prism_last_algo",
     "prism_shard_prepare", "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
+    "prism_set_durations", "prism_critical_path",
 ]
 SHARD_HANDLE_BYTES = 64
 
@@ -61,6 +62,12 @@ class _BuildOpts(ctypes.Structure):
 class _Scenarios(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("amp_q16", ctypes.c_int32), ("seed", ctypes.c_uint64),
                 ("kind_mask", ctypes.c_uint32), ("record", ctypes.c_int32), ("algo", ctypes.c_int32)]
+
+
+class _Durations(ctypes.Structure):
+    _fields_ = [("node_dur", ctypes.c_void_p), ("labels", ctypes.c_void_p), ("label_dur", ctypes.c_void_p),
+                ("n_labels", ctypes.c_int32), ("pad", ctypes.c_int32), ("rank_slow_q16", ctypes.c_void_p),
+                ("node_alloc", ctypes.c_void_p), ("node_free", ctypes.c_void_p)]
 
 
 _ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
@@ -107,11 +114,14 @@ def lib():
         L.prism_shard_connect.argtypes = [P, P]
         L.prism_shard_connect_local.argtypes = [P, P]
         L.prism_shard_adopt.argtypes = [P, P]
+        L.prism_set_durations.argtypes = [P, P]
+        L.prism_critical_path.argtypes = [P, ctypes.c_int32, P, ctypes.c_int64, P, P]
         for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
                      "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
                      "prism_graph_stats", "prism_debug_export", "prism_plan",
                      "prism_last_timing", "prism_last_algo", "prism_shard_prepare",
-                     "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt"):
+                     "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
+                     "prism_set_durations", "prism_critical_path"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
     return _lib
@@ -269,6 +279,41 @@ class Graph:
         fin = np.zeros(max(1, n.value), np.int64)
         _check(lib().prism_query_rank(self._h, rank, scenario, _ptr(start), _ptr(fin), n.value, None, None))
         return start[: n.value], fin[: n.value], tuple(int(c) for c in coords)
+
+    # ---------------------------------------------------------------- rows f1 / f3 / f4
+    def set_durations(self, *, node_dur=None, label_dur=None, rank_slow_q16=None, node_alloc=None,
+                      node_free=None) -> None:
+        """Per-node durations (f1 calibration input), label overrides {label: ns} and per-rank
+        compute slowdown in Q16 (f3 what-if / fault injection), per-node memory deltas (f4); no
+        arguments = back to the templates. Applies to later replays (prism_set_durations)."""
+        keep = []
+
+        def arr(a, dt):
+            if a is None:
+                return None
+            a = np.ascontiguousarray(a, dtype=dt)
+            keep.append(a)
+            return a.ctypes.data
+
+        labs = sorted((label_dur or {}).items())
+        la = np.array([int(k) for k, _ in labs], np.uint32)
+        ld = np.array([int(v) for _, v in labs], np.int64)
+        d = _Durations(arr(node_dur, np.int64), arr(la, np.uint32) if len(la) else None,
+                       arr(ld, np.int64) if len(ld) else None, len(labs), 0, arr(rank_slow_q16, np.int32),
+                       arr(node_alloc, np.int64), arr(node_free, np.int64))
+        _check(lib().prism_set_durations(self._h, ctypes.byref(d)))
+
+    def critical_path(self, scenario: int = 0):
+        """(path [node ids, last first], T) of one scenario of the last recorded replay."""
+        n = ctypes.c_int64(0)
+        T = ctypes.c_int64(0)
+        st = lib().prism_critical_path(self._h, int(scenario), None, 0, ctypes.byref(n), ctypes.byref(T))
+        if st not in (0, 1):
+            _check(st)
+        path = np.zeros(max(1, n.value), np.int32)
+        _check(lib().prism_critical_path(self._h, int(scenario), _ptr(path), n.value, ctypes.byref(n),
+                                         ctypes.byref(T)))
+        return path[: n.value], int(T.value)
 
     # ---------------------------------------------------------------- row e: sharding
     def shard_prepare(self, n_scenarios: int) -> bytes:

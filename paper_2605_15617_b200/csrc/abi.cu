@@ -149,6 +149,8 @@ struct prism_graph_s {
   int64_t launches = 0;
   bool oom = false;
   std::vector<unsigned char> staging;  // packed host tables of the build upload
+  std::vector<uint32_t> tmpl_labels;     // template labels / memory deltas (override validation)
+  std::vector<int64_t> tmpl_alloc, tmpl_free;
   // profiling events: 0/1 expand, 2/3 levels, 4 tail end, 5 reduce end, 6/7 peak
   bool profile = false;
   cudaEvent_t ev[8] = {};
@@ -159,6 +161,16 @@ struct prism_graph_s {
       ev_done[i] = true;
     }
   }
+
+  // rows f1/f3/f4: per-node duration / memory overrides (prism_set_durations)
+  bool ov_active = false;
+  DevGraph dov{};
+  unsigned char *ov = nullptr;
+  size_t ov_bytes = 0;
+  const DevGraph &cur() const { return ov_active ? dov : dg; }
+  // critical-path scratch
+  int32_t *crit = nullptr;
+  size_t crit_bytes = 0;
 
   void *dalloc(size_t bytes) {
     if (bytes == 0) bytes = 16;
@@ -206,6 +218,8 @@ struct prism_graph_s {
     dfree(acc);
     dfree(sync_words);
     dfree(part);
+    dfree(ov);
+    dfree(crit);
     pin_give(h_status);
     for (auto &b : blocks) dfree(b.first);
     cudaStreamSynchronize(stream);
@@ -299,6 +313,14 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   }
   G->plan = std::move(plan);
   const Plan &P = G->plan;
+  G->tmpl_labels.resize(tmpl->n_ops);
+  G->tmpl_alloc.resize(tmpl->n_ops);
+  G->tmpl_free.resize(tmpl->n_ops);
+  for (int64_t i = 0; i < tmpl->n_ops; ++i) {
+    G->tmpl_labels[i] = tmpl->ops[i].label;
+    G->tmpl_alloc[i] = tmpl->ops[i].mem_alloc;
+    G->tmpl_free[i] = tmpl->ops[i].mem_free;
+  }
   DevGraph &d = G->dg;
   d.W = (int32_t)P.W;
   d.pp = P.topo.pp;
@@ -524,10 +546,10 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     if (!G->connected) return fail(PRISM_E_INVALID_ARG, "sharded graph: call prism_shard_prepare and prism_shard_connect first");
     if (S != G->ex_S) return fail(PRISM_E_INVALID_ARG, "sharded graph: the replay's scenario count must equal prism_shard_prepare's");
     if (sc->algo == PRISM_ALGO_LEVELS) return fail(PRISM_E_INVALID_ARG, "sharded replays run on the cell kernel only");
-    if (!cells_fit(G->dg, cell_chunks)) return fail(PRISM_E_INVALID_ARG, "sharded replay: the shard's cells do not fit co-resident on the device");
+    if (!cells_fit(G->cur(), cell_chunks)) return fail(PRISM_E_INVALID_ARG, "sharded replay: the shard's cells do not fit co-resident on the device");
   }
   if (sc->algo != PRISM_ALGO_LEVELS) {
-    cells = cells_fit(G->dg, cell_chunks);
+    cells = cells_fit(G->cur(), cell_chunks);
     if (!cells && sc->algo == PRISM_ALGO_CELLS)
       return fail(PRISM_E_INVALID_ARG, "PRISM_ALGO_CELLS: the cells of this graph do not fit co-resident on the device");
   }
@@ -571,9 +593,9 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     uint32_t *arrive = (uint32_t *)(G->ex + G->link.o_arrive);
     G->rec(2);
     trace("shard: launch cells");
-    const int per_launch = cells_chunks_per_launch(G->dg, nchunks);
+    const int per_launch = cells_chunks_per_launch(G->cur(), nchunks);
     for (int ch = 0; ch < nchunks; ch += per_launch) {
-      CU(launch_cells(G->dg, p, rslot, acc, arrive, status, G->parity, p.record ? G->fin : nullptr, G->fin_node0,
+      CU(launch_cells(G->cur(), p, rslot, acc, arrive, status, G->parity, p.record ? G->fin : nullptr, G->fin_node0,
                       G->gfin, G->rank_end, ch, std::min(per_launch, nchunks - ch), Sp, &G->link, G->stream));
       ++launches;
     }
@@ -584,7 +606,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     trace("shard: memsets");
     G->rec(3);
     G->rec(4);
-    CU(launch_shard_reduce(G->dg, G->link, S, Sp, G->rank_end, G->part, iter_dev, status, G->stream));
+    CU(launch_shard_reduce(G->cur(), G->link, S, Sp, G->rank_end, G->part, iter_dev, status, G->stream));
     trace("shard: reduce launched");
     CU(cudaMemcpyAsync(G->h_status, status, 4, cudaMemcpyDeviceToHost, G->stream));
     trace("shard: status copy");
@@ -608,9 +630,9 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     CU(cudaMemsetAsync(G->sync_words, 0, nwords * 4, G->stream));
     G->rec(2);
     uint32_t *status = G->sync_words + (size_t)P.G_large * nchunks;
-    const int per_launch = cells_chunks_per_launch(G->dg, nchunks);
+    const int per_launch = cells_chunks_per_launch(G->cur(), nchunks);
     for (int ch = 0; ch < nchunks; ch += per_launch) {
-      CU(launch_cells(G->dg, p, G->rslot, G->acc, G->sync_words, status, G->parity,
+      CU(launch_cells(G->cur(), p, G->rslot, G->acc, G->sync_words, status, G->parity,
                       p.record ? G->fin : nullptr, 0, G->gfin, G->rank_end, ch,
                       std::min(per_launch, nchunks - ch), Sp, nullptr, G->stream));
       ++launches;
@@ -626,17 +648,17 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     for (int l = 1; l <= P.levels; ++l) {
       const int32_t t0 = G->lvl_tile_ptr[l], t1 = G->lvl_tile_ptr[l + 1];
       if (t1 == t0) continue;
-      CU(launch_level(G->dg, p, G->tiles + t0, t1 - t0, G->lvl_max_cnt[l], p.record ? G->fin : nullptr,
+      CU(launch_level(G->cur(), p, G->tiles + t0, t1 - t0, G->lvl_max_cnt[l], p.record ? G->fin : nullptr,
                       G->gfin, lanes, nchunks, G->stream));
       ++launches;
     }
     G->rec(3);
-    CU(launch_tail(G->dg, p, p.record ? G->fin : nullptr, G->gfin, G->rank_end, lanes, nchunks, G->stream));
+    CU(launch_tail(G->cur(), p, p.record ? G->fin : nullptr, G->gfin, G->rank_end, lanes, nchunks, G->stream));
     G->rec(4);
     ++launches;
   }
   if (!sharded) {
-    CU(launch_reduce(G->dg.W, S, Sp, G->rank_end, iter_dev, G->stream));
+    CU(launch_reduce(G->cur().W, S, Sp, G->rank_end, iter_dev, G->stream));
     ++launches;
   }
   G->rec(5);
@@ -685,7 +707,7 @@ prism_status prism_peak_memory_async(prism_graph_t G, int64_t *peak_dev) {
   if (!G || !peak_dev) return fail(PRISM_E_INVALID_ARG, "null argument");
   CU(cudaSetDevice(G->device));
   G->rec(6);
-  CU(launch_peak(G->dg, peak_dev, G->stream));
+  CU(launch_peak(G->cur(), peak_dev, G->stream));
   G->rec(7);
   return PRISM_OK;
 }
@@ -696,7 +718,7 @@ prism_status prism_peak_memory(prism_graph_t G, int64_t *peak_out) {
   const size_t bytes = std::max<size_t>(16, (size_t)G->plan.W * 8);
   if (!G->ensure(G->scratch, G->scratch_bytes, bytes)) return fail(PRISM_E_OOM, "scratch allocation failed");
   G->rec(6);
-  CU(launch_peak(G->dg, G->scratch, G->stream));
+  CU(launch_peak(G->cur(), G->scratch, G->stream));
   G->rec(7);
   CU(cudaMemcpyAsync(peak_out, G->scratch, (size_t)G->plan.W * 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaStreamSynchronize(G->stream));
@@ -737,11 +759,156 @@ prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, i
   CU(cudaSetDevice(G->device));
   const size_t bytes = (size_t)n * 16;
   if (!G->ensure(G->scratch, G->scratch_bytes, bytes)) return fail(PRISM_E_OOM, "scratch allocation failed");
-  CU(launch_query(G->dg, G->last, G->last_Sp, G->fin, G->fin_node0, G->gfin, rank, scenario, G->scratch,
+  CU(launch_query(G->cur(), G->last, G->last_Sp, G->fin, G->fin_node0, G->gfin, rank, scenario, G->scratch,
                   G->scratch + n, G->stream));
   CU(cudaMemcpyAsync(start_ns, G->scratch, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaMemcpyAsync(finish_ns, G->scratch + n, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaStreamSynchronize(G->stream));
+  return check_status(G);
+}
+
+// ---- rows f1 / f3 / f4: per-node durations and memory deltas, critical path ---------------
+
+prism_status prism_set_durations(prism_graph_t G, const prism_durations *d) {
+  if (!G) return fail(PRISM_E_INVALID_ARG, "null graph");
+  CU(cudaSetDevice(G->device));
+  const Plan &P = G->plan;
+  G->recorded = 0;
+  const bool any = d && (d->node_dur || d->n_labels > 0 || d->rank_slow_q16 || d->node_alloc || d->node_free);
+  if (!any) {
+    G->ov_active = false;
+    return PRISM_OK;
+  }
+  const int64_t N = P.N, W = P.W, Gn = P.G, M = P.M;
+  if (d->n_labels < 0 || (d->n_labels > 0 && (!d->labels || !d->label_dur)))
+    return fail(PRISM_E_INVALID_ARG, "label overrides: n_labels >= 0 with both arrays");
+  // host validation (the device never sees a malformed override)
+  if (d->node_dur)
+    for (int64_t n = 0; n < N; ++n)
+      if (d->node_dur[n] < 0 || d->node_dur[n] > (1LL << 40))
+        return fail(PRISM_E_INVALID_ARG, "node_dur[" + std::to_string(n) + "] outside [0, 2^40]");
+  std::vector<std::pair<uint32_t, int64_t>> lab;
+  if (d->n_labels > 0) {
+    std::vector<uint32_t> have;
+    have.reserve(64);
+    for (int s = 0; s < P.topo.pp; ++s)  // every template op is instantiated on tp*dp >= 1 ranks
+      for (int64_t i = 0; i < P.stage_len[s]; ++i) have.push_back(G->tmpl_labels[P.stage_op0[s] + i]);
+    std::sort(have.begin(), have.end());
+    for (int32_t i = 0; i < d->n_labels; ++i) {
+      if (d->label_dur[i] < 0 || d->label_dur[i] > (1LL << 40)) return fail(PRISM_E_INVALID_ARG, "label duration outside [0, 2^40]");
+      if (!std::binary_search(have.begin(), have.end(), d->labels[i])) {
+        char b[64];
+        std::snprintf(b, sizeof b, "no node carries label 0x%x", d->labels[i]);
+        return fail(PRISM_E_UNKNOWN_LABEL, b);
+      }
+      lab.emplace_back(d->labels[i], d->label_dur[i]);
+    }
+    std::sort(lab.begin(), lab.end());
+    for (size_t i = 1; i < lab.size(); ++i)
+      if (lab[i].first == lab[i - 1].first) return fail(PRISM_E_INVALID_ARG, "duplicate label override");
+  }
+  if (d->rank_slow_q16)
+    for (int64_t r = 0; r < W; ++r)
+      if (d->rank_slow_q16[r] < 0 || d->rank_slow_q16[r] > (1 << 20))
+        return fail(PRISM_E_INVALID_ARG, "rank_slow_q16 outside [0, 2^20] (a factor of at most 16)");
+  if (d->node_alloc || d->node_free) {  // running allocation of every rank never negative
+    std::vector<int64_t> rank_len(W);
+    for (int64_t r = 0; r < W; ++r) {
+      const int64_t s = P.topo.order == PRISM_ORDER_MEGATRON ? r / ((int64_t)P.topo.tp * P.topo.dp) : (r / P.topo.tp) % P.topo.pp;
+      rank_len[r] = P.stage_len[s];
+    }
+    int64_t n = 0;
+    for (int64_t r = 0; r < W; ++r) {
+      int64_t run = 0;
+      for (int64_t i = 0; i < rank_len[r]; ++i, ++n) {
+        const int64_t s = P.topo.order == PRISM_ORDER_MEGATRON ? r / ((int64_t)P.topo.tp * P.topo.dp) : (r / P.topo.tp) % P.topo.pp;
+        const int64_t a = d->node_alloc ? d->node_alloc[n] : G->tmpl_alloc[P.stage_op0[s] + i];
+        const int64_t f = d->node_free ? d->node_free[n] : G->tmpl_free[P.stage_op0[s] + i];
+        if (a < 0 || f < 0) return fail(PRISM_E_INVALID_ARG, "negative memory delta");
+        run += a - f;
+        if (run < 0) return fail(PRISM_E_NEGATIVE_MEMORY, "running allocation of rank " + std::to_string(r) + " drops below zero");
+      }
+    }
+  }
+  // one device block: inputs + derived arrays
+  size_t off = 0;
+  auto carve = [&off](size_t bytes) {
+    off = (off + 255) & ~(size_t)255;
+    const size_t o = off;
+    off += std::max<size_t>(bytes, 8);
+    return o;
+  };
+  const size_t L = lab.size();
+  const size_t o_base = d->node_dur ? carve(N * 8) : 0, o_lab = carve(L * 4), o_ldur = carve(L * 8);
+  const size_t o_rf = d->rank_slow_q16 ? carve(W * 4) : 0;
+  const size_t o_al = d->node_alloc ? carve(N * 8) : 0, o_fr = d->node_free ? carve(N * 8) : 0;
+  const size_t o_eff = carve(N * 8), o_gd = carve(Gn * 8), o_sd = carve(N * 8), o_hd = carve(M * 8);
+  const size_t total = off;
+  if (!G->ensure(G->ov, G->ov_bytes, total)) return fail(PRISM_E_OOM, "duration override allocation failed");
+  unsigned char *B = G->ov;
+  cudaStream_t st = G->stream;
+  std::vector<uint32_t> hl(L);
+  std::vector<int64_t> hd(L);
+  for (size_t i = 0; i < L; ++i) {
+    hl[i] = lab[i].first;
+    hd[i] = lab[i].second;
+  }
+  if (d->node_dur) CU(cudaMemcpyAsync(B + o_base, d->node_dur, N * 8, cudaMemcpyHostToDevice, st));
+  if (L) {
+    CU(cudaMemcpyAsync(B + o_lab, hl.data(), L * 4, cudaMemcpyHostToDevice, st));
+    CU(cudaMemcpyAsync(B + o_ldur, hd.data(), L * 8, cudaMemcpyHostToDevice, st));
+  }
+  if (d->rank_slow_q16) CU(cudaMemcpyAsync(B + o_rf, d->rank_slow_q16, W * 4, cudaMemcpyHostToDevice, st));
+  if (d->node_alloc) CU(cudaMemcpyAsync(B + o_al, d->node_alloc, N * 8, cudaMemcpyHostToDevice, st));
+  if (d->node_free) CU(cudaMemcpyAsync(B + o_fr, d->node_free, N * 8, cudaMemcpyHostToDevice, st));
+  DevGraph &dv = G->dov;
+  dv = G->dg;
+  int64_t *eff = (int64_t *)(B + o_eff), *gdur = (int64_t *)(B + o_gd), *sdur = (int64_t *)(B + o_sd), *hdur = (int64_t *)(B + o_hd);
+  CU(launch_durations(G->dg, d->node_dur ? (const int64_t *)(B + o_base) : nullptr, (const uint32_t *)(B + o_lab),
+                      (const int64_t *)(B + o_ldur), (int32_t)L, d->rank_slow_q16 ? (const int32_t *)(B + o_rf) : nullptr,
+                      eff, gdur, sdur, hdur, st));
+  dv.node_dur = eff;
+  dv.grp_dur = gdur;
+  dv.node_sdur = sdur;
+  dv.h_dur = hdur;
+  if (d->node_alloc) dv.node_alloc = (int64_t *)(B + o_al);
+  if (d->node_free) dv.node_free = (int64_t *)(B + o_fr);
+  dv.per_rank_dur = 1;
+  CU(cudaStreamSynchronize(st));  // the caller's host arrays may go away
+  G->ov_active = true;
+  return PRISM_OK;
+}
+
+prism_status prism_critical_path(prism_graph_t G, int32_t scenario, int32_t *path_out, int64_t cap,
+                                 int64_t *n_out, int64_t *T_out) {
+  if (!G || !n_out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  if (G->n_shards > 1) return fail(PRISM_E_INVALID_ARG, "critical path of a sharded graph is not supported");
+  if (!G->recorded) return fail(PRISM_E_NOT_REPLAYED, "no replay with record != 0 has run on this graph");
+  if (scenario < 0 || scenario >= G->last.S) return fail(PRISM_E_INVALID_ARG, "scenario outside the last replay");
+  if (cap < 0 || (cap > 0 && !path_out)) return fail(PRISM_E_INVALID_ARG, "bad path capacity");
+  CU(cudaSetDevice(G->device));
+  const Plan &P = G->plan;
+  const int64_t pc = std::min<int64_t>(cap, P.N + 1);
+  // [S iter][start node (4B, padded)][len (8B)][path]
+  const size_t need = (size_t)G->last.S * 8 + 16 + (size_t)std::max<int64_t>(pc, 1) * 4;
+  if (!G->ensure(G->crit, G->crit_bytes, need)) return fail(PRISM_E_OOM, "critical-path scratch allocation failed");
+  int64_t *iter = (int64_t *)G->crit;
+  int32_t *startn = (int32_t *)(iter + G->last.S);
+  int64_t *len = (int64_t *)(startn + 2);
+  int32_t *path = (int32_t *)(len + 1);
+  CU(launch_reduce(P.W, G->last.S, G->last_Sp, G->rank_end, iter, G->stream));
+  CU(launch_critical_path(G->cur(), G->last, G->fin, G->last_Sp, scenario, iter, startn, path, pc, len, G->stream));
+  int64_t hl = 0, hT = 0;
+  CU(cudaMemcpyAsync(&hl, len, 8, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaMemcpyAsync(&hT, iter + scenario, 8, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaStreamSynchronize(G->stream));
+  *n_out = hl;
+  if (T_out) *T_out = hT;
+  if (hl > cap) return fail(PRISM_E_INVALID_ARG, "path capacity too small: need " + std::to_string(hl));
+  if (hl > 0) {
+    CU(cudaMemcpyAsync(path_out, path, (size_t)hl * 4, cudaMemcpyDeviceToHost, G->stream));
+    CU(cudaStreamSynchronize(G->stream));
+  }
   return check_status(G);
 }
 

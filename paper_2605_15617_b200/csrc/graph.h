@@ -14,6 +14,9 @@ struct DevGraph {
   int32_t W, pp, tp, dp, ep, order;
   // row e: this shard replays the ranks with dp_i in [d0, d1) (d0 = 0, d1 = dp unsharded)
   int32_t n_shards, shard, d0, d1;
+  // rows f1/f3/f4: node_sdur / h_dur / node_dur / grp_dur point at per-node override arrays and
+  // compute spans / chained collectives last their own rank's value (prism_set_durations)
+  int32_t per_rank_dur, pad_;
   int64_t N, G, M;
   // rank tables
   int32_t *rank_ptr;        // [W+1] first node of each rank
@@ -129,6 +132,13 @@ cudaError_t launch_shard_reduce(const DevGraph &g, const ShardLink &link, int32_
                                 uint32_t *status, cudaStream_t st);
 // memory.cu
 cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st);
+// whatif.cu (rows f1/f3/f4)
+cudaError_t launch_durations(const DevGraph &g, const int64_t *base, const uint32_t *labels, const int64_t *label_dur,
+                             int32_t n_labels, const int32_t *rank_f, int64_t *eff, int64_t *gdur, int64_t *sdur,
+                             int64_t *hdur, cudaStream_t st);
+cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const int64_t *fin, int32_t Sp, int32_t k,
+                                 const int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
+                                 cudaStream_t st);
 // eager loading of the kernels that can be launched behind a running (waiting) replay
 cudaError_t preload_replay_kernels();
 cudaError_t preload_cells();

@@ -388,7 +388,9 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
   return true;
 }
 
-template <int C, bool SH>
+// PR (rows f1/f3/f4): the graph carries per-node durations (prism_set_durations), so a compute
+// span or chained collective lasts its own rank's value node_sdur[rb[r] + i], loaded one op ahead.
+template <int C, bool SH, bool PR>
 __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
                                                          int64_t *__restrict__ fin,
                                                          int64_t *__restrict__ gfin,
@@ -440,6 +442,11 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
     xo = g.x_ops[xk];
     prefetch_cross<SH>(g, xo, rsh, C, pre);
   }
+  int64_t pd[PR ? C : 1];  // PR: per-rank durations of the next op
+  if (PR) {
+#pragma unroll
+    for (int r = 0; r < C; ++r) pd[r] = len > 0 ? __ldg(g.node_sdur + rb[r]) : 0;
+  }
   // op records of the cell's first rank (the template is shared; the per-rank part of a compute
   // span's uid is rk[r]), 32 ops per coalesced round trip, next batch in flight
   uint32_t ncls = 2;
@@ -471,14 +478,22 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
       const int32_t i = base + j;
       c_n = __shfl_sync(0xffffffffu, bcls, (j + 1) & 31);
       d_n = __shfl_sync(0xffffffffu, bd, (j + 1) & 31);
+      int64_t dr[PR ? C : 1];  // PR: this op's per-rank durations (loaded during the previous op)
+      if (PR) {
+#pragma unroll
+        for (int r = 0; r < C; ++r) {
+          dr[r] = pd[r];
+          if (i + 1 < len) pd[r] = __ldg(g.node_sdur + rb[r] + i + 1);
+        }
+      }
       if (c == 0) {  // compute span: every rank waits out its own perturbed duration
         if (cpert) {
           const uint64_t ix = (uint64_t)i * K_MIX;
 #pragma unroll
-          for (int r = 0; r < C; ++r) t[r] += perturb_x(d, sx ^ (rk[r] + ix), p);
+          for (int r = 0; r < C; ++r) t[r] += perturb_x(PR ? dr[r] : d, sx ^ (rk[r] + ix), p);
         } else {
 #pragma unroll
-          for (int r = 0; r < C; ++r) t[r] += d;
+          for (int r = 0; r < C; ++r) t[r] += PR ? dr[r] : d;
         }
       } else if (c == 1) {  // in-cell TP collective: register-local segmented max
         const uint64_t ux = __shfl_sync(0xffffffffu, bux, j);
@@ -496,10 +511,10 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
           const uint64_t um = ux * K_MIX;
           const uint64_t stepm = ((ux >> 56) == PRISM_ROLE_WORLD ? 0ull : (1ull << 24)) * K_MIX;
 #pragma unroll
-          for (int r = 0; r < C; ++r) t[r] += perturb_x(d, sx ^ (um + (uint64_t)r * stepm), p);
+          for (int r = 0; r < C; ++r) t[r] += perturb_x(PR ? dr[r] : d, sx ^ (um + (uint64_t)r * stepm), p);
         } else {
 #pragma unroll
-          for (int r = 0; r < C; ++r) t[r] += d;
+          for (int r = 0; r < C; ++r) t[r] += PR ? dr[r] : d;
         }
       } else {  // cross-cell synchronization, rank by rank (deposit all first: no self-wait)
 #ifdef PRISM_CELL_STATS
@@ -551,29 +566,32 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
 
 typedef void (*cell_fn)(DevGraph, ScenParams, CellArgs, int64_t *, int64_t *, int64_t *);
 
-template <bool SH>
+template <bool SH, bool PR>
 cell_fn cell_kernel_t(int tp) {
   switch (tp) {
-    case 1: return cell_kernel<1, SH>;
-    case 2: return cell_kernel<2, SH>;
-    case 3: return cell_kernel<3, SH>;
-    case 4: return cell_kernel<4, SH>;
-    case 5: return cell_kernel<5, SH>;
-    case 6: return cell_kernel<6, SH>;
-    case 7: return cell_kernel<7, SH>;
-    case 8: return cell_kernel<8, SH>;
+    case 1: return cell_kernel<1, SH, PR>;
+    case 2: return cell_kernel<2, SH, PR>;
+    case 3: return cell_kernel<3, SH, PR>;
+    case 4: return cell_kernel<4, SH, PR>;
+    case 5: return cell_kernel<5, SH, PR>;
+    case 6: return cell_kernel<6, SH, PR>;
+    case 7: return cell_kernel<7, SH, PR>;
+    case 8: return cell_kernel<8, SH, PR>;
     default: return nullptr;
   }
 }
 cell_fn cell_kernel_for(const DevGraph &g) {
-  return g.n_shards > 1 ? cell_kernel_t<true>(g.tp) : cell_kernel_t<false>(g.tp);
+  if (g.per_rank_dur) return g.n_shards > 1 ? cell_kernel_t<true, true>(g.tp) : cell_kernel_t<false, true>(g.tp);
+  return g.n_shards > 1 ? cell_kernel_t<true, false>(g.tp) : cell_kernel_t<false, false>(g.tp);
 }
 
 cudaError_t preload_cell_kernels() {
   cudaFuncAttributes a;
   for (int tp = 1; tp <= MAX_TP; ++tp) {
-    cudaError_t e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<false>(tp));
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<true>(tp));
+    cudaError_t e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<false, false>(tp));
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<true, false>(tp));
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<false, true>(tp));
+    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<true, true>(tp));
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -1,0 +1,183 @@
+// whatif.cu — rows f1, f3, f4 on the replay engine: per-node durations / memory deltas and the
+// critical path.
+//
+//  * f1 inter-slice calibration (§5.3): the timed graph filled slice by slice (each
+//    rank's nodes measured while it ran as a real rank) is re-timed by the same ASAP replay, which
+//    "shift[s] the receive to occur after the send" and propagates; the input is one measured
+//    duration per node.
+//  * f3 what-if ("a fake GPU kernel that spins for the desired and optimized
+//    duration"; SPEC S:488-505 what_if / fault_inject): label overrides and per-rank compute
+//    slowdown (P:1751-1760 thermal throttling), then the critical path that decides T.
+//  * f4 MoE imbalance (P:1745-1748 mock router): per-(stage, ep-rank) expert / all-to-all
+//    durations and activation sizes arrive as per-node durations and memory deltas.
+// Effective duration of node n: base (measured, else template) -> label override -> (d * f_r) >> 16
+// for compute spans of rank r. A synchronization group lasts the max of its members' effective
+// durations (reading Z2). The replay kernels read these through pointer-swapped DevGraph arrays.
+#include <cuda_runtime.h>
+
+#include "graph.h"
+
+namespace prism {
+
+namespace {
+
+constexpr uint64_t K_GOLD = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t K_MIX = 0xBF58476D1CE4E5B9ULL;
+
+// Effective per-node durations. labels/label_dur sorted by label (binary search).
+__global__ void __launch_bounds__(256) eff_kernel(DevGraph g, const int64_t *__restrict__ base,
+                                                  const uint32_t *__restrict__ labels,
+                                                  const int64_t *__restrict__ label_dur, int32_t n_labels,
+                                                  const int32_t *__restrict__ rank_f, int64_t *__restrict__ eff) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N; n += (int64_t)gridDim.x * blockDim.x) {
+    int64_t d = base ? base[n] : g.node_dur[n];
+    if (n_labels > 0) {
+      const uint32_t L = g.node_label[n];
+      int32_t lo = 0, hi = n_labels - 1;
+      while (lo <= hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        const uint32_t v = labels[mid];
+        if (v == L) {
+          d = label_dur[mid];
+          break;
+        }
+        if (v < L) lo = mid + 1;
+        else hi = mid - 1;
+      }
+    }
+    if (rank_f && g.node_kind[n] == PRISM_KIND_COMPUTE) d = (d * (int64_t)rank_f[g.node_rank[n]]) >> 16;
+    eff[n] = d;
+  }
+}
+
+// Group durations = max over members' effective durations (Z2); then the per-node replay record
+// (compute: own; sync: its first group's) and the per-slot record of the cell kernel.
+__global__ void __launch_bounds__(256) grp_dur_kernel(DevGraph g, const int64_t *__restrict__ eff,
+                                                      int64_t *__restrict__ gdur) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < g.G; x += (int64_t)gridDim.x * blockDim.x) {
+    int64_t m = 0;
+    for (int32_t j = g.grp_ptr[x]; j < g.grp_ptr[x + 1]; ++j) m = max(m, eff[g.grp_mem[j]]);
+    gdur[x] = m;
+  }
+}
+
+__global__ void __launch_bounds__(256) records_kernel(DevGraph g, const int64_t *__restrict__ eff,
+                                                      const int64_t *__restrict__ gdur,
+                                                      int64_t *__restrict__ sdur, int64_t *__restrict__ hdur) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N; n += stride) {
+    const int32_t h0 = g.node_gptr[n], h1 = g.node_gptr[n + 1];
+    sdur[n] = h0 == h1 ? eff[n] : gdur[g.node_grp[h0]];
+  }
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < g.M; h += stride) hdur[h] = gdur[g.node_grp[h]];
+}
+
+__device__ __forceinline__ int64_t perturb_x(int64_t d, uint64_t x, const ScenParams &p) {
+  uint64_t z = x + K_GOLD;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  const uint32_t v = (uint32_t)(z >> 40);
+  const uint64_t low = p.mod_magic * (uint64_t)v;
+  const uint32_t r = (uint32_t)__umul64hi(low, (uint64_t)(uint32_t)p.mod);
+  return (d * (int64_t)(r + (uint32_t)(65536 - p.amp))) >> 16;
+}
+
+// Row f3, step 1: T_k and the lowest node finishing at T_k.
+__global__ void __launch_bounds__(256) crit_start_kernel(DevGraph g, const int64_t *__restrict__ fin,
+                                                         int32_t Sp, int32_t k, const int64_t *__restrict__ iter,
+                                                         int32_t *__restrict__ out_node) {
+  const int64_t T = iter[k];
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N; n += (int64_t)gridDim.x * blockDim.x)
+    if (fin[n * Sp + k] == T) atomicMin(out_node, (int32_t)n);
+}
+
+// Row f3, step 2: the walk back (one warp; lanes split a group's members). Rules = the oracle's
+// (oracle/prism_oracle.cpp oracle_critical_path): compute span <- stream predecessor; sync node <-
+// its group with the max (start + dur') (lowest uid on ties) <- that group's latest-ready member
+// (lowest node id on ties) <- the member's stream predecessor; stop when there is none.
+__global__ void __launch_bounds__(32) crit_walk_kernel(DevGraph g, ScenParams p, const int64_t *__restrict__ fin,
+                                                       int32_t Sp, int32_t k, const int32_t *__restrict__ start_node,
+                                                       int32_t *__restrict__ path, int64_t cap,
+                                                       int64_t *__restrict__ len_out) {
+  const int lane = threadIdx.x;
+  int32_t cur = *start_node;
+  if (cur < 0 || cur >= g.N) cur = -1;  // empty graph: empty path
+  int64_t len = 0;
+  auto first = [&](int32_t n) { return g.rank_ptr[g.node_rank[n]] == n; };
+  auto ready = [&](int32_t m) -> int64_t { return first(m) ? 0 : fin[(int64_t)(m - 1) * Sp + k]; };
+  while (cur >= 0) {
+    if (lane == 0 && len < cap) path[len] = cur;
+    ++len;
+    int32_t next = -1;
+    const int32_t h0 = g.node_gptr[cur], h1 = g.node_gptr[cur + 1];
+    if (h0 == h1) {
+      if (!first(cur)) next = cur - 1;
+    } else {
+      int64_t bf = -1;
+      uint64_t buid = 0;
+      int32_t bg = -1;
+      for (int32_t h = h0; h < h1; ++h) {
+        const int32_t gi = g.node_grp[h];
+        int64_t gs = 0;
+        for (int32_t j = g.grp_ptr[gi] + lane; j < g.grp_ptr[gi + 1]; j += 32) gs = max(gs, ready(g.grp_mem[j]));
+        for (int off = 16; off; off >>= 1) gs = max(gs, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)gs, off));
+        const uint64_t uid = g.grp_uid[gi];
+        const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
+        int64_t d = g.grp_dur[gi];
+        if ((p.mask & gb) && p.amp > 0 && k > 0) d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ (uid * K_MIX), p);
+        const int64_t f = gs + d;
+        if (f > bf || (f == bf && uid < buid)) {
+          bf = f;
+          buid = uid;
+          bg = gi;
+        }
+      }
+      // latest-ready member of the chosen group, lowest node id on ties
+      int64_t br = -1;
+      int32_t bm = 0x7FFFFFFF;
+      for (int32_t j = g.grp_ptr[bg] + lane; j < g.grp_ptr[bg + 1]; j += 32) {
+        const int32_t m = g.grp_mem[j];
+        const int64_t r = ready(m);
+        if (r > br || (r == br && m < bm)) {
+          br = r;
+          bm = m;
+        }
+      }
+      for (int off = 16; off; off >>= 1) {
+        const int64_t r2 = (int64_t)__shfl_xor_sync(0xffffffffu, (long long)br, off);
+        const int32_t m2 = __shfl_xor_sync(0xffffffffu, bm, off);
+        if (r2 > br || (r2 == br && m2 < bm)) {
+          br = r2;
+          bm = m2;
+        }
+      }
+      if (!first(bm)) next = bm - 1;
+    }
+    cur = next;
+  }
+  if (lane == 0) *len_out = len;
+}
+
+}  // namespace
+
+cudaError_t launch_durations(const DevGraph &g, const int64_t *base, const uint32_t *labels, const int64_t *label_dur,
+                             int32_t n_labels, const int32_t *rank_f, int64_t *eff, int64_t *gdur, int64_t *sdur,
+                             int64_t *hdur, cudaStream_t st) {
+  const int blocks = 148 * 8;
+  if (g.N > 0) eff_kernel<<<blocks, 256, 0, st>>>(g, base, labels, label_dur, n_labels, rank_f, eff);
+  if (g.G > 0) grp_dur_kernel<<<blocks, 256, 0, st>>>(g, eff, gdur);
+  if (g.N > 0 || g.M > 0) records_kernel<<<blocks, 256, 0, st>>>(g, eff, gdur, sdur, hdur);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const int64_t *fin, int32_t Sp, int32_t k,
+                                 const int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
+                                 cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(scratch, 0x7F, 4, st);
+  if (e != cudaSuccess) return e;
+  if (g.N > 0) crit_start_kernel<<<148 * 4, 256, 0, st>>>(g, fin, Sp, k, iter, scratch);
+  crit_walk_kernel<<<1, 32, 0, st>>>(g, p, fin, Sp, k, scratch, path, cap, len_out);
+  return cudaGetLastError();
+}
+
+}  // namespace prism
