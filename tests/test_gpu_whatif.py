@@ -156,3 +156,17 @@ def test_critical_path_configs(prism, name):
         path, T = g.critical_path(k)
         rpath, rT = oracle.critical_path(tm, k, amp_q16=6554, kind_mask=7)
         assert T == rT and np.array_equal(path, rpath), (name, k, len(path), len(rpath))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_moe_imbalance_fig3(prism, seed):
+    """f4: the Fig. 3 br profile on the C4-shaped MoE graph: per-node expert / A2A
+    durations and activation sizes; iteration times and every rank's peak equal the oracle's."""
+    import workloads.moe as M
+
+    tm = w.scaled("C4")
+    s = M.derive_schedule(M.FIG3_PROFILE, 32, tm.topo.ep, seed=seed)
+    d, a, f = M.moe_overrides(tm, s)
+    g, ref = _check(prism, tm, 33, d, node_alloc=a, node_free=f)
+    base = oracle.replay(tm, 1)
+    assert ref["peak"][0].max() > base["peak"][0].max()  # imbalance raises the worst rank's peak
