@@ -227,6 +227,9 @@ def run_prism(args):
 
     if rank != 0:
         return None
+    frows = None
+    if ws == 1 and not args.no_f_rows:
+        frows = f_rows_extra(args, tm, sh)
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args)
@@ -264,6 +267,7 @@ def run_prism(args):
             "emulated_iterations_per_s": round(S * (1 if sharded else ws) / (ms_step / 1e3), 2),
             "iteration_time_ns_scenario0": int(iters[0]),
             "device_ms": {k: round(v, 4) for k, v in med.items()},
+            "next_rows": frows,
         },
         "roofline": {
             "bound": "hbm",
@@ -284,6 +288,71 @@ def run_prism(args):
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
+    return out
+
+
+def f_rows_extra(args, tm, sh):
+    """SURVEY.md §8 rows f1/f3/f4 on the same engine, measured once on this GPU (device ms from
+    CUDA events on the graph's stream; node-scenarios/s of the replay):
+      f1 calibration: the benchmark graph re-timed with per-node 'measured' durations (template
+         +-5 % per node, the shape of a slice-filled timed graph), S scenarios on top;
+      f3 what-if: every attention-forward span overridden + one rank slowed 12 % (fault
+         injection), then the critical path of scenario 0 (device walk-back, wall ms);
+      f4 MoE imbalance: C4 (DeepSeek-V3-shaped, EP 64) under the Fig. 3 br profile."""
+    import numpy as np
+
+    import paper_2605_15617_b200 as prism
+    import workloads as w
+    import workloads.moe as moe
+
+    S = args.scenarios
+    kw = dict(amp_q16=args.amp, kind_mask=7, seed=0x5EED)
+    out = {}
+
+    def node_durations(t):
+        parts = []
+        for r in range(t.topo.world):
+            s = (r // t.topo.tp) % t.topo.pp if t.topo.rank_order == 0 else r // (t.topo.tp * t.topo.dp)
+            parts.append(t.stage(s)["dur_ns"])
+        return np.concatenate(parts).astype(np.int64)
+
+    def timed_replay(g, n):
+        best = None
+        for _ in range(3):
+            g.replay(S, record=True, **kw)
+            ms = g.last_timing()["levels"]
+            best = ms if best is None else min(best, ms)
+        return {"replay_ms": round(best, 4), "value": round(n * S / (best / 1e3), 1), "unit": "node-scenarios/s"}
+
+    g = prism.Graph(tm, stream=sh, profile=True)
+    N = g.stats()["nodes"]
+    d = node_durations(tm)
+    d = d * np.random.default_rng(1).integers(95, 106, len(d)) // 100
+    t0 = time.perf_counter()
+    g.set_durations(node_dur=d)
+    set_ms = (time.perf_counter() - t0) * 1e3
+    out["f1_calibrate"] = dict(timed_replay(g, N), set_durations_ms=round(set_ms, 3),
+                               workload=f"{args.config} with per-node measured durations")
+    labs = {int(l): 1 for l in np.unique(tm.ops["label"]) if (int(l) >> 24) == w.OPCODES["ATTN_F"]}
+    f = np.full(tm.topo.world, 65536, np.int32)
+    f[tm.topo.world // 2] = int(1.12 * 65536)
+    g.set_durations(label_dur=labs, rank_slow_q16=f)
+    r = timed_replay(g, N)
+    t0 = time.perf_counter()
+    path, T = g.critical_path(0)
+    cp_ms = (time.perf_counter() - t0) * 1e3
+    out["f3_whatif"] = dict(r, critical_path_ms=round(cp_ms, 3), critical_path_nodes=int(len(path)),
+                            iteration_ns=int(T), workload=f"{args.config}, ATTN_F -> 1 ns, rank {tm.topo.world // 2} x1.12")
+    g.close()
+    c4 = w.config("C4")
+    sched = moe.derive_schedule(moe.FIG3_PROFILE, 64, c4.topo.ep, seed=0)
+    md, ma, mf = moe.moe_overrides(c4, sched)
+    g = prism.Graph(c4, stream=sh, profile=True)
+    g.set_durations(node_dur=md, node_alloc=ma, node_free=mf)
+    r = timed_replay(g, g.stats()["nodes"])
+    pk = g.peak_memory()
+    out["f4_moe_imbalance"] = dict(r, peak_max_bytes=int(pk.max()), workload="C4 under the Fig. 3 br profile")
+    g.close()
     return out
 
 
@@ -367,6 +436,7 @@ def main():
     ap.add_argument("--amp", type=int, default=6554)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU work of the cpu_baseline sample")
+    ap.add_argument("--no-f-rows", action="store_true", help="skip the rows f1/f3/f4 measurements in extra")
     ap.add_argument("--algo", default="auto", choices=["auto", "levels", "cells"])
     ap.add_argument("--shard", default="ranks", choices=["ranks", "replicas"],
                     help="N>1: shard the ranks over the GPUs (row e) or run independent replicas")
