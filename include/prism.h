@@ -106,8 +106,10 @@ typedef struct {
   uint8_t coll;      /* PRISM_COLL_* (COLLECTIVE only)                                        */
   uint8_t role;      /* PRISM_ROLE_TP..WORLD (COLLECTIVE only)                                */
   uint8_t p2p_mask;  /* PRISM_P2P_* bits, nonzero (P2P only)                                  */
-  uint8_t stream;    /* must be 0 (single stream per rank)                                    */
-  uint8_t pad0[3];
+  uint8_t stream;    /* 0..3: the rank's stream the op is issued on (row f2; 0 = single stream) */
+  uint8_t ev_record; /* 0, or 1 + e: the op's finish records event slot e (e < 8)  (row f2)    */
+  uint8_t ev_wait;   /* 0, or 1 + e: the op starts after the latest record of event slot e   */
+  uint8_t pad0;
   uint32_t label;    /* user tag (queries / what-if); not interpreted                         */
   uint32_t pad1;
   int64_t dur_ns;    /* >= 0, <= 2^40. For sync ops: this member's duration of the occurrence */

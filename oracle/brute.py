@@ -5,7 +5,8 @@ A second, independent statement of what the replay computes, used to pin the C++
 equals the makespan of the ASAP schedule").
 
 The graph is rewritten as a plain vertex-weighted DAG:
-  * one vertex per compute node, weight = its duration, with an edge from its stream predecessor;
+  * one vertex per compute node, weight = its duration, with an edge from its stream predecessor
+    (and, row f2, from the latest earlier op recording the event slot it waits on);
   * one vertex per sync group, weight = the group's duration (max of its members' op durations,
     reading Z2), with an edge from the stream predecessor of each member (all
     participants must reach the operation before any can proceed);
@@ -45,15 +46,28 @@ def expand(tm, node_dur=None):
     nodes: List[Tuple[int, int, object]] = []
     rank_nodes: List[List[int]] = []
     groups: Dict[tuple, List[Tuple[int, int]]] = {}
+    dpreds: Dict[int, List[int]] = {}
     for r in range(W):
         tpi, s, dpi, epi, edpi = _coords(topo, r)
         tmpl = tm.stage(s)
         occ: Dict[object, int] = {}
         mine = []
+        last_on: Dict[int, int] = {}
+        last_rec: Dict[int, int] = {}
         for i, op in enumerate(tmpl):
             n = len(nodes)
             nodes.append((r, i, op))
             mine.append(n)
+            # row f2: directional predecessors = previous op of the stream + event source
+            ps = []
+            if int(op["stream"]) in last_on:
+                ps.append(last_on[int(op["stream"])])
+            if int(op["ev_wait"]) and (int(op["ev_wait"]) - 1) in last_rec:
+                ps.append(last_rec[int(op["ev_wait"]) - 1])
+            dpreds[n] = ps
+            last_on[int(op["stream"])] = n
+            if int(op["ev_record"]):
+                last_rec[int(op["ev_record"]) - 1] = n
             if op["kind"] == 1:
                 role = int(op["role"])
                 gid = {1: (s, dpi), 2: (tpi, s), 3: (tpi, s, edpi), 4: (tpi, s, epi), 5: ()}[role]
@@ -69,7 +83,7 @@ def expand(tm, node_dur=None):
                         occ[("b", bit)] = k + 1
                         groups.setdefault(("P", sender, d, k), []).append((n, _d(op, n, node_dur)))
         rank_nodes.append(mine)
-    return nodes, rank_nodes, groups
+    return nodes, rank_nodes, groups, dpreds
 
 
 def _d(op, n, node_dur):
@@ -78,7 +92,7 @@ def _d(op, n, node_dur):
 
 def iteration_time(tm, node_dur=None) -> Tuple[int, List[int]]:
     """(T, finish per node) by exhaustive path enumeration."""
-    nodes, rank_nodes, groups = expand(tm, node_dur)
+    nodes, rank_nodes, groups, dpreds = expand(tm, node_dur)
     # vertices: ("n", node) for every node; ("g", key) for groups
     weight: Dict[tuple, int] = {}
     preds: Dict[tuple, List[tuple]] = {}
@@ -96,16 +110,13 @@ def iteration_time(tm, node_dur=None) -> Tuple[int, List[int]]:
                     preds[v].append(("g", key))
             else:
                 weight[v] = _d(nodes[n][2], n, node_dur)
-                if j > 0:
-                    preds[v].append(("n", mine[j - 1]))
+                preds[v].extend(("n", p) for p in dpreds[n])
     for key, mem in groups.items():
         g = ("g", key)
         weight[g] = max(d for _, d in mem)
         preds[g] = []
         for n, _ in mem:
-            r, i, _op = nodes[n]
-            if i > 0:
-                preds[g].append(("n", rank_nodes[r][i - 1]))
+            preds[g].extend(("n", p) for p in dpreds[n])
     succ: Dict[tuple, List[tuple]] = {v: [] for v in weight}
     for v, ps in preds.items():
         for p in ps:

@@ -18,6 +18,10 @@
 //      sync node arrives at each of its groups; when a group has all members, it starts at the
 //      max of their arrival times and lasts its duration; a member finishes when all of its
 //      groups have finished (max). Iteration time = max finish.
+//      Row f2 (P:699, P:1729 overlapped communication): a rank issues its ops in template order
+//      onto up to 4 streams; a node is released when the previous op of its stream AND (if it
+//      waits on event slot e) the latest earlier op recording e have finished (CUDA-event
+//      semantics; a wait on a never-recorded slot is satisfied at once).
 //   4. Peak memory (P:1578 max_memory_allocated): per rank, events +alloc at op start and
 //      -free at op finish sorted by (time, event index), prefix-summed; peak = static + max(0,
 //      max prefix). A negative running total is an error.
@@ -40,7 +44,7 @@
 namespace {
 
 struct Op {  // one template record, 48 bytes (input format)
-  uint8_t kind, coll, role, p2p_mask, stream, pad0[3];
+  uint8_t kind, coll, role, p2p_mask, stream, ev_record, ev_wait, pad0;
   uint32_t label, pad1;
   int64_t dur, bytes, alloc, free_;
 };
@@ -132,6 +136,9 @@ struct Graph {
   std::vector<std::vector<int32_t>> node_groups;  // group indices per node (in insertion order)
   std::vector<Group> groups;
   std::vector<int64_t> static_of_rank;
+  // row f2 (multi-stream ranks): the previous op issued on the node's stream, and the latest op
+  // issued before it that records the event slot it waits on (-1 = none)
+  std::vector<int32_t> spred, esrc;
   // rows f1/f3/f4: optional per-node overrides of the template durations / memory deltas
   const int64_t *nd_ov = nullptr, *alloc_ov = nullptr, *free_ov = nullptr;
   std::string err;
@@ -169,7 +176,7 @@ int expand(const Topo &t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
     if (tmpl_ptr[s + 1] < tmpl_ptr[s]) { g.err = "tmpl_ptr not monotone"; return E_INVALID_ARG; }
   for (int64_t i = 0; i < n_ops; ++i) {
     const Op &o = ops[i];
-    bool ok = o.kind <= 2 && o.stream == 0 && o.dur >= 0 && o.dur <= (1LL << 40) && o.bytes >= 0 &&
+    bool ok = o.kind <= 2 && o.stream < 4 && o.ev_record <= 8 && o.ev_wait <= 8 && o.dur >= 0 && o.dur <= (1LL << 40) && o.bytes >= 0 &&
               o.alloc >= 0 && o.free_ >= 0;
     if (o.kind == 1) ok = ok && o.role >= 1 && o.role <= 5 && o.coll <= 5;
     if (o.kind == 2) ok = ok && o.p2p_mask >= 1 && o.p2p_mask <= 15 && t.pp > 1;
@@ -196,6 +203,8 @@ int expand(const Topo &t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
   g.node_tidx.resize(g.N);
   g.node_op.resize(g.N);
   g.node_groups.assign(g.N, {});
+  g.spred.assign(g.N, -1);
+  g.esrc.assign(g.N, -1);
   g.static_of_rank.resize(W);
 
   // key: (role, gid, occurrence) -> group index
@@ -220,6 +229,7 @@ int expand(const Topo &t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
     g.static_of_rank[r] = static_mem[s];
     int64_t prev_rank = rank_of(t, c.tp, (s - 1 + t.pp) % t.pp, c.dp);
     int64_t next_rank = rank_of(t, c.tp, (s + 1) % t.pp, c.dp);
+    int32_t last_on[4] = {-1, -1, -1, -1}, last_rec[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
     int64_t occ_role[6] = {0, 0, 0, 0, 0, 0};
     int64_t occ_bit[4] = {0, 0, 0, 0};
     for (int64_t i = tmpl_ptr[s]; i < tmpl_ptr[s + 1]; ++i) {
@@ -229,6 +239,10 @@ int expand(const Topo &t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
       g.node_rank[n] = (int32_t)r;
       g.node_tidx[n] = (int32_t)ti;
       g.node_op[n] = &o;
+      g.spred[n] = last_on[o.stream];
+      g.esrc[n] = o.ev_wait ? last_rec[o.ev_wait - 1] : -1;
+      last_on[o.stream] = n;
+      if (o.ev_record) last_rec[o.ev_record - 1] = n;
       if (o.kind == 1) {
         int64_t occ = occ_role[o.role]++;
         int32_t gi = get_group(o.role, group_id(t, o.role, c), occ);
@@ -325,16 +339,27 @@ int replay(const Graph &g, const std::function<int64_t(int32_t)> &ndur,
       }
     }
   };
-  for (int64_t r = 0; r < g.W; ++r)
-    if (g.rank_base[r + 1] > g.rank_base[r]) release((int32_t)g.rank_base[r], 0);
+  // directional edges ("one operation must complete before another begins"): the stream
+  // predecessor and, row f2, the event source; a node is released once all have finished
+  std::vector<int32_t> deps(N, 0);
+  std::vector<int64_t> rdy(N, 0);
+  std::vector<std::vector<int32_t>> succ(N);
+  for (int64_t n = 0; n < N; ++n) {
+    if (g.spred[n] >= 0) { ++deps[n]; succ[g.spred[n]].push_back((int32_t)n); }
+    if (g.esrc[n] >= 0) { ++deps[n]; succ[g.esrc[n]].push_back((int32_t)n); }
+  }
+  for (int64_t n = 0; n < N; ++n)
+    if (deps[n] == 0) release((int32_t)n, 0);
   while (!heap.empty()) {
     Ev e = heap.top();
     heap.pop();
     int32_t n = e.second;
     finish[n] = e.first;
     ++done;
-    int32_t r = g.node_rank[n];
-    if (n + 1 < g.rank_base[r + 1]) release(n + 1, e.first);
+    for (int32_t d : succ[n]) {
+      rdy[d] = std::max(rdy[d], e.first);
+      if (--deps[d] == 0) release(d, rdy[d]);
+    }
   }
   if (done != N) {
     int64_t incomplete = 0;
@@ -408,9 +433,10 @@ int oracle_expand(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tm
   for (size_t gi = 0; gi < g.groups.size(); ++gi) {
     int64_t mx = 0;
     for (int32_t m : g.groups[gi].members) {
-      // ready(m) = finish of its stream predecessor (0 if first)
-      int32_t r = g.node_rank[m];
-      int64_t ready = (m > g.rank_base[r]) ? lv_fin[m - 1] : 0;
+      // ready(m) = finish of its directional predecessors (stream, event source), 0 if none
+      int64_t ready = 0;
+      if (g.spred[m] >= 0) ready = std::max(ready, lv_fin[g.spred[m]]);
+      if (g.esrc[m] >= 0) ready = std::max(ready, lv_fin[g.esrc[m]]);
       mx = std::max(mx, ready);
     }
     glevel[gi] = mx + 1;
@@ -509,7 +535,8 @@ int oracle_replay(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tm
 // its groups (lowest uid on ties); that group started when its latest member became ready (max
 // ready = finish of the member's stream predecessor; lowest member id on ties), so the walk
 // continues at that member's predecessor; it stops at a node whose start is 0 with no predecessor
-// edge. path_out receives the visited nodes, last first (n_out = count; capacity cap).
+// edge (a node's predecessor: its stream predecessor or event source, whichever finished later,
+// the lower id on ties). path_out receives the visited nodes, last first (n_out = count; capacity cap).
 int oracle_critical_path(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
                          const int64_t *static_mem, const int64_t *node_dur, int32_t k, uint64_t seed,
                          int32_t amp, uint32_t kind_mask, int32_t *path_out, int64_t cap, int64_t *n_out,
@@ -532,14 +559,22 @@ int oracle_critical_path(const Topo *t, const Op *ops, int64_t n_ops, const int6
     }
   if (T_out) *T_out = T;
   int64_t len = 0;
-  auto first_of_rank = [&](int32_t n) { return n == g.rank_base[g.node_rank[n]]; };
-  auto ready = [&](int32_t m) { return first_of_rank(m) ? (int64_t)0 : finish[m - 1]; };
+  // a node's ready time is the finish of its latest directional predecessor (stream predecessor
+  // or, row f2, event source; the lower node id on ties), 0 without one
+  auto pred = [&](int32_t n) -> int32_t {
+    const int32_t a = g.spred[n], b = g.esrc[n];
+    if (a < 0) return b;
+    if (b < 0) return a;
+    if (finish[a] != finish[b]) return finish[a] > finish[b] ? a : b;
+    return std::min(a, b);
+  };
+  auto ready = [&](int32_t m) { const int32_t p = pred(m); return p < 0 ? (int64_t)0 : finish[p]; };
   while (cur >= 0) {
     if (len < cap && path_out) path_out[len] = cur;
     ++len;
     int32_t next = -1;
     if (g.node_groups[cur].empty()) {
-      if (!first_of_rank(cur)) next = cur - 1;
+      next = pred(cur);
     } else {
       int32_t best = -1;
       int64_t bf = -1;
@@ -554,7 +589,7 @@ int oracle_critical_path(const Topo *t, const Op *ops, int64_t n_ops, const int6
       int64_t mr = -1;
       for (int32_t m : G.members)  // members sorted by id: the first max is the lowest id
         if (ready(m) > mr) { mr = ready(m); mstar = m; }
-      if (!first_of_rank(mstar)) next = mstar - 1;
+      next = pred(mstar);
     }
     cur = next;
   }

@@ -34,7 +34,9 @@ OP_DTYPE = np.dtype(
         ("role", "u1"),
         ("p2p_mask", "u1"),
         ("stream", "u1"),
-        ("pad0", "u1", (3,)),
+        ("ev_record", "u1"),
+        ("ev_wait", "u1"),
+        ("pad0", "u1"),
         ("label", "<u4"),
         ("pad1", "<u4"),
         ("dur_ns", "<i8"),
@@ -103,20 +105,24 @@ class _StageBuilder:
     def __init__(self) -> None:
         self.rows: List[tuple] = []
 
-    def op(self, kind, dur, *, coll=0, role=0, mask=0, label=0, nbytes=0, alloc=0, free=0):
-        self.rows.append((kind, coll, role, mask, 0, (0, 0, 0), label, 0, int(dur), int(nbytes),
-                          int(alloc), int(free)))
+    def op(self, kind, dur, *, coll=0, role=0, mask=0, label=0, nbytes=0, alloc=0, free=0, stream=0,
+           record=None, wait=None):
+        """record / wait: event slot (0..7) recorded at the op's finish / waited for before its start
+        (row f2: multi-stream ranks, CUDA-event semantics)."""
+        self.rows.append((kind, coll, role, mask, stream, 0 if record is None else record + 1,
+                          0 if wait is None else wait + 1, 0, label, 0, int(dur), int(nbytes), int(alloc),
+                          int(free)))
 
-    def compute(self, dur, label=0, alloc=0, free=0):
-        self.op(KIND_COMPUTE, dur, label=label, alloc=alloc, free=free)
+    def compute(self, dur, label=0, alloc=0, free=0, **kw):
+        self.op(KIND_COMPUTE, dur, label=label, alloc=alloc, free=free, **kw)
 
-    def coll(self, role, coll, dur, label=0, nbytes=0, alloc=0, free=0):
+    def coll(self, role, coll, dur, label=0, nbytes=0, alloc=0, free=0, **kw):
         self.op(KIND_COLLECTIVE, dur, coll=coll, role=role, label=label, nbytes=nbytes,
-                alloc=alloc, free=free)
+                alloc=alloc, free=free, **kw)
 
-    def p2p(self, mask, dur, label=0, nbytes=0):
+    def p2p(self, mask, dur, label=0, nbytes=0, **kw):
         if mask:
-            self.op(KIND_P2P, dur, mask=mask, label=label, nbytes=nbytes)
+            self.op(KIND_P2P, dur, mask=mask, label=label, nbytes=nbytes, **kw)
 
     def array(self) -> np.ndarray:
         return np.array(self.rows, dtype=OP_DTYPE)
@@ -636,7 +642,7 @@ def scaled(name: str, shrink: int = 8) -> Templates:
 # random template fuzz (acyclic by construction)
 # ---------------------------------------------------------------------------------------------
 def random_templates(seed: int, max_world: int = 64, max_ops: int = 40,
-                     max_dur: int = 1000, p_span0: float = 0.05) -> Templates:
+                     max_dur: int = 1000, p_span0: float = 0.05, streams: int = 1) -> Templates:
     """Random topology and per-stage templates whose sync structure is acyclic by construction:
     stage-spanning sync events (P2P messages between ring neighbours, WORLD collectives) are drawn
     from ONE global sequence that every stage follows in the same order; intra-stage collectives
@@ -728,6 +734,18 @@ def random_templates(seed: int, max_world: int = 64, max_ops: int = 40,
         for a in live:
             if rng.random() < 0.7:
                 b.compute(dur(), label=7, free=a)
-        stages.append(b.array())
+        arr = b.array()
+        if streams > 1:  # row f2: random streams and CUDA-event record / wait pairs
+            srng = np.random.default_rng(seed * 7919 + s)
+            arr["stream"] = srng.integers(0, streams, len(arr))
+            rec = srng.random(len(arr)) < 0.3
+            arr["ev_record"] = np.where(rec, srng.integers(1, 5, len(arr)), 0)
+            wt = srng.random(len(arr)) < 0.3
+            arr["ev_wait"] = np.where(wt, srng.integers(1, 5, len(arr)), 0)
+            # program-order memory deltas are not time-consistent across streams
+            arr["mem_alloc"] = 0
+            arr["mem_free"] = 0
+        stages.append(arr)
         static.append(int(rng.integers(0, 1 << 20)))
-    return assemble(topo, stages, static, f"random{seed}", {"seed": seed})
+    return assemble(topo, stages, static, f"random{seed}" + (f"_s{streams}" if streams > 1 else ""),
+                    {"seed": seed})
