@@ -209,6 +209,14 @@ PRISM_API prism_status prism_replay_async(prism_graph_t g, const prism_scenarios
 PRISM_API prism_status prism_peak_memory(prism_graph_t g, int64_t *peak_bytes_out);
 PRISM_API prism_status prism_peak_memory_async(prism_graph_t g, int64_t *peak_bytes_dev_out);
 
+/* Row f2 (multi-stream ranks): per-rank peak memory with the events in TIME order, (time, event
+ * index), of scenario `scenario` of the last recorded replay (the starts and finishes the replay
+ * computed). For single-stream graphs this equals prism_peak_memory (program order = time order,
+ * reading Z6); prism_peak_memory / _async of a multi-stream graph compute it for scenario 0.
+ * PRISM_E_NOT_REPLAYED without a recorded replay; PRISM_E_NEGATIVE_MEMORY if a running total
+ * drops below zero in time order; PRISM_E_INVALID_ARG beyond 4096 ops per rank or when sharded. */
+PRISM_API prism_status prism_peak_memory_at(prism_graph_t g, int32_t scenario, int64_t *peak_bytes_out);
+
 /* ---- multi-GPU (row e): rank sharding with a fused peer-memory exchange ---------------------
  *
  * The ranks are partitioned by DP block: shard i owns every rank whose dp coordinate lies in

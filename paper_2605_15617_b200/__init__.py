@@ -25,7 +25,7 @@ EXPORTED_SYMBOLS = [
     "prism_peak_memory_async", "prism_query_rank", "prism_graph_stats", "prism_destroy_graph",
     "prism_debug_export", "prism_plan", "prism_last_timing", "prism_last_algo",
     "prism_shard_prepare", "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
-    "prism_set_durations", "prism_critical_path",
+    "prism_set_durations", "prism_critical_path", "prism_peak_memory_at",
 ]
 SHARD_HANDLE_BYTES = 64
 
@@ -115,13 +115,14 @@ def lib():
         L.prism_shard_connect_local.argtypes = [P, P]
         L.prism_shard_adopt.argtypes = [P, P]
         L.prism_set_durations.argtypes = [P, P]
+        L.prism_peak_memory_at.argtypes = [P, ctypes.c_int32, P]
         L.prism_critical_path.argtypes = [P, ctypes.c_int32, P, ctypes.c_int64, P, P]
         for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
                      "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
                      "prism_graph_stats", "prism_debug_export", "prism_plan",
                      "prism_last_timing", "prism_last_algo", "prism_shard_prepare",
                      "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
-                     "prism_set_durations", "prism_critical_path"):
+                     "prism_set_durations", "prism_critical_path", "prism_peak_memory_at"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
     return _lib
@@ -263,6 +264,12 @@ class Graph:
     def peak_memory(self) -> np.ndarray:
         out = np.zeros(self.topo.tp * self.topo.pp * self.topo.dp, np.int64)
         _check(lib().prism_peak_memory(self._h, _ptr(out)))
+        return out
+
+    def peak_memory_at(self, scenario: int = 0) -> np.ndarray:
+        """Row f2: per-rank peak with events in time order, scenario of the last recorded replay."""
+        out = np.zeros(self.topo.tp * self.topo.pp * self.topo.dp, np.int64)
+        _check(lib().prism_peak_memory_at(self._h, int(scenario), _ptr(out)))
         return out
 
     def peak_memory_async(self, peak_dev_ptr: int) -> None:

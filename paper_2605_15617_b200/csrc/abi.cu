@@ -127,6 +127,7 @@ struct prism_graph_s {
   uint32_t *h_status = nullptr;    // pinned copy of the status word
   int last_algo = 0;
   int recorded = 0;
+  bool status_is_memory = false;  // h_status holds a time-ordered memory scan's status
   // fin keeps rows [fin_node0, fin_node0 + fin_rows) (all nodes unless sharded)
   int64_t fin_node0 = 0, fin_rows = 0;
   // row e: sharding (n_shards > 1)
@@ -369,6 +370,8 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t o_ss0 = carve(P.stage_slot0.size() * 8), o_slq = carve(nslot * 4), o_sltd = carve(nslot * 4);
   const size_t o_slr = carve(nslot), o_slf = carve(nslot), o_chq = carve(nch * 4), o_chm = carve(nch * 8);
   const size_t o_tcls = carve(nops), o_xptr = carve((pp + 1) * 4), o_xops = carve(P.x_ops.size() * sizeof(XOp));
+  const bool ms = P.multistream;
+  const size_t o_tms = ms ? carve(nops * 2) : 0, o_tsp2 = ms ? carve(nops * 4) : 0, o_tes = ms ? carve(nops * 4) : 0;
   const size_t table_bytes = off;
   // graph arrays (written by the expand kernels)
   const size_t o_rp = carve((W + 1) * 4), o_rs = carve((W + 1) * 4), o_rst = carve(W * 4);
@@ -379,6 +382,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t o_nsd = carve(N * 8), o_nuid = carve(N * 8), o_gxb = carve(Gn * 8), o_gli = carve(Gn * 4);
   const size_t o_hb = carve(M * 4), o_hm = carve(M * 4), o_hd = carve(M * 8), o_hu = carve(M * 8);
   const size_t o_hs = n_shards > 1 ? carve(M * 4) : 0;
+  const size_t o_nmsk = ms ? carve(N * 2) : 0, o_nsp = ms ? carve(N * 4) : 0, o_nes = ms ? carve(N * 4) : 0;
   const size_t total = off;
   unsigned char *base = G->take<unsigned char>(total);
   if (G->oom || !base) return fail(PRISM_E_OOM, "device allocation failed while building the graph");
@@ -404,6 +408,10 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.t_cls = (const uint8_t *)at(o_tcls);
   d.x_ptr = (const int32_t *)at(o_xptr);
   d.x_ops = (const XOp *)at(o_xops);
+  d.ms = ms ? 1 : 0;
+  d.t_ms = ms ? (const uint16_t *)at(o_tms) : nullptr;
+  d.t_spred = ms ? (const int32_t *)at(o_tsp2) : nullptr;
+  d.t_esrc = ms ? (const int32_t *)at(o_tes) : nullptr;
   d.rank_ptr = (int32_t *)at(o_rp);
   d.rank_slot = (int32_t *)at(o_rs);
   d.rank_stage = (int32_t *)at(o_rst);
@@ -432,6 +440,9 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.h_dur = (int64_t *)at(o_hd);
   d.h_uid = (uint64_t *)at(o_hu);
   d.h_smask = n_shards > 1 ? (uint32_t *)at(o_hs) : nullptr;
+  d.node_ms = ms ? (uint16_t *)at(o_nmsk) : nullptr;
+  d.node_spred = ms ? (int32_t *)at(o_nsp) : nullptr;
+  d.node_esrc = ms ? (int32_t *)at(o_nes) : nullptr;
   d.M_cross = P.M_cross;
   d.G_large = P.G_large;
   cudaStream_t s = G->stream;
@@ -460,6 +471,11 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     put(o_tcls, P.t_cls.data(), nops);
     put(o_xptr, P.x_ptr.data(), (pp + 1) * 4);
     put(o_xops, P.x_ops.data(), P.x_ops.size() * sizeof(XOp));
+    if (ms) {
+      put(o_tms, P.t_ms.data(), nops * 2);
+      put(o_tsp2, P.t_spred.data(), nops * 4);
+      put(o_tes, P.t_esrc.data(), nops * 4);
+    }
     CU(cudaMemcpyAsync(base, h.data(), table_bytes, cudaMemcpyHostToDevice, s));
   }
   if (opts && (opts->flags & PRISM_BUILD_PROFILE)) {
@@ -553,6 +569,9 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     if (!cells && sc->algo == PRISM_ALGO_CELLS)
       return fail(PRISM_E_INVALID_ARG, "PRISM_ALGO_CELLS: the cells of this graph do not fit co-resident on the device");
   }
+  if (!cells && G->plan.multistream)
+    return fail(PRISM_E_INVALID_ARG, "multi-stream graphs (row f2) replay on the cell kernel only, and its "
+                                     "one-rank-per-warp units do not fit co-resident on this device");
   int lanes = 32;
   if (!cells)
     for (lanes = 1; lanes < S && lanes < 32;) lanes <<= 1;
@@ -703,26 +722,73 @@ prism_status prism_replay(prism_graph_t G, const prism_scenarios *sc, int64_t *i
   return check_status(G);
 }
 
+// Peak memory into a device array: program order (single-stream graphs, any time) or, for
+// multi-stream graphs and prism_peak_memory_at, time order of `scenario` of the recorded replay.
+static prism_status peak_impl(prism_graph_t G, int32_t scenario, bool time_ordered, int64_t *peak_dev) {
+  const Plan &P = G->plan;
+  if (!time_ordered) {
+    G->rec(6);
+    CU(launch_peak(G->cur(), peak_dev, G->stream));
+    G->rec(7);
+    return PRISM_OK;
+  }
+  if (!G->recorded)
+    return fail(PRISM_E_NOT_REPLAYED, "time-ordered peak memory needs a replay with record != 0 (multi-stream graphs)");
+  if (scenario < 0 || scenario >= G->last.S) return fail(PRISM_E_INVALID_ARG, "scenario outside the last replay");
+  if (G->n_shards > 1) return fail(PRISM_E_INVALID_ARG, "time-ordered peak memory of a sharded graph is not supported");
+  int64_t max_len = 0;
+  for (int s = 0; s < P.topo.pp; ++s) max_len = std::max(max_len, P.stage_len[s]);
+  if (max_len > kMaxTimeOrderedOps)
+    return fail(PRISM_E_INVALID_ARG, "time-ordered peak memory supports at most 4096 ops per rank");
+  if (!G->h_status && !(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status word unavailable");
+  if (!G->ensure(G->sync_words, G->sync_bytes, std::max<size_t>(G->sync_bytes, 16))) return fail(PRISM_E_OOM, "status allocation failed");
+  uint32_t *status = G->sync_words;  // word 0 (the replays re-zero their words before use)
+  CU(cudaMemsetAsync(status, 0, 4, G->stream));
+  G->rec(6);
+  CU(launch_peak_time(G->cur(), G->last, G->last_Sp, G->fin, G->fin_node0, G->gfin, scenario, (int32_t)max_len,
+                      peak_dev, status, G->stream));
+  G->rec(7);
+  CU(cudaMemcpyAsync(G->h_status, status, 4, cudaMemcpyDeviceToHost, G->stream));
+  G->status_is_memory = true;
+  return PRISM_OK;
+}
+
+static prism_status memory_status(prism_graph_t G) {
+  if (G->status_is_memory) {
+    G->status_is_memory = false;
+    if (*G->h_status == PRISM_E_NEGATIVE_MEMORY) {
+      *G->h_status = 0;
+      return fail(PRISM_E_NEGATIVE_MEMORY, "a rank's running allocation drops below zero in time order");
+    }
+  }
+  return PRISM_OK;
+}
+
 prism_status prism_peak_memory_async(prism_graph_t G, int64_t *peak_dev) {
   if (!G || !peak_dev) return fail(PRISM_E_INVALID_ARG, "null argument");
   CU(cudaSetDevice(G->device));
-  G->rec(6);
-  CU(launch_peak(G->cur(), peak_dev, G->stream));
-  G->rec(7);
-  return PRISM_OK;
+  return peak_impl(G, 0, G->plan.multistream, peak_dev);
+}
+
+static prism_status peak_host(prism_graph_t G, int32_t scenario, bool time_ordered, int64_t *peak_out) {
+  CU(cudaSetDevice(G->device));
+  const size_t bytes = std::max<size_t>(16, (size_t)G->plan.W * 8);
+  if (!G->ensure(G->scratch, G->scratch_bytes, bytes)) return fail(PRISM_E_OOM, "scratch allocation failed");
+  prism_status st = peak_impl(G, scenario, time_ordered, G->scratch);
+  if (st) return st;
+  CU(cudaMemcpyAsync(peak_out, G->scratch, (size_t)G->plan.W * 8, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaStreamSynchronize(G->stream));
+  return memory_status(G);
 }
 
 prism_status prism_peak_memory(prism_graph_t G, int64_t *peak_out) {
   if (!G || !peak_out) return fail(PRISM_E_INVALID_ARG, "null argument");
-  CU(cudaSetDevice(G->device));
-  const size_t bytes = std::max<size_t>(16, (size_t)G->plan.W * 8);
-  if (!G->ensure(G->scratch, G->scratch_bytes, bytes)) return fail(PRISM_E_OOM, "scratch allocation failed");
-  G->rec(6);
-  CU(launch_peak(G->cur(), G->scratch, G->stream));
-  G->rec(7);
-  CU(cudaMemcpyAsync(peak_out, G->scratch, (size_t)G->plan.W * 8, cudaMemcpyDeviceToHost, G->stream));
-  CU(cudaStreamSynchronize(G->stream));
-  return PRISM_OK;
+  return peak_host(G, 0, G->plan.multistream, peak_out);
+}
+
+prism_status prism_peak_memory_at(prism_graph_t G, int32_t scenario, int64_t *peak_out) {
+  if (!G || !peak_out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  return peak_host(G, scenario, true, peak_out);
 }
 
 prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, int64_t *start_ns,

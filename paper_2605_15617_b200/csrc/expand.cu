@@ -136,6 +136,12 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
       g.node_free[n] = o.mem_free;
       g.node_prev_sync[n] = tps < 0 ? -1 : rb + tps;
       g.node_gptr[n] = slot0 + g.t_slot_ptr[op0 + i];
+      if (g.ms) {  // row f2
+        const int32_t sp = g.t_spred[op0 + i], es = g.t_esrc[op0 + i];
+        g.node_ms[n] = g.t_ms[op0 + i];
+        g.node_spred[n] = sp < 0 ? -1 : rb + sp;
+        g.node_esrc[n] = es < 0 ? -1 : rb + es;
+      }
       if (o.kind == PRISM_KIND_COMPUTE) {  // sync nodes get their record from their first slot
         g.node_cls[n] = 0;
         g.node_sdur[n] = o.dur_ns;

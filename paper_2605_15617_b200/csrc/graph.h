@@ -16,7 +16,16 @@ struct DevGraph {
   int32_t n_shards, shard, d0, d1;
   // rows f1/f3/f4: node_sdur / h_dur / node_dur / grp_dur point at per-node override arrays and
   // compute spans / chained collectives last their own rank's value (prism_set_durations)
-  int32_t per_rank_dur, pad_;
+  int32_t per_rank_dur;
+  // row f2: multi-stream ranks (one rank per warp; per-node stream / event fields and directional
+  // predecessors, -1 = none)
+  int32_t ms;
+  const uint16_t *t_ms;      // per template op: stream | ev_record << 4 | ev_wait << 8
+  const int32_t *t_spred;    // per template op: previous op of its stream (template index)
+  const int32_t *t_esrc;     // per template op: event source (template index)
+  uint16_t *node_ms;         // [N] (multi-stream graphs only)
+  int32_t *node_spred;       // [N]
+  int32_t *node_esrc;        // [N]
   int64_t N, G, M;
   // rank tables
   int32_t *rank_ptr;        // [W+1] first node of each rank
@@ -130,6 +139,12 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
 cudaError_t launch_shard_reduce(const DevGraph &g, const ShardLink &link, int32_t S, int32_t Sp,
                                 const int64_t *rank_end, int64_t *part_local, int64_t *iter,
                                 uint32_t *status, cudaStream_t st);
+// row f2: time-ordered peak memory of scenario k of a recorded replay (max_len = longest rank,
+// <= kMaxTimeOrderedOps)
+constexpr int32_t kMaxTimeOrderedOps = 4096;
+cudaError_t launch_peak_time(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin, int64_t node0,
+                             const int64_t *gfin, int32_t k, int32_t max_len, int64_t *peak, uint32_t *status,
+                             cudaStream_t st);
 // memory.cu
 cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st);
 // whatif.cu (rows f1/f3/f4)

@@ -102,7 +102,8 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     for (int64_t i = a; i < b; ++i) {
       const prism_op &o = tm.ops[i];
       int32_t ti = (int32_t)(i - a);
-      bool ok = o.kind <= PRISM_KIND_P2P && o.stream == 0 && o.dur_ns >= 0 &&
+      bool ok = o.kind <= PRISM_KIND_P2P && o.stream < kMaxStreams && o.ev_record <= kMaxEvents &&
+                o.ev_wait <= kMaxEvents && o.dur_ns >= 0 &&
                 o.dur_ns <= (1LL << 40) && o.bytes >= 0 && o.mem_alloc >= 0 && o.mem_free >= 0;
       if (o.kind == PRISM_KIND_COLLECTIVE)
         ok = ok && o.role >= PRISM_ROLE_TP && o.role <= PRISM_ROLE_WORLD && o.coll <= PRISM_COLL_BARRIER;
@@ -111,6 +112,7 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
         err = fmt("malformed op %lld (stage %lld, index %lld)", i, s, ti);
         return PRISM_E_INVALID_ARG;
       }
+      if (o.stream != 0 || o.ev_record || o.ev_wait) P.multistream = true;
       run += o.mem_alloc;
       run -= o.mem_free;
       if (run < 0) {
@@ -138,6 +140,26 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     P.stage_slots[s] = slots;
   }
 
+  // row f2: per template op, the previous op of its stream and the event source (template
+  // indices, -1 = none) and the packed stream/event byte of the cell kernel
+  P.t_spred.assign(tm.n_ops, -1);
+  P.t_esrc.assign(tm.n_ops, -1);
+  P.t_ms.assign(tm.n_ops, 0);
+  if (P.multistream)
+    for (int s = 0; s < pp; ++s) {
+      int32_t last_on[kMaxStreams], last_rec[kMaxEvents];
+      for (auto &x : last_on) x = -1;
+      for (auto &x : last_rec) x = -1;
+      for (int64_t i = tm.tmpl_ptr[s]; i < tm.tmpl_ptr[s + 1]; ++i) {
+        const prism_op &o = tm.ops[i];
+        const int32_t ti = (int32_t)(i - tm.tmpl_ptr[s]);
+        P.t_spred[i] = last_on[o.stream];
+        P.t_esrc[i] = o.ev_wait ? last_rec[o.ev_wait - 1] : -1;
+        P.t_ms[i] = (uint16_t)(o.stream | (o.ev_record << 4) | (o.ev_wait << 8));
+        last_on[o.stream] = ti;
+        if (o.ev_record) last_rec[o.ev_record - 1] = ti;
+      }
+    }
   // replay classes (cell kernel) and per-stage cross-op lists
   P.t_cls.assign(tm.n_ops, 0);
   {
@@ -166,14 +188,16 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
         const prism_op &o = tm.ops[i];
         uint8_t c = 0;
         if (o.kind == PRISM_KIND_COLLECTIVE) {
+          // multi-stream graphs (row f2) replay one rank per warp: a TP group is cross-warp, and
+          // the chained-collective shortcut needs a single stream
           if (o.role == PRISM_ROLE_TP) {
-            c = 1;
+            c = P.multistream ? 2 : 1;
           } else if (o.role == PRISM_ROLE_WORLD) {
-            c = (k < (int32_t)wchain.size() && wchain[k]) ? 3 : 2;
+            c = (!P.multistream && k < (int32_t)wchain.size() && wchain[k]) ? 3 : 2;
             ++k;
           } else {
             const bool same = i > a && tm.ops[i - 1].kind == PRISM_KIND_COLLECTIVE && tm.ops[i - 1].role == o.role;
-            c = same ? 3 : 2;
+            c = (same && !P.multistream) ? 3 : 2;
           }
         } else if (o.kind == PRISM_KIND_P2P) {
           c = 2;
@@ -389,7 +413,7 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     // other group exchanges ready times through global ready slots
     g.xbase = -1;
     g.lbase = -1;
-    if (g.type != PRISM_ROLE_TP) {
+    if (g.type != PRISM_ROLE_TP || P.multistream) {
       if (g.size <= kSmallGroup) {
         g.xbase = X;
         X += (int64_t)g.inst * g.size;

@@ -24,6 +24,9 @@ namespace prism {
 // Cross-cell groups with at most this many members use the value-as-flag protocol of the cell
 // kernel (ready slots); larger ones use max-accumulators + arrival counters.
 constexpr int32_t kSmallGroup = 8;
+// Row f2: streams per rank and CUDA-event slots of the template format.
+constexpr int32_t kMaxStreams = 4;
+constexpr int32_t kMaxEvents = 8;
 
 // One quotient group: a template-level synchronization (all concrete instances are symmetric
 // under the topology, so level / duration / member positions are per quotient group).
@@ -76,6 +79,12 @@ struct Plan {
   // that immediately follows a collective of the same group, so every member is ready exactly at
   // that group's shared finish and start = own ready time (exact)
   std::vector<uint8_t> t_cls;
+  // row f2 (multi-stream ranks): any op off stream 0 or with an event; per template op the
+  // previous op of its stream / the event source (template index, -1) and the packed
+  // stream | ev_record << 4 | ev_wait << 8
+  bool multistream = false;
+  std::vector<int32_t> t_spred, t_esrc;
+  std::vector<uint16_t> t_ms;
   // per stage, the cross-cell ops (class 2) in template order: x_ptr[pp+1] -> XOp
   std::vector<int32_t> x_ptr;
   std::vector<XOp> x_ops;

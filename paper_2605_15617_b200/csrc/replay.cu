@@ -270,36 +270,135 @@ __global__ void __launch_bounds__(1024) shard_exchange_kernel(ShardLink L, int32
 
 // prism_query_rank: start/finish of one rank's ops in one scenario from fin/gfin.
 // fin rows start at node node0 (a sharded replay keeps only its own ranks' rows).
+// Start time of node i (rank r, first node rb) in scenario k of a recorded replay: a compute span
+// starts its perturbed duration before its finish; a node with one sync group spans exactly the
+// group occurrence; a batched P2P node starts at the max over its groups of (group finish - dur').
+__device__ __forceinline__ int64_t node_start(const DevGraph &g, const ScenParams &p, int32_t Sp,
+                                              const int64_t *fin, const int64_t *gfin, int32_t r, int32_t rb,
+                                              int32_t i, int32_t k) {
+  const int32_t h0 = g.node_gptr[i], h1 = g.node_gptr[i + 1];
+  if (h0 == h1) {  // compute span: exact, finish = start + d'
+    int64_t d = g.node_dur[i];
+    if ((p.mask & 1u) && p.amp > 0 && k > 0)
+      d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ ((((uint64_t)r << 32) | (uint32_t)(i - rb)) * K_MIX), p);
+    return fin[(int64_t)i * Sp + k] - d;
+  }
+  if (h1 - h0 == 1) {
+    const int64_t grp = g.node_grp[h0];
+    const uint32_t gbit = (g.grp_uid[grp] >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
+    int64_t d = g.grp_dur[grp];
+    if ((p.mask & gbit) && p.amp > 0 && k > 0) d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
+    return fin[(int64_t)i * Sp + k] - d;
+  }
+  int64_t st = 0;
+  for (int32_t h = h0; h < h1; ++h) {
+    const int64_t grp = g.node_grp[h];
+    const uint32_t gbit = (g.grp_uid[grp] >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
+    int64_t d = g.grp_dur[grp];
+    if ((p.mask & gbit) && p.amp > 0 && k > 0) d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
+    st = max(st, gfin[grp * Sp + k] - d);
+  }
+  return st;
+}
+
 __global__ void query_kernel(DevGraph g, ScenParams p, int32_t Sp, const int64_t *__restrict__ fin0,
                              int64_t node0, const int64_t *__restrict__ gfin, int32_t r, int32_t k,
                              int64_t *__restrict__ start_out, int64_t *__restrict__ finish_out) {
   const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
   const int64_t *fin = fin0 - node0 * Sp;
   for (int32_t i = rb + blockIdx.x * blockDim.x + threadIdx.x; i < re; i += gridDim.x * blockDim.x) {
-    const int32_t h0 = g.node_gptr[i], h1 = g.node_gptr[i + 1];
-    int64_t st;
-    if (h0 == h1) {
-      st = i == rb ? 0 : fin[(int64_t)(i - 1) * Sp + k];
-    } else if (h1 - h0 == 1) {  // one group: the node spans exactly the group occurrence
-      const int64_t grp = g.node_grp[h0];
-      const uint32_t gbit = (g.grp_uid[grp] >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
-      int64_t d = g.grp_dur[grp];
-      if ((p.mask & gbit) && p.amp > 0 && k > 0)
-        d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
-      st = fin[(int64_t)i * Sp + k] - d;
-    } else {  // start = max over groups of (gfin - dur')
-      st = 0;
-      for (int32_t h = h0; h < h1; ++h) {
-        const int64_t grp = g.node_grp[h];
-        const uint32_t gbit = (g.grp_uid[grp] >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
-        int64_t d = g.grp_dur[grp];
-        if ((p.mask & gbit) && p.amp > 0 && k > 0)
-          d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
-        st = max(st, gfin[grp * Sp + k] - d);
+    start_out[i - rb] = node_start(g, p, Sp, fin, gfin, r, rb, i, k);
+    finish_out[i - rb] = fin[(int64_t)i * Sp + k];
+  }
+}
+
+// Row a9 in time order (row f2, multi-stream ranks; P:1578 max_memory_allocated): one block per
+// rank; the rank's events (+alloc at start: index 2i, -free at finish: 2i+1) are keyed
+// (time << 14 | index), bitonic-sorted in shared memory, and prefix-summed; peak = static +
+// max(0, max running total). A running total below zero sets PRISM_E_NEGATIVE_MEMORY.
+__global__ void __launch_bounds__(1024) peak_time_kernel(DevGraph g, ScenParams p, int32_t Sp,
+                                                         const int64_t *__restrict__ fin0, int64_t node0,
+                                                         const int64_t *__restrict__ gfin, int32_t k, int32_t cap,
+                                                         int64_t *__restrict__ peak, uint32_t *status) {
+  extern __shared__ unsigned long long sm[];
+  unsigned long long *key = sm;
+  long long *val = (long long *)(sm + cap);
+  __shared__ long long wsum[32], wmax[32];
+  __shared__ int neg;
+  const int64_t *fin = fin0 - node0 * Sp;
+  for (int32_t r = blockIdx.x; r < g.W; r += gridDim.x) {
+    const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1], len = re - rb;
+    for (int32_t x = threadIdx.x; x < cap; x += blockDim.x) {
+      const int32_t i = x >> 1;
+      if (i < len) {
+        const int32_t n = rb + i;
+        const bool fr = x & 1;
+        const int64_t tm = fr ? fin[(int64_t)n * Sp + k] : node_start(g, p, Sp, fin, gfin, r, rb, n, k);
+        key[x] = ((unsigned long long)tm << 14) | (unsigned)x;
+        val[x] = fr ? -g.node_free[n] : g.node_alloc[n];
+      } else {
+        key[x] = ~0ull;
+        val[x] = 0;
       }
     }
-    start_out[i - rb] = st;
-    finish_out[i - rb] = fin[(int64_t)i * Sp + k];
+    __syncthreads();
+    for (int32_t size = 2; size <= cap; size <<= 1)  // bitonic sort, ascending
+      for (int32_t stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int32_t x = threadIdx.x; x < cap; x += blockDim.x) {
+          const int32_t y = x ^ stride;
+          if (y > x) {
+            const bool up = (x & size) == 0;
+            if ((key[x] > key[y]) == up) {
+              const unsigned long long tk = key[x];
+              key[x] = key[y];
+              key[y] = tk;
+              const long long tv = val[x];
+              val[x] = val[y];
+              val[y] = tv;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    // running total in sorted order: per-thread chunk sums, block scan of the chunks
+    const int32_t per = (cap + (int32_t)blockDim.x - 1) / (int32_t)blockDim.x;
+    const int32_t x0 = threadIdx.x * per;
+    long long s = 0, mx = 0;
+    for (int32_t x = x0; x < x0 + per && x < cap; ++x) {
+      s += val[x];
+      mx = max(mx, s);
+    }
+    // exclusive prefix of chunk sums (warp shuffles + per-warp totals)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    long long incl = s;
+    for (int off = 1; off < 32; off <<= 1) {
+      const long long y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    if (lane == 31) wsum[wid] = incl;
+    if (threadIdx.x == 0) neg = 0;
+    __syncthreads();
+    long long woff = 0;
+    for (int w = 0; w < wid; ++w) woff += wsum[w];
+    const long long before = woff + incl - s;
+    long long run = before, best = 0, low = 0;
+    for (int32_t x = x0; x < x0 + per && x < cap; ++x) {
+      run += val[x];
+      best = max(best, run);
+      low = min(low, run);
+    }
+    (void)mx;
+    if (low < 0) neg = 1;
+    for (int off = 16; off; off >>= 1) best = max(best, (long long)__shfl_xor_sync(0xffffffffu, best, off));
+    if (lane == 0) wmax[wid] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long b = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) b = max(b, wmax[w]);
+      peak[r] = g.static_mem[g.rank_stage[r]] + b;
+      if (neg) atomicCAS(status, 0u, (uint32_t)PRISM_E_NEGATIVE_MEMORY);
+    }
+    __syncthreads();
   }
 }
 
@@ -367,7 +466,8 @@ cudaError_t launch_reduce(int32_t W, int32_t S, int32_t Sp, const int64_t *rank_
 cudaError_t preload_replay_kernels() {
   cudaFuncAttributes a;
   const void *fns[] = {(const void *)reduce_iter_kernel, (const void *)shard_partial_kernel,
-                       (const void *)shard_exchange_kernel, (const void *)query_kernel};
+                       (const void *)shard_exchange_kernel, (const void *)query_kernel,
+                       (const void *)peak_time_kernel};
   for (const void *f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -380,6 +480,19 @@ cudaError_t launch_shard_reduce(const DevGraph &g, const ShardLink &link, int32_
                                 uint32_t *status, cudaStream_t st) {
   shard_partial_kernel<<<S, 256, 0, st>>>(g, Sp, rank_end, part_local);
   shard_exchange_kernel<<<1, 1024, 0, st>>>(link, S, Sp, part_local, iter, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peak_time(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin, int64_t node0,
+                             const int64_t *gfin, int32_t k, int32_t max_len, int64_t *peak, uint32_t *status,
+                             cudaStream_t st) {
+  int32_t cap = 2;
+  while (cap < 2 * max_len) cap <<= 1;
+  const size_t smem = (size_t)cap * 16;
+  cudaError_t e = cudaFuncSetAttribute(peak_time_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int threads = cap >= 1024 ? 1024 : (cap < 32 ? 32 : cap);  // whole warps (shuffle scans)
+  peak_time_kernel<<<g.W < 148 * 2 ? g.W : 148 * 2, threads, smem, st>>>(g, p, Sp, fin, node0, gfin, k, cap, peak, status);
   return cudaGetLastError();
 }
 

@@ -390,7 +390,10 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
 
 // PR (rows f1/f3/f4): the graph carries per-node durations (prism_set_durations), so a compute
 // span or chained collective lasts its own rank's value node_sdur[rb[r] + i], loaded one op ahead.
-template <int C, bool SH, bool PR>
+// MS (row f2, multi-stream ranks; C == 1): a warp replays ONE rank, keeping the finish of the
+// last op of each of its streams and the latest record of each event slot in shared memory; an
+// op starts at max(its stream's last finish, its awaited event), TP collectives are cross-warp.
+template <int C, bool SH, bool PR, bool MS>
 __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
                                                          int64_t *__restrict__ fin,
                                                          int64_t *__restrict__ gfin,
@@ -398,9 +401,10 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   const int lane = threadIdx.x & 31;
   const int32_t unit = blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (unit >= a.n_units) return;
-  const int32_t cells = g.pp * (g.d1 - g.d0);  // this shard's cells (all of them unsharded)
+  const int32_t cells = g.pp * (g.d1 - g.d0) * (MS ? g.tp : 1);  // this shard's cells
   const int32_t cell = unit % cells, chunk = a.chunk0 + unit / cells;
-  const int32_t s = cell % g.pp, dpi = g.d0 + cell / g.pp;
+  const int32_t s = cell % g.pp, dpi = g.d0 + (cell / g.pp) % (g.d1 - g.d0);
+  const int32_t tp0 = MS ? cell / (g.pp * (g.d1 - g.d0)) : 0;  // MS: the warp's TP coordinate
   const int32_t Sp = a.Sp;
   const int32_t k = chunk * SC + lane;
   __shared__ int64_t ts[MAX_TP * 32];  // chain state of the cross-cell path (rolled over ranks)
@@ -411,14 +415,14 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   uint64_t rk[C];  // (rank << 32) * K_MIX: a compute span's uid mix is rk + tidx * K_MIX
 #pragma unroll
   for (int r = 0; r < C; ++r) {
-    const int32_t rr = rank_of(g, r, s, dpi);
+    const int32_t rr = rank_of(g, tp0 + r, s, dpi);
     rb[r] = g.rank_ptr[rr];
     rs[r] = g.node_gptr[rb[r]];
     rk[r] = ((uint64_t)rr << 32) * K_MIX;
     if (lane == 0) rsh[r] = rs[r];
   }
   __syncwarp();
-  const int32_t len = g.rank_ptr[rank_of(g, 0, s, dpi) + 1] - rb[0];
+  const int32_t len = g.rank_ptr[rank_of(g, tp0, s, dpi) + 1] - rb[0];
   const uint64_t sx = p.seed ^ ((uint64_t)k * K_GOLD);
   // per-warp flags pinned in a register (an asm output cannot be rematerialised from the kernel
   // parameters, which the compiler otherwise reloads on every op)
@@ -429,6 +433,12 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   int64_t t[C];
 #pragma unroll
   for (int r = 0; r < C; ++r) t[r] = 0;
+  __shared__ int64_t ms_t[MS ? kMaxStreams : 1][32];  // MS: last finish of each stream
+  __shared__ int64_t ms_ev[MS ? kMaxEvents : 1][32];  // MS: latest record of each event slot
+  if (MS) {
+    for (int x = 0; x < kMaxStreams; ++x) ms_t[x][lane] = 0;
+    for (int x = 0; x < kMaxEvents; ++x) ms_ev[x][lane] = 0;  // a never-recorded slot: satisfied
+  }
 #ifdef PRISM_CELL_STATS
   const long long k_start = clock64();
   if (lane == 0) STAT_ADD(4, globaltimer());
@@ -449,24 +459,27 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   }
   // op records of the cell's first rank (the template is shared; the per-rank part of a compute
   // span's uid is rk[r]), 32 ops per coalesced round trip, next batch in flight
-  uint32_t ncls = 2;
+  uint32_t ncls = 2, nms = 0;
   int64_t nd = 0;
   uint64_t nux = 0;
   if (lane < len) {
     ncls = g.node_cls[rb[0] + lane];
     nd = g.node_sdur[rb[0] + lane];
     nux = g.node_uid[rb[0] + lane];
+    if (MS) nms = g.node_ms[rb[0] + lane];
   }
   for (int32_t base = 0; base < len; base += 32) {
     const int32_t cnt = min(32, len - base);
     const uint32_t bcls = ncls;
     const int64_t bd = nd;
     const uint64_t bux = nux;
+    const uint32_t bms = nms;
     if (base + 32 + lane < len) {
       const int32_t n = rb[0] + base + 32 + lane;
       ncls = g.node_cls[n];
       nd = g.node_sdur[n];
       nux = g.node_uid[n];
+      if (MS) nms = g.node_ms[n];
     }
     // op j's class / duration were fetched during op j-1 (software pipelined: the dispatch
     // branch of an op does not wait on its shuffles)
@@ -478,6 +491,16 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
       const int32_t i = base + j;
       c_n = __shfl_sync(0xffffffffu, bcls, (j + 1) & 31);
       d_n = __shfl_sync(0xffffffffu, bd, (j + 1) & 31);
+      uint32_t ms_st = 0, ms_rec = 0;
+      if (MS) {  // row f2: the op's stream / event edges (C == 1)
+        const uint32_t mb = __shfl_sync(0xffffffffu, bms, j);
+        ms_st = mb & 15u;
+        ms_rec = (mb >> 4) & 15u;
+        const uint32_t wt = (mb >> 8) & 15u;
+        int64_t rd = ms_t[ms_st][lane];
+        if (wt) rd = max(rd, ms_ev[wt - 1][lane]);
+        t[0] = rd;
+      }
       int64_t dr[PR ? C : 1];  // PR: this op's per-rank durations (loaded during the previous op)
       if (PR) {
 #pragma unroll
@@ -548,6 +571,10 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
         }
 #endif
       }
+      if (MS) {
+        ms_t[ms_st][lane] = t[0];
+        if (ms_rec) ms_ev[ms_rec - 1][lane] = t[0];
+      }
       if (record) {
 #pragma unroll
         for (int r = 0; r < C; ++r) fin[(int64_t)(rb[r] + i) * Sp + k] = t[r];
@@ -555,7 +582,11 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
     }
   }
 #pragma unroll
-  for (int r = 0; r < C; ++r) rank_end[(int64_t)rank_of(g, r, s, dpi) * Sp + k] = t[r];
+  if (MS) {  // a multi-stream rank ends with its last stream
+    for (int x = 0; x < kMaxStreams; ++x) t[0] = max(t[0], ms_t[x][lane]);
+  }
+#pragma unroll
+  for (int r = 0; r < C; ++r) rank_end[(int64_t)rank_of(g, tp0 + r, s, dpi) * Sp + k] = t[r];
 #ifdef PRISM_CELL_STATS
   if (lane == 0) {
     STAT_ADD(0, clock64() - k_start);
@@ -569,18 +600,26 @@ typedef void (*cell_fn)(DevGraph, ScenParams, CellArgs, int64_t *, int64_t *, in
 template <bool SH, bool PR>
 cell_fn cell_kernel_t(int tp) {
   switch (tp) {
-    case 1: return cell_kernel<1, SH, PR>;
-    case 2: return cell_kernel<2, SH, PR>;
-    case 3: return cell_kernel<3, SH, PR>;
-    case 4: return cell_kernel<4, SH, PR>;
-    case 5: return cell_kernel<5, SH, PR>;
-    case 6: return cell_kernel<6, SH, PR>;
-    case 7: return cell_kernel<7, SH, PR>;
-    case 8: return cell_kernel<8, SH, PR>;
+    case 1: return cell_kernel<1, SH, PR, false>;
+    case 2: return cell_kernel<2, SH, PR, false>;
+    case 3: return cell_kernel<3, SH, PR, false>;
+    case 4: return cell_kernel<4, SH, PR, false>;
+    case 5: return cell_kernel<5, SH, PR, false>;
+    case 6: return cell_kernel<6, SH, PR, false>;
+    case 7: return cell_kernel<7, SH, PR, false>;
+    case 8: return cell_kernel<8, SH, PR, false>;
     default: return nullptr;
   }
 }
+template <bool SH, bool PR>
+cell_fn cell_kernel_ms() {
+  return cell_kernel<1, SH, PR, true>;
+}
 cell_fn cell_kernel_for(const DevGraph &g) {
+  if (g.ms) {  // multi-stream ranks: one rank per warp, any tp
+    if (g.per_rank_dur) return g.n_shards > 1 ? cell_kernel_ms<true, true>() : cell_kernel_ms<false, true>();
+    return g.n_shards > 1 ? cell_kernel_ms<true, false>() : cell_kernel_ms<false, false>();
+  }
   if (g.per_rank_dur) return g.n_shards > 1 ? cell_kernel_t<true, true>(g.tp) : cell_kernel_t<false, true>(g.tp);
   return g.n_shards > 1 ? cell_kernel_t<true, false>(g.tp) : cell_kernel_t<false, false>(g.tp);
 }
@@ -594,13 +633,19 @@ cudaError_t preload_cell_kernels() {
     if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<true, true>(tp));
     if (e != cudaSuccess) return e;
   }
+  const void *ms[] = {(const void *)cell_kernel_ms<false, false>(), (const void *)cell_kernel_ms<true, false>(),
+                      (const void *)cell_kernel_ms<false, true>(), (const void *)cell_kernel_ms<true, true>()};
+  for (const void *f : ms) {
+    cudaError_t e = cudaFuncGetAttributes(&a, f);
+    if (e != cudaSuccess) return e;
+  }
   return cudaSuccess;
 }
 
 // CTAs needed for `units` warps, if they can all be co-resident.
 bool cell_fit_units(const DevGraph &g, int64_t units, int *ctas) {
   cell_fn fn = cell_kernel_for(g);
-  if (!fn) return false;
+  if (!fn) return false;  // tp > 8 without multi-stream: the level-by-level schedule
   int dev = 0, sms = 0, coop = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -635,15 +680,17 @@ PollPolicy poll_policy() {
 
 // Chunks of 32 scenarios per unit; every chunk of a replay runs in one launch when they all fit,
 // else the caller launches one chunk at a time (chunk groups of 1).
+int64_t cell_count(const DevGraph &g) { return (int64_t)g.pp * (g.d1 - g.d0) * (g.ms ? g.tp : 1); }
+
 bool cells_fit(const DevGraph &g, int nchunks) {
-  return cell_fit_units(g, (int64_t)g.pp * (g.d1 - g.d0), nullptr) && nchunks >= 1;
+  return cell_fit_units(g, cell_count(g), nullptr) && nchunks >= 1;
 }
 
 int cells_chunk_scenarios() { return SC; }
 
 int cells_chunks_per_launch(const DevGraph &g, int nchunks) {
   for (int c = nchunks; c > 1; --c)
-    if (nchunks % c == 0 && cell_fit_units(g, (int64_t)g.pp * (g.d1 - g.d0) * c, nullptr)) return c;
+    if (nchunks % c == 0 && cell_fit_units(g, cell_count(g) * c, nullptr)) return c;
   return 1;
 }
 
@@ -651,7 +698,7 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
                          uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t node0,
                          int64_t *gfin, int64_t *rank_end, int chunk0, int nchunks_launch, int Sp,
                          const ShardLink *link, cudaStream_t st) {
-  const int64_t units = (int64_t)g.pp * (g.d1 - g.d0) * nchunks_launch;
+  const int64_t units = cell_count(g) * nchunks_launch;
   int ctas = 0;
   if (!cell_fit_units(g, units, &ctas)) return cudaErrorCooperativeLaunchTooLarge;
   // the launch covers chunks [chunk0, chunk0 + nchunks_launch) of the replay's Sp / 32 chunks

@@ -103,15 +103,28 @@ __global__ void __launch_bounds__(32) crit_walk_kernel(DevGraph g, ScenParams p,
   int32_t cur = *start_node;
   if (cur < 0 || cur >= g.N) cur = -1;  // empty graph: empty path
   int64_t len = 0;
-  auto first = [&](int32_t n) { return g.rank_ptr[g.node_rank[n]] == n; };
-  auto ready = [&](int32_t m) -> int64_t { return first(m) ? 0 : fin[(int64_t)(m - 1) * Sp + k]; };
+  // a node's directional predecessor: its stream predecessor (row f2: or its event source,
+  // whichever finished later, the lower id on ties)
+  auto pred = [&](int32_t n) -> int32_t {
+    if (!g.ms) return g.rank_ptr[g.node_rank[n]] == n ? -1 : n - 1;
+    const int32_t a = g.node_spred[n], b = g.node_esrc[n];
+    if (a < 0) return b;
+    if (b < 0) return a;
+    const int64_t fa = fin[(int64_t)a * Sp + k], fb = fin[(int64_t)b * Sp + k];
+    if (fa != fb) return fa > fb ? a : b;
+    return min(a, b);
+  };
+  auto ready = [&](int32_t m) -> int64_t {
+    const int32_t q = pred(m);
+    return q < 0 ? 0 : fin[(int64_t)q * Sp + k];
+  };
   while (cur >= 0) {
     if (lane == 0 && len < cap) path[len] = cur;
     ++len;
     int32_t next = -1;
     const int32_t h0 = g.node_gptr[cur], h1 = g.node_gptr[cur + 1];
     if (h0 == h1) {
-      if (!first(cur)) next = cur - 1;
+      next = pred(cur);
     } else {
       int64_t bf = -1;
       uint64_t buid = 0;
@@ -151,7 +164,7 @@ __global__ void __launch_bounds__(32) crit_walk_kernel(DevGraph g, ScenParams p,
           bm = m2;
         }
       }
-      if (!first(bm)) next = bm - 1;
+      next = pred(bm);
     }
     cur = next;
   }

@@ -749,3 +749,55 @@ def random_templates(seed: int, max_world: int = 64, max_ops: int = 40,
         static.append(int(rng.integers(0, 1 << 20)))
     return assemble(topo, stages, static, f"random{seed}" + (f"_s{streams}" if streams > 1 else ""),
                     {"seed": seed})
+
+
+def overlap_grad_reduce(tm: Templates, comm_stream: int = 1) -> Templates:
+    """Row f2 input (P:699 overlapped gradient communication; Megatron overlap_grad_reduce): the DP
+    / EDP gradient buckets that follow a stage's last backward move onto a side stream. Bucket j is
+    issued right after the backward compute span of the last microbatch that completes it (the
+    last microbatch's backward spans are split evenly over the buckets, in order), waits for that
+    span (event slot j mod 4), and the optimizer step waits for the last bucket (slot 7). Every
+    other op keeps stream 0 and its place."""
+    t = tm.topo
+    stages = []
+    for s in range(t.pp):
+        T = tm.stage(s).copy()
+        code = (T["label"].astype(np.int64) >> 24)
+        is_bucket = (T["kind"] == KIND_COLLECTIVE) & np.isin(T["role"], [ROLE_DP, ROLE_EDP]) & \
+            np.isin(code, [OPCODES["DP_SYNC"], OPCODES["EDP_SYNC"]])
+        bidx = np.nonzero(is_bucket)[0]
+        opt = np.nonzero(code == OPCODES["OPT"])[0]
+        if len(bidx) == 0 or len(opt) == 0:
+            stages.append(T)
+            continue
+        first_b = int(bidx[0])
+        # the last microbatch's backward compute spans (after the last P2P before the buckets)
+        p2p_before = np.nonzero(T["kind"][:first_b] == KIND_P2P)[0]
+        seg0 = int(p2p_before[-1]) + 1 if len(p2p_before) else 0
+        bwd = [i for i in range(seg0, first_b) if T["kind"][i] == KIND_COMPUTE]
+        if not bwd:
+            stages.append(T)
+            continue
+        nb = len(bidx)
+        anchor = {}  # backward span index -> buckets issued after it
+        for j in range(nb):
+            a = bwd[min(len(bwd) - 1, ((j + 1) * len(bwd)) // nb - 1)]
+            anchor.setdefault(a, []).append(j)
+        rows = []
+        for i in range(len(T)):
+            if is_bucket[i]:
+                continue
+            r = T[i].copy()
+            if i == int(opt[0]):
+                r["ev_wait"] = 8  # slot 7: the last bucket
+            if i in anchor:
+                r["ev_record"] = (anchor[i][0] % 4) + 1
+            rows.append(r)
+            for j in anchor.get(i, []):
+                b = T[int(bidx[j])].copy()
+                b["stream"] = comm_stream
+                b["ev_wait"] = (anchor[i][0] % 4) + 1
+                b["ev_record"] = 8 if j == nb - 1 else 0
+                rows.append(b)
+        stages.append(np.array(rows, dtype=OP_DTYPE))
+    return assemble(t, stages, list(tm.static_mem), (tm.name or "") + "_overlap", dict(tm.meta or {}))
