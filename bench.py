@@ -298,7 +298,9 @@ def f_rows_extra(args, tm, sh):
          +-5 % per node, the shape of a slice-filled timed graph), S scenarios on top;
       f3 what-if: every attention-forward span overridden + one rank slowed 12 % (fault
          injection), then the critical path of scenario 0 (device walk-back, wall ms);
-      f4 MoE imbalance: C4 (DeepSeek-V3-shaped, EP 64) under the Fig. 3 br profile."""
+      f4 MoE imbalance: C4 (DeepSeek-V3-shaped, EP 64) under the Fig. 3 br profile;
+      f2 multi-stream ranks: C2 with its gradient buckets overlapped on a side stream, replay +
+         time-ordered peak memory."""
     import numpy as np
 
     import paper_2605_15617_b200 as prism
@@ -352,6 +354,14 @@ def f_rows_extra(args, tm, sh):
     r = timed_replay(g, g.stats()["nodes"])
     pk = g.peak_memory()
     out["f4_moe_imbalance"] = dict(r, peak_max_bytes=int(pk.max()), workload="C4 under the Fig. 3 br profile")
+    g.close()
+    c2 = w.overlap_grad_reduce(w.config("C2"))
+    g = prism.Graph(c2, stream=sh, profile=True)
+    r = timed_replay(g, g.stats()["nodes"])
+    g.peak_memory()
+    pk_ms = g.last_timing()["peak"]
+    out["f2_multistream"] = dict(r, time_ordered_peak_ms=round(pk_ms, 4),
+                                 workload="C2 with gradient buckets overlapped on a second stream")
     g.close()
     return out
 
