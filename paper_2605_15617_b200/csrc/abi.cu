@@ -586,6 +586,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   p.record = sc->record ? 1 : 0;
   p.mod = 2 * sc->amp_q16 + 1;
   p.mod_magic = ~0ULL / (uint64_t)p.mod + 1;
+  p.mod_m32 = p.mod > 1 ? (uint32_t)((((uint64_t)1 << 32) + (uint64_t)p.mod - 1) / (uint64_t)p.mod) : 0xFFFFFFFFu;
   G->recorded = 0;
   trace("replay: begin");
   if (p.record) {

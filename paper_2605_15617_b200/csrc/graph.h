@@ -96,7 +96,26 @@ struct ScenParams {
   int32_t record;    // write fin[N][S]
   int32_t mod;       // 2*amp+1
   uint64_t mod_magic;  // Lemire fastmod constant for mod (x < 2^32)
+  uint32_t mod_m32;    // ceil(2^32 / mod): 32-bit quotient estimate for x < 2^24 (perturb_x)
+  uint32_t pad;
 };
+
+// Reading Z8's perturbation with the splitmix64 hash x already mixed: v = splitmix64(x) >> 40
+// (the finaliser's last xorshift leaves bits 40..63 unchanged, so it is skipped), r = v mod (2 amp
+// + 1), d' = (d * (65536 + r - amp)) >> 16. The mod of the 24-bit v uses q = umulhi(v, ceil(2^32 /
+// mod)): q overshoots floor(v / mod) by at most one (v * (M - 2^32/mod) / 2^32 < 2^-8), so one
+// conditional add of mod makes r exact.
+#ifdef __CUDACC__
+__device__ __forceinline__ int64_t perturb_x(int64_t d, uint64_t x, const ScenParams &p) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  const uint32_t v = (uint32_t)(z >> 40);
+  int32_t r = (int32_t)(v - __umulhi(v, p.mod_m32) * (uint32_t)p.mod);
+  if (r < 0) r += p.mod;
+  return (d * (int64_t)((uint32_t)r + (uint32_t)(65536 - p.amp))) >> 16;
+}
+#endif
 
 // Row e: the peer-memory exchange of a sharded replay. Every shard's exchange buffer has the
 // same layout (same plan, same S), so one set of byte offsets addresses all of them.

@@ -25,14 +25,6 @@ constexpr uint64_t K_MIX = 0xBF58476D1CE4E5B9ULL;
 // Reading Z8: d' = (d * (65536 + delta)) >> 16, delta = ((h >> 40) mod (2 amp + 1)) - amp with
 // h = splitmix64(seed ^ k*K_GOLD ^ uid*K_MIX). `x` is that xor already formed. The mod uses
 // Lemire's direct remainder (exact for 32-bit numerators): r = hi64((M * v) mod 2^64, d).
-__device__ __forceinline__ int64_t perturb_x(int64_t d, uint64_t x, const ScenParams &p) {
-  const uint64_t h = splitmix64(x);
-  const uint32_t v = (uint32_t)(h >> 40);
-  const uint64_t low = p.mod_magic * (uint64_t)v;
-  const uint32_t r = (uint32_t)__umul64hi(low, (uint64_t)(uint32_t)p.mod);
-  const int64_t delta = (int64_t)r - p.amp;
-  return (d * (65536 + delta)) >> 16;
-}
 
 template <int SPL>
 struct Vec;

@@ -44,17 +44,6 @@ constexpr int MAX_TP = 8;       // tp of the instantiated cell kernels
 constexpr int SMALL = kSmallGroup;
 constexpr int kPollList = MAX_TP * 4 * (kSmallGroup - 1);  // <= 32 pairs x 7 other members
 
-__device__ __forceinline__ int64_t perturb_x(int64_t d, uint64_t x, const ScenParams &p) {
-  // splitmix64(x) >> 40 (reading Z8): the finaliser's last step z ^ (z >> 31) leaves bits 40..63
-  // unchanged (z >> 31 >> 40 == 0), so it is skipped
-  uint64_t z = x + 0x9E3779B97F4A7C15ULL;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-  const uint32_t v = (uint32_t)(z >> 40);
-  const uint64_t low = p.mod_magic * (uint64_t)v;
-  const uint32_t r = (uint32_t)__umul64hi(low, (uint64_t)(uint32_t)p.mod);
-  return (d * (int64_t)(r + (uint32_t)(65536 - p.amp))) >> 16;
-}
 
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -239,8 +228,12 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
   }
   __syncwarp();
   bool large_any = false;
-  for (int x = 0; x < np; ++x) {
-    const int64_t tr = ts[(x / ns) * 32 + lane];
+  for (int x = 0, r = 0, q = 0; x < np; ++x) {  // x = r * ns + q, no divisions
+    const int64_t tr = ts[r * 32 + lane];
+    if (++q == ns) {
+      q = 0;
+      ++r;
+    }
     const uint32_t meta = cs.meta[x];
     const int32_t base = cs.base[x];
     if (!(meta & 0x80000000u)) {
@@ -319,7 +312,10 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
           }
       }
     }
-    for (int x = 0; x < np; ++x) cs.vmax[x][lane] = ts[(x / ns) * 32 + lane];
+    for (int r = 0, x = 0; r < C; ++r) {
+      const int64_t tr = ts[r * 32 + lane];
+      for (int q = 0; q < ns; ++q, ++x) cs.vmax[x][lane] = tr;
+    }
     __syncwarp();
   }
   uint32_t pending = np >= 32 ? 0xFFFFFFFFu : ((1u << np) - 1u);

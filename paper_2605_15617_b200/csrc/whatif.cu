@@ -72,15 +72,6 @@ __global__ void __launch_bounds__(256) records_kernel(DevGraph g, const int64_t 
   for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < g.M; h += stride) hdur[h] = gdur[g.node_grp[h]];
 }
 
-__device__ __forceinline__ int64_t perturb_x(int64_t d, uint64_t x, const ScenParams &p) {
-  uint64_t z = x + K_GOLD;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-  const uint32_t v = (uint32_t)(z >> 40);
-  const uint64_t low = p.mod_magic * (uint64_t)v;
-  const uint32_t r = (uint32_t)__umul64hi(low, (uint64_t)(uint32_t)p.mod);
-  return (d * (int64_t)(r + (uint32_t)(65536 - p.amp))) >> 16;
-}
 
 // Row f3, step 1: T_k and the lowest node finishing at T_k.
 __global__ void __launch_bounds__(256) crit_start_kernel(DevGraph g, const int64_t *__restrict__ fin,
