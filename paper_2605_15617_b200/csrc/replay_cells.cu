@@ -43,6 +43,7 @@ constexpr int WARPS = 1;        // units per CTA (1: warps spread evenly over th
 constexpr int MAX_TP = 8;       // tp of the instantiated cell kernels
 constexpr int SMALL = kSmallGroup;
 constexpr int kPollList = MAX_TP * 4 * (kSmallGroup - 1);  // <= 32 pairs x 7 other members
+constexpr int kPollBatch = 8;  // poll loads issued back to back per batch (16 raised register pressure: slower)
 
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -276,7 +277,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
   if (tl >= 0 && lane == 0) g_tl[tl * 4 + 1] = globaltimer();
 #endif
   // poll until every (rank, group) pair of the op is resolved. The (pair, member) loads of a
-  // round are flattened into one list and issued 8 at a time before any is folded (a loop with a
+  // round are flattened into one list and issued kPollBatch at a time before any is folded (a loop with a
   // load-dependent branch per pair would serialise one L2 round trip per pair); a pair resolved
   // for this lane is not polled again. Slot values are parity-encoded: v ^ pm is the ready time
   // when >= 0; a large group is resolved when its arrival counter reaches its size.
@@ -323,10 +324,10 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
   uint64_t tw = 0;
   while (true) {
     uint32_t bad = 0;
-    for (int32_t j0 = 0; j0 < nl; j0 += 8) {
-      int64_t v[8];
+    for (int32_t j0 = 0; j0 < nl; j0 += kPollBatch) {
+      int64_t v[kPollBatch];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kPollBatch; ++u) {
         const int32_t j = j0 + u;
         v[u] = 0;
         if (j < nl) {
@@ -342,7 +343,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
         }
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kPollBatch; ++u) {
         const int32_t j = j0 + u;
         if (j < nl) {
           const uint32_t pr = cs.lpair[j];
