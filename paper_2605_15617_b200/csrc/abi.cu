@@ -371,6 +371,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t o_slr = carve(nslot), o_slf = carve(nslot), o_chq = carve(nch * 4), o_chm = carve(nch * 8);
   const size_t o_tcls = carve(nops), o_xptr = carve((pp + 1) * 4), o_xops = carve(P.x_ops.size() * sizeof(XOp));
   const bool ms = P.multistream;
+  const size_t o_tq0 = carve(nops * 4);
   const size_t o_tms = ms ? carve(nops * 2) : 0, o_tsp2 = ms ? carve(nops * 4) : 0, o_tes = ms ? carve(nops * 4) : 0;
   const size_t table_bytes = off;
   // graph arrays (written by the expand kernels)
@@ -408,6 +409,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.t_cls = (const uint8_t *)at(o_tcls);
   d.x_ptr = (const int32_t *)at(o_xptr);
   d.x_ops = (const XOp *)at(o_xops);
+  d.t_q0 = (const int32_t *)at(o_tq0);
   d.ms = ms ? 1 : 0;
   d.t_ms = ms ? (const uint16_t *)at(o_tms) : nullptr;
   d.t_spred = ms ? (const int32_t *)at(o_tsp2) : nullptr;
@@ -469,6 +471,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     put(o_chq, P.chunk_q.data(), nch * 4);
     put(o_chm, P.chunk_m.data(), nch * 8);
     put(o_tcls, P.t_cls.data(), nops);
+    put(o_tq0, P.t_q0.data(), nops * 4);
     put(o_xptr, P.x_ptr.data(), (pp + 1) * 4);
     put(o_xops, P.x_ops.data(), P.x_ops.size() * sizeof(XOp));
     if (ms) {

@@ -117,6 +117,19 @@ __device__ __forceinline__ uint32_t shard_mask(const DevGraph &g, int32_t type, 
 // ops, then over its template slots; every write is a coalesced run along the rank's nodes /
 // membership slots. A slot's group instance and member index follow in closed form from the
 // rank's coordinates (the same enumeration as the group side below).
+// Instance of quotient group q that a rank with these coordinates joins (closed form, a2).
+__device__ __forceinline__ int32_t group_inst(const DevGraph &g, int32_t type, int32_t tpi, int32_t dpi,
+                                              int32_t epi, int32_t edpi) {
+  switch (type) {
+    case PRISM_ROLE_TP: return dpi;
+    case PRISM_ROLE_DP: return tpi;
+    case PRISM_ROLE_EP: return tpi + g.tp * edpi;
+    case PRISM_ROLE_EDP: return tpi + g.tp * epi;
+    case PRISM_ROLE_WORLD: return 0;
+    default: return tpi + g.tp * dpi;  // P2P message (sender or receiver: same tp/dp)
+  }
+}
+
 __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
   for (int32_t r = blockIdx.x; r < g.W; r += gridDim.x) {
     const int32_t s = g.rank_stage[r];
@@ -124,64 +137,71 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
     const int32_t slot0 = g.rank_slot[r];
     const int64_t op0 = g.t_op0[s];
     const int32_t len = (int32_t)g.t_len[s];
+    // coordinates of r
+    const int32_t tpi = r % g.tp;
+    const int32_t dpi = g.order == PRISM_ORDER_MEGATRON ? (r / g.tp) % g.dp : r / (g.tp * g.pp);
+    const int32_t epi = dpi % g.ep, edpi = dpi / g.ep;
+    // node side: every array written coalesced along the rank's nodes; template fields read
+    // through the read-only path (L2-resident tables) so loads of later ops are not ordered
+    // behind this op's stores
     for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
-      const prism_op &o = g.t_ops[op0 + i];
+      const prism_op *o = g.t_ops + op0 + i;
       const int32_t n = rb + i;
-      const int32_t tps = g.t_prev_sync[op0 + i];
+      const uint8_t kind = __ldg(&o->kind);
+      const int64_t dur = __ldg(&o->dur_ns);
+      const int32_t tps = __ldg(g.t_prev_sync + op0 + i);
+      const int32_t q0 = __ldg(g.t_q0 + op0 + i);
       g.node_rank[n] = r;
-      g.node_dur[n] = o.dur_ns;
-      g.node_kind[n] = o.kind;
-      g.node_label[n] = o.label;
-      g.node_alloc[n] = o.mem_alloc;
-      g.node_free[n] = o.mem_free;
+      g.node_dur[n] = dur;
+      g.node_kind[n] = kind;
+      g.node_label[n] = __ldg(&o->label);
+      g.node_alloc[n] = __ldg(&o->mem_alloc);
+      g.node_free[n] = __ldg(&o->mem_free);
       g.node_prev_sync[n] = tps < 0 ? -1 : rb + tps;
-      g.node_gptr[n] = slot0 + g.t_slot_ptr[op0 + i];
+      g.node_gptr[n] = slot0 + __ldg(g.t_slot_ptr + op0 + i);
       if (g.ms) {  // row f2
         const int32_t sp = g.t_spred[op0 + i], es = g.t_esrc[op0 + i];
         g.node_ms[n] = g.t_ms[op0 + i];
         g.node_spred[n] = sp < 0 ? -1 : rb + sp;
         g.node_esrc[n] = es < 0 ? -1 : rb + es;
       }
-      if (o.kind == PRISM_KIND_COMPUTE) {  // sync nodes get their record from their first slot
-        g.node_cls[n] = 0;
-        g.node_sdur[n] = o.dur_ns;
+      // replay record: a compute span carries its own duration and uid; a sync node its first
+      // group's (quotient group q0, instance from the rank's coordinates)
+      g.node_cls[n] = __ldg(g.t_cls + op0 + i);
+      if (q0 < 0) {
+        g.node_sdur[n] = dur;
         g.node_uid[n] = ((uint64_t)r << 32) | (uint32_t)i;
+      } else {
+        const QGroup &q = g.q[q0];
+        g.node_sdur[n] = q.dur;
+        g.node_uid[n] = group_uid(g, q, group_inst(g, q.type, tpi, dpi, epi, edpi));
       }
     }
-    // coordinates of r
-    const int32_t tpi = r % g.tp;
-    const int32_t dpi = g.order == PRISM_ORDER_MEGATRON ? (r / g.tp) % g.dp : r / (g.tp * g.pp);
-    const int32_t epi = dpi % g.ep, edpi = dpi / g.ep;
+    // slot side
     const int64_t u0 = g.stage_slot0[s];
     const int32_t nsl = (int32_t)(g.stage_slot0[s + 1] - u0);
     for (int32_t u = threadIdx.x; u < nsl; u += blockDim.x) {
-      const QGroup &q = g.q[g.slot_q[u0 + u]];
-      int32_t inst, j;
+      const QGroup &q = g.q[__ldg(g.slot_q + u0 + u)];
+      const int32_t inst = group_inst(g, q.type, tpi, dpi, epi, edpi);
+      int32_t j;
       switch (q.type) {
-        case PRISM_ROLE_TP: inst = dpi; j = tpi; break;
-        case PRISM_ROLE_DP: inst = tpi; j = dpi; break;
-        case PRISM_ROLE_EP: inst = tpi + g.tp * edpi; j = epi; break;
-        case PRISM_ROLE_EDP: inst = tpi + g.tp * epi; j = edpi; break;
-        case PRISM_ROLE_WORLD: inst = 0; j = r; break;
-        default: inst = tpi + g.tp * dpi; j = g.slot_role[u0 + u]; break;
+        case PRISM_ROLE_TP: j = tpi; break;
+        case PRISM_ROLE_DP: j = dpi; break;
+        case PRISM_ROLE_EP: j = epi; break;
+        case PRISM_ROLE_EDP: j = edpi; break;
+        case PRISM_ROLE_WORLD: j = r; break;
+        default: j = g.slot_role[u0 + u]; break;
       }
       const int32_t h = slot0 + u;
       const int64_t grp = q.gbase + inst;
-      const uint64_t uid = group_uid(g, q, inst);
       const bool large = q.xbase < 0 && q.lbase >= 0;
       g.node_grp[h] = (int32_t)grp;
       g.node_mslot[h] = (int32_t)(q.mbase + (int64_t)inst * q.size + j);
       g.h_base[h] = large ? (int32_t)(q.lbase + inst) : (q.xbase < 0 ? -1 : (int32_t)(q.xbase + (int64_t)inst * q.size));
       g.h_meta[h] = (uint32_t)min(q.size, 0xFFFF) | ((uint32_t)min(j, 0x7FFF) << 16) | (large ? 0x80000000u : 0u);
       g.h_dur[h] = q.dur;
-      g.h_uid[h] = uid;
+      g.h_uid[h] = group_uid(g, q, inst);
       if (g.h_smask) g.h_smask[h] = shard_mask(g, q.type, dpi, epi, edpi);
-      if (g.slot_first[u0 + u]) {  // the node's first group provides its replay record
-        const int32_t n = rb + g.slot_tidx[u0 + u];
-        g.node_cls[n] = g.t_cls[op0 + g.slot_tidx[u0 + u]];
-        g.node_sdur[n] = q.dur;
-        g.node_uid[n] = uid;
-      }
     }
   }
 }

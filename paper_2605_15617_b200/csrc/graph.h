@@ -83,6 +83,7 @@ struct DevGraph {
   int32_t nchunk;
   const int32_t *wpos;      // WORLD per-stage template indices
   const uint8_t *t_cls;     // replay class per template op (Plan::t_cls)
+  const int32_t *t_q0;      // per template op: quotient group of its first slot (-1: compute)
   const int32_t *x_ptr;     // [pp+1] cross-op list of each stage
   const XOp *x_ops;
 };

@@ -473,6 +473,12 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
       P.chunk_m.push_back(off);
     }
   }
+  P.t_q0.assign(tm.n_ops, -1);
+  for (int s = 0; s < pp; ++s)
+    for (int64_t i = 0; i < P.stage_len[s]; ++i) {
+      const int64_t op = P.stage_op0[s] + i;
+      if (P.t_slots[op] > 0) P.t_q0[op] = P.slot_q[P.stage_slot0[s] + P.t_slot_ptr[op]];
+    }
   TMARK("slots");
   P.level_q_ptr.assign(levels + 2, 0);
   for (const auto &g : P.q) P.level_q_ptr[g.level + 1]++;

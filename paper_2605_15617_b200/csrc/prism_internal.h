@@ -79,6 +79,7 @@ struct Plan {
   // that immediately follows a collective of the same group, so every member is ready exactly at
   // that group's shared finish and start = own ready time (exact)
   std::vector<uint8_t> t_cls;
+  std::vector<int32_t> t_q0;  // quotient group (index into q) of each template op's first slot, -1
   // row f2 (multi-stream ranks): any op off stream 0 or with an event; per template op the
   // previous op of its stream / the event source (template index, -1) and the packed
   // stream | ev_record << 4 | ev_wait << 8
