@@ -343,10 +343,20 @@ int replay(const Graph &g, const std::function<int64_t(int32_t)> &ndur,
   // predecessor and, row f2, the event source; a node is released once all have finished
   std::vector<int32_t> deps(N, 0);
   std::vector<int64_t> rdy(N, 0);
-  std::vector<std::vector<int32_t>> succ(N);
+  // successor lists as a CSR (succ_ptr / succ)
+  std::vector<int64_t> succ_ptr(N + 1, 0);
   for (int64_t n = 0; n < N; ++n) {
-    if (g.spred[n] >= 0) { ++deps[n]; succ[g.spred[n]].push_back((int32_t)n); }
-    if (g.esrc[n] >= 0) { ++deps[n]; succ[g.esrc[n]].push_back((int32_t)n); }
+    if (g.spred[n] >= 0) { ++deps[n]; ++succ_ptr[g.spred[n] + 1]; }
+    if (g.esrc[n] >= 0) { ++deps[n]; ++succ_ptr[g.esrc[n] + 1]; }
+  }
+  for (int64_t n = 0; n < N; ++n) succ_ptr[n + 1] += succ_ptr[n];
+  std::vector<int32_t> succ(succ_ptr[N]);
+  {
+    std::vector<int64_t> fill(succ_ptr.begin(), succ_ptr.end() - 1);
+    for (int64_t n = 0; n < N; ++n) {
+      if (g.spred[n] >= 0) succ[fill[g.spred[n]]++] = (int32_t)n;
+      if (g.esrc[n] >= 0) succ[fill[g.esrc[n]]++] = (int32_t)n;
+    }
   }
   for (int64_t n = 0; n < N; ++n)
     if (deps[n] == 0) release((int32_t)n, 0);
@@ -356,7 +366,8 @@ int replay(const Graph &g, const std::function<int64_t(int32_t)> &ndur,
     int32_t n = e.second;
     finish[n] = e.first;
     ++done;
-    for (int32_t d : succ[n]) {
+    for (int64_t x = succ_ptr[n]; x < succ_ptr[n + 1]; ++x) {
+      const int32_t d = succ[x];
       rdy[d] = std::max(rdy[d], e.first);
       if (--deps[d] == 0) release(d, rdy[d]);
     }
