@@ -132,9 +132,11 @@ def run_prism(args):
     comm = [None]  # sharded: the graph currently holding the connected exchange buffer
 
     def new_graph(profile=False):
+        # asynchronous build: the expansion is queued on the stream and the replay follows it
+        # there without a host round trip
         if not sharded:
-            return prism.Graph(tm, stream=sh, profile=profile)
-        g = prism.Graph(tm, stream=sh, profile=profile, n_shards=ws, shard_index=rank)
+            return prism.Graph(tm, stream=sh, profile=profile, asynchronous=True)
+        g = prism.Graph(tm, stream=sh, profile=profile, n_shards=ws, shard_index=rank, asynchronous=True)
         if comm[0] is None:
             g.shard_connect_dist(S)  # once: exchange-buffer IPC handles over torch.distributed
         else:

@@ -141,7 +141,10 @@ typedef struct {
   int32_t flags;          /* PRISM_BUILD_PROFILE: record CUDA events around every kernel group */
 } prism_build_opts;
 
-enum { PRISM_BUILD_PROFILE = 1 };
+/* PRISM_BUILD_PROFILE: record CUDA events around every kernel group (prism_last_timing).
+ * PRISM_BUILD_ASYNC: return once the expansion is queued on the stream (later calls on the same
+ * stream are ordered after it); by default prism_build_graph waits for it. */
+enum { PRISM_BUILD_PROFILE = 1, PRISM_BUILD_ASYNC = 2 };
 
 /* Scenario batch for what-if sweeps (re-time without structural change).
  * Scenario k gets perturbed durations d' = (d * (65536 + delta)) >> 16 with
@@ -182,7 +185,8 @@ PRISM_API prism_status prism_set_allocator(prism_alloc_fn alloc, prism_free_fn f
  *                              collective type differ between stages
  *   PRISM_E_DEADLOCK           the synchronization structure has a cycle
  *   PRISM_E_NEGATIVE_MEMORY    a template's running allocation drops below zero (program order)
- * On success *out owns the graph. Blocks until the device work is complete. */
+ * On success *out owns the graph. Blocks until the device work is complete unless
+ * opts.flags has PRISM_BUILD_ASYNC. */
 PRISM_API prism_status prism_build_graph(const prism_topology *topo, const prism_templates *tmpl,
                                const prism_build_opts *opts, prism_graph_t *out);
 
@@ -313,6 +317,8 @@ PRISM_API prism_status prism_query_rank(prism_graph_t g, int32_t rank, int32_t s
  * max group size, bytes of device graph structure, replay launches per call. */
 PRISM_API prism_status prism_graph_stats(prism_graph_t g, int64_t out[10]);
 
+/* Releases the graph. Device buffers are freed in stream order (no host wait) unless the graph
+ * is a connected shard (its exchange buffer is synchronously released). */
 PRISM_API void prism_destroy_graph(prism_graph_t g);
 
 /* Schedule used by the last replay: PRISM_ALGO_LEVELS or PRISM_ALGO_CELLS (0 before any). */

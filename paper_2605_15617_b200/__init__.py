@@ -190,12 +190,13 @@ class Graph:
     """An expanded execution graph resident on one GPU (prism_build_graph)."""
 
     def __init__(self, templates, *, stream: Optional[int] = None, device: int = -1,
-                 profile: bool = False, n_shards: int = 1, shard_index: int = 0):
+                 profile: bool = False, n_shards: int = 1, shard_index: int = 0, asynchronous: bool = False):
         L = lib()
         self.topo = templates.topo
         self.n_shards, self.shard_index = int(n_shards), int(shard_index)
         self._topo, self._tm, self._keep = _marshal(templates)
-        self._opts = _BuildOpts(stream or 0, device, self.n_shards, self.shard_index, 1 if profile else 0)
+        flags = (1 if profile else 0) | (2 if asynchronous else 0)
+        self._opts = _BuildOpts(stream or 0, device, self.n_shards, self.shard_index, flags)
         h = ctypes.c_void_p()
         self._h = None
         _check(L.prism_build_graph(ctypes.byref(self._topo), ctypes.byref(self._tm),

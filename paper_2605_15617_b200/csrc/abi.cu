@@ -221,11 +221,19 @@ struct prism_graph_s {
     dfree(part);
     dfree(ov);
     dfree(crit);
-    pin_give(h_status);
-    for (auto &b : blocks) dfree(b.first);
-    cudaStreamSynchronize(stream);
-    for (void *p : ipc_open) cudaIpcCloseMemHandle(p);
-    if (ex) cudaFree(ex);
+    if (h_status) {  // returned to the pool once the stream has passed its pending status copy
+      if (cudaLaunchHostFunc(stream, [](void *w) { pin_give((uint32_t *)w); }, h_status) != cudaSuccess) {
+        cudaGetLastError();
+        cudaStreamSynchronize(stream);
+        pin_give(h_status);
+      }
+    }
+    for (auto &b : blocks) dfree(b.first);  // stream-ordered frees: no host wait needed
+    if (ex || !ipc_open.empty()) {  // the exchange buffer is not stream-ordered memory
+      cudaStreamSynchronize(stream);
+      for (void *p : ipc_open) cudaIpcCloseMemHandle(p);
+      if (ex) cudaFree(ex);
+    }
     for (auto &e : ev)
       if (e) cudaEventDestroy(e);
   }
@@ -499,7 +507,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   G->rec(0);
   CU(launch_expand(d, s));
   G->rec(1);
-  CU(cudaStreamSynchronize(s));
+  if (!(opts && (opts->flags & PRISM_BUILD_ASYNC))) CU(cudaStreamSynchronize(s));
   *out = guard.release();
   return PRISM_OK;
 }
