@@ -419,6 +419,8 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.x_ops = (const XOp *)at(o_xops);
   d.t_q0 = (const int32_t *)at(o_tq0);
   d.ms = ms ? 1 : 0;
+  d.ms_streams = P.ms_streams;
+  d.ms_events = P.ms_events;
   d.t_ms = ms ? (const uint16_t *)at(o_tms) : nullptr;
   d.t_spred = ms ? (const int32_t *)at(o_tsp2) : nullptr;
   d.t_esrc = ms ? (const int32_t *)at(o_tes) : nullptr;
@@ -581,8 +583,8 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
       return fail(PRISM_E_INVALID_ARG, "PRISM_ALGO_CELLS: the cells of this graph do not fit co-resident on the device");
   }
   if (!cells && G->plan.multistream)
-    return fail(PRISM_E_INVALID_ARG, "multi-stream graphs (row f2) replay on the cell kernel only, and its "
-                                     "one-rank-per-warp units do not fit co-resident on this device");
+    return fail(PRISM_E_INVALID_ARG, "multi-stream graphs (row f2) replay on the cell kernel only (tp <= 8, "
+                                     "cells co-resident)");
   int lanes = 32;
   if (!cells)
     for (lanes = 1; lanes < S && lanes < 32;) lanes <<= 1;

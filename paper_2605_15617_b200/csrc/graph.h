@@ -17,9 +17,9 @@ struct DevGraph {
   // rows f1/f3/f4: node_sdur / h_dur / node_dur / grp_dur point at per-node override arrays and
   // compute spans / chained collectives last their own rank's value (prism_set_durations)
   int32_t per_rank_dur;
-  // row f2: multi-stream ranks (one rank per warp; per-node stream / event fields and directional
-  // predecessors, -1 = none)
-  int32_t ms;
+  // row f2: multi-stream ranks (per-node stream / event fields, directional predecessors, -1 =
+  // none); streams and densely renumbered event slots used by the graph
+  int32_t ms, ms_streams, ms_events;
   const uint16_t *t_ms;      // per template op: stream | ev_record << 4 | ev_wait << 8
   const int32_t *t_spred;    // per template op: previous op of its stream (template index)
   const int32_t *t_esrc;     // per template op: event source (template index)

@@ -145,7 +145,17 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
   P.t_spred.assign(tm.n_ops, -1);
   P.t_esrc.assign(tm.n_ops, -1);
   P.t_ms.assign(tm.n_ops, 0);
-  if (P.multistream)
+  if (P.multistream) {
+    // streams used, event slots renumbered densely in order of first use (the cell kernel keeps
+    // (streams + events) x tp x 32 ready times per warp in shared memory)
+    int8_t emap[kMaxEvents];
+    for (auto &x : emap) x = -1;
+    for (int64_t i = 0; i < tm.n_ops; ++i) {
+      const prism_op &o = tm.ops[i];
+      P.ms_streams = std::max<int32_t>(P.ms_streams, o.stream + 1);
+      for (int e : {(int)o.ev_record, (int)o.ev_wait})
+        if (e && emap[e - 1] < 0) emap[e - 1] = (int8_t)P.ms_events++;
+    }
     for (int s = 0; s < pp; ++s) {
       int32_t last_on[kMaxStreams], last_rec[kMaxEvents];
       for (auto &x : last_on) x = -1;
@@ -155,11 +165,13 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
         const int32_t ti = (int32_t)(i - tm.tmpl_ptr[s]);
         P.t_spred[i] = last_on[o.stream];
         P.t_esrc[i] = o.ev_wait ? last_rec[o.ev_wait - 1] : -1;
-        P.t_ms[i] = (uint16_t)(o.stream | (o.ev_record << 4) | (o.ev_wait << 8));
+        const int rec = o.ev_record ? emap[o.ev_record - 1] + 1 : 0, wt = o.ev_wait ? emap[o.ev_wait - 1] + 1 : 0;
+        P.t_ms[i] = (uint16_t)(o.stream | (rec << 4) | (wt << 8));
         last_on[o.stream] = ti;
         if (o.ev_record) last_rec[o.ev_record - 1] = ti;
       }
     }
+  }
   // replay classes (cell kernel) and per-stage cross-op lists
   P.t_cls.assign(tm.n_ops, 0);
   {
@@ -188,10 +200,9 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
         const prism_op &o = tm.ops[i];
         uint8_t c = 0;
         if (o.kind == PRISM_KIND_COLLECTIVE) {
-          // multi-stream graphs (row f2) replay one rank per warp: a TP group is cross-warp, and
-          // the chained-collective shortcut needs a single stream
+          // the chained-collective shortcut needs a single stream (row f2)
           if (o.role == PRISM_ROLE_TP) {
-            c = P.multistream ? 2 : 1;
+            c = 1;
           } else if (o.role == PRISM_ROLE_WORLD) {
             c = (!P.multistream && k < (int32_t)wchain.size() && wchain[k]) ? 3 : 2;
             ++k;
@@ -413,7 +424,7 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     // other group exchanges ready times through global ready slots
     g.xbase = -1;
     g.lbase = -1;
-    if (g.type != PRISM_ROLE_TP || P.multistream) {
+    if (g.type != PRISM_ROLE_TP) {
       if (g.size <= kSmallGroup) {
         g.xbase = X;
         X += (int64_t)g.inst * g.size;

@@ -84,6 +84,7 @@ struct Plan {
   // previous op of its stream / the event source (template index, -1) and the packed
   // stream | ev_record << 4 | ev_wait << 8
   bool multistream = false;
+  int32_t ms_streams = 0, ms_events = 0;  // streams used; distinct event slots (renumbered densely)
   std::vector<int32_t> t_spred, t_esrc;
   std::vector<uint16_t> t_ms;
   // per stage, the cross-cell ops (class 2) in template order: x_ptr[pp+1] -> XOp

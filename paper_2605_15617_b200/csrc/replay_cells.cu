@@ -387,9 +387,10 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
 
 // PR (rows f1/f3/f4): the graph carries per-node durations (prism_set_durations), so a compute
 // span or chained collective lasts its own rank's value node_sdur[rb[r] + i], loaded one op ahead.
-// MS (row f2, multi-stream ranks; C == 1): a warp replays ONE rank, keeping the finish of the
-// last op of each of its streams and the latest record of each event slot in shared memory; an
-// op starts at max(its stream's last finish, its awaited event), TP collectives are cross-warp.
+// MS (row f2, multi-stream ranks): besides its ranks' ready times the warp keeps, per rank, the
+// finish of the last op of each stream and the latest record of each (densely renumbered) event
+// slot in dynamic shared memory; an op starts at max(its stream's last finish, its awaited
+// event). The ranks of a cell still share one template, so TP collectives stay register-local.
 template <int C, bool SH, bool PR, bool MS>
 __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
                                                          int64_t *__restrict__ fin,
@@ -398,10 +399,9 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   const int lane = threadIdx.x & 31;
   const int32_t unit = blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (unit >= a.n_units) return;
-  const int32_t cells = g.pp * (g.d1 - g.d0) * (MS ? g.tp : 1);  // this shard's cells
+  const int32_t cells = g.pp * (g.d1 - g.d0);  // this shard's cells (all of them unsharded)
   const int32_t cell = unit % cells, chunk = a.chunk0 + unit / cells;
-  const int32_t s = cell % g.pp, dpi = g.d0 + (cell / g.pp) % (g.d1 - g.d0);
-  const int32_t tp0 = MS ? cell / (g.pp * (g.d1 - g.d0)) : 0;  // MS: the warp's TP coordinate
+  const int32_t s = cell % g.pp, dpi = g.d0 + cell / g.pp;
   const int32_t Sp = a.Sp;
   const int32_t k = chunk * SC + lane;
   __shared__ int64_t ts[MAX_TP * 32];  // chain state of the cross-cell path (rolled over ranks)
@@ -412,14 +412,14 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   uint64_t rk[C];  // (rank << 32) * K_MIX: a compute span's uid mix is rk + tidx * K_MIX
 #pragma unroll
   for (int r = 0; r < C; ++r) {
-    const int32_t rr = rank_of(g, tp0 + r, s, dpi);
+    const int32_t rr = rank_of(g, r, s, dpi);
     rb[r] = g.rank_ptr[rr];
     rs[r] = g.node_gptr[rb[r]];
     rk[r] = ((uint64_t)rr << 32) * K_MIX;
     if (lane == 0) rsh[r] = rs[r];
   }
   __syncwarp();
-  const int32_t len = g.rank_ptr[rank_of(g, tp0, s, dpi) + 1] - rb[0];
+  const int32_t len = g.rank_ptr[rank_of(g, 0, s, dpi) + 1] - rb[0];
   const uint64_t sx = p.seed ^ ((uint64_t)k * K_GOLD);
   // per-warp flags pinned in a register (an asm output cannot be rematerialised from the kernel
   // parameters, which the compiler otherwise reloads on every op)
@@ -430,11 +430,10 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   int64_t t[C];
 #pragma unroll
   for (int r = 0; r < C; ++r) t[r] = 0;
-  __shared__ int64_t ms_t[MS ? kMaxStreams : 1][32];  // MS: last finish of each stream
-  __shared__ int64_t ms_ev[MS ? kMaxEvents : 1][32];  // MS: latest record of each event slot
+  // MS state: [stream][rank][lane] then [event][rank][lane] (g.ms_streams, g.ms_events)
+  extern __shared__ int64_t ms_dyn[];
   if (MS) {
-    for (int x = 0; x < kMaxStreams; ++x) ms_t[x][lane] = 0;
-    for (int x = 0; x < kMaxEvents; ++x) ms_ev[x][lane] = 0;  // a never-recorded slot: satisfied
+    for (int x = 0; x < (g.ms_streams + g.ms_events) * C; ++x) ms_dyn[x * 32 + lane] = 0;  // unrecorded: satisfied
   }
 #ifdef PRISM_CELL_STATS
   const long long k_start = clock64();
@@ -488,15 +487,19 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
       const int32_t i = base + j;
       c_n = __shfl_sync(0xffffffffu, bcls, (j + 1) & 31);
       d_n = __shfl_sync(0xffffffffu, bd, (j + 1) & 31);
-      uint32_t ms_st = 0, ms_rec = 0;
-      if (MS) {  // row f2: the op's stream / event edges (C == 1)
+      int64_t *ms_sp = nullptr, *ms_rp = nullptr;  // MS: this op's stream / recorded-event rows
+      if (MS) {  // row f2: the op's stream / event edges (same for every rank of the cell)
         const uint32_t mb = __shfl_sync(0xffffffffu, bms, j);
-        ms_st = mb & 15u;
-        ms_rec = (mb >> 4) & 15u;
-        const uint32_t wt = (mb >> 8) & 15u;
-        int64_t rd = ms_t[ms_st][lane];
-        if (wt) rd = max(rd, ms_ev[wt - 1][lane]);
-        t[0] = rd;
+        const uint32_t st = mb & 15u, rec = (mb >> 4) & 15u, wt = (mb >> 8) & 15u;
+        ms_sp = ms_dyn + st * C * 32 + lane;
+        ms_rp = rec ? ms_dyn + (g.ms_streams + rec - 1) * C * 32 + lane : nullptr;
+        const int64_t *wp = wt ? ms_dyn + (g.ms_streams + wt - 1) * C * 32 + lane : nullptr;
+#pragma unroll
+        for (int r = 0; r < C; ++r) {
+          int64_t rd = ms_sp[r * 32];
+          if (wp) rd = max(rd, wp[r * 32]);
+          t[r] = rd;
+        }
       }
       int64_t dr[PR ? C : 1];  // PR: this op's per-rank durations (loaded during the previous op)
       if (PR) {
@@ -569,8 +572,11 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
 #endif
       }
       if (MS) {
-        ms_t[ms_st][lane] = t[0];
-        if (ms_rec) ms_ev[ms_rec - 1][lane] = t[0];
+#pragma unroll
+        for (int r = 0; r < C; ++r) {
+          ms_sp[r * 32] = t[r];
+          if (ms_rp) ms_rp[r * 32] = t[r];
+        }
       }
       if (record) {
 #pragma unroll
@@ -580,10 +586,12 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   }
 #pragma unroll
   if (MS) {  // a multi-stream rank ends with its last stream
-    for (int x = 0; x < kMaxStreams; ++x) t[0] = max(t[0], ms_t[x][lane]);
+#pragma unroll
+    for (int r = 0; r < C; ++r)
+      for (int x = 0; x < g.ms_streams; ++x) t[r] = max(t[r], ms_dyn[(x * C + r) * 32 + lane]);
   }
 #pragma unroll
-  for (int r = 0; r < C; ++r) rank_end[(int64_t)rank_of(g, tp0 + r, s, dpi) * Sp + k] = t[r];
+  for (int r = 0; r < C; ++r) rank_end[(int64_t)rank_of(g, r, s, dpi) * Sp + k] = t[r];
 #ifdef PRISM_CELL_STATS
   if (lane == 0) {
     STAT_ADD(0, clock64() - k_start);
@@ -594,47 +602,48 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
 
 typedef void (*cell_fn)(DevGraph, ScenParams, CellArgs, int64_t *, int64_t *, int64_t *);
 
-template <bool SH, bool PR>
+template <bool SH, bool PR, bool MS>
 cell_fn cell_kernel_t(int tp) {
   switch (tp) {
-    case 1: return cell_kernel<1, SH, PR, false>;
-    case 2: return cell_kernel<2, SH, PR, false>;
-    case 3: return cell_kernel<3, SH, PR, false>;
-    case 4: return cell_kernel<4, SH, PR, false>;
-    case 5: return cell_kernel<5, SH, PR, false>;
-    case 6: return cell_kernel<6, SH, PR, false>;
-    case 7: return cell_kernel<7, SH, PR, false>;
-    case 8: return cell_kernel<8, SH, PR, false>;
+    case 1: return cell_kernel<1, SH, PR, MS>;
+    case 2: return cell_kernel<2, SH, PR, MS>;
+    case 3: return cell_kernel<3, SH, PR, MS>;
+    case 4: return cell_kernel<4, SH, PR, MS>;
+    case 5: return cell_kernel<5, SH, PR, MS>;
+    case 6: return cell_kernel<6, SH, PR, MS>;
+    case 7: return cell_kernel<7, SH, PR, MS>;
+    case 8: return cell_kernel<8, SH, PR, MS>;
     default: return nullptr;
   }
 }
-template <bool SH, bool PR>
-cell_fn cell_kernel_ms() {
-  return cell_kernel<1, SH, PR, true>;
+template <bool MS>
+cell_fn cell_kernel_pick(const DevGraph &g) {
+  if (g.per_rank_dur) return g.n_shards > 1 ? cell_kernel_t<true, true, MS>(g.tp) : cell_kernel_t<false, true, MS>(g.tp);
+  return g.n_shards > 1 ? cell_kernel_t<true, false, MS>(g.tp) : cell_kernel_t<false, false, MS>(g.tp);
 }
 cell_fn cell_kernel_for(const DevGraph &g) {
-  if (g.ms) {  // multi-stream ranks: one rank per warp, any tp
-    if (g.per_rank_dur) return g.n_shards > 1 ? cell_kernel_ms<true, true>() : cell_kernel_ms<false, true>();
-    return g.n_shards > 1 ? cell_kernel_ms<true, false>() : cell_kernel_ms<false, false>();
-  }
-  if (g.per_rank_dur) return g.n_shards > 1 ? cell_kernel_t<true, true>(g.tp) : cell_kernel_t<false, true>(g.tp);
-  return g.n_shards > 1 ? cell_kernel_t<true, false>(g.tp) : cell_kernel_t<false, false>(g.tp);
+  return g.ms ? cell_kernel_pick<true>(g) : cell_kernel_pick<false>(g);
+}
+// dynamic shared memory of the multi-stream state (0 otherwise)
+size_t cell_dyn_smem(const DevGraph &g) {
+  return g.ms ? (size_t)(g.ms_streams + g.ms_events) * g.tp * 32 * 8 : 0;
 }
 
 cudaError_t preload_cell_kernels() {
   cudaFuncAttributes a;
   for (int tp = 1; tp <= MAX_TP; ++tp) {
-    cudaError_t e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<false, false>(tp));
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<true, false>(tp));
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<false, true>(tp));
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&a, (const void *)cell_kernel_t<true, true>(tp));
-    if (e != cudaSuccess) return e;
-  }
-  const void *ms[] = {(const void *)cell_kernel_ms<false, false>(), (const void *)cell_kernel_ms<true, false>(),
-                      (const void *)cell_kernel_ms<false, true>(), (const void *)cell_kernel_ms<true, true>()};
-  for (const void *f : ms) {
-    cudaError_t e = cudaFuncGetAttributes(&a, f);
-    if (e != cudaSuccess) return e;
+    const void *fns[] = {
+        (const void *)cell_kernel_t<false, false, false>(tp), (const void *)cell_kernel_t<true, false, false>(tp),
+        (const void *)cell_kernel_t<false, true, false>(tp), (const void *)cell_kernel_t<true, true, false>(tp),
+        (const void *)cell_kernel_t<false, false, true>(tp), (const void *)cell_kernel_t<true, false, true>(tp),
+        (const void *)cell_kernel_t<false, true, true>(tp), (const void *)cell_kernel_t<true, true, true>(tp)};
+    for (const void *f : fns) {
+      cudaError_t e = cudaFuncGetAttributes(&a, f);
+      if (e != cudaSuccess) return e;
+      // allow the multi-stream state beyond the 48 KB default of dynamic shared memory
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      if (e != cudaSuccess) return e;
+    }
   }
   return cudaSuccess;
 }
@@ -642,13 +651,13 @@ cudaError_t preload_cell_kernels() {
 // CTAs needed for `units` warps, if they can all be co-resident.
 bool cell_fit_units(const DevGraph &g, int64_t units, int *ctas) {
   cell_fn fn = cell_kernel_for(g);
-  if (!fn) return false;  // tp > 8 without multi-stream: the level-by-level schedule
+  if (!fn) return false;  // tp > 8: the level-by-level schedule
   int dev = 0, sms = 0, coop = 0, per_sm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
   if (!coop) return false;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, 0) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, cell_dyn_smem(g)) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
@@ -677,7 +686,7 @@ PollPolicy poll_policy() {
 
 // Chunks of 32 scenarios per unit; every chunk of a replay runs in one launch when they all fit,
 // else the caller launches one chunk at a time (chunk groups of 1).
-int64_t cell_count(const DevGraph &g) { return (int64_t)g.pp * (g.d1 - g.d0) * (g.ms ? g.tp : 1); }
+int64_t cell_count(const DevGraph &g) { return (int64_t)g.pp * (g.d1 - g.d0); }
 
 bool cells_fit(const DevGraph &g, int nchunks) {
   return cell_fit_units(g, cell_count(g), nullptr) && nchunks >= 1;
@@ -709,7 +718,8 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
   // pointer so the kernel indexes it by global node id
   int64_t *fin_g = fin ? (int64_t *)((uintptr_t)fin - (uintptr_t)(node0 * Sp * 8)) : nullptr;
   void *args[] = {&gg, &pp, &a, &fin_g, &gfin, &rank_end};
-  return cudaLaunchCooperativeKernel((const void *)cell_kernel_for(g), dim3(ctas), dim3(WARPS * 32), args, 0, st);
+  return cudaLaunchCooperativeKernel((const void *)cell_kernel_for(g), dim3(ctas), dim3(WARPS * 32), args,
+                                     cell_dyn_smem(g), st);
 }
 
 // Debug statistics of the last cell-kernel launch (PRISM_CELL_STATS builds only).

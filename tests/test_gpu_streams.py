@@ -109,3 +109,14 @@ def test_multistream_full_size_c2(prism):
         assert it[k] == r["iter"][0]
         if k == 0:
             assert np.array_equal(g.peak_memory(), r["peak"][0])
+
+
+@pytest.mark.slow
+def test_multistream_full_size_c5(prism):
+    """The 8192-rank C5 with overlapped gradient buckets (TP cells + per-rank stream / event
+    state): sampled scenarios' iteration times equal the oracle's."""
+    tm = w.overlap_grad_reduce(w.config("C5"))
+    g = _graph(prism, tm)
+    it = g.replay(64, amp_q16=6554, kind_mask=7)
+    for k in (0, 63):
+        assert it[k] == oracle.replay(tm, 1, scen_first=k, amp_q16=6554, kind_mask=7, peaks=False)["iter"][0]
