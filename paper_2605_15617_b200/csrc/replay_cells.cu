@@ -42,7 +42,6 @@ constexpr int SC = 32;          // scenarios per unit (one warp, lane = scenario
 constexpr int WARPS = 1;        // units per CTA (1: warps spread evenly over the SMs)
 constexpr int MAX_TP = 8;       // tp of the instantiated cell kernels
 constexpr int SMALL = kSmallGroup;
-constexpr int kPollList = MAX_TP * 4 * (kSmallGroup - 1);  // <= 32 pairs x 7 other members
 constexpr int kPollBatch = 8;  // poll loads issued back to back per batch (16 raised register pressure: slower)
 
 
@@ -190,18 +189,21 @@ __device__ __forceinline__ void prefetch_cross(const DevGraph &g, const XOp &xo,
 }
 
 // Per-warp shared scratch of the cross-cell path.
+template <int C>
 struct CrossScratch {
-  uint32_t meta[MAX_TP * 4];   // (rank, slot) pair x = r * ns + q: sync record of rank r's q-th group
-  int32_t base[MAX_TP * 4];
-  int32_t grp[MAX_TP * 4];
-  int64_t dur[MAX_TP * 4];
-  uint64_t uid[MAX_TP * 4];
-  uint32_t smask[MAX_TP * 4];  // row e: shards holding members of the pair's group
-  int64_t vmax[MAX_TP * 4][32];  // per pair, per lane: max ready time over the group's members
+  static constexpr int P = C * 4;                      // (rank, slot) pairs: <= 4 slots per op
+  static constexpr int L = P * (kSmallGroup - 1);      // poll-list entries
+  uint32_t meta[P];   // pair x = r * ns + q: sync record of rank r's q-th group
+  int32_t base[P];
+  int32_t grp[P];
+  int64_t dur[P];
+  uint64_t uid[P];
+  uint32_t smask[P];  // row e: shards holding members of the pair's group
+  int64_t vmax[P][32];  // per pair, per lane: max ready time over the group's members
   // poll list: one entry per (pair, other member) of a small group (ready-slot index) or per large
   // group (arrival-counter index), so a poll round issues every load before folding any of them
-  int32_t lidx[kPollList];
-  uint8_t lpair[kPollList];      // pair index | 0x80 for a large group's counter
+  int32_t lidx[L];
+  uint8_t lpair[L];   // pair index | 0x80 for a large group's counter
 };
 
 // Cross-cell node at template index i for all C ranks of the cell (rare: a few % of ops; kept
@@ -211,10 +213,10 @@ struct CrossScratch {
 // of the op. The op's C x ns sync records are staged in shared memory by one lane-parallel load;
 // deposit / arrive for every rank first, then poll (every poll of a pass is an independent load,
 // folded on the fly, the own slot is not read back), then finish = max over groups + dur'.
-template <bool SH>
+template <bool SH, int C>
 __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p, const CellArgs &a,
-                                          int64_t *__restrict__ gfin, int64_t *ts, int C, int32_t ns,
-                                          int32_t k, CrossScratch &cs, const PreRec &pre, int tl) {
+                                          int64_t *__restrict__ gfin, int64_t *ts, int32_t ns,
+                                          int32_t k, CrossScratch<C> &cs, const PreRec &pre, int tl) {
   const int lane = threadIdx.x & 31;
   const int32_t Sp = a.Sp;
   const int32_t ck = k / SC;
@@ -392,7 +394,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
 // slot in dynamic shared memory; an op starts at max(its stream's last finish, its awaited
 // event). The ranks of a cell still share one template, so TP collectives stay register-local.
 template <int C, bool SH, bool PR, bool MS>
-__global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
+__global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
                                                          int64_t *__restrict__ fin,
                                                          int64_t *__restrict__ gfin,
                                                          int64_t *__restrict__ rank_end) {
@@ -404,8 +406,8 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
   const int32_t s = cell % g.pp, dpi = g.d0 + cell / g.pp;
   const int32_t Sp = a.Sp;
   const int32_t k = chunk * SC + lane;
-  __shared__ int64_t ts[MAX_TP * 32];  // chain state of the cross-cell path (rolled over ranks)
-  __shared__ CrossScratch cs;
+  __shared__ int64_t ts[C * 32];  // chain state of the cross-cell path (rolled over ranks)
+  __shared__ CrossScratch<C> cs;
   __shared__ int32_t rsh[MAX_TP];       // first membership slot of each rank
   int32_t rb[C];
   int32_t rs[C];   // first membership slot of each rank (node_gptr of its first node)
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(WARPS * 32, 16) cell_kernel(DevGraph g, ScenPa
 #pragma unroll
         for (int r = 0; r < C; ++r) ts[r * 32 + lane] = t[r];
         __syncwarp();
-        const bool ok = cross_all<SH>(g, p, a, gfin, ts, C, xo.ns, k, cs, pre, tl);
+        const bool ok = cross_all<SH, C>(g, p, a, gfin, ts, xo.ns, k, cs, pre, tl);
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < C; ++r) t[r] = ts[r * 32 + lane];
