@@ -122,6 +122,8 @@ struct prism_graph_s {
   int32_t rslot_Sp = 0;
   int64_t *acc = nullptr;     // large-group accumulators [G_large][Sp]
   size_t acc_bytes = 0;
+  int64_t *rres = nullptr;    // large-group result slots [G_large][Sp] (parity-encoded)
+  size_t rres_bytes = 0;
   uint32_t *sync_words = nullptr;  // arrive[G_large], status[4]
   size_t sync_bytes = 0;
   uint32_t *h_status = nullptr;    // pinned copy of the status word
@@ -217,6 +219,7 @@ struct prism_graph_s {
     dfree(tiles);
     dfree(rslot);
     dfree(acc);
+    dfree(rres);
     dfree(sync_words);
     dfree(part);
     dfree(ov);
@@ -628,7 +631,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     trace("shard: launch cells");
     const int per_launch = cells_chunks_per_launch(G->cur(), nchunks);
     for (int ch = 0; ch < nchunks; ch += per_launch) {
-      CU(launch_cells(G->cur(), p, rslot, acc, arrive, status, G->parity, p.record ? G->fin : nullptr, G->fin_node0,
+      CU(launch_cells(G->cur(), p, rslot, acc, nullptr, arrive, status, G->parity, p.record ? G->fin : nullptr, G->fin_node0,
                       G->gfin, G->rank_end, ch, std::min(per_launch, nchunks - ch), Sp, &G->link, G->stream));
       ++launches;
     }
@@ -651,11 +654,15 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     if (!G->ensure(G->rslot, G->rslot_bytes, rs_bytes)) return fail(PRISM_E_OOM, "ready-slot allocation failed");
     if (!G->ensure(G->acc, G->acc_bytes, std::max<size_t>(16, (size_t)P.G_large * Sp * 8)))
       return fail(PRISM_E_OOM, "accumulator allocation failed");
+    const size_t rr_bytes = std::max<size_t>(16, (size_t)P.G_large * Sp * 8);
+    if (G->rres_bytes < rr_bytes) G->rslot_dirty = true;  // result slots share the ready slots' parity
+    if (!G->ensure(G->rres, G->rres_bytes, rr_bytes)) return fail(PRISM_E_OOM, "result-slot allocation failed");
     const size_t nwords = (size_t)P.G_large * nchunks + 4;
     if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
     if (!G->h_status && !(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status word unavailable");
     if (G->rslot_dirty) {  // all slots read "not yet" under parity 0
       CU(cudaMemsetAsync(G->rslot, 0xFF, G->rslot_bytes, G->stream));
+      CU(cudaMemsetAsync(G->rres, 0xFF, G->rres_bytes, G->stream));
       G->parity = 0;
       G->rslot_dirty = false;
     }
@@ -665,7 +672,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     uint32_t *status = G->sync_words + (size_t)P.G_large * nchunks;
     const int per_launch = cells_chunks_per_launch(G->cur(), nchunks);
     for (int ch = 0; ch < nchunks; ch += per_launch) {
-      CU(launch_cells(G->cur(), p, G->rslot, G->acc, G->sync_words, status, G->parity,
+      CU(launch_cells(G->cur(), p, G->rslot, G->acc, G->rres, G->sync_words, status, G->parity,
                       p.record ? G->fin : nullptr, 0, G->gfin, G->rank_end, ch,
                       std::min(per_launch, nchunks - ch), Sp, nullptr, G->stream));
       ++launches;

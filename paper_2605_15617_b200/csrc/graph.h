@@ -152,7 +152,7 @@ bool cells_fit(const DevGraph &g, int nchunks);
 int cells_chunk_scenarios();
 int cells_chunks_per_launch(const DevGraph &g, int nchunks);
 cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc,
-                         uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t node0,
+                         int64_t *rres, uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t node0,
                          int64_t *gfin, int64_t *rank_end, int chunk0, int nchunks_launch, int Sp,
                          const ShardLink *link, cudaStream_t st);
 // row e: iteration times of a sharded replay (local partial max, peer exchange, global max)

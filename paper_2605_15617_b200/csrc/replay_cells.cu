@@ -111,6 +111,7 @@ __device__ unsigned long long g_tl[16 * 128 * 4];  // dp 0, chunk 0: [stage][cro
 struct CellArgs {
   int64_t *rslot;      // [M_cross][Sp] ready slots of small-group memberships
   int64_t *acc;        // [G_large][Sp] max-accumulators of large groups (zeroed per replay)
+  int64_t *rres;       // [G_large][Sp] result slots of large groups (parity-encoded like rslot)
   uint32_t *arrive;    // [G_large] arrival counters of large groups (zeroed per replay)
   uint32_t *status;    // [0] = abort flag / error code
   uint64_t timeout_ns;
@@ -231,6 +232,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
   }
   __syncwarp();
   bool large_any = false;
+  const int64_t pm_dep = a.parity ? -1 : 0;  // slot encoding of this replay
   for (int x = 0, r = 0, q = 0; x < np; ++x) {  // x = r * ns + q, no divisions
     const int64_t tr = ts[r * 32 + lane];
     if (++q == ns) {
@@ -241,7 +243,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
     const int32_t base = cs.base[x];
     if (!(meta & 0x80000000u)) {
       const int64_t off = (int64_t)(base + (int32_t)((meta >> 16) & 0x7FFF)) * Sp + k;
-      const int64_t enc = a.parity ? ~tr : tr;
+      const int64_t enc = tr ^ pm_dep;
       if (!SH) {
         st_relaxed64(a.rslot + off, enc);
       } else {
@@ -258,22 +260,44 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
       }
     }
   }
+  uint32_t large_done = 0;  // !SH: large pairs this warp completed as their last arriver
   if (large_any) {
-    // the accumulations are performed before the arrival is counted
-    if (SH) __threadfence_system();
-    else __threadfence();
-    __syncwarp();
-    if (lane == 0)
-      for (int x = 0; x < np; ++x)
-        if (cs.meta[x] & 0x80000000u) {
-          const int64_t ai = (int64_t)cs.base[x] * a.nchunks + ck;
-          if (!SH) {
-            atomicAdd(a.arrive + ai, 1u);
-          } else {
+    if (SH) {
+      // the accumulations are performed before the arrival is counted (system scope: peers)
+      __threadfence_system();
+      __syncwarp();
+      if (lane == 0)
+        for (int x = 0; x < np; ++x)
+          if (cs.meta[x] & 0x80000000u) {
+            const int64_t ai = (int64_t)cs.base[x] * a.nchunks + ck;
             for (uint32_t m = cs.smask[x]; m; m &= m - 1)
               atomicAdd_system(peer32(a.L, __ffs(m) - 1, a.L.o_arrive) + ai, 1u);
           }
-        }
+    } else {
+      // last arriver publishes: the lanes' red.max are ordered before lane 0's acq_rel arrival
+      // (bar.warp.sync orders the warp's memory operations); the member whose arrival completes
+      // the count reads the accumulator (acquire: every member's max is visible) and writes the
+      // group's max into a value-as-flag result slot, which the other members poll like a
+      // ready slot — no fence on anyone's path
+      __syncwarp();
+      if (lane == 0)
+        for (int x = 0; x < np; ++x)
+          if (cs.meta[x] & 0x80000000u) {
+            const int64_t ai = (int64_t)cs.base[x] * a.nchunks + ck;
+            uint32_t old;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.arrive + ai) : "memory");
+            if (old + 1 == (cs.meta[x] & 0xFFFF)) large_done |= 1u << x;
+          }
+      large_done = __shfl_sync(0xffffffffu, large_done, 0);
+      __syncwarp();
+      for (uint32_t m = large_done; m; m &= m - 1) {
+        const int x = __ffs(m) - 1;
+        const int64_t off = (int64_t)cs.base[x] * Sp + k;
+        const int64_t v = ld_relaxed64(a.acc + off);
+        st_relaxed64(a.rres + off, v ^ pm_dep);
+        cs.vmax[x][lane] = v;
+      }
+    }
   }
 #ifdef PRISM_CELL_STATS
   if (tl >= 0 && lane == 0) g_tl[tl * 4 + 1] = globaltimer();
@@ -317,11 +341,12 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
     }
     for (int r = 0, x = 0; r < C; ++r) {
       const int64_t tr = ts[r * 32 + lane];
-      for (int q = 0; q < ns; ++q, ++x) cs.vmax[x][lane] = tr;
+      for (int q = 0; q < ns; ++q, ++x)
+        if (!((large_done >> x) & 1u)) cs.vmax[x][lane] = tr;  // completed large pairs hold the max
     }
     __syncwarp();
   }
-  uint32_t pending = np >= 32 ? 0xFFFFFFFFu : ((1u << np) - 1u);
+  uint32_t pending = (np >= 32 ? 0xFFFFFFFFu : ((1u << np) - 1u)) & ~large_done;
   uint32_t spins = 0;
   uint64_t tw = 0;
   while (true) {
@@ -336,9 +361,11 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
           const uint32_t pr = cs.lpair[j];
           if ((pending >> (pr & 31)) & 1u) {
             const int32_t idx = cs.lidx[j];
-            if (pr & 0x80)
+            if ((pr & 0x80) && SH)
               v[u] = (int64_t)poll32<SH>(a.arrive + (int64_t)idx * a.nchunks + ck) -
                      (int64_t)(cs.meta[pr & 31] & 0xFFFF);
+            else if (pr & 0x80)  // the large group's result slot (published by its last arriver)
+              v[u] = poll64<SH>(a.rres + (int64_t)idx * Sp + k) ^ pm;
             else
               v[u] = poll64<SH>(a.rslot + (int64_t)idx * Sp + k) ^ pm;
           }
@@ -352,7 +379,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
           const int x = pr & 31;
           if ((pending >> x) & 1u) {
             if (v[u] < 0) bad |= 1u << x;
-            else if (!(pr & 0x80)) cs.vmax[x][lane] = max(cs.vmax[x][lane], v[u]);
+            else if (!(pr & 0x80) || !SH) cs.vmax[x][lane] = max(cs.vmax[x][lane], v[u]);
           }
         }
       }
@@ -364,15 +391,12 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
 #ifdef PRISM_CELL_STATS
   if (tl >= 0 && lane == 0) g_tl[tl * 4 + 2] = globaltimer();
 #endif
-  if (large_any) {
-    if (SH) fence_acq_rel_sys();
-    else fence_acq_rel();
-  }
+  if (large_any && SH) fence_acq_rel_sys();
   for (int r = 0; r < C; ++r) {
     int64_t fr = 0;
     for (int32_t q = 0; q < ns; ++q) {
       const int x = r * ns + q;
-      int64_t m = (cs.meta[x] & 0x80000000u) ? __ldcg(a.acc + (int64_t)cs.base[x] * Sp + k) : cs.vmax[x][lane];
+      int64_t m = ((cs.meta[x] & 0x80000000u) && SH) ? __ldcg(a.acc + (int64_t)cs.base[x] * Sp + k) : cs.vmax[x][lane];
       const int64_t gd = cs.dur[x];
       const uint64_t uid = cs.uid[x];
       const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
@@ -703,7 +727,7 @@ int cells_chunks_per_launch(const DevGraph &g, int nchunks) {
 }
 
 cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc,
-                         uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t node0,
+                         int64_t *rres, uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t node0,
                          int64_t *gfin, int64_t *rank_end, int chunk0, int nchunks_launch, int Sp,
                          const ShardLink *link, cudaStream_t st) {
   const int64_t units = cell_count(g) * nchunks_launch;
@@ -711,7 +735,7 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
   if (!cell_fit_units(g, units, &ctas)) return cudaErrorCooperativeLaunchTooLarge;
   // the launch covers chunks [chunk0, chunk0 + nchunks_launch) of the replay's Sp / 32 chunks
   static const PollPolicy pol = poll_policy();
-  CellArgs a{rslot, acc, arrive, status, 10ull * 1000 * 1000 * 1000, parity, (int32_t)units, Sp, chunk0,
+  CellArgs a{rslot, acc, rres, arrive, status, 10ull * 1000 * 1000 * 1000, parity, (int32_t)units, Sp, chunk0,
              Sp / SC, pol.spin, pol.sleep0, pol.sleep_max, ShardLink{}};
   if (link) a.L = *link;
   DevGraph gg = g;
