@@ -213,3 +213,17 @@ def test_full_size_sampled(prism, name):
         st, fi, _ = g.query_rank(int(rk), 63)
         assert fi[-1] == res[2]["rank_end"][0, rk] if len(fi) else True
     g.close()
+
+
+def test_wide_tp_uses_levels(prism):
+    """tp > 8 has no cell-kernel instantiation: the auto schedule falls back to one launch per
+    frontier level, bit-exact as well; a multi-stream graph with tp > 8 is refused."""
+    tm = w.uniform_pipeline(16, 2, 2, 4, p2p_c=30)
+    it = _check_replay(prism, tm, 33, times=True)
+    g = _graph(prism, tm)
+    g.replay(2)
+    assert g.last_algo() == "levels"
+    ov = w.overlap_grad_reduce(tm)
+    g2 = _graph(prism, ov)
+    with pytest.raises(prism.PrismError):
+        g2.replay(2)
