@@ -117,6 +117,18 @@ __device__ __forceinline__ uint32_t shard_mask(const DevGraph &g, int32_t type, 
 // ops, then over its template slots; every write is a coalesced run along the rank's nodes /
 // membership slots. A slot's group instance and member index follow in closed form from the
 // rank's coordinates (the same enumeration as the group side below).
+// A quotient group through the read-only path (16-byte loads): the expansion's loads can then be
+// scheduled ahead of its stores (plain loads would be ordered behind them, as they may alias).
+__device__ __forceinline__ QGroup ldg_q(const QGroup *p) {
+  static_assert(sizeof(QGroup) % 16 == 0, "QGroup is loaded as int4 words");
+  QGroup q;
+  const int4 *src = reinterpret_cast<const int4 *>(p);
+  int4 *dst = reinterpret_cast<int4 *>(&q);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(QGroup) / 16); ++i) dst[i] = __ldg(src + i);
+  return q;
+}
+
 // Instance of quotient group q that a rank with these coordinates joins (closed form, a2).
 __device__ __forceinline__ int32_t group_inst(const DevGraph &g, int32_t type, int32_t tpi, int32_t dpi,
                                               int32_t epi, int32_t edpi) {
@@ -144,6 +156,7 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
     // node side: every array written coalesced along the rank's nodes; template fields read
     // through the read-only path (L2-resident tables) so loads of later ops are not ordered
     // behind this op's stores
+#pragma unroll 2
     for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
       const prism_op *o = g.t_ops + op0 + i;
       const int32_t n = rb + i;
@@ -172,7 +185,7 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
         g.node_sdur[n] = dur;
         g.node_uid[n] = ((uint64_t)r << 32) | (uint32_t)i;
       } else {
-        const QGroup &q = g.q[q0];
+        const QGroup q = ldg_q(g.q + q0);
         g.node_sdur[n] = q.dur;
         g.node_uid[n] = group_uid(g, q, group_inst(g, q.type, tpi, dpi, epi, edpi));
       }
@@ -180,8 +193,9 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
     // slot side
     const int64_t u0 = g.stage_slot0[s];
     const int32_t nsl = (int32_t)(g.stage_slot0[s + 1] - u0);
+#pragma unroll 2
     for (int32_t u = threadIdx.x; u < nsl; u += blockDim.x) {
-      const QGroup &q = g.q[__ldg(g.slot_q + u0 + u)];
+      const QGroup q = ldg_q(g.q + __ldg(g.slot_q + u0 + u));
       const int32_t inst = group_inst(g, q.type, tpi, dpi, epi, edpi);
       int32_t j;
       switch (q.type) {
@@ -190,7 +204,7 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
         case PRISM_ROLE_EP: j = epi; break;
         case PRISM_ROLE_EDP: j = edpi; break;
         case PRISM_ROLE_WORLD: j = r; break;
-        default: j = g.slot_role[u0 + u]; break;
+        default: j = __ldg(g.slot_role + u0 + u); break;
       }
       const int32_t h = slot0 + u;
       const int64_t grp = q.gbase + inst;
