@@ -12,8 +12,8 @@ Prints ONE JSON line on rank 0. Metric: replayed graph ops/s = nodes x scenarios
 (plus emulated iterations/s = scenarios / step time in "extra"). Multi-GPU (row e): one process
 per GPU (torchrun); by default the 8192 ranks are sharded over the N GPUs by DP block with the
 cross-shard segmented max fused into the replay kernel over NVLink peer memory, and the scenario
-batch grows with N (N x 64: weak scaling, per-GPU node-scenarios fixed); `--shard replicas` runs N
-independent replicas instead. Time = max over ranks of the device-timed region.
+batch grows with N (N x 64: weak scaling, per-GPU node-scenarios fixed); `--shard replicas` has
+each GPU replay the whole graph for its own block of 64 scenarios of the sweep instead. Time = max over ranks of the device-timed region.
 """
 from __future__ import annotations
 
@@ -126,7 +126,9 @@ def run_prism(args):
     tm = w.config(args.config)
     sharded = ws > 1 and args.shard == "ranks"
     S = args.scenarios * (ws if sharded else 1)  # sharded: N x 64 scenarios over N GPUs (weak)
-    kw = dict(amp_q16=args.amp, kind_mask=7, seed=0x5EED, algo=args.algo)
+    # replicas: GPU i sweeps its own block of scenarios (i*S .. i*S+S-1) of one what-if sweep
+    kw = dict(amp_q16=args.amp, kind_mask=7, seed=0x5EED, algo=args.algo,
+              first=(rank * args.scenarios if (ws > 1 and not sharded) else 0))
     iter_dev = torch.zeros(S, dtype=torch.int64, device="cuda")
     peak_dev = torch.zeros(tm.topo.world, dtype=torch.int64, device="cuda")
     comm = [None]  # sharded: the graph currently holding the connected exchange buffer

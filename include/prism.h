@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PRISM_ABI_VERSION 2
+#define PRISM_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define PRISM_API __attribute__((visibility("default")))
@@ -160,6 +160,11 @@ typedef struct {
   int32_t record;     /* nonzero: keep every node's finish time for prism_query_rank           */
   int32_t algo;       /* PRISM_ALGO_AUTO (cells when they fit on the device, else levels),
                          PRISM_ALGO_LEVELS (one launch per frontier level), PRISM_ALGO_CELLS   */
+  int32_t first;      /* global index of the batch's first scenario: local scenario j is
+                         scenario first + j of the sweep (perturbation key k = first + j; only
+                         global scenario 0 is unperturbed). Lets a sweep run in batches or be
+                         split over GPUs; outputs stay indexed by the local j.                */
+  int32_t pad;
 } prism_scenarios;
 
 enum { PRISM_ALGO_AUTO = 0, PRISM_ALGO_LEVELS = 1, PRISM_ALGO_CELLS = 2 };

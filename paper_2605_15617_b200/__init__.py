@@ -61,7 +61,8 @@ class _BuildOpts(ctypes.Structure):
 
 class _Scenarios(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("amp_q16", ctypes.c_int32), ("seed", ctypes.c_uint64),
-                ("kind_mask", ctypes.c_uint32), ("record", ctypes.c_int32), ("algo", ctypes.c_int32)]
+                ("kind_mask", ctypes.c_uint32), ("record", ctypes.c_int32), ("algo", ctypes.c_int32),
+                ("first", ctypes.c_int32), ("pad", ctypes.c_int32)]
 
 
 class _Durations(ctypes.Structure):
@@ -239,22 +240,22 @@ class Graph:
     ALGOS = {"auto": 0, "levels": 1, "cells": 2}
 
     @classmethod
-    def _scen(cls, n, seed, amp_q16, kind_mask, record, algo):
+    def _scen(cls, n, seed, amp_q16, kind_mask, record, algo, first=0):
         return _Scenarios(int(n), int(amp_q16), int(seed) & (2**64 - 1), int(kind_mask), int(bool(record)),
-                          cls.ALGOS[algo])
+                          cls.ALGOS[algo], int(first), 0)
 
     def replay(self, n: int = 1, *, seed: int = 0x5EED, amp_q16: int = 0, kind_mask: int = 0,
-               record: bool = True, algo: str = "auto") -> np.ndarray:
-        """Iteration time (ns) of each of n scenarios (host result, synchronizing)."""
+               record: bool = True, algo: str = "auto", first: int = 0) -> np.ndarray:
+        """Iteration time (ns) of each of n scenarios first .. first+n-1 (host result, synchronizing)."""
         out = np.zeros(n, np.int64)
-        sc = self._scen(n, seed, amp_q16, kind_mask, record, algo)
+        sc = self._scen(n, seed, amp_q16, kind_mask, record, algo, first)
         _check(lib().prism_replay(self._h, ctypes.byref(sc), _ptr(out)))
         return out
 
     def replay_async(self, iter_dev_ptr: int, n: int = 1, *, seed: int = 0x5EED, amp_q16: int = 0,
-                     kind_mask: int = 0, record: bool = True, algo: str = "auto") -> None:
+                     kind_mask: int = 0, record: bool = True, algo: str = "auto", first: int = 0) -> None:
         """Asynchronous replay writing n int64 iteration times to a DEVICE pointer."""
-        sc = self._scen(n, seed, amp_q16, kind_mask, record, algo)
+        sc = self._scen(n, seed, amp_q16, kind_mask, record, algo, first)
         _check(lib().prism_replay_async(self._h, ctypes.byref(sc), ctypes.c_void_p(iter_dev_ptr)))
 
     def last_algo(self) -> str:

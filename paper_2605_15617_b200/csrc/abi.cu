@@ -565,6 +565,8 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   if (sc->n < 1 || sc->n > (1 << 20) || sc->amp_q16 < 0 || sc->amp_q16 > 65535)
     return fail(PRISM_E_INVALID_ARG, "scenario count must be >= 1 and amp_q16 in [0, 65535]");
   if (sc->algo < PRISM_ALGO_AUTO || sc->algo > PRISM_ALGO_CELLS) return fail(PRISM_E_INVALID_ARG, "unknown algo");
+  if (sc->first < 0 || (int64_t)sc->first + sc->n > (1LL << 31) - 1)
+    return fail(PRISM_E_INVALID_ARG, "first scenario index out of range");
   CU(cudaSetDevice(G->device));
   const int32_t S = sc->n;
   const Plan &P = G->plan;
@@ -596,6 +598,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   const int32_t Sp = nchunks * SC;
   ScenParams p{};
   p.S = S;
+  p.first = sc->first;
   p.amp = sc->amp_q16;
   p.seed = sc->seed;
   p.mask = sc->kind_mask;

@@ -91,6 +91,7 @@ struct DevGraph {
 // Scenario parameters as seen by the kernels.
 struct ScenParams {
   int32_t S;         // scenarios
+  int32_t first;     // global index of local scenario 0 (perturbation key k = first + local)
   int32_t amp;       // amp_q16
   uint64_t seed;
   uint32_t mask;     // kind mask

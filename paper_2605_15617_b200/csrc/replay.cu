@@ -104,8 +104,8 @@ __global__ void __launch_bounds__(256) level_kernel(DevGraph g, ScenParams p,
   bool pj[SPL];  // scenario 0 and unmasked kinds are never perturbed
 #pragma unroll
   for (int j = 0; j < SPL; ++j) {
-    sx[j] = p.seed ^ ((uint64_t)(k0 + j) * K_GOLD);
-    pj[j] = (p.mask & 1u) && p.amp > 0 && (k0 + j) > 0;
+    sx[j] = p.seed ^ ((uint64_t)(p.first + k0 + j) * K_GOLD);
+    pj[j] = (p.mask & 1u) && p.amp > 0 && (p.first + k0 + j) > 0;
   }
   for (int32_t mm = team; mm < nmem; mm += TEAMS) {
     const int32_t n = g.grp_mem[m0 + mm];
@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(256) level_kernel(DevGraph g, ScenParams p,
     const int64_t grp = g0 + gl;
     const int64_t d = g.grp_dur[grp];
     int64_t dd = d;
-    if (gpert && kk > 0) dd = perturb_x(d, p.seed ^ ((uint64_t)kk * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
+    const int32_t kg = p.first + kk;  // global scenario index (perturbation key)
+    if (gpert && kg > 0) dd = perturb_x(d, p.seed ^ ((uint64_t)kg * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
     gfin[grp * Sp + kk] = (int64_t)acc[x] + dd;
   }
 }
@@ -146,8 +147,8 @@ __global__ void __launch_bounds__(256) tail_kernel(DevGraph g, ScenParams p, int
   bool pj[SPL];
 #pragma unroll
   for (int j = 0; j < SPL; ++j) {
-    sx[j] = p.seed ^ ((uint64_t)(k0 + j) * K_GOLD);
-    pj[j] = (p.mask & 1u) && p.amp > 0 && (k0 + j) > 0;
+    sx[j] = p.seed ^ ((uint64_t)(p.first + k0 + j) * K_GOLD);
+    pj[j] = (p.mask & 1u) && p.amp > 0 && (p.first + k0 + j) > 0;
   }
   for (int32_t r = blockIdx.x * TEAMS + team; r < g.W; r += gridDim.x * TEAMS) {
     const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
@@ -269,17 +270,18 @@ __device__ __forceinline__ int64_t node_start(const DevGraph &g, const ScenParam
                                               const int64_t *fin, const int64_t *gfin, int32_t r, int32_t rb,
                                               int32_t i, int32_t k) {
   const int32_t h0 = g.node_gptr[i], h1 = g.node_gptr[i + 1];
+  const int32_t kg = p.first + k;  // global scenario index (perturbation key)
   if (h0 == h1) {  // compute span: exact, finish = start + d'
     int64_t d = g.node_dur[i];
-    if ((p.mask & 1u) && p.amp > 0 && k > 0)
-      d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ ((((uint64_t)r << 32) | (uint32_t)(i - rb)) * K_MIX), p);
+    if ((p.mask & 1u) && p.amp > 0 && kg > 0)
+      d = perturb_x(d, p.seed ^ ((uint64_t)kg * K_GOLD) ^ ((((uint64_t)r << 32) | (uint32_t)(i - rb)) * K_MIX), p);
     return fin[(int64_t)i * Sp + k] - d;
   }
   if (h1 - h0 == 1) {
     const int64_t grp = g.node_grp[h0];
     const uint32_t gbit = (g.grp_uid[grp] >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
     int64_t d = g.grp_dur[grp];
-    if ((p.mask & gbit) && p.amp > 0 && k > 0) d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
+    if ((p.mask & gbit) && p.amp > 0 && kg > 0) d = perturb_x(d, p.seed ^ ((uint64_t)kg * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
     return fin[(int64_t)i * Sp + k] - d;
   }
   int64_t st = 0;
@@ -287,7 +289,7 @@ __device__ __forceinline__ int64_t node_start(const DevGraph &g, const ScenParam
     const int64_t grp = g.node_grp[h];
     const uint32_t gbit = (g.grp_uid[grp] >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
     int64_t d = g.grp_dur[grp];
-    if ((p.mask & gbit) && p.amp > 0 && k > 0) d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
+    if ((p.mask & gbit) && p.amp > 0 && kg > 0) d = perturb_x(d, p.seed ^ ((uint64_t)kg * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
     st = max(st, gfin[grp * Sp + k] - d);
   }
   return st;

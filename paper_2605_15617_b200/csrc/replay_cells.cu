@@ -400,7 +400,8 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
       const int64_t gd = cs.dur[x];
       const uint64_t uid = cs.uid[x];
       const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
-      if ((p.mask & gb) && p.amp > 0 && k > 0) m += perturb_x(gd, p.seed ^ ((uint64_t)k * K_GOLD) ^ (uid * K_MIX), p);
+      const int32_t kg = p.first + k;  // global scenario index (perturbation key)
+      if ((p.mask & gb) && p.amp > 0 && kg > 0) m += perturb_x(gd, p.seed ^ ((uint64_t)kg * K_GOLD) ^ (uid * K_MIX), p);
       else m += gd;
       fr = max(fr, m);
       if (ns > 1) gfin[(int64_t)cs.grp[x] * Sp + k] = m;  // P2P-batch group finishes, for queries
@@ -446,10 +447,11 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
   }
   __syncwarp();
   const int32_t len = g.rank_ptr[rank_of(g, 0, s, dpi) + 1] - rb[0];
-  const uint64_t sx = p.seed ^ ((uint64_t)k * K_GOLD);
+  const int32_t kg = p.first + k;  // global scenario index (perturbation key)
+  const uint64_t sx = p.seed ^ ((uint64_t)kg * K_GOLD);
   // per-warp flags pinned in a register (an asm output cannot be rematerialised from the kernel
   // parameters, which the compiler otherwise reloads on every op)
-  uint32_t fl = (((p.mask & 1u) && p.amp > 0 && k > 0) ? 1u : 0u) | (((p.mask & 2u) && p.amp > 0 && k > 0) ? 2u : 0u) |
+  uint32_t fl = (((p.mask & 1u) && p.amp > 0 && kg > 0) ? 1u : 0u) | (((p.mask & 2u) && p.amp > 0 && kg > 0) ? 2u : 0u) |
                 (p.record ? 4u : 0u);
   asm volatile("" : "+r"(fl));
   const bool cpert = fl & 1u, gpert = fl & 2u, record = fl & 4u;

@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(32) crit_walk_kernel(DevGraph g, ScenParams p,
         const uint64_t uid = g.grp_uid[gi];
         const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
         int64_t d = g.grp_dur[gi];
-        if ((p.mask & gb) && p.amp > 0 && k > 0) d = perturb_x(d, p.seed ^ ((uint64_t)k * K_GOLD) ^ (uid * K_MIX), p);
+        const int32_t kg = p.first + k;  // global scenario index (perturbation key)
+        if ((p.mask & gb) && p.amp > 0 && kg > 0) d = perturb_x(d, p.seed ^ ((uint64_t)kg * K_GOLD) ^ (uid * K_MIX), p);
         const int64_t f = gs + d;
         if (f > bf || (f == bf && uid < buid)) {
           bf = f;

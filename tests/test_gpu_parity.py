@@ -227,3 +227,19 @@ def test_wide_tp_uses_levels(prism):
     g2 = _graph(prism, ov)
     with pytest.raises(prism.PrismError):
         g2.replay(2)
+
+
+def test_scenario_offset(prism):
+    """prism_scenarios.first: a batch replays scenarios first .. first+n-1 of the sweep."""
+    tm = w.scaled("C2")
+    g = _graph(prism, tm)
+    full = g.replay(40, amp_q16=6554, kind_mask=7)
+    part = g.replay(13, amp_q16=6554, kind_mask=7, first=27)
+    assert np.array_equal(part, full[27:40])
+    ref = oracle.replay(tm, 5, scen_first=100, amp_q16=6554, kind_mask=7, threads=NPROC)
+    assert np.array_equal(g.replay(5, amp_q16=6554, kind_mask=7, first=100, algo="levels"), ref["iter"])
+    assert np.array_equal(g.replay(5, amp_q16=6554, kind_mask=7, first=100, algo="cells"), ref["iter"])
+    st, fi, _ = g.query_rank(3, 4)
+    r2 = oracle.replay(tm, 1, scen_first=104, amp_q16=6554, kind_mask=7, times=True)
+    rp = g.export("rank_ptr")
+    assert np.array_equal(st, r2["start"][0, rp[3]:rp[4]]) and np.array_equal(fi, r2["finish"][0, rp[3]:rp[4]])
