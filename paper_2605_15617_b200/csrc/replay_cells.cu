@@ -41,7 +41,6 @@ constexpr uint64_t K_MIX = 0xBF58476D1CE4E5B9ULL;
 constexpr int SC = 32;          // scenarios per unit (one warp, lane = scenario)
 constexpr int WARPS = 1;        // units per CTA (1: warps spread evenly over the SMs)
 constexpr int MAX_TP = 8;       // tp of the instantiated cell kernels
-constexpr int SMALL = kSmallGroup;
 constexpr int kPollBatch = 8;  // poll loads issued back to back per batch (16 raised register pressure: slower)
 
 
@@ -65,7 +64,6 @@ __device__ __forceinline__ int64_t ld_relaxed64(const int64_t *p) {
 __device__ __forceinline__ void st_relaxed64(int64_t *p, int64_t v) {
   asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void red_max(int64_t *p, int64_t v) {
   asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(p), "l"((uint64_t)v) : "memory");
 }
@@ -612,7 +610,6 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
       }
     }
   }
-#pragma unroll
   if (MS) {  // a multi-stream rank ends with its last stream
 #pragma unroll
     for (int r = 0; r < C; ++r)

@@ -114,3 +114,18 @@ def test_no_cpu_fallback():
     with pytest.raises(prism.PrismError) as e:
         prism.Graph(w.config("C1"))
     assert e.value.name == "PRISM_E_CUDA"
+
+
+def test_bench_reference_arm_runs():
+    """bench.py --impl reference (the CPU oracle arm) prints its JSON line on a bounded sample."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "1", "--config", "C2"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
+    assert d["e2e"]["h2d_bytes_per_step"] == 0
