@@ -167,7 +167,9 @@ typedef struct {
   int32_t pad;
 } prism_scenarios;
 
-enum { PRISM_ALGO_AUTO = 0, PRISM_ALGO_LEVELS = 1, PRISM_ALGO_CELLS = 2 };
+/* PRISM_ALGO_RANKS: one scenario, one rank per lane (auto picks it for n == 1 when the graph is
+ * unsharded and single-stream with tp a power of two <= 32). */
+enum { PRISM_ALGO_AUTO = 0, PRISM_ALGO_LEVELS = 1, PRISM_ALGO_CELLS = 2, PRISM_ALGO_RANKS = 3 };
 
 /* ---- entry points ------------------------------------------------------------------------ */
 
@@ -326,7 +328,7 @@ PRISM_API prism_status prism_graph_stats(prism_graph_t g, int64_t out[10]);
  * is a connected shard (its exchange buffer is synchronously released). */
 PRISM_API void prism_destroy_graph(prism_graph_t g);
 
-/* Schedule used by the last replay: PRISM_ALGO_LEVELS or PRISM_ALGO_CELLS (0 before any). */
+/* Schedule used by the last replay: PRISM_ALGO_LEVELS, _CELLS or _RANKS (0 before any). */
 PRISM_API prism_status prism_last_algo(prism_graph_t g, int32_t *algo_out);
 
 /* Device time (ms, CUDA events on the graph's stream) of the last call of each kernel group of a

@@ -237,7 +237,7 @@ class Graph:
         _check(lib().prism_last_timing(self._h, _ptr(out)))
         return dict(zip(["expand", "levels", "tail", "reduce", "peak"], (float(x) for x in out)))
 
-    ALGOS = {"auto": 0, "levels": 1, "cells": 2}
+    ALGOS = {"auto": 0, "levels": 1, "cells": 2, "ranks": 3}
 
     @classmethod
     def _scen(cls, n, seed, amp_q16, kind_mask, record, algo, first=0):
@@ -261,7 +261,7 @@ class Graph:
     def last_algo(self) -> str:
         v = ctypes.c_int32(0)
         _check(lib().prism_last_algo(self._h, ctypes.byref(v)))
-        return {0: "none", 1: "levels", 2: "cells"}[v.value]
+        return {0: "none", 1: "levels", 2: "cells", 3: "ranks"}[v.value]
 
     def peak_memory(self) -> np.ndarray:
         out = np.zeros(self.topo.tp * self.topo.pp * self.topo.dp, np.int64)

@@ -505,6 +505,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     if (std::find(loaded.begin(), loaded.end(), G->device) == loaded.end()) {
       CU(preload_replay_kernels());
       CU(preload_cells());
+      CU(preload_rank_kernels());
       CU(preload_peak_kernel());
       loaded.push_back(G->device);
     }
@@ -560,16 +561,80 @@ prism_status plan_tiles(prism_graph_s *G, int lanes) {
   return PRISM_OK;
 }
 
+// One scenario, lane = rank (replay_ranks.cu): scenario stride 1.
+prism_status replay_ranks_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *iter_dev) {
+  const Plan &P = G->plan;
+  ScenParams p{};
+  p.S = 1;
+  p.first = sc->first;
+  p.amp = sc->amp_q16;
+  p.seed = sc->seed;
+  p.mask = sc->kind_mask;
+  p.record = sc->record ? 1 : 0;
+  p.mod = 2 * sc->amp_q16 + 1;
+  p.mod_magic = ~0ULL / (uint64_t)p.mod + 1;
+  p.mod_m32 = p.mod > 1 ? (uint32_t)((((uint64_t)1 << 32) + (uint64_t)p.mod - 1) / (uint64_t)p.mod) : 0xFFFFFFFFu;
+  G->recorded = 0;
+  const int32_t Sp = 1;
+  if (p.record && !G->ensure(G->fin, G->fin_bytes, (size_t)std::max<int64_t>(1, G->fin_rows) * 8))
+    return fail(PRISM_E_OOM, "fin allocation failed");
+  if (!G->ensure(G->gfin, G->gfin_bytes, (size_t)std::max<int64_t>(1, P.G) * 8)) return fail(PRISM_E_OOM, "gfin allocation failed");
+  if (!G->ensure(G->rank_end, G->rank_end_bytes, (size_t)P.W * 8)) return fail(PRISM_E_OOM, "rank_end allocation failed");
+  const size_t rs_bytes = std::max<size_t>(16, (size_t)P.M_cross * 8);
+  if (G->rslot_bytes < rs_bytes || G->rslot_Sp != Sp) G->rslot_dirty = true;
+  G->rslot_Sp = Sp;
+  if (!G->ensure(G->rslot, G->rslot_bytes, rs_bytes)) return fail(PRISM_E_OOM, "ready-slot allocation failed");
+  const size_t lg = std::max<size_t>(16, (size_t)P.G_large * 8);
+  if (!G->ensure(G->acc, G->acc_bytes, lg)) return fail(PRISM_E_OOM, "accumulator allocation failed");
+  if (G->rres_bytes < lg) G->rslot_dirty = true;
+  if (!G->ensure(G->rres, G->rres_bytes, lg)) return fail(PRISM_E_OOM, "result-slot allocation failed");
+  const size_t nwords = (size_t)P.G_large + 4;
+  if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
+  if (!G->h_status && !(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status word unavailable");
+  if (G->rslot_dirty) {
+    CU(cudaMemsetAsync(G->rslot, 0xFF, G->rslot_bytes, G->stream));
+    CU(cudaMemsetAsync(G->rres, 0xFF, G->rres_bytes, G->stream));
+    G->parity = 0;
+    G->rslot_dirty = false;
+  }
+  CU(cudaMemsetAsync(G->acc, 0, (size_t)P.G_large * 8, G->stream));
+  CU(cudaMemsetAsync(G->sync_words, 0, nwords * 4, G->stream));
+  uint32_t *status = G->sync_words + P.G_large;
+  G->rec(2);
+  CU(launch_ranks(G->cur(), p, G->rslot, G->acc, G->rres, G->sync_words, status, G->parity,
+                  p.record ? G->fin : nullptr, G->gfin, G->rank_end, G->stream));
+  G->parity ^= 1;
+  CU(cudaMemcpyAsync(G->h_status, status, 4, cudaMemcpyDeviceToHost, G->stream));
+  G->rec(3);
+  G->rec(4);
+  CU(launch_reduce(P.W, 1, Sp, G->rank_end, iter_dev, G->stream));
+  G->rec(5);
+  G->launches = 2;
+  G->last = p;
+  G->last_Sp = Sp;
+  G->recorded = p.record;
+  G->last_algo = PRISM_ALGO_RANKS;
+  return PRISM_OK;
+}
+
 prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *iter_dev) {
   if (!G || !sc || !iter_dev) return fail(PRISM_E_INVALID_ARG, "null argument");
   if (sc->n < 1 || sc->n > (1 << 20) || sc->amp_q16 < 0 || sc->amp_q16 > 65535)
     return fail(PRISM_E_INVALID_ARG, "scenario count must be >= 1 and amp_q16 in [0, 65535]");
-  if (sc->algo < PRISM_ALGO_AUTO || sc->algo > PRISM_ALGO_CELLS) return fail(PRISM_E_INVALID_ARG, "unknown algo");
+  if (sc->algo < PRISM_ALGO_AUTO || sc->algo > PRISM_ALGO_RANKS) return fail(PRISM_E_INVALID_ARG, "unknown algo");
   if (sc->first < 0 || (int64_t)sc->first + sc->n > (1LL << 31) - 1)
     return fail(PRISM_E_INVALID_ARG, "first scenario index out of range");
   CU(cudaSetDevice(G->device));
   const int32_t S = sc->n;
   const Plan &P = G->plan;
+  // one scenario: the lane = rank kernel when it applies (auto) or is asked for
+  if (sc->algo == PRISM_ALGO_RANKS || (sc->algo == PRISM_ALGO_AUTO && S == 1)) {
+    const bool fit = S == 1 && ranks_fit(G->cur(), nullptr);
+    if (fit) return replay_ranks_impl(G, sc, iter_dev);
+    if (sc->algo == PRISM_ALGO_RANKS)
+      return fail(PRISM_E_INVALID_ARG, "PRISM_ALGO_RANKS needs one scenario, an unsharded single-stream graph, "
+                                       "tp a power of two <= 32 and co-resident warps");
+  }
   // schedule: the cell kernel (64-scenario chunks, one cooperative launch each) when every cell
   // CTA of a chunk can be co-resident, else one launch per frontier level
   const int cell_sc = cells_chunk_scenarios();
@@ -715,7 +780,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
 
 // Abort status of the last cell-kernel replay (valid once the stream has passed it).
 prism_status check_status(prism_graph_t G) {
-  if (G->last_algo == PRISM_ALGO_CELLS && G->h_status && *G->h_status != 0) {
+  if ((G->last_algo == PRISM_ALGO_CELLS || G->last_algo == PRISM_ALGO_RANKS) && G->h_status && *G->h_status != 0) {
     const uint32_t s = *G->h_status;
     *G->h_status = 0;
     G->recorded = 0;

@@ -166,6 +166,12 @@ constexpr int32_t kMaxTimeOrderedOps = 4096;
 cudaError_t launch_peak_time(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin, int64_t node0,
                              const int64_t *gfin, int32_t k, int32_t max_len, int64_t *peak, uint32_t *status,
                              cudaStream_t st);
+// replay_ranks.cu (one scenario, lane = rank)
+bool ranks_fit(const DevGraph &g, int *blocks);
+cudaError_t preload_rank_kernels();
+cudaError_t launch_ranks(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc, int64_t *rres,
+                         uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t *gfin,
+                         int64_t *rank_end, cudaStream_t st);
 // memory.cu
 cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st);
 // whatif.cu (rows f1/f3/f4)

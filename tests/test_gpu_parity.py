@@ -243,3 +243,51 @@ def test_scenario_offset(prism):
     r2 = oracle.replay(tm, 1, scen_first=104, amp_q16=6554, kind_mask=7, times=True)
     rp = g.export("rank_ptr")
     assert np.array_equal(st, r2["start"][0, rp[3]:rp[4]]) and np.array_equal(fi, r2["finish"][0, rp[3]:rp[4]])
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_single_scenario_rank_kernel_random(prism, seed):
+    """S = 1 on the lane = rank kernel (PRISM_ALGO_RANKS): perturbed (first > 0) and unperturbed,
+    with and without per-node durations."""
+    tm = w.random_templates(seed, max_world=64, max_ops=40)
+    if tm.topo.tp & (tm.topo.tp - 1):
+        pytest.skip("the rank kernel needs tp a power of two")
+    g = _graph(prism, tm)
+    first = [0, 1, 9][seed % 3]
+    it = g.replay(1, amp_q16=6554, kind_mask=7, first=first, algo="ranks")
+    assert g.last_algo() == "ranks"
+    ref = oracle.replay(tm, 1, scen_first=first, amp_q16=6554, kind_mask=7, times=True)
+    assert np.array_equal(it, ref["iter"])
+    rp = g.export("rank_ptr")
+    for r in range(tm.topo.world):
+        st, fi, _ = g.query_rank(r, 0)
+        assert np.array_equal(fi, ref["finish"][0, rp[r]:rp[r + 1]]) and np.array_equal(st, ref["start"][0, rp[r]:rp[r + 1]])
+    if seed % 2:
+        d = np.random.default_rng(seed).integers(0, 700, tm.n_nodes)
+        g.set_durations(node_dur=d)
+        it = g.replay(1, amp_q16=6554, kind_mask=7, first=first)
+        assert g.last_algo() == "ranks"
+        assert np.array_equal(it, oracle.replay(tm, 1, scen_first=first, amp_q16=6554, kind_mask=7, node_dur=d)["iter"])
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_single_scenario_rank_kernel_configs(prism, name):
+    tm = w.config(name) if name == "C1" else w.scaled(name)
+    g = _graph(prism, tm)
+    for first in (0, 5):
+        it = g.replay(1, amp_q16=6554, kind_mask=7, first=first)
+        assert g.last_algo() == "ranks"
+        ref = oracle.replay(tm, 1, scen_first=first, amp_q16=6554, kind_mask=7)
+        assert np.array_equal(it, ref["iter"])
+        path, T = g.critical_path(0)
+        rpath, rT = oracle.critical_path(tm, first, amp_q16=6554, kind_mask=7)
+        assert T == rT and np.array_equal(path, rpath)
+
+
+@pytest.mark.slow
+def test_single_scenario_full_size_c5(prism):
+    tm = w.config("C5")
+    g = _graph(prism, tm)
+    it = g.replay(1, amp_q16=6554, kind_mask=7, first=3)
+    assert g.last_algo() == "ranks"
+    assert it[0] == oracle.replay(tm, 1, scen_first=3, amp_q16=6554, kind_mask=7, peaks=False)["iter"][0]

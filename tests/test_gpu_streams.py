@@ -37,7 +37,7 @@ def _check(P, tm, S, node_dur=None, ranks=16):
     if node_dur is not None:
         g.set_durations(node_dur=node_dur)
     it = g.replay(S, amp_q16=6554, kind_mask=7)
-    assert g.last_algo() == "cells"
+    assert g.last_algo() in ("cells", "ranks")  # "ranks": S = 1 on a graph that drew no side stream
     ref = oracle.replay(tm, S, amp_q16=6554, kind_mask=7, node_dur=node_dur, times=True, threads=min(NPROC, S))
     assert np.array_equal(it, ref["iter"]), (it[:4], ref["iter"][:4])
     for k in sorted({0, S - 1}):
