@@ -123,6 +123,8 @@ struct CellArgs {
   uint32_t poll_spin;      // polls before the first sleep
   uint32_t poll_sleep0;    // first sleep (ns), doubled per further poll ...
   uint32_t poll_sleep_max; // ... up to this
+  uint32_t fast_spin, fast_sleep0, fast_sleep_max;  // the fast wait's policy (fast_sleep_max 0: off)
+  uint32_t lean;       // cross_pairs enabled (PRISM_LEAN=0 turns it off: experiments)
   ShardLink L;         // row e: peer exchange buffers (sharded kernels only)
 };
 
@@ -144,11 +146,12 @@ __device__ __forceinline__ int32_t rank_of(const DevGraph &g, int32_t tp_i, int3
 // geometrically from poll_sleep0 to poll_sleep_max ns: a short wait costs one short handoff, a long
 // wait (a pipeline stage idling through the 1F1B warm-up) stops stealing issue slots from the
 // computing warps of its SM.
-__device__ __forceinline__ bool wait_tick(const CellArgs &a, uint32_t &spins, uint64_t &t0) {
+__device__ __forceinline__ bool wait_tick(const CellArgs &a, uint32_t &spins, uint64_t &t0, uint32_t sleep0,
+                                          uint32_t sleep_max) {
   ++spins;
   if ((threadIdx.x & 31) == 0) STAT_ADD(3, 1);
   const uint32_t sh = min(spins, 16u);
-  __nanosleep(min(a.poll_sleep_max, a.poll_sleep0 << sh));
+  __nanosleep(min(sleep_max, sleep0 << sh));
   if ((spins & 63) == 0) {
     if (ld_relaxed(a.status) != 0) return true;
     if (t0 == 0) t0 = globaltimer();
@@ -347,6 +350,29 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
   uint32_t pending = (np >= 32 ? 0xFFFFFFFFu : ((1u << np) - 1u)) & ~large_done;
   uint32_t spins = 0;
   uint64_t tw = 0;
+  // fast wait: spin on ONE pending entry — the last of the list, which the partners deposit last
+  // (they deposit rank by rank in the same order) — with a loop of a few instructions, so a long
+  // wait costs its SM almost no issue slots and the handoff is detected within one short sleep;
+  // the full rounds below then usually resolve everything at once
+  if (a.fast_sleep_max) {
+    int32_t jr = nl - 1;
+    while (jr >= 0 && !((pending >> (cs.lpair[jr] & 31)) & 1u)) --jr;
+    if (jr >= 0) {
+      const uint32_t pr = cs.lpair[jr];
+      const int32_t idx = cs.lidx[jr];
+      const bool cnt = (pr & 0x80) && SH;
+      const int64_t *p64 = (pr & 0x80) ? a.rres + (int64_t)idx * Sp + k : a.rslot + (int64_t)idx * Sp + k;
+      const uint32_t *p32 = a.arrive + (int64_t)idx * a.nchunks + ck;
+      const int64_t need = (int64_t)(cs.meta[pr & 31] & 0xFFFF);
+      uint32_t fs = 0, fsl = 0;
+      while (true) {
+        const int64_t v = cnt ? (int64_t)poll32<SH>(p32) - need : poll64<SH>(p64) ^ pm;
+        if (__all_sync(0xffffffffu, v >= 0)) break;
+        if (fs < a.fast_spin) ++fs;
+        else if (wait_tick(a, fsl, tw, a.fast_sleep0, a.fast_sleep_max)) return false;
+      }
+    }
+  }
   while (true) {
     uint32_t bad = 0;
     for (int32_t j0 = 0; j0 < nl; j0 += kPollBatch) {
@@ -384,7 +410,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
     }
     pending &= bad;
     if (__all_sync(0xffffffffu, pending == 0)) break;
-    if (++spins > a.poll_spin && wait_tick(a, spins, tw)) return false;
+    if (++spins > a.poll_spin && wait_tick(a, spins, tw, a.poll_sleep0, a.poll_sleep_max)) return false;
   }
 #ifdef PRISM_CELL_STATS
   if (tl >= 0 && lane == 0) g_tl[tl * 4 + 2] = globaltimer();
@@ -405,6 +431,104 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
       if (ns > 1) gfin[(int64_t)cs.grp[x] * Sp + k] = m;  // P2P-batch group finishes, for queries
     }
     ts[r * 32 + lane] = fr;
+  }
+  __syncwarp();
+  return true;
+}
+
+// Lean cross-cell path for the common op whose every (rank, slot) pair is a 2-member small group
+// (a P2P message, reading Z3, or a 2-member EDP group) on an unsharded replay: lane x < C * ns
+// holds pair x's prefetched record, so its own and its partner's ready-slot indices come by
+// shuffle — no record staging, no poll list — and a poll round is one independent load per pending
+// pair, issued kPollBatch at a time before any is folded. Same slots, encoding and results as
+// cross_all (which handles every other op).
+template <int C>
+__device__ __forceinline__ bool cross_pairs(const ScenParams &p, const CellArgs &a, int64_t *__restrict__ gfin,
+                                            int64_t *ts, int32_t ns, int32_t k, CrossScratch<C> &cs,
+                                            const PreRec &pre, int tl) {
+  const int lane = threadIdx.x & 31;
+  const int32_t Sp = a.Sp;
+  const int np = C * ns;  // <= 32
+  constexpr int PB = C <= 2 ? 4 : kPollBatch;  // loads per batch (small cells: fewer live registers)
+  const int64_t pm = a.parity ? -1 : 0;  // slot encoding of this replay
+  const int32_t own = (int32_t)((pre.meta >> 16) & 0x7FFF);
+  const int32_t oslot = pre.base + own, pslot = pre.base + (own ^ 1);
+  for (int x = 0, r = 0, q = 0; x < np; ++x) {  // deposit every pair first: no self-wait
+    const int32_t os = __shfl_sync(0xffffffffu, oslot, x);
+    st_relaxed64(a.rslot + (int64_t)os * Sp + k, ts[r * 32 + lane] ^ pm);
+    if (++q == ns) {
+      q = 0;
+      ++r;
+    }
+  }
+#ifdef PRISM_CELL_STATS
+  if (tl >= 0 && lane == 0) g_tl[tl * 4 + 1] = globaltimer();
+#endif
+  uint32_t pending = np >= 32 ? 0xFFFFFFFFu : ((1u << np) - 1u);
+  uint32_t spins = 0, fs = 0, fsl = 0;
+  uint64_t tw = 0;
+  const int32_t kg = p.first + k;  // global scenario index (perturbation key)
+  const bool pert_ok = p.amp > 0 && kg > 0;
+  const uint64_t sx = p.seed ^ ((uint64_t)kg * K_GOLD);
+  if (a.fast_sleep_max) {  // fast wait on the pair the partners deposit last (see cross_all)
+    const int32_t ps = __shfl_sync(0xffffffffu, pslot, np - 1);
+    const int64_t *p64 = a.rslot + (int64_t)ps * Sp + k;
+    while (!__all_sync(0xffffffffu, (ld_relaxed64(p64) ^ pm) >= 0)) {
+      if (fs < a.fast_spin) ++fs;
+      else if (wait_tick(a, fsl, tw, a.fast_sleep0, a.fast_sleep_max)) return false;
+    }
+  }
+  while (true) {
+    for (int x0 = 0; x0 < np; x0 += PB) {
+      int64_t v[PB];
+#pragma unroll
+      for (int u = 0; u < PB; ++u) {
+        const int x = x0 + u;
+        const int32_t ps = __shfl_sync(0xffffffffu, pslot, x & 31);
+        v[u] = -1;
+        if (x < np && ((pending >> x) & 1u)) v[u] = ld_relaxed64(a.rslot + (int64_t)ps * Sp + k) ^ pm;
+      }
+#pragma unroll
+      for (int u = 0; u < PB; ++u) {
+        const int x = x0 + u;
+        if (x < np && ((pending >> x) & 1u) && v[u] >= 0) {
+          cs.vmax[x][lane] = v[u];
+          pending &= ~(1u << x);
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, pending == 0)) break;
+    if (++spins > a.poll_spin && wait_tick(a, spins, tw, a.poll_sleep0, a.poll_sleep_max)) return false;
+  }
+#ifdef PRISM_CELL_STATS
+  if (tl >= 0 && lane == 0) g_tl[tl * 4 + 2] = globaltimer();
+#endif
+  // finish = max(own, partner) + dur'_g; one slot per rank (the common case): unrolled over the
+  // ranks so the C hashes run as independent chains
+  if (ns == 1) {
+#pragma unroll
+    for (int r = 0; r < C; ++r) {
+      const int64_t gd = __shfl_sync(0xffffffffu, pre.dur, r);
+      const uint64_t uid = __shfl_sync(0xffffffffu, pre.uid, r);
+      const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
+      ts[r * 32 + lane] = max(ts[r * 32 + lane], cs.vmax[r][lane]) +
+                          (((p.mask & gb) && pert_ok) ? perturb_x(gd, sx ^ (uid * K_MIX), p) : gd);
+    }
+  } else {
+    for (int r = 0, x = 0; r < C; ++r) {
+      const int64_t tr = ts[r * 32 + lane];
+      int64_t fr = 0;
+      for (int32_t q = 0; q < ns; ++q, ++x) {
+        const int64_t gd = __shfl_sync(0xffffffffu, pre.dur, x);
+        const uint64_t uid = __shfl_sync(0xffffffffu, pre.uid, x);
+        const int32_t grp = __shfl_sync(0xffffffffu, pre.grp, x);
+        const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
+        const int64_t m = max(tr, cs.vmax[x][lane]) + (((p.mask & gb) && pert_ok) ? perturb_x(gd, sx ^ (uid * K_MIX), p) : gd);
+        fr = max(fr, m);
+        gfin[(int64_t)grp * Sp + k] = m;  // P2P-batch group finishes, for queries
+      }
+      ts[r * 32 + lane] = fr;
+    }
   }
   __syncwarp();
   return true;
@@ -577,7 +701,11 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
 #pragma unroll
         for (int r = 0; r < C; ++r) ts[r * 32 + lane] = t[r];
         __syncwarp();
-        const bool ok = cross_all<SH, C>(g, p, a, gfin, ts, xo.ns, k, cs, pre, tl);
+        // every pair a 2-member small group (P2P messages): the lean path (TP >= 4 cells; for
+        // TP = 1 / 2 cells it measured slower than cross_all on C4)
+        const bool lean = !SH && C >= 4 && a.lean && __all_sync(0xffffffffu, lane >= C * xo.ns || (pre.meta & 0x8000FFFFu) == 2u);
+        const bool ok = lean ? cross_pairs<C>(p, a, gfin, ts, xo.ns, k, cs, pre, tl)
+                             : cross_all<SH, C>(g, p, a, gfin, ts, xo.ns, k, cs, pre, tl);
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < C; ++r) t[r] = ts[r * 32 + lane];
@@ -697,14 +825,22 @@ cudaError_t preload_cells() { return preload_cell_kernels(); }
 
 // Poll/backoff policy of the waiting warps; PRISM_POLL="spin,sleep0,sleep_max" overrides it
 // (tuning experiments, tools/poll_sweep.py).
+// PRISM_POLL_FAST="spin,sleep0,sleep_max" the fast wait's (sleep_max 0 turns it off).
 struct PollPolicy {
   uint32_t spin, sleep0, sleep_max;
+  uint32_t fspin, fsleep0, fsleep_max;
+  uint32_t lean;
 };
 PollPolicy poll_policy() {
-  PollPolicy p{2, 32, 1024};
+  PollPolicy p{2, 32, 1024, 4, 32, 256, 1};
+  if (const char *e = std::getenv("PRISM_LEAN")) p.lean = std::atoi(e) != 0;
   if (const char *e = std::getenv("PRISM_POLL")) {
     unsigned a = 0, b = 0, c = 0;
-    if (std::sscanf(e, "%u,%u,%u", &a, &b, &c) == 3) p = {a, b, c};
+    if (std::sscanf(e, "%u,%u,%u", &a, &b, &c) == 3) p.spin = a, p.sleep0 = b, p.sleep_max = c;
+  }
+  if (const char *e = std::getenv("PRISM_POLL_FAST")) {
+    unsigned a = 0, b = 0, c = 0;
+    if (std::sscanf(e, "%u,%u,%u", &a, &b, &c) == 3) p.fspin = a, p.fsleep0 = b, p.fsleep_max = c;
   }
   return p;
 }
@@ -735,7 +871,7 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
   // the launch covers chunks [chunk0, chunk0 + nchunks_launch) of the replay's Sp / 32 chunks
   static const PollPolicy pol = poll_policy();
   CellArgs a{rslot, acc, rres, arrive, status, 10ull * 1000 * 1000 * 1000, parity, (int32_t)units, Sp, chunk0,
-             Sp / SC, pol.spin, pol.sleep0, pol.sleep_max, ShardLink{}};
+             Sp / SC, pol.spin, pol.sleep0, pol.sleep_max, pol.fspin, pol.fsleep0, pol.fsleep_max, pol.lean, ShardLink{}};
   if (link) a.L = *link;
   DevGraph gg = g;
   ScenParams pp = p;
