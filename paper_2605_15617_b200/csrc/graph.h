@@ -117,6 +117,36 @@ __device__ __forceinline__ int64_t perturb_x(int64_t d, uint64_t x, const ScenPa
   if (r < 0) r += p.mod;
   return (d * (int64_t)((uint32_t)r + (uint32_t)(65536 - p.amp))) >> 16;
 }
+
+// The same function for C independent (d, x) pairs, t[r] += perturb_x(d[r], x[r]), written step by
+// step across r (structure of arrays): ptxas otherwise emits the C hash chains one after another,
+// and a lone warp pays each chain's full dependency latency (958 vs 603 cycles per 8-rank op,
+// tools/micro/hashop.cu). The top word of the last product is formed from 32-bit halves:
+// hi32(y * M) = umulhi(lo, M_lo) + lo * M_hi + hi * M_lo (mod 2^32).
+template <int C>
+__device__ __forceinline__ void perturb_add(int64_t (&t)[C], const int64_t (&d)[C], const uint64_t (&x)[C],
+                                            const ScenParams &p) {
+  uint64_t z[C];
+#pragma unroll
+  for (int r = 0; r < C; ++r) z[r] = x[r] + 0x9E3779B97F4A7C15ULL;
+#pragma unroll
+  for (int r = 0; r < C; ++r) z[r] = (z[r] ^ (z[r] >> 30)) * 0xBF58476D1CE4E5B9ULL;
+#pragma unroll
+  for (int r = 0; r < C; ++r) z[r] = z[r] ^ (z[r] >> 27);
+  uint32_t v[C];
+#pragma unroll
+  for (int r = 0; r < C; ++r) {
+    const uint32_t lo = (uint32_t)z[r], hi = (uint32_t)(z[r] >> 32);
+    v[r] = (__umulhi(lo, 0x133111EBu) + lo * 0x94D049BBu + hi * 0x133111EBu) >> 8;
+  }
+  int32_t m[C];
+#pragma unroll
+  for (int r = 0; r < C; ++r) m[r] = (int32_t)(v[r] - __umulhi(v[r], p.mod_m32) * (uint32_t)p.mod);
+#pragma unroll
+  for (int r = 0; r < C; ++r) m[r] += m[r] < 0 ? p.mod : 0;
+#pragma unroll
+  for (int r = 0; r < C; ++r) t[r] += (d[r] * (int64_t)((uint32_t)m[r] + (uint32_t)(65536 - p.amp))) >> 16;
+}
 #endif
 
 // Row e: the peer-memory exchange of a sharded replay. Every shard's exchange buffer has the

@@ -505,15 +505,25 @@ __device__ __forceinline__ bool cross_pairs(const ScenParams &p, const CellArgs 
 #endif
   // finish = max(own, partner) + dur'_g; one slot per rank (the common case): unrolled over the
   // ranks so the C hashes run as independent chains
-  if (ns == 1) {
+  if (ns == 1) {  // the pairs of one op share a role (all P2P messages, or all EDP groups)
+    int64_t tt[C], dd[C];
+    uint64_t xx[C];
 #pragma unroll
     for (int r = 0; r < C; ++r) {
-      const int64_t gd = __shfl_sync(0xffffffffu, pre.dur, r);
+      dd[r] = __shfl_sync(0xffffffffu, pre.dur, r);
       const uint64_t uid = __shfl_sync(0xffffffffu, pre.uid, r);
-      const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
-      ts[r * 32 + lane] = max(ts[r * 32 + lane], cs.vmax[r][lane]) +
-                          (((p.mask & gb) && pert_ok) ? perturb_x(gd, sx ^ (uid * K_MIX), p) : gd);
+      xx[r] = sx ^ (uid * K_MIX);
+      tt[r] = max(ts[r * 32 + lane], cs.vmax[r][lane]);
     }
+    const uint32_t gb = (__shfl_sync(0xffffffffu, pre.uid, 0) >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
+    if ((p.mask & gb) && pert_ok) {
+      perturb_add<C>(tt, dd, xx, p);
+    } else {
+#pragma unroll
+      for (int r = 0; r < C; ++r) tt[r] += dd[r];
+    }
+#pragma unroll
+    for (int r = 0; r < C; ++r) ts[r * 32 + lane] = tt[r];
   } else {
     for (int r = 0, x = 0; r < C; ++r) {
       const int64_t tr = ts[r * 32 + lane];
@@ -662,8 +672,14 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
       if (c == 0) {  // compute span: every rank waits out its own perturbed duration
         if (cpert) {
           const uint64_t ix = (uint64_t)i * K_MIX;
+          int64_t dd[C];
+          uint64_t xx[C];
 #pragma unroll
-          for (int r = 0; r < C; ++r) t[r] += perturb_x(PR ? dr[r] : d, sx ^ (rk[r] + ix), p);
+          for (int r = 0; r < C; ++r) {
+            dd[r] = PR ? dr[r] : d;
+            xx[r] = sx ^ (rk[r] + ix);
+          }
+          perturb_add<C>(t, dd, xx, p);
         } else {
 #pragma unroll
           for (int r = 0; r < C; ++r) t[r] += PR ? dr[r] : d;
@@ -683,8 +699,14 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
           // rank r's group uid = ux + r * 2^24 (gid = tp_i + ...), WORLD: one group
           const uint64_t um = ux * K_MIX;
           const uint64_t stepm = ((ux >> 56) == PRISM_ROLE_WORLD ? 0ull : (1ull << 24)) * K_MIX;
+          int64_t dd[C];
+          uint64_t xx[C];
 #pragma unroll
-          for (int r = 0; r < C; ++r) t[r] += perturb_x(PR ? dr[r] : d, sx ^ (um + (uint64_t)r * stepm), p);
+          for (int r = 0; r < C; ++r) {
+            dd[r] = PR ? dr[r] : d;
+            xx[r] = sx ^ (um + (uint64_t)r * stepm);
+          }
+          perturb_add<C>(t, dd, xx, p);
         } else {
 #pragma unroll
           for (int r = 0; r < C; ++r) t[r] += PR ? dr[r] : d;
