@@ -383,6 +383,10 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t o_tcls = carve(nops), o_xptr = carve((pp + 1) * 4), o_xops = carve(P.x_ops.size() * sizeof(XOp));
   const bool ms = P.multistream;
   const size_t o_tq0 = carve(nops * 4);
+  // the template fields the expansion copies, as structure-of-arrays (coalesced loads; the 48-byte
+  // prism_op records would cost the expander 12 cache lines per warp per field)
+  const size_t o_tdur = carve(nops * 8), o_tal = carve(nops * 8), o_tfr = carve(nops * 8), o_tsd = carve(nops * 8);
+  const size_t o_tlab = carve(nops * 4), o_tkind = carve(nops);
   const size_t o_tms = ms ? carve(nops * 2) : 0, o_tsp2 = ms ? carve(nops * 4) : 0, o_tes = ms ? carve(nops * 4) : 0;
   const size_t table_bytes = off;
   // graph arrays (written by the expand kernels)
@@ -421,6 +425,12 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.x_ptr = (const int32_t *)at(o_xptr);
   d.x_ops = (const XOp *)at(o_xops);
   d.t_q0 = (const int32_t *)at(o_tq0);
+  d.t_dur = (const int64_t *)at(o_tdur);
+  d.t_alloc = (const int64_t *)at(o_tal);
+  d.t_free = (const int64_t *)at(o_tfr);
+  d.t_sdur = (const int64_t *)at(o_tsd);
+  d.t_label = (const uint32_t *)at(o_tlab);
+  d.t_kind = (const uint8_t *)at(o_tkind);
   d.ms = ms ? 1 : 0;
   d.ms_streams = P.ms_streams;
   d.ms_events = P.ms_events;
@@ -485,6 +495,22 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     put(o_chm, P.chunk_m.data(), nch * 8);
     put(o_tcls, P.t_cls.data(), nops);
     put(o_tq0, P.t_q0.data(), nops * 4);
+    {
+      int64_t *tdur = (int64_t *)(h.data() + o_tdur), *tal = (int64_t *)(h.data() + o_tal);
+      int64_t *tfr = (int64_t *)(h.data() + o_tfr), *tsd = (int64_t *)(h.data() + o_tsd);
+      uint32_t *tlab = (uint32_t *)(h.data() + o_tlab);
+      uint8_t *tkind = h.data() + o_tkind;
+      for (size_t i = 0; i < nops; ++i) {
+        const prism_op &o = tmpl->ops[i];
+        tdur[i] = o.dur_ns;
+        tal[i] = o.mem_alloc;
+        tfr[i] = o.mem_free;
+        tlab[i] = o.label;
+        tkind[i] = o.kind;
+        // replay record duration: a compute span's own, a sync node's first group's (Z2)
+        tsd[i] = P.t_q0[i] < 0 ? o.dur_ns : P.q[P.t_q0[i]].dur;
+      }
+    }
     put(o_xptr, P.x_ptr.data(), (pp + 1) * 4);
     put(o_xops, P.x_ops.data(), P.x_ops.size() * sizeof(XOp));
     if (ms) {

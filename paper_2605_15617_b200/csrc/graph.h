@@ -84,6 +84,11 @@ struct DevGraph {
   const int32_t *wpos;      // WORLD per-stage template indices
   const uint8_t *t_cls;     // replay class per template op (Plan::t_cls)
   const int32_t *t_q0;      // per template op: quotient group of its first slot (-1: compute)
+  // per template op, structure-of-arrays copies of the prism_op fields the expansion writes, and
+  // the replay-record duration (compute span: dur_ns; sync node: its first group's duration)
+  const int64_t *t_dur, *t_alloc, *t_free, *t_sdur;
+  const uint32_t *t_label;
+  const uint8_t *t_kind;
   const int32_t *x_ptr;     // [pp+1] cross-op list of each stage
   const XOp *x_ops;
 };

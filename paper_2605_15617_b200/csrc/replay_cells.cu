@@ -163,6 +163,19 @@ __device__ __forceinline__ bool wait_tick(const CellArgs &a, uint32_t &spins, ui
   return false;
 }
 
+// max over t[0..C) as a balanced tree (depth log2 C instead of a chain of C - 1 dependent maxima)
+template <int C>
+__device__ __forceinline__ int64_t tree_max(const int64_t (&t)[C]) {
+  int64_t m[C];
+#pragma unroll
+  for (int r = 0; r < C; ++r) m[r] = t[r];
+#pragma unroll
+  for (int w = 1; w < C; w *= 2)
+#pragma unroll
+    for (int r = 0; r + w < C; r += 2 * w) m[r] = max(m[r], m[r + w]);
+  return m[0];
+}
+
 // Sync records of the next cross-cell op, one (rank, slot) pair per lane, loaded right after the
 // previous cross op so that their latency overlaps the compute spans in between (the handoff path
 // of a rendezvous then starts with no dependent global load).
@@ -686,9 +699,7 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
         }
       } else if (c == 1) {  // in-cell TP collective: register-local segmented max
         const uint64_t ux = __shfl_sync(0xffffffffu, bux, j);
-        int64_t m = t[0];
-#pragma unroll
-        for (int r = 1; r < C; ++r) m = max(m, t[r]);
+        int64_t m = tree_max<C>(t);
         m += gpert ? perturb_x(d, sx ^ (ux * K_MIX), p) : d;
 #pragma unroll
         for (int r = 0; r < C; ++r) t[r] = m;

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(32, 16) rank_kernel(DevGraph g, ScenParams p, 
     const int32_t q0 = __ldg(g.t_q0 + op);
     uint32_t type = 0;
     occ = 0;
-    dur = __ldg(&g.t_ops[op].dur_ns);
+    dur = __ldg(g.t_dur + op);
     if (q0 >= 0) {
       type = (uint32_t)__ldg(&g.q[q0].type);
       occ = (uint32_t)__ldg(&g.q[q0].occ);
