@@ -32,6 +32,29 @@ std::mutex g_pin_mu;
 uint32_t *g_pin = nullptr;
 std::vector<int> g_pin_free;
 constexpr int kPinWords = 4096;
+// A word whose graph was destroyed is reclaimed once the event recorded behind its last status
+// copy has completed (a host callback on the stream would stall the stream's next kernels until
+// the host ran it: a bubble in every bench step).
+struct PinPending {
+  int idx;
+  cudaEvent_t ev;
+  int dev;
+};
+std::vector<PinPending> g_pin_pending;
+std::vector<PinPending> g_pin_events;  // completed events for reuse (idx unused)
+void pin_reclaim_locked() {
+  for (size_t i = 0; i < g_pin_pending.size();) {
+    PinPending &q = g_pin_pending[i];
+    if (cudaEventQuery(q.ev) == cudaSuccess) {
+      g_pin_free.push_back(q.idx);
+      g_pin_events.push_back(q);
+      q = g_pin_pending.back();
+      g_pin_pending.pop_back();
+    } else {
+      ++i;
+    }
+  }
+}
 uint32_t *pin_take() {
   std::lock_guard<std::mutex> lk(g_pin_mu);
   if (!g_pin) {
@@ -41,16 +64,38 @@ uint32_t *pin_take() {
     }
     for (int i = kPinWords - 1; i >= 0; --i) g_pin_free.push_back(i);
   }
+  if (g_pin_free.empty()) {
+    pin_reclaim_locked();
+    cudaGetLastError();  // cudaErrorNotReady of the queries is not an error
+  }
   if (g_pin_free.empty()) return nullptr;
   const int i = g_pin_free.back();
   g_pin_free.pop_back();
   g_pin[i] = 0;
   return g_pin + i;
 }
-void pin_give(uint32_t *p) {
+// Returns word p once the work queued so far on stream st (device dev) has completed.
+void pin_give_after(uint32_t *p, cudaStream_t st, int dev) {
   if (!p) return;
   std::lock_guard<std::mutex> lk(g_pin_mu);
-  g_pin_free.push_back((int)(p - g_pin));
+  const int idx = (int)(p - g_pin);
+  cudaEvent_t ev = nullptr;
+  for (size_t i = 0; i < g_pin_events.size(); ++i)
+    if (g_pin_events[i].dev == dev) {
+      ev = g_pin_events[i].ev;
+      g_pin_events[i] = g_pin_events.back();
+      g_pin_events.pop_back();
+      break;
+    }
+  if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) ev = nullptr;
+  if (ev && cudaEventRecord(ev, st) == cudaSuccess) {
+    g_pin_pending.push_back(PinPending{idx, ev, dev});
+    return;
+  }
+  cudaGetLastError();
+  cudaStreamSynchronize(st);
+  g_pin_free.push_back(idx);
+  if (ev) g_pin_events.push_back(PinPending{-1, ev, dev});
 }
 std::mutex g_alloc_mu;
 prism_alloc_fn g_alloc = nullptr;
@@ -91,6 +136,77 @@ struct MallocTuning {
     mallopt(M_TRIM_THRESHOLD, 256 << 20);
   }
 } g_malloc_tuning;
+
+// Pinned staging buffers of the build uploads. From pageable memory cudaMemcpyAsync returns only
+// after the copy engine has taken the data — i.e. after every earlier operation on the stream (the
+// previous step's replay) — so the host could not plan the next graph while the device replays;
+// from pinned memory the upload is queued and the host runs ahead. A small process-wide ring of
+// buffers; a slot is reused once the event recorded after its copy has completed.
+struct PinnedRing {
+  struct Slot {
+    unsigned char *p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    int dev = -1;
+  };
+  std::mutex mu;
+  Slot slot[4];
+  int next = 0;
+};
+PinnedRing &pinned_ring() {
+  static PinnedRing *r = new PinnedRing;  // never destroyed: the buffers live for the process
+  return *r;
+}
+struct PinnedStage {
+  unsigned char *ptr = nullptr;
+  int idx = -1;
+  explicit PinnedStage(size_t bytes) {
+    PinnedRing &R = pinned_ring();
+    std::lock_guard<std::mutex> lk(R.mu);
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    const int i = R.next;
+    PinnedRing::Slot &S = R.slot[i];
+    if (S.ev) {
+      cudaEventSynchronize(S.ev);  // the slot's previous copy has completed
+      if (S.dev != dev) {
+        cudaEventDestroy(S.ev);
+        S.ev = nullptr;
+      }
+    }
+    if (!S.ev) {
+      if (cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming) != cudaSuccess) {
+        S.ev = nullptr;
+        cudaGetLastError();
+        return;
+      }
+      S.dev = dev;
+    }
+    if (S.cap < bytes) {
+      if (S.p) cudaFreeHost(S.p);
+      S.p = nullptr;
+      S.cap = 0;
+      const size_t cap = std::max(bytes + bytes / 4, (size_t)1 << 20);
+      if (cudaMallocHost((void **)&S.p, cap) != cudaSuccess) {
+        S.p = nullptr;
+        cudaGetLastError();
+        return;
+      }
+      S.cap = cap;
+    }
+    R.next = (i + 1) % 4;
+    idx = i;
+    ptr = S.p;
+  }
+  // records the completion event of the copy just queued on `st`; the slot is not handed out
+  // again before that event has completed
+  void release(cudaStream_t st) {
+    if (idx < 0) return;
+    PinnedRing &R = pinned_ring();
+    std::lock_guard<std::mutex> lk(R.mu);
+    cudaEventRecord(R.slot[idx].ev, st);
+  }
+};
 }  // namespace
 
 struct prism_graph_s {
@@ -225,11 +341,11 @@ struct prism_graph_s {
     dfree(ov);
     dfree(crit);
     if (h_status) {  // returned to the pool once the stream has passed its pending status copy
-      if (cudaLaunchHostFunc(stream, [](void *w) { pin_give((uint32_t *)w); }, h_status) != cudaSuccess) {
-        cudaGetLastError();
-        cudaStreamSynchronize(stream);
-        pin_give(h_status);
-      }
+      int cur = -1;
+      cudaGetDevice(&cur);
+      if (device >= 0 && cur != device) cudaSetDevice(device);
+      pin_give_after(h_status, stream, device);
+      if (device >= 0 && cur >= 0 && cur != device) cudaSetDevice(cur);
     }
     for (auto &b : blocks) dfree(b.first);  // stream-ordered frees: no host wait needed
     if (ex || !ipc_open.empty()) {  // the exchange buffer is not stream-ordered memory
@@ -278,10 +394,12 @@ prism_status prism_set_allocator(prism_alloc_fn alloc, prism_free_fn free_fn, vo
 
 prism_status prism_plan(const prism_topology *topo, const prism_templates *tmpl, int64_t out[8]) {
   if (!topo || !tmpl || !out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  trace("build: begin");
   Plan plan;
   std::string err;
   prism_status st = plan_graph(*topo, *tmpl, plan, err);
   if (st != PRISM_OK) return fail(st, err);
+  trace("build: planned");
   out[0] = plan.W;
   out[1] = plan.N;
   out[2] = plan.G;
@@ -303,10 +421,12 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     return fail(PRISM_E_INVALID_ARG, "n_shards must be in [1, 16] and shard_index in [0, n_shards)");
   if (topo->dp < 1 || topo->dp % n_shards != 0)
     return fail(PRISM_E_INVALID_SPEC, "dp must be a multiple of n_shards (ranks are sharded by DP block)");
+  trace("build: begin");
   Plan plan;
   std::string err;
   prism_status st = plan_graph(*topo, *tmpl, plan, err);
   if (st != PRISM_OK) return fail(st, err);
+  trace("build: planned");
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -400,7 +520,9 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t o_hs = n_shards > 1 ? carve(M * 4) : 0;
   const size_t o_nmsk = ms ? carve(N * 2) : 0, o_nsp = ms ? carve(N * 4) : 0, o_nes = ms ? carve(N * 4) : 0;
   const size_t total = off;
+  trace("build: tables sized");
   unsigned char *base = G->take<unsigned char>(total);
+  trace("build: allocated");
   if (G->oom || !base) return fail(PRISM_E_OOM, "device allocation failed while building the graph");
   auto at = [base](size_t o) { return (void *)(base + o); };
   prism_op *t_ops = (prism_op *)at(o_ops);
@@ -471,11 +593,17 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.M_cross = P.M_cross;
   d.G_large = P.G_large;
   cudaStream_t s = G->stream;
-  {  // packed upload of the host tables
-    std::vector<unsigned char> &h = G->staging;
-    h.assign(table_bytes, 0);
-    auto put = [&h](size_t o, const void *src, size_t bytes) {
-      if (bytes) std::memcpy(h.data() + o, src, bytes);
+  {  // packed upload of the host tables, from a pinned staging buffer when one is available
+    PinnedStage ps(table_bytes);
+    unsigned char *hb = ps.ptr;
+    if (!hb) {  // no pinned memory: pageable fallback (the copy then waits for the stream)
+      G->staging.assign(table_bytes, 0);
+      hb = G->staging.data();
+    } else {
+      std::memset(hb, 0, table_bytes);
+    }
+    auto put = [hb](size_t o, const void *src, size_t bytes) {
+      if (bytes) std::memcpy(hb + o, src, bytes);
     };
     put(o_ops, tmpl->ops, nops * sizeof(prism_op));
     put(o_tps, P.t_prev_sync.data(), nops * 4);
@@ -496,10 +624,10 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     put(o_tcls, P.t_cls.data(), nops);
     put(o_tq0, P.t_q0.data(), nops * 4);
     {
-      int64_t *tdur = (int64_t *)(h.data() + o_tdur), *tal = (int64_t *)(h.data() + o_tal);
-      int64_t *tfr = (int64_t *)(h.data() + o_tfr), *tsd = (int64_t *)(h.data() + o_tsd);
-      uint32_t *tlab = (uint32_t *)(h.data() + o_tlab);
-      uint8_t *tkind = h.data() + o_tkind;
+      int64_t *tdur = (int64_t *)(hb + o_tdur), *tal = (int64_t *)(hb + o_tal);
+      int64_t *tfr = (int64_t *)(hb + o_tfr), *tsd = (int64_t *)(hb + o_tsd);
+      uint32_t *tlab = (uint32_t *)(hb + o_tlab);
+      uint8_t *tkind = hb + o_tkind;
       for (size_t i = 0; i < nops; ++i) {
         const prism_op &o = tmpl->ops[i];
         tdur[i] = o.dur_ns;
@@ -518,7 +646,10 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
       put(o_tsp2, P.t_spred.data(), nops * 4);
       put(o_tes, P.t_esrc.data(), nops * 4);
     }
-    CU(cudaMemcpyAsync(base, h.data(), table_bytes, cudaMemcpyHostToDevice, s));
+    trace("build: packed");
+    CU(cudaMemcpyAsync(base, hb, table_bytes, cudaMemcpyHostToDevice, s));
+    ps.release(s);
+    trace("build: upload queued");
   }
   if (opts && (opts->flags & PRISM_BUILD_PROFILE)) {
     G->profile = true;
@@ -539,6 +670,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   G->rec(0);
   CU(launch_expand(d, s));
   G->rec(1);
+  trace("build: expand launched");
   if (!(opts && (opts->flags & PRISM_BUILD_ASYNC))) CU(cudaStreamSynchronize(s));
   *out = guard.release();
   return PRISM_OK;
