@@ -152,6 +152,51 @@ __device__ __forceinline__ void perturb_add(int64_t (&t)[C], const int64_t (&d)[
 #pragma unroll
   for (int r = 0; r < C; ++r) t[r] += (d[r] * (int64_t)((uint32_t)m[r] + (uint32_t)(65536 - p.amp))) >> 16;
 }
+
+// perturb_add for the compute spans of one op of C ranks: x[r] = sx ^ (rk[r] + ix) with
+// rk[r] = (rank_r << 32) * K_MIX, whose low word is zero, so x's low word and the carry of x + G
+// are shared by the C ranks and only the high words differ (rkhi[r] = rk[r] >> 32). With one
+// duration d for all ranks (PR: per-rank d[r]) the product d * (m + 65536 - amp) is split as
+// d * m + d * (65536 - amp). Bit-identical to perturb_x (tools/micro/hashop.cu checksum); a lone
+// warp's 8-rank op 603 -> 486 cycles.
+template <int C, bool PERD>
+__device__ __forceinline__ void perturb_add_span(int64_t (&t)[C], const int64_t (&d)[C], uint64_t sx,
+                                                 const uint32_t (&rkhi)[C], uint64_t ix, const ScenParams &p) {
+  const uint32_t xlo = (uint32_t)sx ^ (uint32_t)ix;
+  const uint32_t zlo = xlo + 0x7F4A7C15u;
+  const uint32_t cg = 0x9E3779B9u + (zlo < xlo ? 1u : 0u);
+  const uint32_t sxh = (uint32_t)(sx >> 32), ixh = (uint32_t)(ix >> 32);
+  const uint32_t zlo30 = zlo >> 30;
+  uint64_t z[C];
+#pragma unroll
+  for (int r = 0; r < C; ++r) {
+    const uint32_t zh = (sxh ^ (ixh + rkhi[r])) + cg;
+    const uint32_t lo = zlo ^ (zlo30 | (zh << 2)), hi = zh ^ (zh >> 30);
+    z[r] = ((uint64_t)hi << 32 | lo) * 0xBF58476D1CE4E5B9ULL;
+  }
+#pragma unroll
+  for (int r = 0; r < C; ++r) z[r] = z[r] ^ (z[r] >> 27);
+  uint32_t v[C];
+#pragma unroll
+  for (int r = 0; r < C; ++r) {
+    const uint32_t lo = (uint32_t)z[r], hi = (uint32_t)(z[r] >> 32);
+    v[r] = (__umulhi(lo, 0x133111EBu) + lo * 0x94D049BBu + hi * 0x133111EBu) >> 8;
+  }
+  int32_t m[C];
+#pragma unroll
+  for (int r = 0; r < C; ++r) {
+    m[r] = (int32_t)(v[r] - __umulhi(v[r], p.mod_m32) * (uint32_t)p.mod);
+    m[r] += (int32_t)((uint32_t)m[r] >> 31) * p.mod;
+  }
+  if (PERD) {
+#pragma unroll
+    for (int r = 0; r < C; ++r) t[r] += (d[r] * (int64_t)((uint32_t)m[r] + (uint32_t)(65536 - p.amp))) >> 16;
+  } else {
+    const int64_t dc = d[0] * (int64_t)(uint32_t)(65536 - p.amp);
+#pragma unroll
+    for (int r = 0; r < C; ++r) t[r] += (d[0] * (int64_t)(uint32_t)m[r] + dc) >> 16;
+  }
+}
 #endif
 
 // Row e: the peer-memory exchange of a sharded replay. Every shard's exchange buffer has the

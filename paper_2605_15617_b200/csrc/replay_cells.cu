@@ -581,13 +581,14 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
   __shared__ int32_t rsh[MAX_TP];       // first membership slot of each rank
   int32_t rb[C];
   int32_t rs[C];   // first membership slot of each rank (node_gptr of its first node)
-  uint64_t rk[C];  // (rank << 32) * K_MIX: a compute span's uid mix is rk + tidx * K_MIX
+  uint32_t rkh[C];  // high word of (rank << 32) * K_MIX (its low word is zero): a compute span's
+                    // uid mix is that + tidx * K_MIX (perturb_add_span)
 #pragma unroll
   for (int r = 0; r < C; ++r) {
     const int32_t rr = rank_of(g, r, s, dpi);
     rb[r] = g.rank_ptr[rr];
     rs[r] = g.node_gptr[rb[r]];
-    rk[r] = ((uint64_t)rr << 32) * K_MIX;
+    rkh[r] = (uint32_t)((((uint64_t)rr << 32) * K_MIX) >> 32);
     if (lane == 0) rsh[r] = rs[r];
   }
   __syncwarp();
@@ -684,15 +685,10 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
       }
       if (c == 0) {  // compute span: every rank waits out its own perturbed duration
         if (cpert) {
-          const uint64_t ix = (uint64_t)i * K_MIX;
           int64_t dd[C];
-          uint64_t xx[C];
 #pragma unroll
-          for (int r = 0; r < C; ++r) {
-            dd[r] = PR ? dr[r] : d;
-            xx[r] = sx ^ (rk[r] + ix);
-          }
-          perturb_add<C>(t, dd, xx, p);
+          for (int r = 0; r < C; ++r) dd[r] = PR ? dr[r] : d;
+          perturb_add_span<C, PR>(t, dd, sx, rkh, (uint64_t)i * K_MIX, p);
         } else {
 #pragma unroll
           for (int r = 0; r < C; ++r) t[r] += PR ? dr[r] : d;
