@@ -638,6 +638,10 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
     nux = g.node_uid[rb[0] + lane];
     if (MS) nms = g.node_ms[rb[0] + lane];
   }
+  // fin row of op i of rank r: the cell's ranks are consecutive and run one template, so rank r's
+  // rows sit r * len rows after rank 0's (one moving pointer, a constant stride per rank)
+  int64_t *fp = fin + (int64_t)rb[0] * Sp + k;
+  const int64_t fst = (int64_t)len * Sp;
   for (int32_t base = 0; base < len; base += 32) {
     const int32_t cnt = min(32, len - base);
     const uint32_t bcls = ncls;
@@ -763,7 +767,11 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
       }
       if (record) {
 #pragma unroll
-        for (int r = 0; r < C; ++r) fin[(int64_t)(rb[r] + i) * Sp + k] = t[r];
+        for (int r = 0; r < C; ++r) {
+          if (C >= 4 && !PR) fp[r * fst] = t[r];
+          else fin[(int64_t)(rb[r] + i) * Sp + k] = t[r];  // small cells, PR: fewer live registers
+        }
+        if (C >= 4 && !PR) fp += Sp;
       }
     }
   }
