@@ -291,3 +291,31 @@ def test_single_scenario_full_size_c5(prism):
     it = g.replay(1, amp_q16=6554, kind_mask=7, first=3)
     assert g.last_algo() == "ranks"
     assert it[0] == oracle.replay(tm, 1, scen_first=3, amp_q16=6554, kind_mask=7, peaks=False)["iter"][0]
+
+
+# ------------------------------------------------------------------ asynchronous build pipeline
+def test_async_builds_pipelined(prism):
+    """Ten graphs built back to back with asynchronous builds on one stream (more than the four
+    pinned staging buffers of the build upload, so the ring wraps while earlier uploads may still
+    be queued behind a long replay), replayed in reverse order and destroyed out of order: every
+    result equals the oracle's (a staging buffer reused before its copy completed would corrupt a
+    graph's tables)."""
+    import torch
+
+    sh = torch.cuda.current_stream().cuda_stream
+    big = prism.Graph(w.scaled("C5", 16), stream=sh, asynchronous=True)
+    it_dev = torch.zeros(64, dtype=torch.int64, device="cuda")
+    big.replay_async(it_dev.data_ptr(), 64, amp_q16=6554, kind_mask=7)  # keeps the stream busy
+    tms = [w.random_templates(100 + i, max_world=32, max_ops=40) for i in range(10)]
+    graphs = [prism.Graph(tm, stream=sh, asynchronous=True) for tm in tms]
+    for i in reversed(range(10)):
+        S = [1, 3, 17, 64][i % 4]
+        it = graphs[i].replay(S, amp_q16=6554, kind_mask=7)
+        ref = oracle.replay(tms[i], S, amp_q16=6554, kind_mask=7, times=False, threads=min(NPROC, S))
+        assert np.array_equal(it, ref["iter"]), i
+        assert np.array_equal(graphs[i].peak_memory(), ref["peak"][0]), i
+        if i % 3 == 0:
+            graphs[i].close()
+    for g in graphs:
+        g.close()
+    big.close()
