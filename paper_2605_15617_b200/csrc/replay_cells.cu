@@ -629,14 +629,22 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
   }
   // op records of the cell's first rank (the template is shared; the per-rank part of a compute
   // span's uid is rk[r]), 32 ops per coalesced round trip, next batch in flight
+  // The record pointers are loop-carried and each batch loads at a constant offset from them:
+  // address temporaries of the batch loads would be reused by the next op's shuffles, and a
+  // register still feeding an in-flight load's address stalls its next writer (long scoreboard at
+  // every op's dispatch in the v10 profile)
+  const uint8_t *p_cls = g.node_cls + rb[0] + lane;
+  const int64_t *p_sd = g.node_sdur + rb[0] + lane;
+  const uint64_t *p_uid = g.node_uid + rb[0] + lane;
+  const uint16_t *p_ms = MS ? g.node_ms + rb[0] + lane : nullptr;
   uint32_t ncls = 2, nms = 0;
   int64_t nd = 0;
   uint64_t nux = 0;
   if (lane < len) {
-    ncls = g.node_cls[rb[0] + lane];
-    nd = g.node_sdur[rb[0] + lane];
-    nux = g.node_uid[rb[0] + lane];
-    if (MS) nms = g.node_ms[rb[0] + lane];
+    ncls = *p_cls;
+    nd = *p_sd;
+    nux = *p_uid;
+    if (MS) nms = *p_ms;
   }
   // fin row of op i of rank r: the cell's ranks are consecutive and run one template, so rank r's
   // rows sit r * len rows after rank 0's (one moving pointer, a constant stride per rank)
@@ -649,11 +657,24 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
     const uint64_t bux = nux;
     const uint32_t bms = nms;
     if (base + 32 + lane < len) {
-      const int32_t n = rb[0] + base + 32 + lane;
-      ncls = g.node_cls[n];
-      nd = g.node_sdur[n];
-      nux = g.node_uid[n];
-      if (MS) nms = g.node_ms[n];
+      if (C >= 4) {
+        ncls = p_cls[32];
+        nd = p_sd[32];
+        nux = p_uid[32];
+        if (MS) nms = p_ms[32];
+      } else {  // small cells: fewer live registers
+        const int32_t n = rb[0] + base + 32 + lane;
+        ncls = g.node_cls[n];
+        nd = g.node_sdur[n];
+        nux = g.node_uid[n];
+        if (MS) nms = g.node_ms[n];
+      }
+    }
+    if (C >= 4) {
+      p_cls += 32;
+      p_sd += 32;
+      p_uid += 32;
+      if (MS) p_ms += 32;
     }
     // op j's class / duration were fetched during op j-1 (software pipelined: the dispatch
     // branch of an op does not wait on its shuffles)
