@@ -756,8 +756,12 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
         for (int r = 0; r < C; ++r) ts[r * 32 + lane] = t[r];
         __syncwarp();
         // every pair a 2-member small group (P2P messages): the lean path (TP >= 4 cells; for
-        // TP = 1 / 2 cells it measured slower than cross_all on C4)
-        const bool lean = !SH && C >= 4 && a.lean && __all_sync(0xffffffffu, lane >= C * xo.ns || (pre.meta & 0x8000FFFFu) == 2u);
+        // TP = 1 / 2 cells it measured slower than cross_all on C4). Sharded: only groups whose
+        // members are all on this shard (P2P messages never leave a DP block, reading R9) — no
+        // peer touches their ready slots in the local exchange buffer, so gpu scope suffices
+        const bool lean = C >= 4 && a.lean &&
+                          __all_sync(0xffffffffu, lane >= C * xo.ns || ((pre.meta & 0x8000FFFFu) == 2u &&
+                                                                        (!SH || pre.smask == (1u << a.L.self))));
         const bool ok = lean ? cross_pairs<C>(p, a, gfin, ts, xo.ns, k, cs, pre, tl)
                              : cross_all<SH, C>(g, p, a, gfin, ts, xo.ns, k, cs, pre, tl);
         __syncwarp();
