@@ -599,9 +599,8 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     if (!hb) {  // no pinned memory: pageable fallback (the copy then waits for the stream)
       G->staging.assign(table_bytes, 0);
       hb = G->staging.data();
-    } else {
-      std::memset(hb, 0, table_bytes);
     }
+    // every table below is written in full; the alignment gaps between them are never read
     auto put = [hb](size_t o, const void *src, size_t bytes) {
       if (bytes) std::memcpy(hb + o, src, bytes);
     };

@@ -124,7 +124,7 @@ struct CellArgs {
   uint32_t poll_sleep0;    // first sleep (ns), doubled per further poll ...
   uint32_t poll_sleep_max; // ... up to this
   uint32_t fast_spin, fast_sleep0, fast_sleep_max;  // the fast wait's policy (fast_sleep_max 0: off)
-  uint32_t lean;       // cross_pairs enabled (PRISM_LEAN=0 turns it off: experiments)
+  uint32_t lean;       // cross_pairs: 0 off, 1 TP >= 4 cells (default), 2 every cell (PRISM_LEAN, experiments)
   ShardLink L;         // row e: peer exchange buffers (sharded kernels only)
 };
 
@@ -759,7 +759,7 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
         // TP = 1 / 2 cells it measured slower than cross_all on C4). Sharded: only groups whose
         // members are all on this shard (P2P messages never leave a DP block, reading R9) — no
         // peer touches their ready slots in the local exchange buffer, so gpu scope suffices
-        const bool lean = C >= 4 && a.lean &&
+        const bool lean = (C >= 4 || a.lean > 1) && a.lean &&
                           __all_sync(0xffffffffu, lane >= C * xo.ns || ((pre.meta & 0x8000FFFFu) == 2u &&
                                                                         (!SH || pre.smask == (1u << a.L.self))));
         const bool ok = lean ? cross_pairs<C>(p, a, gfin, ts, xo.ns, k, cs, pre, tl)
@@ -895,7 +895,7 @@ struct PollPolicy {
 };
 PollPolicy poll_policy() {
   PollPolicy p{2, 32, 1024, 4, 32, 256, 1};
-  if (const char *e = std::getenv("PRISM_LEAN")) p.lean = std::atoi(e) != 0;
+  if (const char *e = std::getenv("PRISM_LEAN")) p.lean = (uint32_t)std::atoi(e);
   if (const char *e = std::getenv("PRISM_POLL")) {
     unsigned a = 0, b = 0, c = 0;
     if (std::sscanf(e, "%u,%u,%u", &a, &b, &c) == 3) p.spin = a, p.sleep0 = b, p.sleep_max = c;
