@@ -657,12 +657,12 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
     const uint64_t bux = nux;
     const uint32_t bms = nms;
     if (base + 32 + lane < len) {
-      if (C >= 4) {
+      if (C >= 4 && !PR) {
         ncls = p_cls[32];
         nd = p_sd[32];
         nux = p_uid[32];
         if (MS) nms = p_ms[32];
-      } else {  // small cells: fewer live registers
+      } else {  // small cells, per-rank durations: fewer live registers (PR measured slower)
         const int32_t n = rb[0] + base + 32 + lane;
         ncls = g.node_cls[n];
         nd = g.node_sdur[n];
@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
         if (MS) nms = g.node_ms[n];
       }
     }
-    if (C >= 4) {
+    if (C >= 4 && !PR) {
       p_cls += 32;
       p_sd += 32;
       p_uid += 32;
