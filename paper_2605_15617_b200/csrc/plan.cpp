@@ -217,6 +217,11 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
         if (c == 2) P.x_ops.push_back(XOp{(int32_t)(i - a), P.t_slot_ptr[i], P.t_slots[i], 0});
       }
       P.x_ptr[s + 1] = (int32_t)P.x_ops.size();
+      // flag 0x10: a compute span directly followed by a TP collective (the cell kernel runs the
+      // pair in one iteration); consumers compare the class as t_cls & 0xF
+      if (!P.multistream)
+        for (int64_t i = a; i + 1 < b; ++i)
+          if (P.t_cls[i] == 0 && tm.ops[i].kind == PRISM_KIND_COMPUTE && P.t_cls[i + 1] == 1) P.t_cls[i] |= 0x10;
     }
   }
   TMARK("scan");

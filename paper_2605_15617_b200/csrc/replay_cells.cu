@@ -571,6 +571,7 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
   const int lane = threadIdx.x & 31;
   const int32_t unit = blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (unit >= a.n_units) return;
+  constexpr bool PAIR = C >= 4 && !PR && !MS;  // (compute, TP) pairs in one iteration
   const int32_t cells = g.pp * (g.d1 - g.d0);  // this shard's cells (all of them unsharded)
   const int32_t cell = unit % cells, chunk = a.chunk0 + unit / cells;
   const int32_t s = cell % g.pp, dpi = g.d0 + cell / g.pp;
@@ -681,7 +682,10 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
     uint32_t c_n = __shfl_sync(0xffffffffu, bcls, 0);
     int64_t d_n = __shfl_sync(0xffffffffu, bd, 0);
     for (int32_t j = 0; j < cnt; ++j) {
-      const uint32_t c = c_n;
+      const uint32_t c = c_n & 0xFu;
+      // pair: this compute span is followed by a TP collective of this batch (plan flag 0x10);
+      // both run in this iteration (plain variant only)
+      const bool pair = PAIR && (c_n & 0x10u) && j + 1 < cnt;
       const int64_t d = d_n;
       const int32_t i = base + j;
       c_n = __shfl_sync(0xffffffffu, bcls, (j + 1) & 31);
@@ -708,7 +712,32 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
           if (i + 1 < len) pd[r] = __ldg(g.node_sdur + rb[r] + i + 1);
         }
       }
-      if (c == 0) {  // compute span: every rank waits out its own perturbed duration
+      if (pair) {  // compute span i, then the TP collective i + 1 (its hash beside the span chains)
+        const uint64_t uxn = __shfl_sync(0xffffffffu, bux, (j + 1) & 31);
+        int64_t tq = d_n;
+        if (cpert) {
+          int64_t dd[C];
+#pragma unroll
+          for (int r = 0; r < C; ++r) dd[r] = d;
+          if (gpert) tq = perturb_x(d_n, sx ^ (uxn * K_MIX), p);
+          perturb_add_span<C, false>(t, dd, sx, rkh, (uint64_t)i * K_MIX, p);
+        } else {
+          if (gpert) tq = perturb_x(d_n, sx ^ (uxn * K_MIX), p);
+#pragma unroll
+          for (int r = 0; r < C; ++r) t[r] += d;
+        }
+        if (record) {  // op i's finishes; the tail below writes op i + 1's
+#pragma unroll
+          for (int r = 0; r < C; ++r) fp[r * fst] = t[r];
+          fp += Sp;
+        }
+        const int64_t m = tree_max<C>(t) + tq;
+#pragma unroll
+        for (int r = 0; r < C; ++r) t[r] = m;
+        ++j;  // op i + 1 done
+        c_n = __shfl_sync(0xffffffffu, bcls, (j + 1) & 31);
+        d_n = __shfl_sync(0xffffffffu, bd, (j + 1) & 31);
+      } else if (c == 0) {  // compute span: every rank waits out its own perturbed duration
         if (cpert) {
           int64_t dd[C];
 #pragma unroll

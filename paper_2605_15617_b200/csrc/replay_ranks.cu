@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(32, 16) rank_kernel(DevGraph g, ScenParams p, 
   int64_t ndur = 0;
   auto load_rec = [&](int32_t i, uint32_t &cw, uint32_t &occ, int64_t &dur) {
     const int64_t op = op0 + i;
-    const uint32_t c = __ldg(g.t_cls + op);
+    const uint32_t c = __ldg(g.t_cls + op) & 0xFu;  // bit 0x10: (compute, TP) pair flag of the cell kernel
     const int32_t q0 = __ldg(g.t_q0 + op);
     uint32_t type = 0;
     occ = 0;
