@@ -506,7 +506,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   // the template fields the expansion copies, as structure-of-arrays (coalesced loads; the 48-byte
   // prism_op records would cost the expander 12 cache lines per warp per field)
   const size_t o_tdur = carve(nops * 8), o_tal = carve(nops * 8), o_tfr = carve(nops * 8), o_tsd = carve(nops * 8);
-  const size_t o_tlab = carve(nops * 4), o_tkind = carve(nops);
+  const size_t o_tlab = carve(nops * 4), o_tkind = carve(nops), o_tqi = carve(nops * 8);
   const size_t o_tms = ms ? carve(nops * 2) : 0, o_tsp2 = ms ? carve(nops * 4) : 0, o_tes = ms ? carve(nops * 4) : 0;
   const size_t table_bytes = off;
   // graph arrays (written by the expand kernels)
@@ -553,6 +553,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.t_sdur = (const int64_t *)at(o_tsd);
   d.t_label = (const uint32_t *)at(o_tlab);
   d.t_kind = (const uint8_t *)at(o_tkind);
+  d.t_qinfo = (const uint64_t *)at(o_tqi);
   d.ms = ms ? 1 : 0;
   d.ms_streams = P.ms_streams;
   d.ms_events = P.ms_events;
@@ -627,6 +628,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
       int64_t *tfr = (int64_t *)(hb + o_tfr), *tsd = (int64_t *)(hb + o_tsd);
       uint32_t *tlab = (uint32_t *)(hb + o_tlab);
       uint8_t *tkind = hb + o_tkind;
+      uint64_t *tqi = (uint64_t *)(hb + o_tqi);
       for (size_t i = 0; i < nops; ++i) {
         const prism_op &o = tmpl->ops[i];
         tdur[i] = o.dur_ns;
@@ -636,6 +638,12 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
         tkind[i] = o.kind;
         // replay record duration: a compute span's own, a sync node's first group's (Z2)
         tsd[i] = P.t_q0[i] < 0 ? o.dur_ns : P.q[P.t_q0[i]].dur;
+        tqi[i] = 0;
+        if (P.t_q0[i] >= 0) {
+          const QGroup &q = P.q[P.t_q0[i]];
+          tqi[i] = (uint64_t)(q.type & 0xFF) | ((uint64_t)(q.dir & 0xFF) << 8) |
+                   ((uint64_t)(q.stage & 0xFFFF) << 16) | ((uint64_t)(uint32_t)q.occ << 32);
+        }
       }
     }
     put(o_xptr, P.x_ptr.data(), (pp + 1) * 4);

@@ -90,6 +90,21 @@ __device__ __forceinline__ uint64_t group_gid(const DevGraph &g, const QGroup &q
 __device__ __forceinline__ uint64_t group_uid(const DevGraph &g, const QGroup &q, int32_t inst) {
   return ((uint64_t)q.type << 56) | (group_gid(g, q, inst) << 24) | (uint64_t)q.occ;
 }
+// The same from a host-packed t_qinfo word (type | dir << 8 | stage << 16 | occurrence << 32).
+__device__ __forceinline__ uint64_t group_uid_packed(const DevGraph &g, uint64_t qi, int32_t inst) {
+  const int32_t type = (int32_t)(qi & 0xFF), dir = (int32_t)((qi >> 8) & 0xFF);
+  const int32_t s = (int32_t)((qi >> 16) & 0xFFFF);
+  uint64_t gid;
+  switch (type) {
+    case PRISM_ROLE_TP: gid = (uint64_t)s + (uint64_t)g.pp * inst; break;
+    case PRISM_ROLE_DP: gid = (uint64_t)inst + (uint64_t)g.tp * s; break;
+    case PRISM_ROLE_EP:
+    case PRISM_ROLE_EDP: gid = (uint64_t)(inst % g.tp) + (uint64_t)g.tp * (s + (uint64_t)g.pp * (inst / g.tp)); break;
+    case PRISM_ROLE_WORLD: gid = 0; break;
+    default: gid = (uint64_t)rank_of(g, inst % g.tp, s, inst / g.tp) * 2 + dir; break;
+  }
+  return ((uint64_t)type << 56) | (gid << 24) | (qi >> 32);
+}
 
 // Row e: the shards holding a member of the group of a rank with DP coordinates (dpi, epi, edpi)
 // under the DP-block sharding (shard of dp_i = dp_i / (dp / n_shards)); TP groups and P2P
@@ -144,13 +159,46 @@ __device__ __forceinline__ int32_t group_inst(const DevGraph &g, int32_t type, i
   }
 }
 
+// Template fields of one op that the node-side expansion writes (expand_nodes_kernel).
+struct OpF {
+  int64_t dur, al, fr, sdur;
+  uint64_t qinfo;
+  int32_t tps, q0, tsp, sp, es;
+  uint32_t lab;
+  uint16_t msv;
+  uint8_t kind, cls;
+};
+__device__ __forceinline__ OpF load_opf(const DevGraph &g, int64_t ti) {
+  OpF f;
+  f.tps = __ldg(g.t_prev_sync + ti);
+  f.q0 = __ldg(g.t_q0 + ti);
+  f.dur = __ldg(g.t_dur + ti);
+  f.al = __ldg(g.t_alloc + ti);
+  f.fr = __ldg(g.t_free + ti);
+  f.sdur = __ldg(g.t_sdur + ti);
+  f.lab = __ldg(g.t_label + ti);
+  f.kind = __ldg(g.t_kind + ti);
+  f.cls = __ldg(g.t_cls + ti);
+  f.tsp = __ldg(g.t_slot_ptr + ti);
+  f.qinfo = __ldg(g.t_qinfo + ti);
+  f.sp = -1;
+  f.es = -1;
+  f.msv = 0;
+  if (g.ms) {  // row f2
+    f.sp = g.t_spred[ti];
+    f.es = g.t_esrc[ti];
+    f.msv = g.t_ms[ti];
+  }
+  return f;
+}
+
 // One block per batch of kRanksPerBlock ranks of one stage: a thread loads template op i's fields
 // (and its quotient group) once and writes node i of every rank of the batch, so the L2-resident
 // template tables are read W / pp / kRanksPerBlock times instead of once per rank (the per-rank
 // version moved 2.3 GB of template reads through L2 for 1.3 GB of graph writes on C5).
 constexpr int kRanksPerBlock = 8;
 
-__global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
+__global__ void __launch_bounds__(256, 2) expand_nodes_kernel(DevGraph g) {
   __shared__ int32_t s_r[kRanksPerBlock], s_rb[kRanksPerBlock], s_slot0[kRanksPerBlock];
   __shared__ int32_t s_tpi[kRanksPerBlock], s_dpi[kRanksPerBlock];
   const int32_t per_stage = g.W / g.pp;  // tp * dp ranks run each stage template
@@ -173,56 +221,42 @@ __global__ void __launch_bounds__(256) expand_nodes_kernel(DevGraph g) {
     const int64_t op0 = g.t_op0[s];
     const int32_t len = (int32_t)g.t_len[s];
     // node side: template fields read once (coalesced SoA loads), written for every rank of the
-    // batch (coalesced along each rank's nodes)
+    // batch (coalesced along each rank's nodes); the next op's fields are loaded before this op's
+    // stores (software pipelined: the loads' latency overlaps the stores)
+    OpF cur;
+    if ((int32_t)threadIdx.x < len) cur = load_opf(g, op0 + threadIdx.x);
     for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
-      const int64_t ti = op0 + i;
-      const int32_t tps = __ldg(g.t_prev_sync + ti);
-      const int32_t q0 = __ldg(g.t_q0 + ti);
-      const int64_t dur = __ldg(g.t_dur + ti), al = __ldg(g.t_alloc + ti), fr = __ldg(g.t_free + ti);
-      const int64_t sdur = __ldg(g.t_sdur + ti);
-      const uint32_t lab = __ldg(g.t_label + ti);
-      const uint8_t kind = __ldg(g.t_kind + ti), cls = __ldg(g.t_cls + ti);
-      const int32_t tsp = __ldg(g.t_slot_ptr + ti);
-      int32_t qtype = 0;
-      QGroup q;
-      if (q0 >= 0) {
-        q = ldg_q(g.q + q0);
-        qtype = q.type;
-      }
-      int32_t sp = -1, es = -1;
-      uint16_t msv = 0;
-      if (g.ms) {  // row f2
-        sp = g.t_spred[ti];
-        es = g.t_esrc[ti];
-        msv = g.t_ms[ti];
-      }
+      OpF nxt;
+      if (i + (int32_t)blockDim.x < len) nxt = load_opf(g, op0 + i + blockDim.x);
+      const int32_t qtype = (int32_t)(cur.qinfo & 0xFF);  // a sync node's first group (t_qinfo)
       for (int32_t j = 0; j < nr; ++j) {
         const int32_t r = s_r[j], rb = s_rb[j];
         const int32_t n = rb + i;
         g.node_rank[n] = r;
-        g.node_dur[n] = dur;
-        g.node_kind[n] = kind;
-        g.node_label[n] = lab;
-        g.node_alloc[n] = al;
-        g.node_free[n] = fr;
-        g.node_prev_sync[n] = tps < 0 ? -1 : rb + tps;
-        g.node_gptr[n] = s_slot0[j] + tsp;
+        g.node_dur[n] = cur.dur;
+        g.node_kind[n] = cur.kind;
+        g.node_label[n] = cur.lab;
+        g.node_alloc[n] = cur.al;
+        g.node_free[n] = cur.fr;
+        g.node_prev_sync[n] = cur.tps < 0 ? -1 : rb + cur.tps;
+        g.node_gptr[n] = s_slot0[j] + cur.tsp;
         if (g.ms) {
-          g.node_ms[n] = msv;
-          g.node_spred[n] = sp < 0 ? -1 : rb + sp;
-          g.node_esrc[n] = es < 0 ? -1 : rb + es;
+          g.node_ms[n] = cur.msv;
+          g.node_spred[n] = cur.sp < 0 ? -1 : rb + cur.sp;
+          g.node_esrc[n] = cur.es < 0 ? -1 : rb + cur.es;
         }
         // replay record: a compute span carries its own duration and uid; a sync node its first
         // group's (quotient group q0, instance from the rank's coordinates)
-        g.node_cls[n] = cls;
-        g.node_sdur[n] = sdur;
-        if (q0 < 0) {
+        g.node_cls[n] = cur.cls;
+        g.node_sdur[n] = cur.sdur;
+        if (cur.q0 < 0) {
           g.node_uid[n] = ((uint64_t)r << 32) | (uint32_t)i;
         } else {
           const int32_t dpi = s_dpi[j];
-          g.node_uid[n] = group_uid(g, q, group_inst(g, qtype, s_tpi[j], dpi, dpi % g.ep, dpi / g.ep));
+          g.node_uid[n] = group_uid_packed(g, cur.qinfo, group_inst(g, qtype, s_tpi[j], dpi, dpi % g.ep, dpi / g.ep));
         }
       }
+      cur = nxt;
     }
     // slot side: one quotient group load per template slot, written for every rank of the batch
     const int64_t u0 = g.stage_slot0[s];

@@ -89,6 +89,9 @@ struct DevGraph {
   const int64_t *t_dur, *t_alloc, *t_free, *t_sdur;
   const uint32_t *t_label;
   const uint8_t *t_kind;
+  // per template op: its first quotient group's type | dir << 8 | stage << 16 | occurrence << 32
+  // (0 for compute spans): what the node's replay uid needs, without the 96-byte QGroup
+  const uint64_t *t_qinfo;
   const int32_t *x_ptr;     // [pp+1] cross-op list of each stage
   const XOp *x_ops;
 };

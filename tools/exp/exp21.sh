@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:expand_nodes -c 6 --csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-f-rows > gpurun_out/exp21_ncu.csv 2>&1
+timeout 600 python bench.py --no-cpu-baseline --no-f-rows --steps 20 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['steps'], d['ms_per_step'], d['extra']['device_ms'])" > gpurun_out/exp21.txt 2>&1
+timeout 1200 python -m pytest tests -x -q -m gpu >> gpurun_out/exp21.txt 2>&1
