@@ -25,40 +25,60 @@ __device__ __forceinline__ int32_t rank_of(const DevGraph &g, int32_t tp_i, int3
                                          : tp_i + g.tp * (pp_i + g.pp * dp_i);
 }
 
-// Exclusive scans of per-rank node / slot counts (one block; W <= 2^30 but small in practice).
+// Exclusive scans of per-rank node / slot counts (one block of 1024 threads, 1024 ranks per
+// round: warp shuffle scans, then a scan of the 32 warp totals; W <= 2^30 but small in practice).
 __global__ void __launch_bounds__(1024) rank_tables_kernel(DevGraph g) {
-  __shared__ int64_t s_nodes[1024], s_slots[1024];
+  __shared__ int64_t w_nodes[32], w_slots[32];
   __shared__ int64_t carry_n, carry_s;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x == 0) carry_n = carry_s = 0;
   __syncthreads();
   for (int32_t base = 0; base < g.W; base += 1024) {
-    int32_t r = base + threadIdx.x;
+    const int32_t r = base + threadIdx.x;
     int64_t n = 0, sl = 0;
     if (r < g.W) {
-      int32_t s = stage_of(g, r);
+      const int32_t s = stage_of(g, r);
       g.rank_stage[r] = s;
       n = g.t_len[s];
       sl = g.t_slots_total[s];
     }
-    s_nodes[threadIdx.x] = n;
-    s_slots[threadIdx.x] = sl;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {  // Hillis-Steele inclusive scan
-      int64_t a = threadIdx.x >= off ? s_nodes[threadIdx.x - off] : 0;
-      int64_t b = threadIdx.x >= off ? s_slots[threadIdx.x - off] : 0;
-      __syncthreads();
-      s_nodes[threadIdx.x] += a;
-      s_slots[threadIdx.x] += b;
-      __syncthreads();
+    int64_t xn = n, xs = sl;  // inclusive scans within the warp
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t yn = __shfl_up_sync(0xffffffffu, xn, off), ys = __shfl_up_sync(0xffffffffu, xs, off);
+      if (lane >= off) {
+        xn += yn;
+        xs += ys;
+      }
     }
+    if (lane == 31) {
+      w_nodes[wid] = xn;
+      w_slots[wid] = xs;
+    }
+    __syncthreads();
+    if (wid == 0) {  // exclusive scan of the warp totals
+      int64_t tn = w_nodes[lane], ts = w_slots[lane];
+      int64_t un = tn, us = ts;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int64_t yn = __shfl_up_sync(0xffffffffu, un, off), ys = __shfl_up_sync(0xffffffffu, us, off);
+        if (lane >= off) {
+          un += yn;
+          us += ys;
+        }
+      }
+      w_nodes[lane] = un - tn;
+      w_slots[lane] = us - ts;
+    }
+    __syncthreads();
     if (r < g.W) {
-      g.rank_ptr[r] = (int32_t)(carry_n + s_nodes[threadIdx.x] - n);
-      g.rank_slot[r] = (int32_t)(carry_s + s_slots[threadIdx.x] - sl);
+      g.rank_ptr[r] = (int32_t)(carry_n + w_nodes[wid] + xn - n);
+      g.rank_slot[r] = (int32_t)(carry_s + w_slots[wid] + xs - sl);
     }
     __syncthreads();
-    if (threadIdx.x == 1023) {
-      carry_n += s_nodes[1023];
-      carry_s += s_slots[1023];
+    if (threadIdx.x == 1023) {  // the round's totals
+      carry_n += w_nodes[31] + xn;
+      carry_s += w_slots[31] + xs;
     }
     __syncthreads();
   }

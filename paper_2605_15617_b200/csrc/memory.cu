@@ -5,7 +5,8 @@
 // finish_{i-1} >= start_{i-1}), so that order IS program order (Z6) and the peak
 // does not depend on the scenario: peak_r = static + max(0, max_i (R_i + alloc_i)) where R_i is
 // the exclusive prefix sum of (alloc - free) — the running total right after op i's allocation.
-// One warp per rank: 32 ops per step, 64-bit warp inclusive scan with shuffles, HBM read-bound
+// One warp per rank: 32 ops per step, 64-bit warp inclusive scan with shuffles, the running
+// maximum kept per lane (one warp reduction per rank); HBM read-bound
 // (16 B per node: alloc + free), 8 B per rank written.
 #include <cuda_runtime.h>
 
@@ -20,7 +21,7 @@ __global__ void __launch_bounds__(256) peak_kernel(DevGraph g, int64_t *__restri
   const int32_t warps = gridDim.x * (blockDim.x >> 5);
   for (int32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < g.W; r += warps) {
     const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
-    int64_t carry = 0, best = 0;
+    int64_t carry = 0, best = 0;  // best: this lane's max of R_i + alloc_i (warp max at the end)
     for (int32_t base = rb; base < re; base += 32) {
       const int32_t i = base + lane;
       int64_t a = 0, f = 0;
@@ -34,13 +35,11 @@ __global__ void __launch_bounds__(256) peak_kernel(DevGraph g, int64_t *__restri
         const int64_t y = __shfl_up_sync(0xffffffffu, x, off);
         if (lane >= off) x += y;
       }
-      const int64_t after_alloc = carry + x - (a - f) + a;  // R_i + alloc_i
-      int64_t m = i < re ? after_alloc : 0;
-#pragma unroll
-      for (int off = 16; off; off >>= 1) m = max(m, (int64_t)__shfl_xor_sync(0xffffffffu, m, off));
-      best = max(best, m);
+      if (i < re) best = max(best, carry + x - (a - f) + a);  // R_i + alloc_i
       carry += __shfl_sync(0xffffffffu, x, 31);
     }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) best = max(best, (int64_t)__shfl_xor_sync(0xffffffffu, best, off));
     if (lane == 0) peak[r] = g.static_mem[g.rank_stage[r]] + best;
   }
 }
