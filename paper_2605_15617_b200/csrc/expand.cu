@@ -321,8 +321,9 @@ __global__ void __launch_bounds__(256) build_groups_kernel(DevGraph g) {
     const int64_t m_end = min(mq, g.chunk_m[c] + 2048);
     const int32_t s = q.stage;
     for (int64_t local = g.chunk_m[c] + threadIdx.x; local < m_end; local += blockDim.x) {
-      const int32_t inst = (int32_t)(local / q.size);
-      const int32_t j = (int32_t)(local - (int64_t)inst * q.size);
+      // local < M < 2^31 (checked by the plan): 32-bit division
+      const int32_t inst = (int32_t)local / q.size;
+      const int32_t j = (int32_t)local - inst * q.size;
       const int64_t m = q.mbase + local;
       const int64_t grp = q.gbase + inst;
       int32_t rank, tidx = q.tidx;
