@@ -13,6 +13,8 @@
 // block then writes gfin for its groups. All arithmetic is int64; results are exact.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "graph.h"
 
 namespace prism {
@@ -167,19 +169,25 @@ __global__ void __launch_bounds__(256) tail_kernel(DevGraph g, ScenParams p, int
 }
 
 // Row a8: T_k = max over ranks of the rank's last finish (every chain is non-decreasing).
-__global__ void __launch_bounds__(256) reduce_iter_kernel(int32_t W, int32_t Sp,
+// Row a8: iteration time of each scenario = max over ranks of rank_end[r][k] (all >= 0). Block
+// (x, y): 32 consecutive scenarios (coalesced 256-byte rows) x 8 rank lanes, ranks strided over
+// grid.y; a shared-memory max over the 8 rank lanes, then one atomicMax per scenario into iter,
+// which the launcher zeroes first.
+__global__ void __launch_bounds__(256) reduce_iter_kernel(int32_t W, int32_t S, int32_t Sp,
                                                           const int64_t *__restrict__ rank_end,
                                                           int64_t *__restrict__ iter) {
-  const int32_t k = blockIdx.x;
+  const int kx = threadIdx.x & 31, ry = threadIdx.x >> 5;
+  const int32_t k = blockIdx.x * 32 + kx;
   int64_t m = 0;
-  for (int32_t r = threadIdx.x; r < W; r += blockDim.x) m = max(m, rank_end[(int64_t)r * Sp + k]);
-  for (int off = 16; off; off >>= 1) m = max(m, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off));
-  __shared__ int64_t wm[8];
-  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  if (k < Sp)
+    for (int32_t r = blockIdx.y * 8 + ry; r < W; r += gridDim.y * 8) m = max(m, rank_end[(int64_t)r * Sp + k]);
+  __shared__ int64_t sm[8][32];
+  sm[ry][kx] = m;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; ++w) m = max(m, wm[w]);
-    iter[k] = max(m, wm[0]);
+  if (ry == 0) {
+#pragma unroll
+    for (int y = 1; y < 8; ++y) m = max(m, sm[y][kx]);
+    if (k < S) atomicMax((unsigned long long *)(iter + k), (unsigned long long)m);
   }
 }
 
@@ -449,7 +457,11 @@ cudaError_t launch_tail(const DevGraph &g, const ScenParams &p, int64_t *fin, co
 
 cudaError_t launch_reduce(int32_t W, int32_t S, int32_t Sp, const int64_t *rank_end, int64_t *iter,
                           cudaStream_t st) {
-  reduce_iter_kernel<<<S, 256, 0, st>>>(W, Sp, rank_end, iter);
+  if (S <= 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(iter, 0, (size_t)S * 8, st);
+  if (e != cudaSuccess) return e;
+  const int ry = std::max(1, std::min(64, (W + 7) / 8));
+  reduce_iter_kernel<<<dim3((S + 31) / 32, ry), 256, 0, st>>>(W, S, Sp, rank_end, iter);
   return cudaGetLastError();
 }
 
