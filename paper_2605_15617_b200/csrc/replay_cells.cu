@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
         }
         if (record) {  // op i's finishes; the tail below writes op i + 1's
 #pragma unroll
-          for (int r = 0; r < C; ++r) fp[r * fst] = t[r];
+          for (int r = 0; r < C; ++r) __stcs(fp + r * fst, (long long)t[r]);
           fp += Sp;
         }
         const int64_t m = tree_max<C>(t) + tq;
@@ -822,8 +822,8 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
       if (record) {
 #pragma unroll
         for (int r = 0; r < C; ++r) {
-          if (C >= 4 && !PR) fp[r * fst] = t[r];
-          else fin[(int64_t)(rb[r] + i) * Sp + k] = t[r];  // small cells, PR: fewer live registers
+          if (C >= 4 && !PR) __stcs(fp + r * fst, (long long)t[r]);
+          else __stcs(fin + (int64_t)(rb[r] + i) * Sp + k, (long long)t[r]);  // small cells, PR: fewer live registers
         }
         if (C >= 4 && !PR) fp += Sp;
       }
