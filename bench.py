@@ -18,6 +18,7 @@ each GPU replay the whole graph for its own block of 64 scenarios of the sweep i
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -173,12 +174,16 @@ def run_prism(args):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    gc_was = gc.isenabled()
+    gc.disable()  # no collector pause inside the timed loop (host work is on the step's path)
     with Clocks(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             step(timed=True)
         e1.record(stream)
         torch.cuda.synchronize()
+    if gc_was:
+        gc.enable()
     ms = e0.elapsed_time(e1)
     iters = iter_dev.cpu().numpy().copy()
     st = graphs[0].stats()
