@@ -495,7 +495,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     return o;
   };
   // tables (uploaded)
-  const size_t o_ops = carve(nops * sizeof(prism_op)), o_tps = carve(nops * 4), o_tsp = carve(nops * 4);
+  const size_t o_tps = carve(nops * 4), o_tsp = carve(nops * 4);
   const size_t o_op0 = carve(pp * 8), o_len = carve(pp * 8), o_slt = carve(pp * 8), o_stat = carve(pp * 8);
   const size_t o_q = carve(P.q.size() * sizeof(QGroup)), o_wpos = carve(P.wpos.size() * 4);
   const size_t o_ss0 = carve(P.stage_slot0.size() * 8), o_slq = carve(nslot * 4), o_sltd = carve(nslot * 4);
@@ -525,8 +525,6 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   trace("build: allocated");
   if (G->oom || !base) return fail(PRISM_E_OOM, "device allocation failed while building the graph");
   auto at = [base](size_t o) { return (void *)(base + o); };
-  prism_op *t_ops = (prism_op *)at(o_ops);
-  d.t_ops = t_ops;
   d.t_prev_sync = (int32_t *)at(o_tps);
   d.t_slot_ptr = (int32_t *)at(o_tsp);
   d.t_op0 = (int64_t *)at(o_op0);
@@ -605,7 +603,6 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     auto put = [hb](size_t o, const void *src, size_t bytes) {
       if (bytes) std::memcpy(hb + o, src, bytes);
     };
-    put(o_ops, tmpl->ops, nops * sizeof(prism_op));
     put(o_tps, P.t_prev_sync.data(), nops * 4);
     put(o_tsp, P.t_slot_ptr.data(), nops * 4);
     put(o_op0, P.stage_op0.data(), pp * 8);

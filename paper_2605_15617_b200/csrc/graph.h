@@ -63,7 +63,6 @@ struct DevGraph {
   uint32_t *h_smask;        // sharded graphs: bit m = shard m holds a member of the slot's group
   int64_t M_cross, G_large;
   // per-stage template tables (tiny; L2 resident)
-  const prism_op *t_ops;    // concatenated templates
   int64_t *t_op0;           // [pp] first op of each stage
   int64_t *t_len;           // [pp]
   int32_t *t_prev_sync;     // per op
