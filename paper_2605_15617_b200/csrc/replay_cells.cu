@@ -13,10 +13,14 @@
 //                       valid: an aligned 8-byte store is single-copy atomic, so the value is its own
 //                       flag (parity-encoded per replay, see CellArgs) and no fence is needed
 //   large cross-cell  : (DP, WORLD, big EP) red.max of the ready times into the group's accumulator,
-//   group               fence, arrive on its counter; members poll the counter, then read the
-//                       accumulator (the segmented max is done by the L2 atomics)
-// and a node finishes at the max over its groups' (start + dur'_g) (reading Z3). fin stores are
-// 256-byte coalesced rows (32 scenarios of one node).
+//   group               then one acq_rel arrival per warp on its counter; the member completing the
+//                       count reads the accumulator and publishes the maximum in a value-as-flag
+//                       result slot the others poll (sharded replays: fenced system-scope variant,
+//                       members poll the counter, then read the accumulator)
+// and a node finishes at the max over its groups' (start + dur'_g) (reading Z3). Ops whose pairs
+// are all 2-member groups take the lean path (cross_pairs); a compute span followed by a TP
+// collective runs as one iteration (plan flag 0x10). fin stores are 256-byte coalesced rows (32
+// scenarios of one node), evict-first.
 //
 // Scheduling: every warp of the launch is co-resident (cudaLaunchCooperativeKernel refuses
 // otherwise and the caller falls back to the level-by-level path), so a waiting warp cannot starve
