@@ -1,0 +1,23 @@
+// cells_k_stm.cu — instantiation unit of the cell kernel (cell_kernel.cuh), variant
+// SH=true (sharded), PR=false (per-rank durations), MS=true (multi-stream), tp = 1..8.
+#ifndef PRISM_CELL_STATS
+#include "cell_kernel.cuh"
+
+namespace prism {
+
+const void *cell_kernel_get_stm(int tp) {
+  switch (tp) {
+    case 1: return (const void *)cell_kernel<1, true, false, true>;
+    case 2: return (const void *)cell_kernel<2, true, false, true>;
+    case 3: return (const void *)cell_kernel<3, true, false, true>;
+    case 4: return (const void *)cell_kernel<4, true, false, true>;
+    case 5: return (const void *)cell_kernel<5, true, false, true>;
+    case 6: return (const void *)cell_kernel<6, true, false, true>;
+    case 7: return (const void *)cell_kernel<7, true, false, true>;
+    case 8: return (const void *)cell_kernel<8, true, false, true>;
+    default: return nullptr;
+  }
+}
+
+}  // namespace prism
+#endif

@@ -1,0 +1,23 @@
+// cells_k_upo.cu — instantiation unit of the cell kernel (cell_kernel.cuh), variant
+// SH=false (sharded), PR=true (per-rank durations), MS=false (multi-stream), tp = 1..8.
+#ifndef PRISM_CELL_STATS
+#include "cell_kernel.cuh"
+
+namespace prism {
+
+const void *cell_kernel_get_upo(int tp) {
+  switch (tp) {
+    case 1: return (const void *)cell_kernel<1, false, true, false>;
+    case 2: return (const void *)cell_kernel<2, false, true, false>;
+    case 3: return (const void *)cell_kernel<3, false, true, false>;
+    case 4: return (const void *)cell_kernel<4, false, true, false>;
+    case 5: return (const void *)cell_kernel<5, false, true, false>;
+    case 6: return (const void *)cell_kernel<6, false, true, false>;
+    case 7: return (const void *)cell_kernel<7, false, true, false>;
+    case 8: return (const void *)cell_kernel<8, false, true, false>;
+    default: return nullptr;
+  }
+}
+
+}  // namespace prism
+#endif
