@@ -131,6 +131,7 @@ def run_prism(args):
     kw = dict(amp_q16=args.amp, kind_mask=7, seed=0x5EED, algo=args.algo,
               first=(rank * args.scenarios if (ws > 1 and not sharded) else 0))
     iter_dev = torch.zeros(S, dtype=torch.int64, device="cuda")
+    iter_steps = torch.zeros(max(1, args.steps), S, dtype=torch.int64, device="cuda")  # per timed step
     peak_dev = torch.zeros(tm.topo.world, dtype=torch.int64, device="cuda")
     comm = [None]  # sharded: the graph currently holding the connected exchange buffer
 
@@ -150,7 +151,7 @@ def run_prism(args):
     graphs = []
     replay_events = []  # (start, end) CUDA events around each timed replay, on its stream
 
-    def step(timed=False):
+    def step(timed=False, i=0):
         # build first (a sharded build adopts the previous graph's exchange buffer), then release
         # the previous step's graph; the last one survives the timed region
         g = new_graph()
@@ -159,7 +160,8 @@ def run_prism(args):
         if timed:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record(stream)
-        g.replay_async(iter_dev.data_ptr(), S, record=True, **kw)
+        out = iter_steps[i] if timed else iter_dev
+        g.replay_async(out.data_ptr(), S, record=True, **kw)
         if timed:
             ev[1].record(stream)
             replay_events.append(ev)
@@ -178,14 +180,18 @@ def run_prism(args):
     gc.disable()  # no collector pause inside the timed loop (host work is on the step's path)
     with Clocks(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
-            step(timed=True)
+        for i in range(args.steps):
+            step(timed=True, i=i)
         e1.record(stream)
         torch.cuda.synchronize()
     if gc_was:
         gc.enable()
     ms = e0.elapsed_time(e1)
-    iters = iter_dev.cpu().numpy().copy()
+    graphs[0].sync()  # raises if the device watchdog aborted a replay (prism_sync)
+    its = iter_steps.cpu().numpy()
+    iters = its[0].copy()
+    # every timed step replays the same workload: identical results, or a step went wrong
+    assert (its == iters[None, :]).all(), "timed steps disagree"
     st = graphs[0].stats()
     launches_per_step = st["replay_launches"] + 3 + 1  # expand: rank tables, nodes, groups; peak
     if ws > 1:

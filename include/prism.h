@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PRISM_ABI_VERSION 3
+#define PRISM_ABI_VERSION 4
 
 #if defined(__GNUC__)
 #define PRISM_API __attribute__((visibility("default")))
@@ -210,8 +210,20 @@ PRISM_API prism_status prism_plan(const prism_topology *topo, const prism_templa
 PRISM_API prism_status prism_replay(prism_graph_t g, const prism_scenarios *sc, int64_t *iter_ns_out);
 
 /* Same as prism_replay but asynchronous: writes T_k into iter_ns_dev_out (DEVICE pointer, n
- * int64) on the graph's stream and returns without synchronizing. */
+ * int64) on the graph's stream and returns without synchronizing. The returned status covers the
+ * host-side checks only; whether the device finished the replay is reported by the next
+ * synchronizing call on the graph (prism_sync, prism_replay, prism_query_rank, ...): if a replay
+ * queued since the last such call was aborted by the device watchdog, that call returns
+ * PRISM_E_DEADLOCK once, and the iteration times of those replays are invalid. */
 PRISM_API prism_status prism_replay_async(prism_graph_t g, const prism_scenarios *sc, int64_t *iter_ns_dev_out);
+
+/* Waits for every call queued on the graph's stream and reports what the device found since the
+ * last synchronizing call: PRISM_E_DEADLOCK if a replay was aborted by the device watchdog (a
+ * waiting warp saw no progress for the watchdog period, 10 s by default), PRISM_E_NEGATIVE_MEMORY
+ * if a time-ordered memory scan found a negative running total; PRISM_OK otherwise. After an
+ * abort the next replay of an unsharded graph first resets its ready slots (bit-exact results
+ * again); a sharded graph must be re-prepared (prism_shard_prepare / _connect). */
+PRISM_API prism_status prism_sync(prism_graph_t g);
 
 /* Row a9: per-rank peak memory in bytes, peak_r = static_mem[stage(r)] + max(0, max prefix sum of
  * the rank's events +alloc at op start / -free at op finish ordered by (time, event index)); for
@@ -336,6 +348,13 @@ PRISM_API prism_status prism_last_algo(prism_graph_t g, int32_t *algo_out);
  * last replay (a5-a7), out[2] tail (a6), out[3] iteration reduce (a8), out[4] peak scan (a9).
  * Synchronizes on the recorded events. PRISM_E_INVALID_ARG if profiling is off. */
 PRISM_API prism_status prism_last_timing(prism_graph_t g, float out[5]);
+
+/* Test hooks of the device watchdog: PRISM_DEBUG_WATCHDOG_NS sets the period after which a
+ * waiting replay kernel aborts with PRISM_E_DEADLOCK (default 10 s, >= 1000); PRISM_DEBUG_STALL_UNIT
+ * >= 0 makes that warp (cell kernel unit / rank kernel warp) of the following replays return at
+ * once without arriving anywhere, so its partners time out (-1 = off). */
+enum { PRISM_DEBUG_WATCHDOG_NS = 0, PRISM_DEBUG_STALL_UNIT = 1 };
+PRISM_API prism_status prism_debug_set(prism_graph_t g, int32_t key, int64_t value);
 
 /* Test hook: copy one device array of the graph to host memory (bytes = capacity of host_out).
  * which: 0 rank_ptr[W+1] i32, 1 node_rank[N] i32, 2 node_dur[N] i64, 3 node_kind[N] u8,

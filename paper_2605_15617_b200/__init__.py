@@ -25,7 +25,8 @@ EXPORTED_SYMBOLS = [
     "prism_peak_memory_async", "prism_query_rank", "prism_graph_stats", "prism_destroy_graph",
     "prism_debug_export", "prism_plan", "prism_last_timing", "prism_last_algo",
     "prism_shard_prepare", "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
-    "prism_set_durations", "prism_critical_path", "prism_peak_memory_at",
+    "prism_set_durations", "prism_critical_path", "prism_peak_memory_at", "prism_sync",
+    "prism_debug_set",
 ]
 SHARD_HANDLE_BYTES = 64
 
@@ -118,12 +119,15 @@ def lib():
         L.prism_set_durations.argtypes = [P, P]
         L.prism_peak_memory_at.argtypes = [P, ctypes.c_int32, P]
         L.prism_critical_path.argtypes = [P, ctypes.c_int32, P, ctypes.c_int64, P, P]
+        L.prism_sync.argtypes = [P]
+        L.prism_debug_set.argtypes = [P, ctypes.c_int32, ctypes.c_int64]
         for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
                      "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
                      "prism_graph_stats", "prism_debug_export", "prism_plan",
                      "prism_last_timing", "prism_last_algo", "prism_shard_prepare",
                      "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
-                     "prism_set_durations", "prism_critical_path", "prism_peak_memory_at"):
+                     "prism_set_durations", "prism_critical_path", "prism_peak_memory_at",
+                     "prism_sync", "prism_debug_set"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
     return _lib
@@ -135,8 +139,12 @@ def _check(status: int):
 
 
 def use_torch_allocator() -> None:
-    """Route the library's device allocations through PyTorch's caching allocator."""
+    """Route the library's device allocations through PyTorch's caching allocator. Idempotent: a
+    graph keeps the hooks it was built with, so the ctypes thunks are installed once and live for
+    the process (replacing them would leave older graphs calling freed thunks on destroy)."""
     global _hooks
+    if _hooks is not None:
+        return
     import torch
 
     def _alloc(nbytes, stream, ctx):
@@ -257,6 +265,15 @@ class Graph:
         """Asynchronous replay writing n int64 iteration times to a DEVICE pointer."""
         sc = self._scen(n, seed, amp_q16, kind_mask, record, algo, first)
         _check(lib().prism_replay_async(self._h, ctypes.byref(sc), ctypes.c_void_p(iter_dev_ptr)))
+
+    def sync(self) -> None:
+        """Wait for the graph's queued work; raises PrismError(PRISM_E_DEADLOCK) if a replay since the
+        last synchronising call was aborted by the device watchdog (prism_sync)."""
+        _check(lib().prism_sync(self._h))
+
+    def debug_set(self, key: str, value: int) -> None:
+        """Watchdog test hooks: key 'watchdog_ns' or 'stall_unit' (prism_debug_set)."""
+        _check(lib().prism_debug_set(self._h, {"watchdog_ns": 0, "stall_unit": 1}[key], int(value)))
 
     def last_algo(self) -> str:
         v = ctypes.c_int32(0)

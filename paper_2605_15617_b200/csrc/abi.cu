@@ -26,12 +26,14 @@ namespace {
 
 thread_local std::string t_err;
 
-// Pinned host words for the cell kernel's abort status, shared by all graphs (cudaHostAlloc /
-// cudaFreeHost per graph would synchronize the device on every build/destroy).
+// Pinned host status slots (4 words per graph: [0] abort status of the last waiting replay, [1]
+// sticky first abort of earlier replays, [2] time-ordered memory scan status), shared by all graphs
+// (cudaHostAlloc / cudaFreeHost per graph would synchronize the device on every build/destroy).
 std::mutex g_pin_mu;
 uint32_t *g_pin = nullptr;
 std::vector<int> g_pin_free;
 constexpr int kPinWords = 4096;
+constexpr int kPinSlot = 4;  // words per graph
 // A word whose graph was destroyed is reclaimed once the event recorded behind its last status
 // copy has completed (a host callback on the stream would stall the stream's next kernels until
 // the host ran it: a bubble in every bench step).
@@ -62,7 +64,7 @@ uint32_t *pin_take() {
       g_pin = nullptr;
       return nullptr;
     }
-    for (int i = kPinWords - 1; i >= 0; --i) g_pin_free.push_back(i);
+    for (int i = kPinWords - kPinSlot; i >= 0; i -= kPinSlot) g_pin_free.push_back(i);
   }
   if (g_pin_free.empty()) {
     pin_reclaim_locked();
@@ -71,7 +73,7 @@ uint32_t *pin_take() {
   if (g_pin_free.empty()) return nullptr;
   const int i = g_pin_free.back();
   g_pin_free.pop_back();
-  g_pin[i] = 0;
+  for (int j = 0; j < kPinSlot; ++j) g_pin[i + j] = 0;
   return g_pin + i;
 }
 // Returns word p once the work queued so far on stream st (device dev) has completed.
@@ -240,12 +242,13 @@ struct prism_graph_s {
   size_t acc_bytes = 0;
   int64_t *rres = nullptr;    // large-group result slots [G_large][Sp] (parity-encoded)
   size_t rres_bytes = 0;
-  uint32_t *sync_words = nullptr;  // arrive[G_large], status[4]
+  uint32_t *sync_words = nullptr;  // arrive[G_large x chunks] (sharded: unused)
   size_t sync_bytes = 0;
-  uint32_t *h_status = nullptr;    // pinned copy of the status word
+  uint32_t *words = nullptr;       // device: [0] replay abort status, [1] sticky abort, [2] memory
+                                   // scan status (part of the structure allocation, zeroed at build)
+  uint32_t *h_status = nullptr;    // pinned copy of words[0..2] (slot of kPinSlot words)
   int last_algo = 0;
   int recorded = 0;
-  bool status_is_memory = false;  // h_status holds a time-ordered memory scan's status
   // fin keeps rows [fin_node0, fin_node0 + fin_rows) (all nodes unless sharded)
   int64_t fin_node0 = 0, fin_rows = 0;
   // row e: sharding (n_shards > 1)
@@ -327,6 +330,7 @@ struct prism_graph_s {
     return p != nullptr;
   }
   ~prism_graph_s() {
+    trace("destroy: begin");
     dfree(fin);
     dfree(gfin);
     dfree(rank_end);
@@ -340,6 +344,7 @@ struct prism_graph_s {
     dfree(part);
     dfree(ov);
     dfree(crit);
+    trace("destroy: buffers freed");
     if (h_status) {  // returned to the pool once the stream has passed its pending status copy
       int cur = -1;
       cudaGetDevice(&cur);
@@ -347,7 +352,9 @@ struct prism_graph_s {
       pin_give_after(h_status, stream, device);
       if (device >= 0 && cur >= 0 && cur != device) cudaSetDevice(cur);
     }
+    trace("destroy: status slot returned");
     for (auto &b : blocks) dfree(b.first);  // stream-ordered frees: no host wait needed
+    trace("destroy: structure freed");
     if (ex || !ipc_open.empty()) {  // the exchange buffer is not stream-ordered memory
       cudaStreamSynchronize(stream);
       for (void *p : ipc_open) cudaIpcCloseMemHandle(p);
@@ -519,6 +526,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t o_hb = carve(M * 4), o_hm = carve(M * 4), o_hd = carve(M * 8), o_hu = carve(M * 8);
   const size_t o_hs = n_shards > 1 ? carve(M * 4) : 0;
   const size_t o_nmsk = ms ? carve(N * 2) : 0, o_nsp = ms ? carve(N * 4) : 0, o_nes = ms ? carve(N * 4) : 0;
+  const size_t o_words = carve(16);
   const size_t total = off;
   trace("build: tables sized");
   unsigned char *base = G->take<unsigned char>(total);
@@ -591,6 +599,9 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.node_esrc = ms ? (int32_t *)at(o_nes) : nullptr;
   d.M_cross = P.M_cross;
   d.G_large = P.G_large;
+  d.stall_unit = -1;
+  d.watchdog_ns = 10ull * 1000 * 1000 * 1000;
+  G->words = (uint32_t *)at(o_words);
   cudaStream_t s = G->stream;
   {  // packed upload of the host tables, from a pinned staging buffer when one is available
     PinnedStage ps(table_bytes);
@@ -671,6 +682,8 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
       loaded.push_back(G->device);
     }
   }
+  CU(cudaMemsetAsync(G->words, 0, 16, s));
+  if (!(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status words unavailable");
   G->rec(0);
   CU(launch_expand(d, s));
   G->rec(1);
@@ -750,28 +763,28 @@ prism_status replay_ranks_impl(prism_graph_t G, const prism_scenarios *sc, int64
   if (!G->ensure(G->acc, G->acc_bytes, lg)) return fail(PRISM_E_OOM, "accumulator allocation failed");
   if (G->rres_bytes < lg) G->rslot_dirty = true;
   if (!G->ensure(G->rres, G->rres_bytes, lg)) return fail(PRISM_E_OOM, "result-slot allocation failed");
-  const size_t nwords = (size_t)P.G_large + 4;
+  const size_t nwords = std::max<size_t>(1, (size_t)P.G_large);
   if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
-  if (!G->h_status && !(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status word unavailable");
   if (G->rslot_dirty) {
     CU(cudaMemsetAsync(G->rslot, 0xFF, G->rslot_bytes, G->stream));
     CU(cudaMemsetAsync(G->rres, 0xFF, G->rres_bytes, G->stream));
     G->parity = 0;
     G->rslot_dirty = false;
   }
+  CU(launch_replay_guard(G->words, G->rslot, G->rslot_bytes / 8, G->rres, G->rres_bytes / 8, G->parity, G->stream));
   CU(cudaMemsetAsync(G->acc, 0, (size_t)P.G_large * 8, G->stream));
   CU(cudaMemsetAsync(G->sync_words, 0, nwords * 4, G->stream));
-  uint32_t *status = G->sync_words + P.G_large;
+  uint32_t *status = G->words;
   G->rec(2);
   CU(launch_ranks(G->cur(), p, G->rslot, G->acc, G->rres, G->sync_words, status, G->parity,
                   p.record ? G->fin : nullptr, G->gfin, G->rank_end, G->stream));
   G->parity ^= 1;
-  CU(cudaMemcpyAsync(G->h_status, status, 4, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaMemcpyAsync(G->h_status, G->words, 8, cudaMemcpyDeviceToHost, G->stream));
   G->rec(3);
   G->rec(4);
   CU(launch_reduce(P.W, 1, Sp, G->rank_end, iter_dev, G->stream));
   G->rec(5);
-  G->launches = 2;
+  G->launches = 3;  // guard, rank kernel, reduce
   G->last = p;
   G->last_Sp = Sp;
   G->recorded = p.record;
@@ -847,13 +860,13 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     // row e: ready slots / accumulators / counters live in the peer-mapped exchange buffer; they
     // were reset at prepare, and the accumulators and counters are reset again right after the
     // cell kernel, before this shard publishes its partial (the peers' next pushes wait for it)
-    const size_t nwords = 4;
-    if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
-    if (!G->h_status && !(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status word unavailable");
     if (!G->ensure(G->part, G->part_bytes, (size_t)Sp * 8)) return fail(PRISM_E_OOM, "partial allocation failed");
-    CU(cudaMemsetAsync(G->sync_words, 0, nwords * 4, G->stream));
+    // an abort leaves the peers' exchange state inconsistent: the graph is re-prepared instead of
+    // reset (check_status disconnects it), so the guard only folds the status
+    CU(launch_replay_guard(G->words, nullptr, 0, nullptr, 0, G->parity, G->stream));
+    ++launches;
     G->link.epoch += 1;
-    uint32_t *status = G->sync_words;
+    uint32_t *status = G->words;
     int64_t *rslot = (int64_t *)(G->ex + G->link.o_rslot);
     int64_t *acc = (int64_t *)(G->ex + G->link.o_acc);
     uint32_t *arrive = (uint32_t *)(G->ex + G->link.o_arrive);
@@ -874,7 +887,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     G->rec(4);
     CU(launch_shard_reduce(G->cur(), G->link, S, Sp, G->rank_end, G->part, iter_dev, status, G->stream));
     trace("shard: reduce launched");
-    CU(cudaMemcpyAsync(G->h_status, status, 4, cudaMemcpyDeviceToHost, G->stream));
+    CU(cudaMemcpyAsync(G->h_status, G->words, 8, cudaMemcpyDeviceToHost, G->stream));
     trace("shard: status copy");
     launches += 2;
   } else if (cells) {
@@ -887,19 +900,20 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     const size_t rr_bytes = std::max<size_t>(16, (size_t)P.G_large * Sp * 8);
     if (G->rres_bytes < rr_bytes) G->rslot_dirty = true;  // result slots share the ready slots' parity
     if (!G->ensure(G->rres, G->rres_bytes, rr_bytes)) return fail(PRISM_E_OOM, "result-slot allocation failed");
-    const size_t nwords = (size_t)P.G_large * nchunks + 4;
+    const size_t nwords = std::max<size_t>(1, (size_t)P.G_large * nchunks);
     if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
-    if (!G->h_status && !(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status word unavailable");
     if (G->rslot_dirty) {  // all slots read "not yet" under parity 0
       CU(cudaMemsetAsync(G->rslot, 0xFF, G->rslot_bytes, G->stream));
       CU(cudaMemsetAsync(G->rres, 0xFF, G->rres_bytes, G->stream));
       G->parity = 0;
       G->rslot_dirty = false;
     }
+    CU(launch_replay_guard(G->words, G->rslot, G->rslot_bytes / 8, G->rres, G->rres_bytes / 8, G->parity, G->stream));
+    ++launches;
     CU(cudaMemsetAsync(G->acc, 0, (size_t)P.G_large * Sp * 8, G->stream));
     CU(cudaMemsetAsync(G->sync_words, 0, nwords * 4, G->stream));
     G->rec(2);
-    uint32_t *status = G->sync_words + (size_t)P.G_large * nchunks;
+    uint32_t *status = G->words;
     const int per_launch = cells_chunks_per_launch(G->cur(), nchunks);
     for (int ch = 0; ch < nchunks; ch += per_launch) {
       CU(launch_cells(G->cur(), p, G->rslot, G->acc, G->rres, G->sync_words, status, G->parity,
@@ -908,7 +922,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
       ++launches;
     }
     G->parity ^= 1;
-    CU(cudaMemcpyAsync(G->h_status, status, 4, cudaMemcpyDeviceToHost, G->stream));
+    CU(cudaMemcpyAsync(G->h_status, G->words, 8, cudaMemcpyDeviceToHost, G->stream));
     G->rec(3);
     G->rec(4);
   } else {
@@ -940,17 +954,23 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   return PRISM_OK;
 }
 
-// Abort status of the last cell-kernel replay (valid once the stream has passed it).
+// Abort status of the waiting replays queued so far (valid once the stream has passed them, i.e.
+// after a stream synchronisation): the last one's word and the sticky first abort of the earlier
+// ones (folded by the next replay's guard kernel). Reported once, then cleared on both sides.
 prism_status check_status(prism_graph_t G) {
-  if ((G->last_algo == PRISM_ALGO_CELLS || G->last_algo == PRISM_ALGO_RANKS) && G->h_status && *G->h_status != 0) {
-    const uint32_t s = *G->h_status;
-    *G->h_status = 0;
-    G->recorded = 0;
-    G->rslot_dirty = true;
-    G->connected = false;  // a sharded graph must be re-prepared after an aborted replay
-    return fail((prism_status)s, "replay aborted by the device watchdog (no progress for 10 s)");
-  }
-  return PRISM_OK;
+  if (!G->h_status) return PRISM_OK;
+  const uint32_t s = G->h_status[1] ? G->h_status[1] : G->h_status[0];
+  if (s == 0) return PRISM_OK;
+  G->h_status[0] = G->h_status[1] = 0;
+  G->recorded = 0;
+  G->rslot_dirty = true;
+  G->connected = false;  // a sharded graph must be re-prepared after an aborted replay
+  cudaMemsetAsync(G->words, 0, 8, G->stream);  // stream is idle here (synchronised by the caller)
+  cudaStreamSynchronize(G->stream);
+  char b[160];
+  std::snprintf(b, sizeof b, "replay aborted by the device watchdog (no progress for %.3f s); results of the "
+                "replays since the last synchronising call are invalid", (double)G->dg.watchdog_ns * 1e-9);
+  return fail((prism_status)s, b);
 }
 
 }  // namespace
@@ -991,28 +1011,48 @@ static prism_status peak_impl(prism_graph_t G, int32_t scenario, bool time_order
   for (int s = 0; s < P.topo.pp; ++s) max_len = std::max(max_len, P.stage_len[s]);
   if (max_len > kMaxTimeOrderedOps)
     return fail(PRISM_E_INVALID_ARG, "time-ordered peak memory supports at most 4096 ops per rank");
-  if (!G->h_status && !(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status word unavailable");
-  if (!G->ensure(G->sync_words, G->sync_bytes, std::max<size_t>(G->sync_bytes, 16))) return fail(PRISM_E_OOM, "status allocation failed");
-  uint32_t *status = G->sync_words;  // word 0 (the replays re-zero their words before use)
+  uint32_t *status = G->words + 2;
   CU(cudaMemsetAsync(status, 0, 4, G->stream));
   G->rec(6);
   CU(launch_peak_time(G->cur(), G->last, G->last_Sp, G->fin, G->fin_node0, G->gfin, scenario, (int32_t)max_len,
                       peak_dev, status, G->stream));
   G->rec(7);
-  CU(cudaMemcpyAsync(G->h_status, status, 4, cudaMemcpyDeviceToHost, G->stream));
-  G->status_is_memory = true;
+  CU(cudaMemcpyAsync(G->h_status + 2, status, 4, cudaMemcpyDeviceToHost, G->stream));
   return PRISM_OK;
 }
 
+// Status of the time-ordered memory scans queued so far (after a stream synchronisation).
 static prism_status memory_status(prism_graph_t G) {
-  if (G->status_is_memory) {
-    G->status_is_memory = false;
-    if (*G->h_status == PRISM_E_NEGATIVE_MEMORY) {
-      *G->h_status = 0;
-      return fail(PRISM_E_NEGATIVE_MEMORY, "a rank's running allocation drops below zero in time order");
-    }
+  if (G->h_status && G->h_status[2] != 0) {
+    const uint32_t s = G->h_status[2];
+    G->h_status[2] = 0;
+    return fail((prism_status)s, "a rank's running allocation drops below zero in time order");
   }
   return PRISM_OK;
+}
+
+prism_status prism_sync(prism_graph_t G) {
+  if (!G) return fail(PRISM_E_INVALID_ARG, "null graph");
+  CU(cudaSetDevice(G->device));
+  CU(cudaStreamSynchronize(G->stream));
+  prism_status st = check_status(G);
+  const prism_status ms = memory_status(G);
+  return st ? st : ms;
+}
+
+prism_status prism_debug_set(prism_graph_t G, int32_t key, int64_t value) {
+  if (!G) return fail(PRISM_E_INVALID_ARG, "null graph");
+  switch (key) {
+    case PRISM_DEBUG_WATCHDOG_NS:
+      if (value < 1000) return fail(PRISM_E_INVALID_ARG, "watchdog must be >= 1 us");
+      G->dg.watchdog_ns = G->dov.watchdog_ns = (uint64_t)value;
+      return PRISM_OK;
+    case PRISM_DEBUG_STALL_UNIT:
+      if (value < -1 || value > INT32_MAX) return fail(PRISM_E_INVALID_ARG, "stall unit out of range");
+      G->dg.stall_unit = G->dov.stall_unit = (int32_t)value;
+      return PRISM_OK;
+    default: return fail(PRISM_E_INVALID_ARG, "unknown debug key");
+  }
 }
 
 prism_status prism_peak_memory_async(prism_graph_t G, int64_t *peak_dev) {

@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
                                                          int64_t *__restrict__ rank_end) {
   const int lane = threadIdx.x & 31;
   const int32_t unit = blockIdx.x * WARPS + (threadIdx.x >> 5);
-  if (unit >= a.n_units) return;
+  if (unit >= a.n_units || unit == g.stall_unit) return;  // stall_unit: watchdog test hook
   constexpr bool PAIR = C >= 4 && !PR && !MS;  // (compute, TP) pairs in one iteration
   const int32_t cells = g.pp * (g.d1 - g.d0);  // this shard's cells (all of them unsharded)
   const int32_t cell = unit % cells, chunk = a.chunk0 + unit / cells;

@@ -17,6 +17,11 @@ struct DevGraph {
   // rows f1/f3/f4: node_sdur / h_dur / node_dur / grp_dur point at per-node override arrays and
   // compute spans / chained collectives last their own rank's value (prism_set_durations)
   int32_t per_rank_dur;
+  // device watchdog of the waiting replay kernels (prism_debug_set): abort with PRISM_E_DEADLOCK
+  // after watchdog_ns without progress; stall_unit >= 0 makes that warp of the next replays
+  // return at once (test hook: forces the watchdog)
+  int32_t stall_unit;
+  uint64_t watchdog_ns;
   // row f2: multi-stream ranks (per-node stream / event fields, directional predecessors, -1 =
   // none); streams and densely renumbered event slots used by the graph
   int32_t ms, ms_streams, ms_events;
@@ -263,6 +268,12 @@ cudaError_t launch_durations(const DevGraph &g, const int64_t *base, const uint3
 cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const int64_t *fin, int32_t Sp, int32_t k,
                                  const int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
                                  cudaStream_t st);
+// Start of every waiting replay (cells / ranks): the previous replay's abort status (word 0) is
+// folded into the sticky word (1) and cleared; after an abort the ready / result slots are reset
+// to "not yet" under this replay's parity (fill), since the aborted replay left some unwritten.
+// rslot == nullptr: no reset (sharded replays: the exchange buffer is re-prepared instead).
+cudaError_t launch_replay_guard(uint32_t *words, int64_t *rslot, size_t rslot_words, int64_t *rres, size_t rres_words,
+                                int parity, cudaStream_t st);
 // eager loading of the kernels that can be launched behind a running (waiting) replay
 cudaError_t preload_replay_kernels();
 cudaError_t preload_cells();

@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(256) shard_partial_kernel(DevGraph g, int32_t 
 __global__ void __launch_bounds__(1024) shard_exchange_kernel(ShardLink L, int32_t S, int32_t Sp,
                                                               const int64_t *__restrict__ part,
                                                               int64_t *__restrict__ iter,
-                                                              uint32_t *status) {
+                                                              uint32_t *status, uint64_t watchdog_ns) {
   const int64_t slab = (int64_t)L.n * Sp;  // int64 per epoch-parity buffer
   const int64_t po = (int64_t)(L.epoch & 1) * slab + (int64_t)L.self * Sp;
   for (int m = 0; m < L.n; ++m) {
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(1024) shard_exchange_kernel(ShardLink L, int32
         uint64_t now;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
         if (t0 == 0) t0 = now;
-        if (now - t0 > 10ull * 1000 * 1000 * 1000) {
+        if (now - t0 > watchdog_ns) {
           atomicCAS(status, 0u, (uint32_t)PRISM_E_DEADLOCK);
           aborted = 1;
           break;
@@ -455,6 +455,34 @@ cudaError_t launch_tail(const DevGraph &g, const ScenParams &p, int64_t *fin, co
   }
 }
 
+// One block: word 0 = abort status of the previous waiting replay, word 1 = sticky first error
+// (reported and cleared by the host at its next synchronising call). Reading word 0, folding it
+// and clearing it happen in one block (ordered by __syncthreads), before this replay's kernel.
+__global__ void __launch_bounds__(1024) replay_guard_kernel(uint32_t *words, int64_t *rslot, size_t rslot_words,
+                                                           int64_t *rres, size_t rres_words, int64_t fill) {
+  __shared__ uint32_t s;
+  if (threadIdx.x == 0) s = words[0];
+  __syncthreads();
+  if (s == 0) return;
+  if (rslot) {
+    for (size_t i = threadIdx.x; i < rslot_words; i += blockDim.x) rslot[i] = fill;
+    for (size_t i = threadIdx.x; i < rres_words; i += blockDim.x) rres[i] = fill;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (words[1] == 0) words[1] = s;
+    words[0] = 0;
+  }
+}
+
+cudaError_t launch_replay_guard(uint32_t *words, int64_t *rslot, size_t rslot_words, int64_t *rres, size_t rres_words,
+                                int parity, cudaStream_t st) {
+  // "not yet" under the replay's parity: slots hold t (parity 0) or ~t (parity 1), valid when the
+  // decoded value is >= 0, so -1 reads "not yet" under parity 0 and 0 (~0 = -1) under parity 1
+  replay_guard_kernel<<<1, 1024, 0, st>>>(words, rslot, rslot_words, rres, rres_words, parity ? 0 : -1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_reduce(int32_t W, int32_t S, int32_t Sp, const int64_t *rank_end, int64_t *iter,
                           cudaStream_t st) {
   if (S <= 0) return cudaSuccess;
@@ -473,7 +501,7 @@ cudaError_t preload_replay_kernels() {
   cudaFuncAttributes a;
   const void *fns[] = {(const void *)reduce_iter_kernel, (const void *)shard_partial_kernel,
                        (const void *)shard_exchange_kernel, (const void *)query_kernel,
-                       (const void *)peak_time_kernel};
+                       (const void *)peak_time_kernel, (const void *)replay_guard_kernel};
   for (const void *f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
@@ -485,7 +513,7 @@ cudaError_t launch_shard_reduce(const DevGraph &g, const ShardLink &link, int32_
                                 const int64_t *rank_end, int64_t *part_local, int64_t *iter,
                                 uint32_t *status, cudaStream_t st) {
   shard_partial_kernel<<<S, 256, 0, st>>>(g, Sp, rank_end, part_local);
-  shard_exchange_kernel<<<1, 1024, 0, st>>>(link, S, Sp, part_local, iter, status);
+  shard_exchange_kernel<<<1, 1024, 0, st>>>(link, S, Sp, part_local, iter, status, g.watchdog_ns);
   return cudaGetLastError();
 }
 

@@ -159,7 +159,7 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
   if (!cell_fit_units(g, units, &ctas)) return cudaErrorCooperativeLaunchTooLarge;
   // the launch covers chunks [chunk0, chunk0 + nchunks_launch) of the replay's Sp / 32 chunks
   static const PollPolicy pol = poll_policy();
-  CellArgs a{rslot, acc, rres, arrive, status, 10ull * 1000 * 1000 * 1000, parity, (int32_t)units, Sp, chunk0,
+  CellArgs a{rslot, acc, rres, arrive, status, g.watchdog_ns, parity, (int32_t)units, Sp, chunk0,
              Sp / SC, pol.spin, pol.sleep0, pol.sleep_max, pol.fspin, pol.fsleep0, pol.fsleep_max, pol.lean, ShardLink{}};
   if (link) a.L = *link;
   DevGraph gg = g;

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(32, 16) rank_kernel(DevGraph g, ScenParams p, 
                                                      int64_t *__restrict__ gfin, int64_t *__restrict__ rank_end) {
   const int lane = threadIdx.x & 31;
   const int32_t w = blockIdx.x;
+  if (w == g.stall_unit) return;  // watchdog test hook (prism_debug_set)
   const int32_t s = w / a.warps_per_stage;
   const int32_t tpi = lane % g.tp;
   const int32_t dpi = (w % a.warps_per_stage) * a.per_warp_dp + lane / g.tp;
@@ -271,7 +272,7 @@ cudaError_t launch_ranks(const DevGraph &g, const ScenParams &p, int64_t *rslot,
   int blocks = 0;
   if (!ranks_fit(g, &blocks)) return cudaErrorCooperativeLaunchTooLarge;
   const int32_t per_warp_dp = 32 / g.tp;
-  RankArgs a{rslot, acc, rres, arrive, status, 10ull * 1000 * 1000 * 1000, parity, per_warp_dp,
+  RankArgs a{rslot, acc, rres, arrive, status, g.watchdog_ns, parity, per_warp_dp,
              (int32_t)((g.dp + per_warp_dp - 1) / per_warp_dp)};
   DevGraph gg = g;
   ScenParams pp = p;

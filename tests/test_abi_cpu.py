@@ -31,7 +31,7 @@ def test_library_exports_declared_symbols():
     for name in declared:
         assert hasattr(L, name), name
     assert set(prism.EXPORTED_SYMBOLS) == declared
-    assert L.prism_abi_version() == 3
+    assert L.prism_abi_version() == 4
     assert L.prism_status_string(5) == b"PRISM_E_DEADLOCK"
 
 

@@ -45,6 +45,7 @@ def _check_csr(P, tm):
     rank_ptr = g.export("rank_ptr")
     node_rank = g.export("node_rank")
     dur = g.export("node_dur")
+    alloc, free = g.export("node_alloc"), g.export("node_free")
     t = tm.topo
     for r in range(t.world):
         s = (r // t.tp) % t.pp if t.rank_order == 0 else r // (t.tp * t.dp)
@@ -53,7 +54,7 @@ def _check_csr(P, tm):
         assert b - a == len(tmpl)
         assert (node_rank[a:b] == r).all()
         assert (dur[a:b] == tmpl["dur_ns"]).all()
-        assert (g.export("node_alloc")[a:b] == tmpl["mem_alloc"]).all() if r == 0 else True
+        assert (alloc[a:b] == tmpl["mem_alloc"]).all() and (free[a:b] == tmpl["mem_free"]).all()
     # groups: same uid set, same members / duration / level per uid
     uid = g.export("grp_uid")
     gptr = g.export("grp_ptr")
