@@ -374,12 +374,14 @@ def f_rows_extra(args, tm, sh):
     g.close()
     c4 = w.config("C4")
     sched = moe.derive_schedule(moe.FIG3_PROFILE, 64, c4.topo.ep, seed=0)
-    md, ma, mf = moe.moe_overrides(c4, sched)
     g = prism.Graph(c4, stream=sh, profile=True)
-    g.set_durations(node_dur=md, node_alloc=ma, node_free=mf)
+    t0 = time.perf_counter()
+    g.set_moe_load(moe.op_events(c4, 64), moe.br_q16(sched))
+    moe_ms = (time.perf_counter() - t0) * 1e3
     r = timed_replay(g, g.stats()["nodes"])
     pk = g.peak_memory()
-    out["f4_moe_imbalance"] = dict(r, peak_max_bytes=int(pk.max()), workload="C4 under the Fig. 3 br profile")
+    out["f4_moe_imbalance"] = dict(r, peak_max_bytes=int(pk.max()), set_moe_load_ms=round(moe_ms, 3),
+                                   workload="C4 under the Fig. 3 br profile (prism_set_moe_load)")
     g.close()
     c2 = w.overlap_grad_reduce(w.config("C2"))
     g = prism.Graph(c2, stream=sh, profile=True)

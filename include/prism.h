@@ -290,17 +290,19 @@ PRISM_API prism_status prism_shard_adopt(prism_graph_t g, prism_graph_t from);
  * f3, what-if attribution ("a fake GPU kernel that spins for the desired and
  * optimized duration"): label overrides, per-rank compute slowdown (fault
  * injection) and the critical path (prism_critical_path).
- * f4, MoE imbalance (P:1745-1748 mock router): per-(stage, ep rank) durations and activation
- * sizes enter as node_dur / node_alloc / node_free.
+ * f4, MoE imbalance (P:1745-1748 mock router; App. F): prism_set_moe_load below.
  * Effective duration of node n (node order = rank-major, program order, as prism_query_rank):
- *   d = node_dur ? node_dur[n] : template dur_ns;  d = label_dur[i] if label(n) == labels[i];
+ *   d = node_dur ? node_dur[n] : template dur_ns;  d = (d * br) >> 16 if the node's template op is
+ *   routed (prism_set_moe_load);  d = label_dur[i] if label(n) == labels[i];
  *   d = (d * rank_slow_q16[rank(n)]) >> 16 if node n is a compute span.
  * A synchronization group lasts the max of its members' effective durations (reading Z2), and
  * scenario perturbation (prism_scenarios) applies on top. Arrays are host, copied. Applies to all
  * later replays / peak scans until reset with d == NULL (or all fields empty); invalidates the
- * recorded replay. Errors: PRISM_E_INVALID_ARG (duration outside [0, 2^40], factor outside
- * [0, 2^20], duplicate label), PRISM_E_UNKNOWN_LABEL (no node carries a label),
- * PRISM_E_NEGATIVE_MEMORY (a rank's running allocation would drop below zero). */
+ * recorded replay. Errors: PRISM_E_INVALID_ARG (duration outside [0, 2^40], memory delta outside
+ * [0, 2^43], factor outside [0, 2^20], duplicate label), PRISM_E_UNKNOWN_LABEL (no node carries a
+ * label), PRISM_E_NEGATIVE_MEMORY (a rank's running allocation would drop below zero in
+ * program order). Per-node values are validated on the device; a failed call leaves the graph's
+ * previous overrides in place. Synchronizes the stream. */
 typedef struct {
   const int64_t *node_dur;       /* [N] or NULL                                                  */
   const uint32_t *labels;        /* [n_labels] label overrides ...                               */
@@ -313,6 +315,31 @@ typedef struct {
 } prism_durations;
 
 PRISM_API prism_status prism_set_durations(prism_graph_t g, const prism_durations *d);
+
+/* Row f4, MoE imbalance: the mock router of App. F ("The br represents the ratio of the
+ * actual data volume possessed by a specific rank to the volume it would possess under a
+ * perfectly uniform distribution ... multiple gating operations occur, each requiring control
+ * via br"). Gating event v is one routing decision (one per MoE layer and microbatch, reading R7);
+ * br_q16[v * ep + e] is the balance ratio of EP rank e in event v, Q16 (65536 = the uniform share).
+ * Every node running a template op i with op_event[i] = v >= 0 on a rank with EP coordinate e
+ * processes br times the uniform volume, so (scale bits) its duration, its allocation at start and
+ * its free at finish are scaled: x' = (x * br_q16[v * ep + e]) >> 16 (floor). A routed all-to-all's
+ * members then last different times and the group lasts their max (reading Z2). Applied on top of
+ * prism_set_durations' base values (measured, else template) and before its label overrides and
+ * rank slowdown; both calls compose. m == NULL or m->n_events == 0 clears the load.
+ * Arrays are host, copied: op_event [n_ops of the templates] in [-1, n_events), br_q16
+ * [n_events][ep] in [0, 2^20]. Errors: PRISM_E_INVALID_ARG (out-of-range entries, unknown scale
+ * bits), PRISM_E_NEGATIVE_MEMORY (scaled allocations and frees that drive a rank's running
+ * allocation below zero). Invalidates the recorded replay; synchronizes the stream. */
+enum { PRISM_MOE_DUR = 1, PRISM_MOE_ALLOC = 2, PRISM_MOE_FREE = 4 };
+typedef struct {
+  const int32_t *op_event;  /* [n_ops] gating event of each template op, -1 = not routed        */
+  const int32_t *br_q16;    /* [n_events][ep] balance ratios, Q16                                */
+  int32_t n_events;
+  uint32_t scale;           /* PRISM_MOE_* bits: which of duration / alloc / free scale with br  */
+} prism_moe_load;
+
+PRISM_API prism_status prism_set_moe_load(prism_graph_t g, const prism_moe_load *m);
 
 /* Row f3: the critical path of scenario `scenario` of the last recorded replay, walked back from
  * the lowest-numbered node finishing at T: a compute span continues at its stream predecessor; a

@@ -68,6 +68,9 @@ def _load():
                                                  ctypes.c_uint64, ctypes.c_int32, ctypes.c_uint32, P,
                                                  ctypes.c_int64, P, P, ctypes.c_char_p, ctypes.c_int]
             lib.oracle_critical_path.restype = ctypes.c_int
+            lib.oracle_moe_load.argtypes = [P, P, ctypes.c_int64, P, P, P, ctypes.c_int32, ctypes.c_uint32,
+                                            P, P, P, P, P, P]
+            lib.oracle_moe_load.restype = ctypes.c_int
             lib.oracle_splitmix64.argtypes = [ctypes.c_uint64]
             lib.oracle_splitmix64.restype = ctypes.c_uint64
             lib.oracle_perturb.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32,
@@ -232,6 +235,28 @@ def whatif_durations(tm, *, node_dur=None, label_dur=None, rank_factor_q16=None)
         for i in np.nonzero(comp)[0]:  # plain loop: the definition, element by element
             d[i] = (int(d[i]) * int(f[nt["rank"][i]])) >> 16
     return d
+
+
+def moe_load(tm, op_event, br_q16, scale: int = 7, *, node_dur=None, node_alloc=None, node_free=None):
+    """Row f4 (App. F mock router; reading R7): per-node (duration, alloc, free) when
+    every op routed by gating event v on a rank with EP coordinate e processes br_q16[v, e] / 65536
+    times the uniform volume (floor; scale bits 1 duration, 2 alloc, 4 free). Base values: the given
+    per-node arrays, else the templates. Feed the result to replay(node_dur=..., ...)."""
+    lib = _load()
+    topo = _topo_buf(tm.topo)
+    ops, ptr, _ = _inputs(tm)
+    ev = np.ascontiguousarray(op_event, dtype=np.int32)
+    br = np.ascontiguousarray(br_q16, dtype=np.int32)
+    if len(ev) != len(ops) or br.ndim != 2 or br.shape[1] != tm.topo.ep:
+        raise ValueError("op_event must have one entry per template op, br_q16 shape (events, ep)")
+    N = tm.n_nodes
+    d, a, f = np.zeros(N, np.int64), np.zeros(N, np.int64), np.zeros(N, np.int64)
+    nd, na, nf = _opt64(node_dur, N), _opt64(node_alloc, N), _opt64(node_free, N)
+    s = lib.oracle_moe_load(_ptr(topo), _ptr(ops), len(ops), _ptr(ptr), _ptr(ev), _ptr(br), br.shape[0],
+                            int(scale), _ptr(nd), _ptr(na), _ptr(nf), _ptr(d), _ptr(a), _ptr(f))
+    if s:
+        raise OracleError(s, "op_event / template mismatch")
+    return d, a, f
 
 
 def slice_local_finish(tm, node_dur, slices) -> np.ndarray:

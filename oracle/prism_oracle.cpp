@@ -608,6 +608,43 @@ int oracle_critical_path(const Topo *t, const Op *ops, int64_t n_ops, const int6
   return OK;
 }
 
+// Row f4, the MoE mock router (App. F): "The br represents the ratio of the actual data
+// volume possessed by a specific rank to the volume it would possess under a perfectly uniform
+// distribution ... multiple gating operations occur, each requiring control via br". A rank whose
+// EP coordinate is e processes br[v][e] times the uniform share of gating event v's tokens, so the
+// work and the buffers of every op routed by event v on that rank scale by it (reading R7):
+// x' = floor(x * br / 65536) with br in Q16. Plain loops over ranks and their template ops, in the
+// oracle's node order (rank-major, program order); base values = the template's unless given.
+// scale bits: 1 duration, 2 allocation, 4 free.
+int oracle_moe_load(const Topo *t, const Op *ops, int64_t n_ops, const int64_t *tmpl_ptr,
+                    const int32_t *op_event, const int32_t *br_q16, int32_t n_events, uint32_t scale,
+                    const int64_t *base_dur, const int64_t *base_alloc, const int64_t *base_free,
+                    int64_t *dur_out, int64_t *alloc_out, int64_t *free_out) {
+  const int64_t W = (int64_t)t->tp * t->pp * t->dp;
+  int64_t n = 0;
+  for (int64_t r = 0; r < W; ++r) {
+    const Coords c = coords_of(*t, r);
+    for (int64_t i = tmpl_ptr[c.pp]; i < tmpl_ptr[c.pp + 1]; ++i, ++n) {
+      if (i >= n_ops) return E_INVALID_ARG;
+      int64_t d = base_dur ? base_dur[n] : ops[i].dur;
+      int64_t a = base_alloc ? base_alloc[n] : ops[i].alloc;
+      int64_t f = base_free ? base_free[n] : ops[i].free_;
+      const int32_t v = op_event[i];
+      if (v >= n_events) return E_INVALID_ARG;
+      if (v >= 0) {
+        const int64_t br = br_q16[(int64_t)v * t->ep + c.ep];  // this rank's share of event v
+        if (scale & 1) d = d * br / 65536;  // non-negative operands: division = floor
+        if (scale & 2) a = a * br / 65536;
+        if (scale & 4) f = f * br / 65536;
+      }
+      dur_out[n] = d;
+      alloc_out[n] = a;
+      free_out[n] = f;
+    }
+  }
+  return OK;
+}
+
 uint64_t oracle_splitmix64(uint64_t x) { return splitmix64(x); }
 int64_t oracle_perturb(int64_t d, uint64_t uid, int32_t k, uint64_t seed, int32_t amp) {
   return perturb(d, uid, k, seed, amp);

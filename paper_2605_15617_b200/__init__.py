@@ -26,7 +26,7 @@ EXPORTED_SYMBOLS = [
     "prism_debug_export", "prism_plan", "prism_last_timing", "prism_last_algo",
     "prism_shard_prepare", "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
     "prism_set_durations", "prism_critical_path", "prism_peak_memory_at", "prism_sync",
-    "prism_debug_set",
+    "prism_debug_set", "prism_set_moe_load",
 ]
 SHARD_HANDLE_BYTES = 64
 
@@ -64,6 +64,14 @@ class _Scenarios(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("amp_q16", ctypes.c_int32), ("seed", ctypes.c_uint64),
                 ("kind_mask", ctypes.c_uint32), ("record", ctypes.c_int32), ("algo", ctypes.c_int32),
                 ("first", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class _MoeLoad(ctypes.Structure):
+    _fields_ = [("op_event", ctypes.c_void_p), ("br_q16", ctypes.c_void_p), ("n_events", ctypes.c_int32),
+                ("scale", ctypes.c_uint32)]
+
+
+MOE_DUR, MOE_ALLOC, MOE_FREE = 1, 2, 4
 
 
 class _Durations(ctypes.Structure):
@@ -120,6 +128,7 @@ def lib():
         L.prism_peak_memory_at.argtypes = [P, ctypes.c_int32, P]
         L.prism_critical_path.argtypes = [P, ctypes.c_int32, P, ctypes.c_int64, P, P]
         L.prism_sync.argtypes = [P]
+        L.prism_set_moe_load.argtypes = [P, P]
         L.prism_debug_set.argtypes = [P, ctypes.c_int32, ctypes.c_int64]
         for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
                      "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
@@ -127,7 +136,7 @@ def lib():
                      "prism_last_timing", "prism_last_algo", "prism_shard_prepare",
                      "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
                      "prism_set_durations", "prism_critical_path", "prism_peak_memory_at",
-                     "prism_sync", "prism_debug_set"):
+                     "prism_sync", "prism_debug_set", "prism_set_moe_load"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
     return _lib
@@ -328,6 +337,19 @@ class Graph:
                        arr(ld, np.int64) if len(ld) else None, len(labs), 0, arr(rank_slow_q16, np.int32),
                        arr(node_alloc, np.int64), arr(node_free, np.int64))
         _check(lib().prism_set_durations(self._h, ctypes.byref(d)))
+
+    def set_moe_load(self, op_event=None, br_q16=None, scale: int = MOE_DUR | MOE_ALLOC | MOE_FREE) -> None:
+        """Row f4 (prism_set_moe_load): op_event[n_ops] = gating event of each template op (-1 = not
+        routed), br_q16[n_events, ep] = balance ratios in Q16; None clears the load."""
+        if op_event is None:
+            _check(lib().prism_set_moe_load(self._h, None))
+            return
+        ev = np.ascontiguousarray(op_event, dtype=np.int32)
+        br = np.ascontiguousarray(br_q16, dtype=np.int32)
+        if br.ndim != 2 or br.shape[1] != self.topo.ep:
+            raise ValueError("br_q16 must have shape (n_events, ep)")
+        m = _MoeLoad(ev.ctypes.data, br.ctypes.data, br.shape[0], int(scale))
+        _check(lib().prism_set_moe_load(self._h, ctypes.byref(m)))
 
     def critical_path(self, scenario: int = 0):
         """(path [node ids, last first], T) of one scenario of the last recorded replay."""

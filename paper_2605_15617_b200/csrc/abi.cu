@@ -271,8 +271,7 @@ struct prism_graph_s {
   int64_t launches = 0;
   bool oom = false;
   std::vector<unsigned char> staging;  // packed host tables of the build upload
-  std::vector<uint32_t> tmpl_labels;     // template labels / memory deltas (override validation)
-  std::vector<int64_t> tmpl_alloc, tmpl_free;
+  std::vector<uint32_t> tmpl_labels;     // template labels (label-override validation)
   // profiling events: 0/1 expand, 2/3 levels, 4 tail end, 5 reduce end, 6/7 peak
   bool profile = false;
   cudaEvent_t ev[8] = {};
@@ -284,11 +283,17 @@ struct prism_graph_s {
     }
   }
 
-  // rows f1/f3/f4: per-node duration / memory overrides (prism_set_durations)
+  // rows f1/f3/f4: per-node duration / memory overrides. The inputs of prism_set_durations (din)
+  // and prism_set_moe_load (moe) are kept on the device; the derived arrays (ov) are recomputed
+  // from both whenever either changes, and the replay reads them through dov's pointers.
   bool ov_active = false;
   DevGraph dov{};
   unsigned char *ov = nullptr;
-  size_t ov_bytes = 0;
+  DurIn din{};
+  bool din_any = false;
+  unsigned char *din_blk = nullptr;
+  MoeIn moe{};
+  unsigned char *moe_blk = nullptr;
   const DevGraph &cur() const { return ov_active ? dov : dg; }
   // critical-path scratch
   int32_t *crit = nullptr;
@@ -343,6 +348,8 @@ struct prism_graph_s {
     dfree(sync_words);
     dfree(part);
     dfree(ov);
+    dfree(din_blk);
+    dfree(moe_blk);
     dfree(crit);
     trace("destroy: buffers freed");
     if (h_status) {  // returned to the pool once the stream has passed its pending status copy
@@ -453,13 +460,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   G->plan = std::move(plan);
   const Plan &P = G->plan;
   G->tmpl_labels.resize(tmpl->n_ops);
-  G->tmpl_alloc.resize(tmpl->n_ops);
-  G->tmpl_free.resize(tmpl->n_ops);
-  for (int64_t i = 0; i < tmpl->n_ops; ++i) {
-    G->tmpl_labels[i] = tmpl->ops[i].label;
-    G->tmpl_alloc[i] = tmpl->ops[i].mem_alloc;
-    G->tmpl_free[i] = tmpl->ops[i].mem_free;
-  }
+  for (int64_t i = 0; i < tmpl->n_ops; ++i) G->tmpl_labels[i] = tmpl->ops[i].label;
   DevGraph &d = G->dg;
   d.W = (int32_t)P.W;
   d.pp = P.topo.pp;
@@ -1126,24 +1127,99 @@ prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, i
 
 // ---- rows f1 / f3 / f4: per-node durations and memory deltas, critical path ---------------
 
+}  // extern "C"
+
+namespace {
+
+// Layout helper of the override blocks (256-byte aligned arrays in one allocation).
+struct Carve {
+  size_t off = 0;
+  size_t operator()(size_t bytes) {
+    off = (off + 255) & ~(size_t)255;
+    const size_t o = off;
+    off += std::max<size_t>(bytes, 8);
+    return o;
+  }
+};
+
+// Recomputes the derived per-node arrays from the set_durations inputs `din` and the MoE load `me`
+// into a new block; on success it replaces the graph's block (stream-ordered free of the old one,
+// which earlier replays may still read), else the graph keeps its previous overrides.
+prism_status apply_overrides(prism_graph_t G, const DurIn &din, bool din_any, const MoeIn &me) {
+  const Plan &P = G->plan;
+  if (!din_any && me.n_events == 0) {
+    G->ov_active = false;
+    G->recorded = 0;
+    return PRISM_OK;
+  }
+  const int64_t N = P.N, Gn = P.G, M = P.M;
+  const bool mem = din.al || din.fr || (me.n_events > 0 && (me.scale & (PRISM_MOE_ALLOC | PRISM_MOE_FREE)));
+  Carve c;
+  const size_t o_eff = c(N * 8), o_gd = c(Gn * 8), o_sd = c(N * 8), o_hd = c(M * 8);
+  const size_t o_al = mem ? c(N * 8) : 0, o_fr = mem ? c(N * 8) : 0;
+  unsigned char *B = (unsigned char *)G->dalloc(c.off);
+  if (!B) return fail(PRISM_E_OOM, "duration override allocation failed");
+  cudaStream_t st = G->stream;
+  int64_t *eff = (int64_t *)(B + o_eff), *gdur = (int64_t *)(B + o_gd), *sdur = (int64_t *)(B + o_sd);
+  int64_t *hdur = (int64_t *)(B + o_hd);
+  int64_t *eal = mem ? (int64_t *)(B + o_al) : nullptr, *efr = mem ? (int64_t *)(B + o_fr) : nullptr;
+  uint32_t *status = G->words + 3;
+  cudaError_t e = cudaMemsetAsync(status, 0, 4, st);
+  if (e == cudaSuccess) e = launch_durations(G->dg, din, me, eff, eal, efr, gdur, sdur, hdur, status, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(G->h_status + 3, status, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    G->dfree(B);
+    return fail(PRISM_E_CUDA, std::string("override kernels: ") + cudaGetErrorString(e));
+  }
+  const uint32_t bad = G->h_status[3];
+  if (bad) {
+    G->dfree(B);
+    return fail((prism_status)bad, bad == PRISM_E_NEGATIVE_MEMORY
+                                       ? "a rank's running allocation drops below zero (program order)"
+                                       : "a per-node duration / memory delta is out of range (duration [0, 2^40], "
+                                         "memory [0, 2^43])");
+  }
+  G->dfree(G->ov);
+  G->ov = B;
+  DevGraph &dv = G->dov;
+  dv = G->dg;
+  dv.node_dur = eff;
+  dv.grp_dur = gdur;
+  dv.node_sdur = sdur;
+  dv.h_dur = hdur;
+  if (mem) {
+    dv.node_alloc = eal;
+    dv.node_free = efr;
+  }
+  dv.per_rank_dur = 1;
+  G->ov_active = true;
+  G->recorded = 0;
+  return PRISM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 prism_status prism_set_durations(prism_graph_t G, const prism_durations *d) {
   if (!G) return fail(PRISM_E_INVALID_ARG, "null graph");
   CU(cudaSetDevice(G->device));
   const Plan &P = G->plan;
-  G->recorded = 0;
   const bool any = d && (d->node_dur || d->n_labels > 0 || d->rank_slow_q16 || d->node_alloc || d->node_free);
   if (!any) {
-    G->ov_active = false;
+    prism_status st = apply_overrides(G, DurIn{}, false, G->moe);
+    if (st) return st;
+    G->dfree(G->din_blk);
+    G->din_blk = nullptr;
+    G->din = DurIn{};
+    G->din_any = false;
     return PRISM_OK;
   }
-  const int64_t N = P.N, W = P.W, Gn = P.G, M = P.M;
+  const int64_t N = P.N, W = P.W;
   if (d->n_labels < 0 || (d->n_labels > 0 && (!d->labels || !d->label_dur)))
     return fail(PRISM_E_INVALID_ARG, "label overrides: n_labels >= 0 with both arrays");
-  // host validation (the device never sees a malformed override)
-  if (d->node_dur)
-    for (int64_t n = 0; n < N; ++n)
-      if (d->node_dur[n] < 0 || d->node_dur[n] > (1LL << 40))
-        return fail(PRISM_E_INVALID_ARG, "node_dur[" + std::to_string(n) + "] outside [0, 2^40]");
+  // host validation of the small inputs (per-node arrays are checked on the device)
   std::vector<std::pair<uint32_t, int64_t>> lab;
   if (d->n_labels > 0) {
     std::vector<uint32_t> have;
@@ -1168,41 +1244,13 @@ prism_status prism_set_durations(prism_graph_t G, const prism_durations *d) {
     for (int64_t r = 0; r < W; ++r)
       if (d->rank_slow_q16[r] < 0 || d->rank_slow_q16[r] > (1 << 20))
         return fail(PRISM_E_INVALID_ARG, "rank_slow_q16 outside [0, 2^20] (a factor of at most 16)");
-  if (d->node_alloc || d->node_free) {  // running allocation of every rank never negative
-    std::vector<int64_t> rank_len(W);
-    for (int64_t r = 0; r < W; ++r) {
-      const int64_t s = P.topo.order == PRISM_ORDER_MEGATRON ? r / ((int64_t)P.topo.tp * P.topo.dp) : (r / P.topo.tp) % P.topo.pp;
-      rank_len[r] = P.stage_len[s];
-    }
-    int64_t n = 0;
-    for (int64_t r = 0; r < W; ++r) {
-      int64_t run = 0;
-      for (int64_t i = 0; i < rank_len[r]; ++i, ++n) {
-        const int64_t s = P.topo.order == PRISM_ORDER_MEGATRON ? r / ((int64_t)P.topo.tp * P.topo.dp) : (r / P.topo.tp) % P.topo.pp;
-        const int64_t a = d->node_alloc ? d->node_alloc[n] : G->tmpl_alloc[P.stage_op0[s] + i];
-        const int64_t f = d->node_free ? d->node_free[n] : G->tmpl_free[P.stage_op0[s] + i];
-        if (a < 0 || f < 0) return fail(PRISM_E_INVALID_ARG, "negative memory delta");
-        run += a - f;
-        if (run < 0) return fail(PRISM_E_NEGATIVE_MEMORY, "running allocation of rank " + std::to_string(r) + " drops below zero");
-      }
-    }
-  }
-  // one device block: inputs + derived arrays
-  size_t off = 0;
-  auto carve = [&off](size_t bytes) {
-    off = (off + 255) & ~(size_t)255;
-    const size_t o = off;
-    off += std::max<size_t>(bytes, 8);
-    return o;
-  };
   const size_t L = lab.size();
-  const size_t o_base = d->node_dur ? carve(N * 8) : 0, o_lab = carve(L * 4), o_ldur = carve(L * 8);
-  const size_t o_rf = d->rank_slow_q16 ? carve(W * 4) : 0;
-  const size_t o_al = d->node_alloc ? carve(N * 8) : 0, o_fr = d->node_free ? carve(N * 8) : 0;
-  const size_t o_eff = carve(N * 8), o_gd = carve(Gn * 8), o_sd = carve(N * 8), o_hd = carve(M * 8);
-  const size_t total = off;
-  if (!G->ensure(G->ov, G->ov_bytes, total)) return fail(PRISM_E_OOM, "duration override allocation failed");
-  unsigned char *B = G->ov;
+  Carve c;
+  const size_t o_base = d->node_dur ? c(N * 8) : 0, o_lab = c(L * 4), o_ldur = c(L * 8);
+  const size_t o_rf = d->rank_slow_q16 ? c(W * 4) : 0;
+  const size_t o_al = d->node_alloc ? c(N * 8) : 0, o_fr = d->node_free ? c(N * 8) : 0;
+  unsigned char *B = (unsigned char *)G->dalloc(c.off);
+  if (!B) return fail(PRISM_E_OOM, "duration override allocation failed");
   cudaStream_t st = G->stream;
   std::vector<uint32_t> hl(L);
   std::vector<int64_t> hd(L);
@@ -1210,29 +1258,82 @@ prism_status prism_set_durations(prism_graph_t G, const prism_durations *d) {
     hl[i] = lab[i].first;
     hd[i] = lab[i].second;
   }
-  if (d->node_dur) CU(cudaMemcpyAsync(B + o_base, d->node_dur, N * 8, cudaMemcpyHostToDevice, st));
-  if (L) {
-    CU(cudaMemcpyAsync(B + o_lab, hl.data(), L * 4, cudaMemcpyHostToDevice, st));
-    CU(cudaMemcpyAsync(B + o_ldur, hd.data(), L * 8, cudaMemcpyHostToDevice, st));
+  cudaError_t e = cudaSuccess;
+  auto up = [&](size_t o, const void *src, size_t bytes) {
+    if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(B + o, src, bytes, cudaMemcpyHostToDevice, st);
+  };
+  if (d->node_dur) up(o_base, d->node_dur, N * 8);
+  up(o_lab, hl.data(), L * 4);
+  up(o_ldur, hd.data(), L * 8);
+  if (d->rank_slow_q16) up(o_rf, d->rank_slow_q16, W * 4);
+  if (d->node_alloc) up(o_al, d->node_alloc, N * 8);
+  if (d->node_free) up(o_fr, d->node_free, N * 8);
+  if (e != cudaSuccess) {
+    G->dfree(B);
+    return fail(PRISM_E_CUDA, cudaGetErrorString(e));
   }
-  if (d->rank_slow_q16) CU(cudaMemcpyAsync(B + o_rf, d->rank_slow_q16, W * 4, cudaMemcpyHostToDevice, st));
-  if (d->node_alloc) CU(cudaMemcpyAsync(B + o_al, d->node_alloc, N * 8, cudaMemcpyHostToDevice, st));
-  if (d->node_free) CU(cudaMemcpyAsync(B + o_fr, d->node_free, N * 8, cudaMemcpyHostToDevice, st));
-  DevGraph &dv = G->dov;
-  dv = G->dg;
-  int64_t *eff = (int64_t *)(B + o_eff), *gdur = (int64_t *)(B + o_gd), *sdur = (int64_t *)(B + o_sd), *hdur = (int64_t *)(B + o_hd);
-  CU(launch_durations(G->dg, d->node_dur ? (const int64_t *)(B + o_base) : nullptr, (const uint32_t *)(B + o_lab),
-                      (const int64_t *)(B + o_ldur), (int32_t)L, d->rank_slow_q16 ? (const int32_t *)(B + o_rf) : nullptr,
-                      eff, gdur, sdur, hdur, st));
-  dv.node_dur = eff;
-  dv.grp_dur = gdur;
-  dv.node_sdur = sdur;
-  dv.h_dur = hdur;
-  if (d->node_alloc) dv.node_alloc = (int64_t *)(B + o_al);
-  if (d->node_free) dv.node_free = (int64_t *)(B + o_fr);
-  dv.per_rank_dur = 1;
-  CU(cudaStreamSynchronize(st));  // the caller's host arrays may go away
-  G->ov_active = true;
+  DurIn in{};
+  in.base = d->node_dur ? (const int64_t *)(B + o_base) : nullptr;
+  in.labels = (const uint32_t *)(B + o_lab);
+  in.label_dur = (const int64_t *)(B + o_ldur);
+  in.n_labels = (int32_t)L;
+  in.rank_f = d->rank_slow_q16 ? (const int32_t *)(B + o_rf) : nullptr;
+  in.al = d->node_alloc ? (const int64_t *)(B + o_al) : nullptr;
+  in.fr = d->node_free ? (const int64_t *)(B + o_fr) : nullptr;
+  prism_status s2 = apply_overrides(G, in, true, G->moe);  // synchronizes: the host arrays may go away
+  if (s2) {
+    G->dfree(B);
+    return s2;
+  }
+  G->dfree(G->din_blk);
+  G->din_blk = B;
+  G->din = in;
+  G->din_any = true;
+  return PRISM_OK;
+}
+
+prism_status prism_set_moe_load(prism_graph_t G, const prism_moe_load *m) {
+  if (!G) return fail(PRISM_E_INVALID_ARG, "null graph");
+  CU(cudaSetDevice(G->device));
+  const Plan &P = G->plan;
+  if (!m || m->n_events == 0) {
+    prism_status st = apply_overrides(G, G->din, G->din_any, MoeIn{});
+    if (st) return st;
+    G->dfree(G->moe_blk);
+    G->moe_blk = nullptr;
+    G->moe = MoeIn{};
+    return PRISM_OK;
+  }
+  if (m->n_events < 0 || !m->op_event || !m->br_q16) return fail(PRISM_E_INVALID_ARG, "MoE load: n_events >= 0 with both arrays");
+  if (m->scale & ~(uint32_t)(PRISM_MOE_DUR | PRISM_MOE_ALLOC | PRISM_MOE_FREE))
+    return fail(PRISM_E_INVALID_ARG, "MoE load: unknown scale bits");
+  const int64_t nops = (int64_t)G->tmpl_labels.size(), ep = P.topo.ep;
+  for (int64_t i = 0; i < nops; ++i)
+    if (m->op_event[i] < -1 || m->op_event[i] >= m->n_events)
+      return fail(PRISM_E_INVALID_ARG, "op_event[" + std::to_string(i) + "] outside [-1, n_events)");
+  const int64_t nbr = (int64_t)m->n_events * ep;
+  for (int64_t i = 0; i < nbr; ++i)
+    if (m->br_q16[i] < 0 || m->br_q16[i] > (1 << 20))
+      return fail(PRISM_E_INVALID_ARG, "br_q16[" + std::to_string(i) + "] outside [0, 2^20]");
+  Carve c;
+  const size_t o_ev = c(nops * 4), o_br = c(nbr * 4);
+  unsigned char *B = (unsigned char *)G->dalloc(c.off);
+  if (!B) return fail(PRISM_E_OOM, "MoE load allocation failed");
+  cudaError_t e = cudaMemcpyAsync(B + o_ev, m->op_event, nops * 4, cudaMemcpyHostToDevice, G->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(B + o_br, m->br_q16, nbr * 4, cudaMemcpyHostToDevice, G->stream);
+  if (e != cudaSuccess) {
+    G->dfree(B);
+    return fail(PRISM_E_CUDA, cudaGetErrorString(e));
+  }
+  MoeIn me{(const int32_t *)(B + o_ev), (const int32_t *)(B + o_br), m->n_events, m->scale};
+  prism_status st = apply_overrides(G, G->din, G->din_any, me);
+  if (st) {
+    G->dfree(B);
+    return st;
+  }
+  G->dfree(G->moe_blk);
+  G->moe_blk = B;
+  G->moe = me;
   return PRISM_OK;
 }
 

@@ -364,7 +364,7 @@ cudaError_t launch_expand(const DevGraph &g, cudaStream_t st) {
   rank_tables_kernel<<<1, 1024, 0, st>>>(g);
   if (g.N > 0) {
     const int64_t batches = (int64_t)g.pp * ((g.W / g.pp + kRanksPerBlock - 1) / kRanksPerBlock);
-    const int blocks = (int)std::min<int64_t>(batches, 148 * 16);
+    const int blocks = (int)std::min<int64_t>(batches, num_sms() * 16);
     expand_nodes_kernel<<<blocks, 256, 0, st>>>(g);
   }
   if (g.M > 0 && g.nchunk > 0) build_groups_kernel<<<g.nchunk, 256, 0, st>>>(g);

@@ -261,10 +261,27 @@ cudaError_t launch_ranks(const DevGraph &g, const ScenParams &p, int64_t *rslot,
                          int64_t *rank_end, cudaStream_t st);
 // memory.cu
 cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st);
-// whatif.cu (rows f1/f3/f4)
-cudaError_t launch_durations(const DevGraph &g, const int64_t *base, const uint32_t *labels, const int64_t *label_dur,
-                             int32_t n_labels, const int32_t *rank_f, int64_t *eff, int64_t *gdur, int64_t *sdur,
-                             int64_t *hdur, cudaStream_t st);
+// whatif.cu (rows f1/f3/f4): device copies of prism_set_durations' inputs ...
+struct DurIn {
+  const int64_t *base;       // [N] measured durations or nullptr (template)
+  const uint32_t *labels;    // [n_labels] sorted
+  const int64_t *label_dur;  // [n_labels]
+  int32_t n_labels;
+  const int32_t *rank_f;     // [W] Q16 compute slowdown or nullptr
+  const int64_t *al, *fr;    // [N] memory deltas or nullptr (template)
+};
+// ... and of prism_set_moe_load's (n_events == 0: no MoE load)
+struct MoeIn {
+  const int32_t *op_event;   // [n_ops] gating event of each template op, -1 = not routed
+  const int32_t *br;         // [n_events][ep] Q16
+  int32_t n_events;
+  uint32_t scale;            // PRISM_MOE_DUR | _ALLOC | _FREE
+};
+// effective durations (eff), memory deltas (eal / efr, nullptr = unchanged), group durations and
+// the replay records; *status = first invalid input (PRISM_E_INVALID_ARG / _NEGATIVE_MEMORY)
+cudaError_t launch_durations(const DevGraph &g, const DurIn &in, const MoeIn &me, int64_t *eff, int64_t *eal,
+                             int64_t *efr, int64_t *gdur, int64_t *sdur, int64_t *hdur, uint32_t *status,
+                             cudaStream_t st);
 cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const int64_t *fin, int32_t Sp, int32_t k,
                                  const int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
                                  cudaStream_t st);
@@ -274,6 +291,8 @@ cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const i
 // rslot == nullptr: no reset (sharded replays: the exchange buffer is re-prepared instead).
 cudaError_t launch_replay_guard(uint32_t *words, int64_t *rslot, size_t rslot_words, int64_t *rres, size_t rres_words,
                                 int parity, cudaStream_t st);
+// SM count of the current device (grid sizing; cached per device)
+int num_sms();
 // eager loading of the kernels that can be launched behind a running (waiting) replay
 cudaError_t preload_replay_kernels();
 cudaError_t preload_cells();

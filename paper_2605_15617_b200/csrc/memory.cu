@@ -54,7 +54,7 @@ cudaError_t preload_peak_kernel() {
 cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st) {
   if (g.W == 0) return cudaSuccess;
   int blocks = (g.W + 7) / 8;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
   peak_kernel<<<blocks, 256, 0, st>>>(g, peak);
   return cudaGetLastError();
 }

@@ -483,6 +483,18 @@ cudaError_t launch_replay_guard(uint32_t *words, int64_t *rslot, size_t rslot_wo
   return cudaGetLastError();
 }
 
+int num_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (cache[dev] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
 cudaError_t launch_reduce(int32_t W, int32_t S, int32_t Sp, const int64_t *rank_end, int64_t *iter,
                           cudaStream_t st) {
   if (S <= 0) return cudaSuccess;
@@ -526,7 +538,7 @@ cudaError_t launch_peak_time(const DevGraph &g, const ScenParams &p, int32_t Sp,
   cudaError_t e = cudaFuncSetAttribute(peak_time_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int threads = cap >= 1024 ? 1024 : (cap < 32 ? 32 : cap);  // whole warps (shuffle scans)
-  peak_time_kernel<<<g.W < 148 * 2 ? g.W : 148 * 2, threads, smem, st>>>(g, p, Sp, fin, node0, gfin, k, cap, peak, status);
+  peak_time_kernel<<<g.W < num_sms() * 2 ? g.W : num_sms() * 2, threads, smem, st>>>(g, p, Sp, fin, node0, gfin, k, cap, peak, status);
   return cudaGetLastError();
 }
 

@@ -24,29 +24,81 @@ namespace {
 constexpr uint64_t K_GOLD = 0x9E3779B97F4A7C15ULL;
 constexpr uint64_t K_MIX = 0xBF58476D1CE4E5B9ULL;
 
-// Effective per-node durations. labels/label_dur sorted by label (binary search).
-__global__ void __launch_bounds__(256) eff_kernel(DevGraph g, const int64_t *__restrict__ base,
-                                                  const uint32_t *__restrict__ labels,
-                                                  const int64_t *__restrict__ label_dur, int32_t n_labels,
-                                                  const int32_t *__restrict__ rank_f, int64_t *__restrict__ eff) {
+// Effective per-node durations and memory deltas (rows f1/f3/f4), one thread per node n of rank r
+// running template op ti of its stage:
+//   d = measured (in.base[n]) else template;  d = (d * br) >> 16 if op ti is routed by gating event
+//   v (MoE mock router: br[v][ep_i(r)] = the rank's share of event v's tokens
+//   relative to the uniform share, Q16);  d = label_dur[i] if label(n) == labels[i];
+//   d = (d * rank_f[r]) >> 16 for compute spans (fault injection).
+//   alloc / free = given (in.al / in.fr) else template, then scaled by br like d (scale bits).
+// Out-of-range inputs set *status (validation runs here, not in an O(N) host loop).
+__global__ void __launch_bounds__(256) eff_kernel(DevGraph g, DurIn in, MoeIn me, int64_t *__restrict__ eff,
+                                                  int64_t *__restrict__ eal, int64_t *__restrict__ efr,
+                                                  uint32_t *status) {
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N; n += (int64_t)gridDim.x * blockDim.x) {
-    int64_t d = base ? base[n] : g.node_dur[n];
-    if (n_labels > 0) {
+    int64_t d = in.base ? in.base[n] : g.node_dur[n];
+    if (d < 0 || d > (1LL << 40)) atomicCAS(status, 0u, (uint32_t)PRISM_E_INVALID_ARG);
+    const int32_t r = g.node_rank[n];
+    int32_t b = 65536;  // br of the node's gating event on its EP rank (Q16), 1.0 if not routed
+    if (me.n_events > 0) {
+      const int32_t s = g.rank_stage[r];
+      const int64_t ti = g.t_op0[s] + (n - g.rank_ptr[r]);
+      const int32_t v = me.op_event[ti];
+      if (v >= 0) {
+        const int32_t dpi = g.order == PRISM_ORDER_MEGATRON ? (r / g.tp) % g.dp : r / (g.tp * g.pp);
+        b = me.br[(int64_t)v * g.ep + dpi % g.ep];
+      }
+    }
+    if (me.scale & PRISM_MOE_DUR) d = (d * (int64_t)b) >> 16;
+    if (in.n_labels > 0) {
       const uint32_t L = g.node_label[n];
-      int32_t lo = 0, hi = n_labels - 1;
+      int32_t lo = 0, hi = in.n_labels - 1;
       while (lo <= hi) {
         const int32_t mid = (lo + hi) >> 1;
-        const uint32_t v = labels[mid];
+        const uint32_t v = in.labels[mid];
         if (v == L) {
-          d = label_dur[mid];
+          d = in.label_dur[mid];
           break;
         }
         if (v < L) lo = mid + 1;
         else hi = mid - 1;
       }
     }
-    if (rank_f && g.node_kind[n] == PRISM_KIND_COMPUTE) d = (d * (int64_t)rank_f[g.node_rank[n]]) >> 16;
+    if (in.rank_f && g.node_kind[n] == PRISM_KIND_COMPUTE) d = (d * (int64_t)in.rank_f[r]) >> 16;
     eff[n] = d;
+    if (eal) {
+      int64_t a = in.al ? in.al[n] : g.node_alloc[n], f = in.fr ? in.fr[n] : g.node_free[n];
+      if (a < 0 || f < 0 || a > (1LL << 43) || f > (1LL << 43)) atomicCAS(status, 0u, (uint32_t)PRISM_E_INVALID_ARG);
+      if (me.scale & PRISM_MOE_ALLOC) a = (a * (int64_t)b) >> 16;
+      if (me.scale & PRISM_MOE_FREE) f = (f * (int64_t)b) >> 16;
+      eal[n] = a;
+      efr[n] = f;
+    }
+  }
+}
+
+// The running allocation of every rank never drops below zero (program order, reading Z6): one
+// warp per rank, 64-bit warp scan of (alloc - free) with the running minimum per lane.
+__global__ void __launch_bounds__(256) mem_check_kernel(DevGraph g, const int64_t *__restrict__ al,
+                                                        const int64_t *__restrict__ fr, uint32_t *status) {
+  const int lane = threadIdx.x & 31;
+  const int32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (int32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < g.W; r += warps) {
+    const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
+    int64_t carry = 0;
+    bool neg = false;
+    for (int32_t base = rb; base < re; base += 32) {
+      const int32_t i = base + lane;
+      int64_t x = i < re ? al[i] - fr[i] : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      neg |= i < re && carry + x < 0;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (__any_sync(0xffffffffu, neg) && lane == 0) atomicCAS(status, 0u, (uint32_t)PRISM_E_NEGATIVE_MEMORY);
   }
 }
 
@@ -165,11 +217,12 @@ __global__ void __launch_bounds__(32) crit_walk_kernel(DevGraph g, ScenParams p,
 
 }  // namespace
 
-cudaError_t launch_durations(const DevGraph &g, const int64_t *base, const uint32_t *labels, const int64_t *label_dur,
-                             int32_t n_labels, const int32_t *rank_f, int64_t *eff, int64_t *gdur, int64_t *sdur,
-                             int64_t *hdur, cudaStream_t st) {
-  const int blocks = 148 * 8;
-  if (g.N > 0) eff_kernel<<<blocks, 256, 0, st>>>(g, base, labels, label_dur, n_labels, rank_f, eff);
+cudaError_t launch_durations(const DevGraph &g, const DurIn &in, const MoeIn &me, int64_t *eff, int64_t *eal,
+                             int64_t *efr, int64_t *gdur, int64_t *sdur, int64_t *hdur, uint32_t *status,
+                             cudaStream_t st) {
+  const int blocks = num_sms() * 8;
+  if (g.N > 0) eff_kernel<<<blocks, 256, 0, st>>>(g, in, me, eff, eal, efr, status);
+  if (eal && g.W > 0) mem_check_kernel<<<blocks, 256, 0, st>>>(g, eal, efr, status);
   if (g.G > 0) grp_dur_kernel<<<blocks, 256, 0, st>>>(g, eff, gdur);
   if (g.N > 0 || g.M > 0) records_kernel<<<blocks, 256, 0, st>>>(g, eff, gdur, sdur, hdur);
   return cudaGetLastError();
@@ -180,7 +233,7 @@ cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const i
                                  cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(scratch, 0x7F, 4, st);
   if (e != cudaSuccess) return e;
-  if (g.N > 0) crit_start_kernel<<<148 * 4, 256, 0, st>>>(g, fin, Sp, k, iter, scratch);
+  if (g.N > 0) crit_start_kernel<<<num_sms() * 4, 256, 0, st>>>(g, fin, Sp, k, iter, scratch);
   crit_walk_kernel<<<1, 32, 0, st>>>(g, p, fin, Sp, k, scratch, path, cap, len_out);
   return cudaGetLastError();
 }

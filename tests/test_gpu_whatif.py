@@ -107,11 +107,10 @@ def test_whatif_labels_and_fault_injection(prism):
     assert e.value.name == "PRISM_E_UNKNOWN_LABEL"
 
 
-def test_moe_memory_deltas(prism):
-    """f4 shape: per-node activation sizes scaled per EP rank; peaks equal the oracle's and a
-    running total below zero is refused."""
+def test_memory_deltas(prism):
+    """Per-node activation sizes scaled per rank; peaks equal the oracle's and a running total below
+    zero is refused (device-side validation) with the previous overrides kept."""
     tm = w.scaled("C4")
-    nt = oracle.node_table(tm)
     ex_alloc = np.zeros(tm.n_nodes, np.int64)
     ex_free = np.zeros(tm.n_nodes, np.int64)
     # rebuild alloc/free from the templates, scaled by (1 + rank % 3) / 2 per rank
@@ -124,13 +123,18 @@ def test_moe_memory_deltas(prism):
         ex_alloc[n:n + len(T)] = T["mem_alloc"] * k // 2
         ex_free[n:n + len(T)] = T["mem_free"] * k // 2
         n += len(T)
-    _check(prism, tm, 16, None, node_alloc=ex_alloc, node_free=ex_free, times=False)
-    g = _graph(prism, tm)
+    g, ref = _check(prism, tm, 16, None, node_alloc=ex_alloc, node_free=ex_free, times=False)
     bad = ex_free.copy()
     bad[np.argmax(bad)] += 1 << 40
     with pytest.raises(prism.PrismError) as e:
         g.set_durations(node_alloc=ex_alloc, node_free=bad)
     assert e.value.name == "PRISM_E_NEGATIVE_MEMORY"
+    assert np.array_equal(g.peak_memory(), ref["peak"][0])  # the previous overrides stand
+    neg = ex_alloc.copy()
+    neg[3] = -1
+    with pytest.raises(prism.PrismError) as e:
+        g.set_durations(node_alloc=neg, node_free=ex_free)
+    assert e.value.name == "PRISM_E_INVALID_ARG"
 
 
 @pytest.mark.parametrize("seed", range(20))
@@ -158,15 +162,106 @@ def test_critical_path_configs(prism, name):
         assert T == rT and np.array_equal(path, rpath), (name, k, len(path), len(rpath))
 
 
-@pytest.mark.parametrize("seed", range(3))
-def test_moe_imbalance_fig3(prism, seed):
-    """f4: the Fig. 3 br profile on the C4-shaped MoE graph: per-node expert / A2A
-    durations and activation sizes; iteration times and every rank's peak equal the oracle's."""
+def _moe_inputs(tm, seed, events=32):
     import workloads.moe as M
 
+    s = M.derive_schedule(M.FIG3_PROFILE, events, tm.topo.ep, seed=seed)
+    return M.op_events(tm, events), M.br_q16(s)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_moe_imbalance_fig3(prism, seed):
+    """f4 (App. F mock router): the Fig. 3 br profile on the C4-shaped MoE
+    graph through prism_set_moe_load, against the oracle's own plain-loop br scaling
+    (oracle.moe_load) replayed by the DES: iteration times, per-op times, every rank's peak."""
     tm = w.scaled("C4")
-    s = M.derive_schedule(M.FIG3_PROFILE, 32, tm.topo.ep, seed=seed)
-    d, a, f = M.moe_overrides(tm, s)
-    g, ref = _check(prism, tm, 33, d, node_alloc=a, node_free=f)
+    ev, br = _moe_inputs(tm, seed)
+    g = _graph(prism, tm)
+    g.set_moe_load(ev, br)
+    S = 33
+    it = g.replay(S, amp_q16=6554, kind_mask=7)
+    d, a, f = oracle.moe_load(tm, ev, br)
+    ref = oracle.replay(tm, S, amp_q16=6554, kind_mask=7, node_dur=d, node_alloc=a, node_free=f, times=True,
+                        threads=min(NPROC, S))
+    assert np.array_equal(it, ref["iter"])
+    assert np.array_equal(g.peak_memory(), ref["peak"][0])
+    rp = g.export("rank_ptr")
+    for r in np.random.default_rng(seed).choice(tm.topo.world, 24, replace=False):
+        st, fi, _ = g.query_rank(int(r), S - 1)
+        assert np.array_equal(fi, ref["finish"][S - 1, rp[r]:rp[r + 1]])
+        assert np.array_equal(st, ref["start"][S - 1, rp[r]:rp[r + 1]])
     base = oracle.replay(tm, 1)
     assert ref["peak"][0].max() > base["peak"][0].max()  # imbalance raises the worst rank's peak
+    g.set_moe_load(None)  # cleared: the template graph again
+    assert np.array_equal(g.replay(2, amp_q16=6554, kind_mask=7), oracle.replay(tm, 2, amp_q16=6554, kind_mask=7,
+                                                                              peaks=False)["iter"])
+
+
+@pytest.mark.parametrize("scale", [1, 2, 6, 7])
+def test_moe_load_composes_with_overrides(prism, scale):
+    """MoE load on top of measured durations, then label overrides and a slowed rank (include/
+    prism.h order: base -> br -> label -> rank slowdown), either call first."""
+    tm = w.scaled("C4")
+    ev, br = _moe_inputs(tm, 5, events=7)
+    rng = np.random.default_rng(scale)
+    base = oracle.node_table(tm)["dur"] * rng.integers(90, 111, tm.n_nodes) // 100
+    lab = {int(l): 1234 for l in np.unique(tm.ops["label"])[:3]}
+    f = np.full(tm.topo.world, 65536, np.int32)
+    f[3] = 2 * 65536
+    d, a, fr = oracle.moe_load(tm, ev, br, scale, node_dur=base)
+    d = oracle.whatif_durations(tm, node_dur=d, label_dur=lab, rank_factor_q16=f)
+    ref = oracle.replay(tm, 5, amp_q16=6554, kind_mask=7, node_dur=d, node_alloc=a, node_free=fr,
+                        threads=min(NPROC, 5))
+    for order in (0, 1):
+        g = _graph(prism, tm)
+        if order == 0:
+            g.set_moe_load(ev, br, scale)
+            g.set_durations(node_dur=base, label_dur=lab, rank_slow_q16=f)
+        else:
+            g.set_durations(node_dur=base, label_dur=lab, rank_slow_q16=f)
+            g.set_moe_load(ev, br, scale)
+        assert np.array_equal(g.replay(5, amp_q16=6554, kind_mask=7), ref["iter"])
+        assert np.array_equal(g.peak_memory(), ref["peak"][0])
+
+
+def test_moe_load_errors(prism):
+    tm = w.scaled("C4")
+    ev, br = _moe_inputs(tm, 0, events=32)
+    g = _graph(prism, tm)
+    with pytest.raises(prism.PrismError):
+        g.set_moe_load(np.full_like(ev, br.shape[0]), br)  # event outside [-1, n_events)
+    bad = br.copy()
+    bad[0, 0] = -5
+    with pytest.raises(prism.PrismError):
+        g.set_moe_load(ev, bad)
+    # scaling frees but not allocations drives the running total negative (br > 1 on some rank)
+    with pytest.raises(prism.PrismError) as e:
+        g.set_moe_load(ev, np.full_like(br, 2 * 65536), 1 | 4)
+    assert e.value.name == "PRISM_E_NEGATIVE_MEMORY"
+
+
+@pytest.mark.slow
+def test_moe_fig3_full_c4(prism):
+    """Full-size C4 (2048 ranks, EP 64) under the Fig. 3 profile, as bench.py's f4 row runs it."""
+    tm = w.config("C4")
+    ev, br = _moe_inputs(tm, 0, events=64)
+    g = _graph(prism, tm)
+    g.set_moe_load(ev, br)
+    it = g.replay(64, amp_q16=6554, kind_mask=7)
+    d, a, f = oracle.moe_load(tm, ev, br)
+    ref = oracle.replay(tm, 64, amp_q16=6554, kind_mask=7, node_dur=d, node_alloc=a, node_free=f, threads=NPROC)
+    assert np.array_equal(it, ref["iter"]) and np.array_equal(g.peak_memory(), ref["peak"][0])
+
+
+def test_moe_two_rank_golden(prism):
+    """The hand-worked two-rank example (tests/golden/moe_two_rank_example.txt) on the GPU."""
+    from test_moe_router import _golden, _two_rank_templates
+    import workloads.moe as M
+
+    G = _golden()
+    tm = _two_rank_templates()
+    g = _graph(prism, tm)
+    g.set_moe_load(M.op_events(tm, 1), np.array([G["br_q16"]], np.int32))
+    assert g.replay(1)[0] == G["iter"][0]
+    assert g.peak_memory().tolist() == G["peak"]
+    assert g.query_rank(0)[1].tolist() == G["finish_rank0"] and g.query_rank(1)[1].tolist() == G["finish_rank1"]

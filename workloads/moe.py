@@ -1,8 +1,9 @@
 """MoE mock-router inputs (row f4; Appendix F "MoE Mock Router", and the
 imbalance statistics of Fig. 3's caption): a balance-ratio (br) schedule per gating event
-and EP rank with the given pooled statistics, and the per-node durations / memory deltas it
-implies for a template set. An INPUT generator (seeded, host-only): it holds none of the replay
-arithmetic, and both the CUDA path and the oracle consume its per-node arrays.
+and EP rank with the given pooled statistics, its Q16 encoding, and which template op belongs to
+which gating event. An INPUT generator (seeded, host-only): it holds none of the method's
+arithmetic — how br scales a rank's work and buffers is implemented independently by the CUDA path
+(prism_set_moe_load) and the oracle (oracle.moe_load), which both consume these arrays.
 
 Readings (R6-R8): br of (event, rank) = tokens the rank's experts process / the
 uniform share (Appendix F); one gating event per (MoE layer, microbatch); an EP rank's expert
@@ -16,7 +17,6 @@ from __future__ import annotations
 
 import dataclasses
 import math
-from typing import Dict, Tuple
 
 import numpy as np
 
@@ -123,37 +123,24 @@ def br_to_counts(row, total_tokens: int, normalize: bool = True) -> np.ndarray:
     return base
 
 
-def _q16(x: float) -> int:
-    return int(round(x * 65536))
+def br_q16(sched) -> np.ndarray:
+    """Input encoding of a float br schedule [events, ep] as the ABI's Q16 integers (nearest)."""
+    return np.rint(np.asarray(sched, dtype=np.float64) * 65536).astype(np.int32)
 
 
-def moe_overrides(tm, sched: np.ndarray) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
-    """Per-node (duration, alloc, free) of a template set under a br schedule [events, ep]: the
-    node order is rank-major program order; an EXPERT_F / EXPERT_B / EP_A2A node of MoE layer L,
-    microbatch mb on a rank with EP coordinate e is scaled by br[event(L, mb), e] (Q16, floor);
-    every other node keeps its template values."""
+def op_events(tm, n_events: int) -> np.ndarray:
+    """Which gating event routes each template op (structure of the input, from the generator's
+    own labels): the ops of MoE layer L in microbatch mb (EXPERT_F / EXPERT_B and their EP all-to-
+    alls) belong to gating event (L, mb) (reading R7: one routing decision per MoE layer and
+    microbatch, forward and backward); the distinct (L, mb) keys in sorted order are numbered and
+    folded onto n_events schedule rows (index mod n_events); -1 = not routed."""
     from . import OPCODES  # label codes of the generator
 
-    t = tm.topo
-    codes = {OPCODES["EXPERT_F"], OPCODES["EXPERT_B"], OPCODES["EP_A2A"]}
-    events: Dict[Tuple[int, int], int] = {}
-    durs, allocs, frees = [], [], []
-    for r in range(t.world):
-        s = (r // t.tp) % t.pp if t.rank_order == 0 else r // (t.tp * t.dp)
-        dpi = r // (t.tp * t.pp) if t.rank_order == 0 else (r // t.tp) % t.dp
-        e = dpi % t.ep
-        T = tm.stage(s)
-        d = T["dur_ns"].astype(np.int64).copy()
-        a = T["mem_alloc"].astype(np.int64).copy()
-        f = T["mem_free"].astype(np.int64).copy()
-        lab = T["label"].astype(np.int64)
-        for i in np.nonzero(np.isin(lab >> 24, list(codes)))[0]:
-            key = (int((lab[i] >> 12) & 0xFFF), int(lab[i] & 0xFFF))
-            ev = events.setdefault(key, len(events)) % sched.shape[0]
-            q = _q16(float(sched[ev, e]))
-            d[i] = (int(d[i]) * q) >> 16
-            a[i] = (int(a[i]) * q) >> 16
-            f[i] = (int(f[i]) * q) >> 16
-        durs.append(d), allocs.append(a), frees.append(f)
-    cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64)
-    return cat(durs), cat(allocs), cat(frees)
+    lab = tm.ops["label"].astype(np.int64)
+    routed = np.isin(lab >> 24, [OPCODES["EXPERT_F"], OPCODES["EXPERT_B"], OPCODES["EP_A2A"]])
+    keys = sorted({(int((x >> 12) & 0xFFF), int(x & 0xFFF)) for x in lab[routed]})
+    index = {k: i for i, k in enumerate(keys)}
+    ev = np.full(len(lab), -1, np.int32)
+    for i in np.nonzero(routed)[0]:
+        ev[i] = index[(int((lab[i] >> 12) & 0xFFF), int(lab[i] & 0xFFF))] % n_events
+    return ev
