@@ -26,7 +26,8 @@
 //      -free at op finish sorted by (time, event index), prefix-summed; peak = static + max(0,
 //      max prefix). A negative running total is an error.
 // Readings of silent points are DESIGN.md §3 (Z1-Z16); the perturbation formula is Z8's text.
-// Parity pins for this file: tests/test_oracle_pins.py (closed forms, brute force, SPEC worked
+// Parity pins for this file: tests/test_oracle_pins.py (closed forms, brute force, hand-worked levels
+// (tests/golden/levels_hand.txt), perturbation worked through SplitMix64's published outputs, SPEC worked
 // examples, invariants).
 #include <algorithm>
 #include <cstdint>

@@ -60,20 +60,100 @@ def test_perturb_identities_and_bounds():
     assert abs(np.mean(ds)) < 0.15
 
 
+GOLD_K = 0x9E3779B97F4A7C15
+MIX_K = 0xBF58476D1CE4E5B9
+M64 = 2**64 - 1
+
+
+def test_perturb_worked_examples():
+    """Reading Z8 composed with SplitMix64's published outputs (tests/golden/splitmix64_seed0.txt):
+    the seed is chosen so that x = seed ^ k*G ^ uid*M is 0, G or 2G, i.e. h is published output
+    1, 2 or 3; the rest is worked by hand (Z8 worked examples):
+      h = 0xE220A8397B1DCDAF, h>>40 = 14819496, mod 13109 = 6326, delta = -228,
+          d = 10^6 -> 10^6 * 65308 >> 16 = 996520                        (amp 6554)
+      h = 0x6E789E6AA1B965F4, h>>40 = 7239838, mod 201 = 19, delta = -81,
+          d = 4400 -> 4400 * 65455 >> 16 = 4394                           (amp 100)
+      h = 0x06C45D188009454F, h>>40 = 443485, mod 131071 = 50272, delta = -15263,
+          d = 2^40 -> 2^24 * 50273 = 843440979968                         (amp 65535)
+    A k / uid mix-up, a different shift of h or a wrong delta offset all miss these."""
+    cases = [  # (k, uid, x target, amp, d, expected d')
+        (1, 1, 0, 6554, 10**6, 996520),
+        (2, (5 << 32) | 7, GOLD_K, 100, 4400, 4394),
+        (63, (6 << 56) | (12345 << 24) | 9, (2 * GOLD_K) & M64, 65535, 2**40, 843440979968),
+    ]
+    for k, uid, x, amp, d, want in cases:
+        seed = x ^ ((k * GOLD_K) & M64) ^ ((uid * MIX_K) & M64)  # input chosen, not an expected value
+        assert oracle.perturb(d, uid, k, seed, amp) == want, (k, uid)
+
+
+def _golden_levels():
+    rows, kv = [], {}
+    for line in open(os.path.join(GOLD, "levels_hand.txt")):
+        if not line.strip() or line.startswith("#"):
+            continue
+        p = line.split()
+        if p[0] == "A":
+            rows.append((int(p[1]), int(p[2]), int(p[3])))
+        else:
+            kv[p[0]] = [int(x) for x in p[1:]]
+    return rows, kv
+
+
+def test_levels_hand_worked():
+    """Row a5 (reading R2) against tests/golden/levels_hand.txt, derived by hand."""
+    rows, kv = _golden_levels()
+    ex = oracle.expand(w.uniform_pipeline(1, 2, 2, 2))
+    got = sorted((int(ex["mem"][ex["ptr"][g]]), int(ex["mem"][ex["ptr"][g] + 1]), int(ex["level"][g]))
+                 for g in range(ex["groups"]))
+    assert got == sorted(rows) and ex["levels"] == kv["A_levels"][0]
+    c1 = oracle.expand(w.config("C1"))
+    assert c1["levels"] == kv["C1_levels"][0]
+    role = (c1["uid"] >> np.uint64(56)).astype(int)
+    dp = [int(g) for g in np.nonzero(role == w.ROLE_DP)[0]]
+    per_rank = c1["nodes"] // 8
+    by_stage = {}
+    for g in dp:  # stage of a DP group = stage of its members (TP_PP_DP rank order)
+        r = int(c1["mem"][c1["ptr"][g]]) // per_rank
+        by_stage.setdefault((r // 2) % 2, set()).add(int(c1["level"][g]))
+    assert by_stage == {0: {kv["C1_dp_levels"][0]}, 1: {kv["C1_dp_levels"][1]}}
+
+
 # ------------------------------------------------------------------ SPEC worked examples
+def _spec_golden():
+    """tests/golden/spec_worked_examples.txt: name -> {key: value} (values as printed by SPEC)."""
+    out = {}
+    for line in open(os.path.join(GOLD, "spec_worked_examples.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, _src, *kv = line.split()
+        out[name] = dict(x.split("=") for x in kv)
+    return out
+
+
 def test_spec_examples():
+    G = _spec_golden()
+    T = lambda name: int(G[name]["T"])
     one = w.Topology(1, 1, 1)
-    assert oracle.replay(_tm(one, [[("c", 5)]]))["iter"][0] == 5
+    assert oracle.replay(_tm(one, [[("c", 5)]]))["iter"][0] == T("single_node_5")            # S:95
     r = oracle.replay(_tm(one, [[("c", 5)]]), times=True)
-    assert r["start"][0, 0] == 0 and r["finish"][0, 0] == 5
-    assert oracle.replay(_tm(w.Topology(1, 2, 1), [[("c", 3)], [("c", 7)]]))["iter"][0] == 7
-    assert oracle.replay(_tm(one, [[("c", 3), ("c", 7)]]))["iter"][0] == 10
-    assert oracle.replay(_tm(one, [[]]))["iter"][0] == 0
+    assert r["start"][0, 0] == int(G["one_node_start0"]["start"]) and r["finish"][0, 0] == T("one_node_start0")  # S:320
+    assert oracle.replay(_tm(w.Topology(1, 2, 1), [[("c", 3)], [("c", 7)]]))["iter"][0] == T("two_independent_3_7")  # S:96
+    assert oracle.replay(_tm(one, [[("c", 3), ("c", 7)]]))["iter"][0] == T("chain_3_7")      # S:328
+    assert oracle.replay(_tm(one, [[]]))["iter"][0] == T("empty_graph")                      # S:327
     # S:319 (Fig. 5): the send finishes at 12, the matched receive is locally ready at 3
     tm = _tm(w.Topology(1, 2, 1), [[("c", 12), ("p2p", w.SEND_NEXT, 0)],
                                    [("c", 3), ("p2p", w.RECV_PREV, 0)]])
     r = oracle.replay(tm, times=True)
-    assert r["start"][0, 3] == 12 and r["finish"][0, 3] == 12 and r["iter"][0] == 12
+    want = int(G["fig5_send12_recv3"]["recv_start"])
+    assert r["start"][0, 3] == want and r["finish"][0, 3] == want and r["iter"][0] == want
+    # S:159: pp=2, ga=2 1F1B stage orders
+    order = {s: ",".join(f"{it[0]}{it[1] + 1}" for it in w.schedule_1f1b(2, s, 2) if it[0] != "P") for s in (0, 1)}
+    assert order[0] == G["pp2_ga2_stage_orders"]["stage0"] and order[1] == G["pp2_ga2_stage_orders"]["stage1"]
+    # S:150: tp=2 pp=2 dp=2 -> 4 TP, 4 DP groups (one op of each role per stage)
+    ex = oracle.expand(_tm(w.Topology(2, 2, 2), [[("coll", w.ROLE_TP, 0, 1), ("coll", w.ROLE_DP, 0, 1)]] * 2))
+    role = (ex["uid"] >> np.uint64(56)).astype(int)
+    want = G["tp2pp2dp2_group_counts"]
+    assert int((role == 1).sum()) == int(want["TP"]) and int((role == 2).sum()) == int(want["DP"])
 
 
 def test_group_counts_tp2pp2dp2():
@@ -97,6 +177,21 @@ def test_group_counts_tp2pp2dp2():
         for g in np.nonzero(role == 1)[0]:
             mem = ex["mem"][ex["ptr"][g]:ex["ptr"][g + 1]] // per_rank
             assert len({coords[int(m)][1:] for m in mem}) == 1
+        # every role's member sets = the classes of ranks sharing the role's fixed coordinates
+        # (row a2): DP = same (tp, pp); EP = same (tp, pp, edp = dp // ep), ep_i = dp % ep varies;
+        # EDP = same (tp, pp, ep_i); WORLD = everyone
+        key = {2: lambda c: (c[0], c[1]), 3: lambda c: (c[0], c[1], c[2] // ep),
+               4: lambda c: (c[0], c[1], c[2] % ep), 5: lambda c: ()}
+        for rr, f in key.items():
+            want = {}
+            for r, c in coords.items():
+                want.setdefault(f(c), set()).add(r)
+            got = [frozenset(int(m) // per_rank for m in ex["mem"][ex["ptr"][g]:ex["ptr"][g + 1]])
+                   for g in np.nonzero(role == rr)[0]]
+            assert sorted(map(sorted, got)) == sorted(map(sorted, want.values())), (tp, pp, dp, ep, rr)
+            if rr == 3:  # an EP group spans ep consecutive dp coordinates (ep carved out of dp)
+                for m in got:
+                    assert sorted(coords[r][2] % ep for r in m) == list(range(ep))
 
 
 # ------------------------------------------------------------------ pipeline closed forms
