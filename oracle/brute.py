@@ -90,8 +90,8 @@ def _d(op, n, node_dur):
     return int(op["dur_ns"]) if node_dur is None else int(node_dur[n])
 
 
-def iteration_time(tm, node_dur=None) -> Tuple[int, List[int]]:
-    """(T, finish per node) by exhaustive path enumeration."""
+def _dag(tm, node_dur=None):
+    """The plain vertex-weighted DAG of the module docstring: (n_nodes, weight, preds)."""
     nodes, rank_nodes, groups, dpreds = expand(tm, node_dur)
     # vertices: ("n", node) for every node; ("g", key) for groups
     weight: Dict[tuple, int] = {}
@@ -117,6 +117,12 @@ def iteration_time(tm, node_dur=None) -> Tuple[int, List[int]]:
         preds[g] = []
         for n, _ in mem:
             preds[g].extend(("n", p) for p in dpreds[n])
+    return len(nodes), weight, preds
+
+
+def iteration_time(tm, node_dur=None) -> Tuple[int, List[int]]:
+    """(T, finish per node) by exhaustive path enumeration."""
+    n_nodes, weight, preds = _dag(tm, node_dur)
     succ: Dict[tuple, List[tuple]] = {v: [] for v in weight}
     for v, ps in preds.items():
         for p in ps:
@@ -133,7 +139,35 @@ def iteration_time(tm, node_dur=None) -> Tuple[int, List[int]]:
     for v in weight:
         if not preds[v]:
             walk(v, 0)
-    fin = [best[("n", n)] for n in range(len(nodes))]
+    fin = [best[("n", n)] for n in range(n_nodes)]
     if any(f < 0 for f in fin):
         raise RuntimeError("deadlock: some node is unreachable from every source")
+    return (max(fin) if fin else 0), fin
+
+
+def fixed_point(tm, node_dur=None) -> Tuple[int, List[int]]:
+    """(T, finish per node) by a Bellman-Ford-style fixed point on the same
+    DAG: starting from f = -inf everywhere, sweep every vertex v in an arbitrary (here: reversed
+    creation) order setting f(v) = weight(v) + max(0, max over preds f(p)) once all its preds are
+    finite, until a sweep changes nothing (<= |V| sweeps on a DAG). Polynomial, so it runs on graphs
+    far beyond path enumeration; no priority queue, no topological order."""
+    n_nodes, weight, preds = _dag(tm, node_dur)
+    order = list(reversed(list(weight)))
+    NEG = None
+    f: Dict[tuple, object] = {v: NEG for v in order}
+    for _ in range(len(order) + 1):
+        changed = False
+        for v in order:
+            ps = preds[v]
+            if any(f[p] is NEG for p in ps):
+                continue
+            val = weight[v] + max([0] + [f[p] for p in ps])
+            if f[v] is NEG or val != f[v]:
+                f[v] = val
+                changed = True
+        if not changed:
+            break
+    fin = [f[("n", n)] for n in range(n_nodes)]
+    if any(x is NEG for x in fin):
+        raise RuntimeError("deadlock: some node never becomes ready")
     return (max(fin) if fin else 0), fin

@@ -412,3 +412,25 @@ def test_errors():
     with pytest.raises(oracle.OracleError) as e:
         oracle.replay(_tm(w.Topology(1, 1, 3, 2), [[("c", 1)]]))
     assert e.value.name == "INVALID_SPEC"
+
+
+# ------------------------------------------------------------------ fixed-point cross-check
+@pytest.mark.parametrize("seed", range(12))
+def test_fixed_point_matches_des_random(seed):
+    """a Bellman-Ford-style fixed point on the weighted DAG equals the DES on
+    medium random graphs (far beyond path enumeration), per node."""
+    tm = w.random_templates(seed, max_world=24, max_ops=30)
+    T, fin = brute.fixed_point(tm)
+    r = oracle.replay(tm, times=True)
+    assert T == r["iter"][0] and fin == r["finish"][0].tolist()
+
+
+@pytest.mark.parametrize("name", ["C1"])
+def test_fixed_point_matches_des_configs(name):
+    tm = w.config(name)
+    T, fin = brute.fixed_point(tm)
+    r = oracle.replay(tm, times=True)
+    assert T == r["iter"][0] == 64800 and fin == r["finish"][0].tolist()
+    tm = w.uniform_pipeline(2, 3, 2, 6, vpp=3, p2p_c=7)  # interleaved, P2P cost
+    T, fin = brute.fixed_point(tm)
+    assert fin == oracle.replay(tm, times=True)["finish"][0].tolist()
