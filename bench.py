@@ -99,13 +99,18 @@ def _dist():
 
 
 def algorithmic_bytes(st, S: int, record: bool = True):
-    """SURVEY.md §8(d) / DESIGN.md §6 algorithmic bytes of one replay (rows a6-a8) and one
-    build (a1-a4) and one peak scan (a9)."""
+    """SURVEY.md §8(d) algorithmic bytes: replay (rows a6-a8) = 8 B per node-scenario
+    (the start/finish time written) + 16 B per node per call (structure read); durations are
+    hashed in-kernel, so no 4 B per node-scenario term. Expander (a1-a4) = 24 B per node + 8 B per
+    membership; peak scan (a9) = 16 B per node + 8 B per rank. `replay_state` is the
+    implementation's extra state traffic (ready slots, group accumulators, rank_end), reported
+    beside the roofline, not in it."""
     N, G, M, W = st["nodes"], st["groups"], st["memberships"], st["world"]
-    replay = (N * S * 8 if record else 0) + G * S * 16 + N * 16 + M * 8 + W * S * 8
-    build = N * 41 + M * 8 + G * 24
+    replay = (N * S * 8 if record else 0) + N * 16
+    state = G * S * 16 + M * 8 + W * S * 8
+    build = N * 24 + M * 8
     peak = N * 16 + W * 8
-    return {"replay": replay, "build": build, "peak": peak}
+    return {"replay": replay, "replay_state": state, "build": build, "peak": peak}
 
 
 def run_prism(args):
@@ -257,13 +262,16 @@ def run_prism(args):
     cpu = None
     if ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args)
-    traffic = None
+    traffic, traffic_src = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(args.config, {}).get(str(S))
+            tj = json.load(open(tf))
+            traffic = tj.get(args.config, {}).get(str(S))
+            traffic_src = tj.get("_source")
         except Exception:
             traffic = None
+    s1 = s1_line(args, tm, sh) if ws == 1 and not args.no_f_rows else None
     out = {
         "metric": METRIC,
         "value": round(value, 1),
@@ -292,7 +300,15 @@ def run_prism(args):
             "iteration_time_ns_scenario0": int(iters[0]),
             "device_ms": {k: round(v, 4) for k, v in med.items()},
             "replay_ms_timed_steps": round(replay_ms, 4),
+            "s1": s1,
             "next_rows": frows,
+            "paper_context": {
+                "replay_model": "the paper replays virtual ranks in real time on assistant GPUs (P:1295-1298): one "
+                                "emulated iteration takes about one real iteration, 5.6-12.0 s in Table 1 "
+                                "(P:1727-1731), i.e. ~0.08-0.18 emulated iterations/s per replay",
+                "accuracy": "0.58% avg iteration-time error, <0.01% peak-memory error (P:72-73); 8192 GPUs "
+                            "emulated with <1% of the physical GPUs (P:74-75), on an unnamed 2048-GPU testbed",
+            },
         },
         "roofline": {
             "bound": "hbm",
@@ -306,7 +322,10 @@ def run_prism(args):
             "unit": "GB/s",
             "frac": round(achieved / peak_bw, 4),
             "alg_bytes_per_call": ab["replay"],
+            "alg_bytes_rule": "SURVEY 8(d): 8 B per node-scenario written + 16 B per node per call",
+            "state_bytes_per_call": ab["replay_state"],
             "traffic": traffic,
+            "traffic_source": (f"{traffic_src} (not measured in this run)" if traffic is not None else None),
         },
         "e2e": {"value": round(units / (e2e_ms / 1e3), 1), "unit": "node-scenarios/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3)},
@@ -315,6 +334,28 @@ def run_prism(args):
         "cpu_baseline": cpu,
     }
     return out
+
+
+def s1_line(args, tm, sh):
+    """The S = 1 configuration of SURVEY §8.3 ("every run at S = 1 and S = 64"): one unperturbed
+    scenario of the same graph on the rank kernel (lane = rank), device-timed (CUDA events on the
+    graph's stream), best of 5, with its own roofline fraction on the same §8(d) bytes."""
+    import paper_2605_15617_b200 as prism
+
+    g = prism.Graph(tm, stream=sh, profile=True)
+    st = g.stats()
+    best = None
+    for _ in range(6):
+        g.replay(1, record=True)
+        ms = g.last_timing()["levels"]
+        best = ms if best is None else min(best, ms)
+    algo = g.last_algo()
+    g.close()
+    ab = algorithmic_bytes(st, 1)["replay"]
+    peak_bw, _ = _peaks()
+    return {"replay_ms": round(best, 4), "value": round(st["nodes"] / (best / 1e3), 1), "unit": "node-scenarios/s",
+            "emulated_iterations_per_s": round(1 / (best / 1e3), 1), "schedule": algo,
+            "roofline_frac": round(ab / (best / 1e3) / 1e9 / peak_bw, 4), "alg_bytes_per_call": ab}
 
 
 def f_rows_extra(args, tm, sh):
@@ -394,6 +435,16 @@ def f_rows_extra(args, tm, sh):
     return out
 
 
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(args, sample_dp: int = 8):
     """The oracle as it stands, on a bounded sample of the same workload: the C5 templates with
     DP cut to `sample_dp` replicas, nproc scenarios (one thread each), expansion included."""
@@ -411,6 +462,10 @@ def cpu_baseline(args, sample_dp: int = 8):
     cores = os.cpu_count() or 1
     S = max(1, min(args.scenarios, cores))
     oracle.build()
+    # single thread, one scenario (SURVEY §8.3 "Oracle timing" (a))
+    t1 = time.perf_counter()
+    oracle.replay(tm, 1, amp_q16=args.amp, kind_mask=7, peaks=True, threads=1)
+    one = time.perf_counter() - t1
     # repeat the sample until ~10 s of CPU work (the contract's 10-30 s bounded sample)
     reps, t0 = 0, time.perf_counter()
     while True:
@@ -420,7 +475,9 @@ def cpu_baseline(args, sample_dp: int = 8):
         if dt >= args.cpu_seconds or reps >= 200:
             break
     return {"value": round(reps * tm.n_nodes * S / dt, 1), "unit": "node-scenarios/s", "cores": min(S, cores),
-            "kind": "oracle", "seconds": round(dt, 2),
+            "kind": "oracle", "seconds": round(dt, 2), "cpu_model": _cpu_model(), "nproc": cores,
+            "single_thread_one_scenario": {"seconds": round(one, 3),
+                                           "value": round(tm.n_nodes / one, 1), "unit": "node-scenarios/s"},
             "sample": f"{args.config} templates at dp={dp} ({tm.topo.world} of {t.world} ranks, "
                       f"{tm.n_nodes} nodes), {S} scenarios, one thread each, expansion + DES + peak, "
                       f"repeated {reps}x"}
@@ -480,6 +537,20 @@ def main():
                     help="N>1: shard the ranks over the GPUs (row e) or run independent replicas")
     args = ap.parse_args()
     args.config = args.config.upper()
+    ws_env = os.environ.get("WORLD_SIZE")
+    if args.impl == "prism" and args.gpus > 1 and ws_env is None:
+        # one process per GPU: re-launch this command under torch.distributed.run (the driver's
+        # own launch sets WORLD_SIZE and lands below)
+        import socket
+
+        with socket.socket() as s_:
+            s_.bind(("127.0.0.1", 0))
+            port = s_.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
+    if args.impl == "prism" and ws_env is not None and int(ws_env) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}: launch one process per GPU")
     if args.warmup < 3 and args.impl == "prism":
         args.warmup = 3
     out = run_reference(args) if args.impl == "reference" else run_prism(args)
