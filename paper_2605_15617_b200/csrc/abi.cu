@@ -488,6 +488,8 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
       G->fin_node0 = 0;
       G->fin_rows = P.N;
     }
+    d.fin_node0 = G->fin_node0;
+    d.fin_rows = G->fin_rows;
   }
   const size_t W = P.W, N = P.N, M = P.M, Gn = P.G, pp = P.topo.pp;
   const size_t nops = (size_t)tmpl->n_ops;
@@ -875,7 +877,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     trace("shard: launch cells");
     const int per_launch = cells_chunks_per_launch(G->cur(), nchunks);
     for (int ch = 0; ch < nchunks; ch += per_launch) {
-      CU(launch_cells(G->cur(), p, rslot, acc, nullptr, arrive, status, G->parity, p.record ? G->fin : nullptr, G->fin_node0,
+      CU(launch_cells(G->cur(), p, rslot, acc, nullptr, arrive, status, G->parity, p.record ? G->fin : nullptr,
                       G->gfin, G->rank_end, ch, std::min(per_launch, nchunks - ch), Sp, &G->link, G->stream));
       ++launches;
     }
@@ -918,7 +920,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     const int per_launch = cells_chunks_per_launch(G->cur(), nchunks);
     for (int ch = 0; ch < nchunks; ch += per_launch) {
       CU(launch_cells(G->cur(), p, G->rslot, G->acc, G->rres, G->sync_words, status, G->parity,
-                      p.record ? G->fin : nullptr, 0, G->gfin, G->rank_end, ch,
+                      p.record ? G->fin : nullptr, G->gfin, G->rank_end, ch,
                       std::min(per_launch, nchunks - ch), Sp, nullptr, G->stream));
       ++launches;
     }
@@ -1015,7 +1017,7 @@ static prism_status peak_impl(prism_graph_t G, int32_t scenario, bool time_order
   uint32_t *status = G->words + 2;
   CU(cudaMemsetAsync(status, 0, 4, G->stream));
   G->rec(6);
-  CU(launch_peak_time(G->cur(), G->last, G->last_Sp, G->fin, G->fin_node0, G->gfin, scenario, (int32_t)max_len,
+  CU(launch_peak_time(G->cur(), G->last, G->last_Sp, G->fin, G->gfin, scenario, (int32_t)max_len,
                       peak_dev, status, G->stream));
   G->rec(7);
   CU(cudaMemcpyAsync(G->h_status + 2, status, 4, cudaMemcpyDeviceToHost, G->stream));
@@ -1117,7 +1119,7 @@ prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, i
   CU(cudaSetDevice(G->device));
   const size_t bytes = (size_t)n * 16;
   if (!G->ensure(G->scratch, G->scratch_bytes, bytes)) return fail(PRISM_E_OOM, "scratch allocation failed");
-  CU(launch_query(G->cur(), G->last, G->last_Sp, G->fin, G->fin_node0, G->gfin, rank, scenario, G->scratch,
+  CU(launch_query(G->cur(), G->last, G->last_Sp, G->fin, G->gfin, rank, scenario, G->scratch,
                   G->scratch + n, G->stream));
   CU(cudaMemcpyAsync(start_ns, G->scratch, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaMemcpyAsync(finish_ns, G->scratch + n, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
@@ -1561,6 +1563,24 @@ extern "C" PRISM_API prism_status prism_debug_export(prism_graph_t G, int32_t wh
   if (bytes < need) return fail(PRISM_E_INVALID_ARG, "buffer too small: need " + std::to_string(need));
   if (need == 0) return PRISM_OK;
   CU(cudaSetDevice(G->device));
+  if (which == 15) {  // fin: device layout (graph.h fin_off) -> canonical [row = node][Sp], rank-major
+    const int64_t rows = G->fin_rows, Sp = G->last_Sp, cw = Sp < 32 ? Sp : 32, n0 = G->fin_node0;
+    std::vector<int64_t> raw((size_t)(rows * Sp));
+    std::vector<int32_t> rp32((size_t)d.W + 1);
+    CU(cudaMemcpyAsync(raw.data(), src, (size_t)need, cudaMemcpyDeviceToHost, G->stream));
+    CU(cudaMemcpyAsync(rp32.data(), d.rank_ptr, (size_t)(d.W + 1) * 4, cudaMemcpyDeviceToHost, G->stream));
+    CU(cudaStreamSynchronize(G->stream));
+    int64_t *out = (int64_t *)host_out;
+    for (int64_t r = 0; r < d.W; ++r) {
+      const int64_t tpi = r % d.tp, c0 = rp32[r - tpi];
+      for (int64_t n = rp32[r]; n < rp32[r + 1]; ++n) {
+        if (n < n0 || n >= n0 + rows) continue;
+        const int64_t row = c0 + (n - rp32[r]) * d.tp + tpi - n0;
+        for (int64_t k = 0; k < Sp; ++k) out[(n - n0) * Sp + k] = raw[(size_t)(((k / cw) * rows + row) * cw + k % cw)];
+      }
+    }
+    return PRISM_OK;
+  }
   CU(cudaMemcpyAsync(host_out, src, (size_t)need, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaStreamSynchronize(G->stream));
   return PRISM_OK;

@@ -625,10 +625,9 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
     nux = *p_uid;
     if (MS) nms = *p_ms;
   }
-  // fin row of op i of rank r: the cell's ranks are consecutive and run one template, so rank r's
-  // rows sit r * len rows after rank 0's (one moving pointer, a constant stride per rank)
-  int64_t *fp = fin + (int64_t)rb[0] * Sp + k;
-  const int64_t fst = (int64_t)len * Sp;
+  // fin rows of op i (graph.h fin_off): the cell's C ranks are C consecutive 32-lane rows of this
+  // chunk, and op i + 1's rows follow: one moving pointer, rank r at the constant offset r * 32
+  int64_t *fp = fin ? fin + fin_off(g, (int64_t)rb[0], k, Sp) : nullptr;
   for (int32_t base = 0; base < len; base += 32) {
     const int32_t cnt = min(32, len - base);
     const uint32_t bcls = ncls;
@@ -706,8 +705,8 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
         }
         if (record) {  // op i's finishes; the tail below writes op i + 1's
 #pragma unroll
-          for (int r = 0; r < C; ++r) __stcs(fp + r * fst, (long long)t[r]);
-          fp += Sp;
+          for (int r = 0; r < C; ++r) __stcs(fp + r * SC, (long long)t[r]);
+          fp += C * SC;
         }
         const int64_t m = tree_max<C>(t) + tq;
 #pragma unroll
@@ -800,10 +799,9 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
       if (record) {
 #pragma unroll
         for (int r = 0; r < C; ++r) {
-          if (C >= 4 && !PR) __stcs(fp + r * fst, (long long)t[r]);
-          else __stcs(fin + (int64_t)(rb[r] + i) * Sp + k, (long long)t[r]);  // small cells, PR: fewer live registers
+          __stcs(fp + r * SC, (long long)t[r]);
         }
-        if (C >= 4 && !PR) fp += Sp;
+        fp += C * SC;
       }
     }
   }

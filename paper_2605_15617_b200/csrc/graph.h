@@ -22,6 +22,8 @@ struct DevGraph {
   // return at once (test hook: forces the watchdog)
   int32_t stall_unit;
   uint64_t watchdog_ns;
+  // fin rows kept by this graph: [fin_node0, fin_node0 + fin_rows) of the row order below
+  int64_t fin_node0, fin_rows;
   // row f2: multi-stream ranks (per-node stream / event fields, directional predecessors, -1 =
   // none); streams and densely renumbered event slots used by the graph
   int32_t ms, ms_streams, ms_events;
@@ -99,6 +101,26 @@ struct DevGraph {
   const int32_t *x_ptr;     // [pp+1] cross-op list of each stage
   const XOp *x_ops;
 };
+
+// Layout of the recorded finish times fin. Rows are nodes in CELL-INTERLEAVED
+// order: the tp ranks of a (stage, dp) cell run one template, so op i of the cell's rank tp_i is
+// row cell_first_node + i * tp + tp_i (a cell's rows are one contiguous block either way, so a DP
+// block's rows stay contiguous for sharding). Scenarios are grouped in chunks of cw = min(32, Sp)
+// lanes, chunk-major: element (row, k) sits at ((k / cw) * rows + row - node0) * cw + k % cw. A
+// cell kernel warp (one cell, one 32-scenario chunk) thus writes op i of its ranks as C
+// consecutive 256-byte rows at constant offsets (no per-op address arithmetic), and its ops follow
+// each other contiguously.
+#ifdef __CUDACC__
+__device__ __forceinline__ int64_t fin_row(const DevGraph &g, int32_t n) {
+  const int32_t r = g.node_rank[n];
+  const int32_t tpi = r % g.tp;
+  return (int64_t)g.rank_ptr[r - tpi] + (int64_t)(n - g.rank_ptr[r]) * g.tp + tpi;
+}
+__device__ __forceinline__ int64_t fin_off(const DevGraph &g, int64_t row, int32_t k, int32_t Sp) {
+  const int32_t cw = Sp < 32 ? Sp : 32;
+  return ((int64_t)(k / cw) * g.fin_rows + (row - g.fin_node0)) * cw + (k % cw);
+}
+#endif
 
 // Scenario parameters as seen by the kernels.
 struct ScenParams {
@@ -233,14 +255,14 @@ cudaError_t launch_tail(const DevGraph &g, const ScenParams &p, int64_t *fin, co
 cudaError_t launch_reduce(int32_t W, int32_t S, int32_t Sp, const int64_t *rank_end, int64_t *iter,
                           cudaStream_t st);
 cudaError_t launch_query(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin,
-                         int64_t node0, const int64_t *gfin, int32_t rank, int32_t scen, int64_t *start_out,
+                         const int64_t *gfin, int32_t rank, int32_t scen, int64_t *start_out,
                          int64_t *finish_out, cudaStream_t st);
 // replay_cells.cu (cell kernel); cudaErrorCooperativeLaunchTooLarge = does not fit, use levels
 bool cells_fit(const DevGraph &g, int nchunks);
 int cells_chunk_scenarios();
 int cells_chunks_per_launch(const DevGraph &g, int nchunks);
 cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc,
-                         int64_t *rres, uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t node0,
+                         int64_t *rres, uint32_t *arrive, uint32_t *status, int parity, int64_t *fin,
                          int64_t *gfin, int64_t *rank_end, int chunk0, int nchunks_launch, int Sp,
                          const ShardLink *link, cudaStream_t st);
 // row e: iteration times of a sharded replay (local partial max, peer exchange, global max)
@@ -250,7 +272,7 @@ cudaError_t launch_shard_reduce(const DevGraph &g, const ShardLink &link, int32_
 // row f2: time-ordered peak memory of scenario k of a recorded replay (max_len = longest rank,
 // <= kMaxTimeOrderedOps)
 constexpr int32_t kMaxTimeOrderedOps = 4096;
-cudaError_t launch_peak_time(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin, int64_t node0,
+cudaError_t launch_peak_time(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin,
                              const int64_t *gfin, int32_t k, int32_t max_len, int64_t *peak, uint32_t *status,
                              cudaStream_t st);
 // replay_ranks.cu (one scenario, lane = rank)

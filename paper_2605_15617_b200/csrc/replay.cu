@@ -66,7 +66,7 @@ __device__ __forceinline__ void walk_segment(const DevGraph &g, const ScenParams
       const int64_t grp = g.node_grp[h];
       Vec<SPL>::load_max(gfin + grp * Sp + k0, t);
     }
-    if (write) Vec<SPL>::store(fin + (int64_t)ps * Sp + k0, t);
+    if (write) Vec<SPL>::store(fin + fin_off(g, fin_row(g, ps), k0, Sp), t);
   }
   const uint64_t rhi = (uint64_t)r << 32;
   for (int32_t i = (ps >= 0 ? ps + 1 : rb); i < end; ++i) {
@@ -77,7 +77,7 @@ __device__ __forceinline__ void walk_segment(const DevGraph &g, const ScenParams
       const int64_t dd = pj[j] ? perturb_x(d, sx[j] ^ uidx, p) : d;
       t[j] += dd;
     }
-    if (write) Vec<SPL>::store(fin + (int64_t)i * Sp + k0, t);
+    if (write) Vec<SPL>::store(fin + fin_off(g, fin_row(g, i), k0, Sp), t);
   }
 }
 
@@ -269,8 +269,8 @@ __global__ void __launch_bounds__(1024) shard_exchange_kernel(ShardLink L, int32
   }
 }
 
-// prism_query_rank: start/finish of one rank's ops in one scenario from fin/gfin.
-// fin rows start at node node0 (a sharded replay keeps only its own ranks' rows).
+// prism_query_rank: start/finish of one rank's ops in one scenario from fin/gfin (fin layout:
+// graph.h fin_off; a sharded replay keeps only its own ranks' rows).
 // Start time of node i (rank r, first node rb) in scenario k of a recorded replay: a compute span
 // starts its perturbed duration before its finish; a node with one sync group spans exactly the
 // group occurrence; a batched P2P node starts at the max over its groups of (group finish - dur').
@@ -283,14 +283,14 @@ __device__ __forceinline__ int64_t node_start(const DevGraph &g, const ScenParam
     int64_t d = g.node_dur[i];
     if ((p.mask & 1u) && p.amp > 0 && kg > 0)
       d = perturb_x(d, p.seed ^ ((uint64_t)kg * K_GOLD) ^ ((((uint64_t)r << 32) | (uint32_t)(i - rb)) * K_MIX), p);
-    return fin[(int64_t)i * Sp + k] - d;
+    return fin[fin_off(g, fin_row(g, i), k, Sp)] - d;
   }
   if (h1 - h0 == 1) {
     const int64_t grp = g.node_grp[h0];
     const uint32_t gbit = (g.grp_uid[grp] >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
     int64_t d = g.grp_dur[grp];
     if ((p.mask & gbit) && p.amp > 0 && kg > 0) d = perturb_x(d, p.seed ^ ((uint64_t)kg * K_GOLD) ^ (g.grp_uid[grp] * K_MIX), p);
-    return fin[(int64_t)i * Sp + k] - d;
+    return fin[fin_off(g, fin_row(g, i), k, Sp)] - d;
   }
   int64_t st = 0;
   for (int32_t h = h0; h < h1; ++h) {
@@ -303,31 +303,31 @@ __device__ __forceinline__ int64_t node_start(const DevGraph &g, const ScenParam
   return st;
 }
 
-__global__ void query_kernel(DevGraph g, ScenParams p, int32_t Sp, const int64_t *__restrict__ fin0,
-                             int64_t node0, const int64_t *__restrict__ gfin, int32_t r, int32_t k,
+__global__ void query_kernel(DevGraph g, ScenParams p, int32_t Sp, const int64_t *__restrict__ fin,
+                             const int64_t *__restrict__ gfin, int32_t r, int32_t k,
                              int64_t *__restrict__ start_out, int64_t *__restrict__ finish_out) {
   const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
-  const int64_t *fin = fin0 - node0 * Sp;
   for (int32_t i = rb + blockIdx.x * blockDim.x + threadIdx.x; i < re; i += gridDim.x * blockDim.x) {
     start_out[i - rb] = node_start(g, p, Sp, fin, gfin, r, rb, i, k);
-    finish_out[i - rb] = fin[(int64_t)i * Sp + k];
+    finish_out[i - rb] = fin[fin_off(g, fin_row(g, i), k, Sp)];
   }
 }
 
 // Row a9 in time order (row f2, multi-stream ranks; P:1578 max_memory_allocated): one block per
-// rank; the rank's events (+alloc at start: index 2i, -free at finish: 2i+1) are keyed
-// (time << 14 | index), bitonic-sorted in shared memory, and prefix-summed; peak = static +
-// max(0, max running total). A running total below zero sets PRISM_E_NEGATIVE_MEMORY.
+// rank; the rank's events (+alloc at start: index 2i, -free at finish: 2i+1) are sorted by
+// (time, index) — the full 64-bit time, the index as the tie-break — with a bitonic sort in shared
+// memory, and prefix-summed; peak = static + max(0, max running total). A running total below
+// zero sets PRISM_E_NEGATIVE_MEMORY.
 __global__ void __launch_bounds__(1024) peak_time_kernel(DevGraph g, ScenParams p, int32_t Sp,
-                                                         const int64_t *__restrict__ fin0, int64_t node0,
+                                                         const int64_t *__restrict__ fin,
                                                          const int64_t *__restrict__ gfin, int32_t k, int32_t cap,
                                                          int64_t *__restrict__ peak, uint32_t *status) {
   extern __shared__ unsigned long long sm[];
   unsigned long long *key = sm;
   long long *val = (long long *)(sm + cap);
+  uint16_t *kix = (uint16_t *)(sm + 2 * (size_t)cap);
   __shared__ long long wsum[32], wmax[32];
   __shared__ int neg;
-  const int64_t *fin = fin0 - node0 * Sp;
   for (int32_t r = blockIdx.x; r < g.W; r += gridDim.x) {
     const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1], len = re - rb;
     for (int32_t x = threadIdx.x; x < cap; x += blockDim.x) {
@@ -335,11 +335,13 @@ __global__ void __launch_bounds__(1024) peak_time_kernel(DevGraph g, ScenParams 
       if (i < len) {
         const int32_t n = rb + i;
         const bool fr = x & 1;
-        const int64_t tm = fr ? fin[(int64_t)n * Sp + k] : node_start(g, p, Sp, fin, gfin, r, rb, n, k);
-        key[x] = ((unsigned long long)tm << 14) | (unsigned)x;
+        const int64_t tm = fr ? fin[fin_off(g, fin_row(g, n), k, Sp)] : node_start(g, p, Sp, fin, gfin, r, rb, n, k);
+        key[x] = (unsigned long long)tm;
+        kix[x] = (uint16_t)x;
         val[x] = fr ? -g.node_free[n] : g.node_alloc[n];
       } else {
         key[x] = ~0ull;
+        kix[x] = 0xFFFF;
         val[x] = 0;
       }
     }
@@ -350,10 +352,14 @@ __global__ void __launch_bounds__(1024) peak_time_kernel(DevGraph g, ScenParams 
           const int32_t y = x ^ stride;
           if (y > x) {
             const bool up = (x & size) == 0;
-            if ((key[x] > key[y]) == up) {
+            const bool gt = key[x] > key[y] || (key[x] == key[y] && kix[x] > kix[y]);
+            if (gt == up) {
               const unsigned long long tk = key[x];
               key[x] = key[y];
               key[y] = tk;
+              const uint16_t ti = kix[x];
+              kix[x] = kix[y];
+              kix[y] = ti;
               const long long tv = val[x];
               val[x] = val[y];
               val[y] = tv;
@@ -529,23 +535,23 @@ cudaError_t launch_shard_reduce(const DevGraph &g, const ShardLink &link, int32_
   return cudaGetLastError();
 }
 
-cudaError_t launch_peak_time(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin, int64_t node0,
+cudaError_t launch_peak_time(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin,
                              const int64_t *gfin, int32_t k, int32_t max_len, int64_t *peak, uint32_t *status,
                              cudaStream_t st) {
   int32_t cap = 2;
   while (cap < 2 * max_len) cap <<= 1;
-  const size_t smem = (size_t)cap * 16;
+  const size_t smem = (size_t)cap * 18;
   cudaError_t e = cudaFuncSetAttribute(peak_time_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const int threads = cap >= 1024 ? 1024 : (cap < 32 ? 32 : cap);  // whole warps (shuffle scans)
-  peak_time_kernel<<<g.W < num_sms() * 2 ? g.W : num_sms() * 2, threads, smem, st>>>(g, p, Sp, fin, node0, gfin, k, cap, peak, status);
+  peak_time_kernel<<<g.W < num_sms() * 2 ? g.W : num_sms() * 2, threads, smem, st>>>(g, p, Sp, fin, gfin, k, cap, peak, status);
   return cudaGetLastError();
 }
 
 cudaError_t launch_query(const DevGraph &g, const ScenParams &p, int32_t Sp, const int64_t *fin,
-                         int64_t node0, const int64_t *gfin, int32_t rank, int32_t scen,
+                         const int64_t *gfin, int32_t rank, int32_t scen,
                          int64_t *start_out, int64_t *finish_out, cudaStream_t st) {
-  query_kernel<<<64, 256, 0, st>>>(g, p, Sp, fin, node0, gfin, rank, scen, start_out, finish_out);
+  query_kernel<<<64, 256, 0, st>>>(g, p, Sp, fin, gfin, rank, scen, start_out, finish_out);
   return cudaGetLastError();
 }
 

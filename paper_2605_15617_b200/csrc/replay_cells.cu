@@ -151,7 +151,7 @@ int cells_chunks_per_launch(const DevGraph &g, int nchunks) {
 }
 
 cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc,
-                         int64_t *rres, uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t node0,
+                         int64_t *rres, uint32_t *arrive, uint32_t *status, int parity, int64_t *fin,
                          int64_t *gfin, int64_t *rank_end, int chunk0, int nchunks_launch, int Sp,
                          const ShardLink *link, cudaStream_t st) {
   const int64_t units = cell_count(g) * nchunks_launch;
@@ -164,9 +164,7 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
   if (link) a.L = *link;
   DevGraph gg = g;
   ScenParams pp = p;
-  // fin keeps only rows [node0, ...) (a sharded replay stores its own ranks' rows): rebase the
-  // pointer so the kernel indexes it by global node id
-  int64_t *fin_g = fin ? (int64_t *)((uintptr_t)fin - (uintptr_t)(node0 * Sp * 8)) : nullptr;
+  int64_t *fin_g = fin;
   void *args[] = {&gg, &pp, &a, &fin_g, &gfin, &rank_end};
   return cudaLaunchCooperativeKernel(cell_kernel_for(g), dim3(ctas), dim3(WARPS * 32), args,
                                      cell_dyn_smem(g), st);

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) crit_start_kernel(DevGraph g, const int64
                                                          int32_t *__restrict__ out_node) {
   const int64_t T = iter[k];
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N; n += (int64_t)gridDim.x * blockDim.x)
-    if (fin[n * Sp + k] == T) atomicMin(out_node, (int32_t)n);
+    if (fin[fin_off(g, fin_row(g, (int32_t)n), k, Sp)] == T) atomicMin(out_node, (int32_t)n);
 }
 
 // Row f3, step 2: the walk back (one warp; lanes split a group's members). Rules = the oracle's
@@ -153,13 +153,13 @@ __global__ void __launch_bounds__(32) crit_walk_kernel(DevGraph g, ScenParams p,
     const int32_t a = g.node_spred[n], b = g.node_esrc[n];
     if (a < 0) return b;
     if (b < 0) return a;
-    const int64_t fa = fin[(int64_t)a * Sp + k], fb = fin[(int64_t)b * Sp + k];
+    const int64_t fa = fin[fin_off(g, fin_row(g, a), k, Sp)], fb = fin[fin_off(g, fin_row(g, b), k, Sp)];
     if (fa != fb) return fa > fb ? a : b;
     return min(a, b);
   };
   auto ready = [&](int32_t m) -> int64_t {
     const int32_t q = pred(m);
-    return q < 0 ? 0 : fin[(int64_t)q * Sp + k];
+    return q < 0 ? 0 : fin[fin_off(g, fin_row(g, q), k, Sp)];
   };
   while (cur >= 0) {
     if (lane == 0 && len < cap) path[len] = cur;

@@ -24,8 +24,13 @@ def main():
     pols = sys.argv[2:] or ["0,32,256", "6,32,256", "2,32,1024", "2,64,2048", "0,64,4096", "1,128,8192",
                             "4,16,512", "2,32,512"]
     ref = None
-    for p in pols:
-        env = dict(os.environ, PRISM_POLL=p)
+    for p in pols:  # "a,b,c" = PRISM_POLL, "F:a,b,c" = PRISM_POLL_FAST, "a,b,c+F:d,e,f" = both
+        env = dict(os.environ)
+        for part in p.split("+"):
+            if part.startswith("F:"):
+                env["PRISM_POLL_FAST"] = part[2:]
+            else:
+                env["PRISM_POLL"] = part
         r = subprocess.run([sys.executable, "-c", CHILD % (ROOT, cfg)], env=env, capture_output=True, text=True)
         line = [l for l in r.stdout.splitlines() if l.startswith("RESULT")]
         if not line:
@@ -33,7 +38,7 @@ def main():
             continue
         _, best, med, h = line[0].split()
         ref = ref or h
-        print(f"{cfg} poll={p:14s} best={float(best):7.3f} ms med={float(med):7.3f} ms same={h == ref}", flush=True)
+        print(f"{cfg} poll={p:28s} best={float(best):7.3f} ms med={float(med):7.3f} ms same={h == ref}", flush=True)
 
 
 if __name__ == "__main__":
