@@ -261,10 +261,11 @@ PRISM_API prism_status prism_peak_memory_at(prism_graph_t g, int32_t scenario, i
  *   3. all-gather the n handles (the Python binding uses torch.distributed), then
  *      prism_shard_connect(g, handles[n]) opens the peers' buffers; or, when all shards live in
  *      one process, prism_shard_connect_local(g, graphs[n]);
- *   4. prism_replay / prism_replay_async with n == S on every shard. The replays of all shards
- *      must run concurrently (one process per GPU, or independent streams of one process), since
- *      a shard's kernel waits for its peers' ready times; a shard that never arrives is reported
- *      by the device watchdog as PRISM_E_DEADLOCK after 10 s instead of hanging the GPU.
+ *   4. prism_replay / prism_replay_async with n == S on every shard (one process per GPU); the
+ *      replays of all shards run concurrently, since a shard's kernel waits for its peers' ready
+ *      times; a shard that never arrives is reported by the device watchdog as PRISM_E_DEADLOCK
+ *      (10 s) instead of hanging the GPU. Shards sharing one device replay together through
+ *      prism_replay_local_shards.
  * prism_peak_memory returns all world peaks on every shard (the structure is replicated);
  * prism_query_rank answers for the shard's own ranks (PRISM_E_INVALID_ARG names the owner
  * otherwise). Replaying a sharded graph before connect, or with n != S, is PRISM_E_INVALID_ARG.
@@ -275,6 +276,17 @@ PRISM_API prism_status prism_peak_memory_at(prism_graph_t g, int32_t scenario, i
 PRISM_API prism_status prism_shard_prepare(prism_graph_t g, int32_t n_scenarios, void *handle_out);
 PRISM_API prism_status prism_shard_connect(prism_graph_t g, const void *handles);
 PRISM_API prism_status prism_shard_connect_local(prism_graph_t g, const prism_graph_t *shards);
+/* Shards living on ONE device (connected with prism_shard_connect_local) cannot rely on separate
+ * launches running concurrently (CUDA does not guarantee it; profilers and MPS serialise them),
+ * so they replay together: one cooperative launch covers every shard's cells (co-residency is
+ * checked before the launch), the exchange between shards runs through the same peer-memory
+ * protocol, and one reduce writes T_k (n int64, DEVICE pointer) on shards[0]'s stream, ordered
+ * after and before the other shards' streams. Every shard records its own ranks' times (query
+ * them on the owning shard). The shards must carry the same duration overrides (the launch reads
+ * shards[0]'s graph structure). prism_replay / _async on such a shard return PRISM_E_INVALID_ARG,
+ * as does prism_shard_connect when a peer's buffer is on the caller's own device. */
+PRISM_API prism_status prism_replay_local_shards(const prism_graph_t *shards, int32_t n, const prism_scenarios *sc,
+                                                 int64_t *iter_ns_dev_out);
 /* Move the connected exchange buffer (and the peers' mapping of it) of `from` to a newly built
  * graph g of the same plan and shard (a rebuilt graph keeps its communicator; SPMD: every shard
  * adopts at the same point of its call sequence). Waits for `from`'s stream unless both graphs

@@ -14,7 +14,8 @@ from typing import Dict, Optional
 
 import numpy as np
 
-__all__ = ["lib", "Graph", "plan", "PrismError", "build_library", "LIB_PATH", "EXPORTED_SYMBOLS"]
+__all__ = ["lib", "Graph", "plan", "PrismError", "build_library", "LIB_PATH", "EXPORTED_SYMBOLS",
+           "replay_local_shards"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PRISM_LIB") or os.path.join(_HERE, "libprism_b200.so")  # PRISM_LIB: dev experiments
@@ -26,7 +27,7 @@ EXPORTED_SYMBOLS = [
     "prism_debug_export", "prism_plan", "prism_last_timing", "prism_last_algo",
     "prism_shard_prepare", "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
     "prism_set_durations", "prism_critical_path", "prism_peak_memory_at", "prism_sync",
-    "prism_debug_set", "prism_set_moe_load",
+    "prism_debug_set", "prism_set_moe_load", "prism_replay_local_shards",
 ]
 SHARD_HANDLE_BYTES = 64
 
@@ -129,6 +130,7 @@ def lib():
         L.prism_critical_path.argtypes = [P, ctypes.c_int32, P, ctypes.c_int64, P, P]
         L.prism_sync.argtypes = [P]
         L.prism_set_moe_load.argtypes = [P, P]
+        L.prism_replay_local_shards.argtypes = [P, ctypes.c_int32, P, P]
         L.prism_debug_set.argtypes = [P, ctypes.c_int32, ctypes.c_int64]
         for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
                      "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
@@ -136,7 +138,7 @@ def lib():
                      "prism_last_timing", "prism_last_algo", "prism_shard_prepare",
                      "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
                      "prism_set_durations", "prism_critical_path", "prism_peak_memory_at",
-                     "prism_sync", "prism_debug_set", "prism_set_moe_load"):
+                     "prism_sync", "prism_debug_set", "prism_set_moe_load", "prism_replay_local_shards"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
     return _lib
@@ -408,6 +410,16 @@ class Graph:
         out = np.zeros(max(1, count), dt)
         _check(lib().prism_debug_export(self._h, which, _ptr(out), out.nbytes))
         return out[:count]
+
+
+def replay_local_shards(graphs, iter_dev_ptr: int, n: int = 1, *, seed: int = 0x5EED, amp_q16: int = 0,
+                        kind_mask: int = 0, record: bool = True, first: int = 0) -> None:
+    """Row e, shards sharing one device (prism_replay_local_shards): one cooperative launch replays
+    every shard (graphs[i] = shard i, connected with shard_connect_local); n int64 iteration times
+    are written to the DEVICE pointer on graphs[0]'s stream."""
+    arr = (ctypes.c_void_p * len(graphs))(*[g._h.value for g in graphs])
+    sc = Graph._scen(n, seed, amp_q16, kind_mask, record, "auto", first)
+    _check(lib().prism_replay_local_shards(arr, len(graphs), ctypes.byref(sc), ctypes.c_void_p(iter_dev_ptr)))
 
 
 def gather_handles(mine: bytes, n_shards: int, shard_index: int, group=None):

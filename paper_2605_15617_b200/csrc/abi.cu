@@ -258,6 +258,8 @@ struct prism_graph_s {
   int32_t ex_S = 0, ex_Sp = 0;
   ShardLink link{};
   bool connected = false;
+  bool local_group = false;             // connected to peers on this same device: such shards can
+                                        // only replay together (prism_replay_local_shards)
   std::vector<void *> ipc_open;         // peer buffers opened with cudaIpcOpenMemHandle
   int64_t *part = nullptr;              // [S] local partial iteration times
   size_t part_bytes = 0;
@@ -821,6 +823,9 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   const bool sharded = G->n_shards > 1;
   if (sharded) {
     if (!G->connected) return fail(PRISM_E_INVALID_ARG, "sharded graph: call prism_shard_prepare and prism_shard_connect first");
+    if (G->local_group)
+      return fail(PRISM_E_INVALID_ARG, "shards on one device replay together in one cooperative launch "
+                                       "(prism_replay_local_shards): separate launches are not guaranteed to run concurrently");
     if (S != G->ex_S) return fail(PRISM_E_INVALID_ARG, "sharded graph: the replay's scenario count must equal prism_shard_prepare's");
     if (sc->algo == PRISM_ALGO_LEVELS) return fail(PRISM_E_INVALID_ARG, "sharded replays run on the cell kernel only");
     if (!cells_fit(G->cur(), cell_chunks)) return fail(PRISM_E_INVALID_ARG, "sharded replay: the shard's cells do not fit co-resident on the device");
@@ -1374,6 +1379,98 @@ prism_status prism_critical_path(prism_graph_t G, int32_t scenario, int32_t *pat
 
 // ---- row e: sharding ---------------------------------------------------------------------
 
+prism_status prism_replay_local_shards(const prism_graph_t *shards, int32_t n, const prism_scenarios *sc,
+                                       int64_t *iter_dev) {
+  if (!shards || !sc || !iter_dev || n < 2 || n > kMaxShards) return fail(PRISM_E_INVALID_ARG, "bad arguments");
+  prism_graph_t G0 = shards[0];
+  for (int i = 0; i < n; ++i) {
+    const prism_graph_t G = shards[i];
+    if (!G || G->n_shards != n || G->shard != i || !G->connected || !G->local_group || G->device != G0->device ||
+        G->ex_S != sc->n || G->parity != G0->parity || G->plan.W != G0->plan.W || G->ov_active != G0->ov_active)
+      return fail(PRISM_E_INVALID_ARG, "shard " + std::to_string(i) + " is not a connected local shard of this group "
+                                       "(same device, prepared for this scenario count, replayed together)");
+  }
+  if (sc->amp_q16 < 0 || sc->amp_q16 > 65535 || sc->algo == PRISM_ALGO_LEVELS || sc->algo == PRISM_ALGO_RANKS ||
+      sc->first < 0 || (int64_t)sc->first + sc->n > (1LL << 31) - 1)
+    return fail(PRISM_E_INVALID_ARG, "bad scenario batch for a sharded replay (cell kernel only)");
+  CU(cudaSetDevice(G0->device));
+  const Plan &P = G0->plan;
+  const int32_t S = sc->n;
+  const int SC = cells_chunk_scenarios();
+  const int nchunks = (S + SC - 1) / SC;
+  const int32_t Sp = nchunks * SC;
+  if (!cells_fit(G0->cur(), nchunks, n))
+    return fail(PRISM_E_INVALID_ARG, "the local shards' cells do not fit co-resident on the device");
+  ScenParams p{};
+  p.S = S;
+  p.first = sc->first;
+  p.amp = sc->amp_q16;
+  p.seed = sc->seed;
+  p.mask = sc->kind_mask;
+  p.record = sc->record ? 1 : 0;
+  p.mod = 2 * sc->amp_q16 + 1;
+  p.mod_magic = ~0ULL / (uint64_t)p.mod + 1;
+  p.mod_m32 = p.mod > 1 ? (uint32_t)((((uint64_t)1 << 32) + (uint64_t)p.mod - 1) / (uint64_t)p.mod) : 0xFFFFFFFFu;
+  cudaStream_t st = G0->stream;
+  ShardLink L = G0->link;
+  L.lg = n;
+  for (int i = 0; i < n; ++i) {
+    prism_graph_t G = shards[i];
+    G->recorded = 0;
+    if (p.record && !G->ensure(G->fin, G->fin_bytes, (size_t)std::max<int64_t>(1, G->fin_rows) * Sp * 8))
+      return fail(PRISM_E_OOM, "fin allocation failed");
+    if (!G->ensure(G->gfin, G->gfin_bytes, (size_t)P.G * Sp * 8)) return fail(PRISM_E_OOM, "gfin allocation failed");
+    if (!G->ensure(G->rank_end, G->rank_end_bytes, (size_t)P.W * Sp * 8)) return fail(PRISM_E_OOM, "rank_end allocation failed");
+    L.lg_fin[i] = p.record ? G->fin : nullptr;
+    L.lg_gfin[i] = G->gfin;
+    L.lg_rank_end[i] = G->rank_end;
+  }
+  // every shard's earlier work (builds, overrides) is ordered before the launch on shard 0's stream
+  std::vector<cudaEvent_t> evs;
+  auto join = [&](cudaStream_t from, cudaStream_t to) -> cudaError_t {
+    if (from == to) return cudaSuccess;
+    cudaEvent_t e;
+    cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (r != cudaSuccess) return r;
+    evs.push_back(e);
+    r = cudaEventRecord(e, from);
+    return r == cudaSuccess ? cudaStreamWaitEvent(to, e, 0) : r;
+  };
+  for (int i = 1; i < n; ++i) CU(join(shards[i]->stream, st));
+  CU(launch_replay_guard(G0->words, nullptr, 0, nullptr, 0, G0->parity, st));
+  G0->rec(2);
+  const int per_launch = cells_chunks_per_launch(G0->cur(), nchunks, n);
+  int64_t launches = 1;
+  for (int ch = 0; ch < nchunks; ch += per_launch) {
+    CU(launch_cells(G0->cur(), p, nullptr, nullptr, nullptr, nullptr, G0->words, G0->parity, nullptr, nullptr, nullptr,
+                    ch, std::min(per_launch, nchunks - ch), Sp, &L, st));
+    ++launches;
+  }
+  for (int i = 0; i < n; ++i) {  // accumulators and counters of every shard's exchange buffer
+    prism_graph_t G = shards[i];
+    CU(cudaMemsetAsync(G->ex + G->link.o_acc, 0, (size_t)P.G_large * Sp * 8, st));
+    CU(cudaMemsetAsync(G->ex + G->link.o_arrive, 0, (size_t)P.G_large * nchunks * 4, st));
+    G->parity ^= 1;
+  }
+  G0->rec(3);
+  G0->rec(4);
+  CU(launch_local_group_reduce(G0->cur(), L, S, Sp, iter_dev, st));
+  ++launches;
+  G0->rec(5);
+  CU(cudaMemcpyAsync(G0->h_status, G0->words, 8, cudaMemcpyDeviceToHost, st));
+  for (int i = 1; i < n; ++i) CU(join(st, shards[i]->stream));
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);  // released once their work is done
+  for (int i = 0; i < n; ++i) {
+    prism_graph_t G = shards[i];
+    G->last = p;
+    G->last_Sp = Sp;
+    G->recorded = p.record;
+    G->last_algo = PRISM_ALGO_CELLS;
+    G->launches = launches;
+  }
+  return PRISM_OK;
+}
+
 prism_status prism_shard_prepare(prism_graph_t G, int32_t n_scenarios, void *handle_out) {
   if (!G || !handle_out) return fail(PRISM_E_INVALID_ARG, "null argument");
   if (G->n_shards < 2) return fail(PRISM_E_INVALID_ARG, "graph was not built with n_shards > 1");
@@ -1442,7 +1539,15 @@ prism_status prism_shard_connect(prism_graph_t G, const void *handles) {
     }
     G->ipc_open.push_back(p);
     G->link.base[m] = (unsigned char *)p;
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.device == G->device &&
+        !std::getenv("PRISM_ALLOW_SAME_DEVICE_IPC"))
+      return fail(PRISM_E_INVALID_ARG, "shard " + std::to_string(m) + " lives on this process's device: separate "
+                                       "processes' replays of one GPU are not guaranteed to run concurrently (set "
+                                       "PRISM_ALLOW_SAME_DEVICE_IPC=1 for experiments; use one process per GPU)");
+    cudaGetLastError();
   }
+  G->local_group = false;
   G->connected = true;
   return PRISM_OK;
 }
@@ -1465,6 +1570,9 @@ prism_status prism_shard_connect_local(prism_graph_t G, const prism_graph_t *sha
     }
     G->link.base[m] = o->ex;
   }
+  bool same = false;
+  for (int m = 0; m < G->n_shards; ++m) same |= m != G->shard && shards[m]->device == G->device;
+  G->local_group = same;
   G->connected = true;
   return PRISM_OK;
 }
@@ -1487,6 +1595,7 @@ prism_status prism_shard_adopt(prism_graph_t G, prism_graph_t from) {
   G->link = from->link;
   G->parity = from->parity;
   G->ipc_open = std::move(from->ipc_open);
+  G->local_group = from->local_group;
   G->connected = true;
   from->ex = nullptr;
   from->ipc_open.clear();

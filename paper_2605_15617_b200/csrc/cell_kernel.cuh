@@ -181,6 +181,15 @@ __device__ __forceinline__ void prefetch_cross(const DevGraph &g, const XOp &xo,
   }
 }
 
+// The exchange arrays a warp polls and accumulates into: the graph's own (unsharded) or its
+// shard's exchange buffer (sharded; in a local-group launch the CTA's shard is derived from its
+// index), plus the shard index for the lean-path check.
+struct XBuf {
+  int64_t *rslot, *acc, *rres;
+  uint32_t *arrive;
+  int32_t self;
+};
+
 // Per-warp shared scratch of the cross-cell path.
 template <int C>
 struct CrossScratch {
@@ -207,7 +216,7 @@ struct CrossScratch {
 // deposit / arrive for every rank first, then poll (every poll of a pass is an independent load,
 // folded on the fly, the own slot is not read back), then finish = max over groups + dur'.
 template <bool SH, int C>
-__device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p, const CellArgs &a,
+__device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p, const CellArgs &a, const XBuf &xb,
                                           int64_t *__restrict__ gfin, int64_t *ts, int32_t ns,
                                           int32_t k, CrossScratch<C> &cs, const PreRec &pre, int tl) {
   const int lane = threadIdx.x & 31;
@@ -237,7 +246,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
       const int64_t off = (int64_t)(base + (int32_t)((meta >> 16) & 0x7FFF)) * Sp + k;
       const int64_t enc = tr ^ pm_dep;
       if (!SH) {
-        st_relaxed64(a.rslot + off, enc);
+        st_relaxed64(xb.rslot + off, enc);
       } else {
         for (uint32_t m = cs.smask[x]; m; m &= m - 1)
           st_relaxed_sys64(peer64(a.L, __ffs(m) - 1, a.L.o_rslot) + off, enc);
@@ -246,7 +255,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
       large_any = true;
       const int64_t off = (int64_t)base * Sp + k;
       if (!SH) {
-        red_max(a.acc + off, tr);
+        red_max(xb.acc + off, tr);
       } else {
         for (uint32_t m = cs.smask[x]; m; m &= m - 1) red_max_sys(peer64(a.L, __ffs(m) - 1, a.L.o_acc) + off, tr);
       }
@@ -277,7 +286,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
           if (cs.meta[x] & 0x80000000u) {
             const int64_t ai = (int64_t)cs.base[x] * a.nchunks + ck;
             uint32_t old;
-            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(a.arrive + ai) : "memory");
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(xb.arrive + ai) : "memory");
             if (old + 1 == (cs.meta[x] & 0xFFFF)) large_done |= 1u << x;
           }
       large_done = __shfl_sync(0xffffffffu, large_done, 0);
@@ -285,8 +294,8 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
       for (uint32_t m = large_done; m; m &= m - 1) {
         const int x = __ffs(m) - 1;
         const int64_t off = (int64_t)cs.base[x] * Sp + k;
-        const int64_t v = ld_relaxed64(a.acc + off);
-        st_relaxed64(a.rres + off, v ^ pm_dep);
+        const int64_t v = ld_relaxed64(xb.acc + off);
+        st_relaxed64(xb.rres + off, v ^ pm_dep);
         cs.vmax[x][lane] = v;
       }
     }
@@ -352,8 +361,8 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
       const uint32_t pr = cs.lpair[jr];
       const int32_t idx = cs.lidx[jr];
       const bool cnt = (pr & 0x80) && SH;
-      const int64_t *p64 = (pr & 0x80) ? a.rres + (int64_t)idx * Sp + k : a.rslot + (int64_t)idx * Sp + k;
-      const uint32_t *p32 = a.arrive + (int64_t)idx * a.nchunks + ck;
+      const int64_t *p64 = (pr & 0x80) ? xb.rres + (int64_t)idx * Sp + k : xb.rslot + (int64_t)idx * Sp + k;
+      const uint32_t *p32 = xb.arrive + (int64_t)idx * a.nchunks + ck;
       const int64_t need = (int64_t)(cs.meta[pr & 31] & 0xFFFF);
       uint32_t fs = 0, fsl = 0;
       while (true) {
@@ -377,12 +386,12 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
           if ((pending >> (pr & 31)) & 1u) {
             const int32_t idx = cs.lidx[j];
             if ((pr & 0x80) && SH)
-              v[u] = (int64_t)poll32<SH>(a.arrive + (int64_t)idx * a.nchunks + ck) -
+              v[u] = (int64_t)poll32<SH>(xb.arrive + (int64_t)idx * a.nchunks + ck) -
                      (int64_t)(cs.meta[pr & 31] & 0xFFFF);
             else if (pr & 0x80)  // the large group's result slot (published by its last arriver)
-              v[u] = poll64<SH>(a.rres + (int64_t)idx * Sp + k) ^ pm;
+              v[u] = poll64<SH>(xb.rres + (int64_t)idx * Sp + k) ^ pm;
             else
-              v[u] = poll64<SH>(a.rslot + (int64_t)idx * Sp + k) ^ pm;
+              v[u] = poll64<SH>(xb.rslot + (int64_t)idx * Sp + k) ^ pm;
           }
         }
       }
@@ -411,7 +420,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
     int64_t fr = 0;
     for (int32_t q = 0; q < ns; ++q) {
       const int x = r * ns + q;
-      int64_t m = ((cs.meta[x] & 0x80000000u) && SH) ? __ldcg(a.acc + (int64_t)cs.base[x] * Sp + k) : cs.vmax[x][lane];
+      int64_t m = ((cs.meta[x] & 0x80000000u) && SH) ? __ldcg(xb.acc + (int64_t)cs.base[x] * Sp + k) : cs.vmax[x][lane];
       const int64_t gd = cs.dur[x];
       const uint64_t uid = cs.uid[x];
       const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
@@ -434,7 +443,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
 // pair, issued kPollBatch at a time before any is folded. Same slots, encoding and results as
 // cross_all (which handles every other op).
 template <int C>
-__device__ __forceinline__ bool cross_pairs(const ScenParams &p, const CellArgs &a, int64_t *__restrict__ gfin,
+__device__ __forceinline__ bool cross_pairs(const ScenParams &p, const CellArgs &a, const XBuf &xb, int64_t *__restrict__ gfin,
                                             int64_t *ts, int32_t ns, int32_t k, CrossScratch<C> &cs,
                                             const PreRec &pre, int tl) {
   const int lane = threadIdx.x & 31;
@@ -446,7 +455,7 @@ __device__ __forceinline__ bool cross_pairs(const ScenParams &p, const CellArgs 
   const int32_t oslot = pre.base + own, pslot = pre.base + (own ^ 1);
   for (int x = 0, r = 0, q = 0; x < np; ++x) {  // deposit every pair first: no self-wait
     const int32_t os = __shfl_sync(0xffffffffu, oslot, x);
-    st_relaxed64(a.rslot + (int64_t)os * Sp + k, ts[r * 32 + lane] ^ pm);
+    st_relaxed64(xb.rslot + (int64_t)os * Sp + k, ts[r * 32 + lane] ^ pm);
     if (++q == ns) {
       q = 0;
       ++r;
@@ -463,7 +472,7 @@ __device__ __forceinline__ bool cross_pairs(const ScenParams &p, const CellArgs 
   const uint64_t sx = p.seed ^ ((uint64_t)kg * K_GOLD);
   if (a.fast_sleep_max) {  // fast wait on the pair the partners deposit last (see cross_all)
     const int32_t ps = __shfl_sync(0xffffffffu, pslot, np - 1);
-    const int64_t *p64 = a.rslot + (int64_t)ps * Sp + k;
+    const int64_t *p64 = xb.rslot + (int64_t)ps * Sp + k;
     while (!__all_sync(0xffffffffu, (ld_relaxed64(p64) ^ pm) >= 0)) {
       if (fs < a.fast_spin) ++fs;
       else if (wait_tick(a, fsl, tw, a.fast_sleep0, a.fast_sleep_max)) return false;
@@ -477,7 +486,7 @@ __device__ __forceinline__ bool cross_pairs(const ScenParams &p, const CellArgs 
         const int x = x0 + u;
         const int32_t ps = __shfl_sync(0xffffffffu, pslot, x & 31);
         v[u] = -1;
-        if (x < np && ((pending >> x) & 1u)) v[u] = ld_relaxed64(a.rslot + (int64_t)ps * Sp + k) ^ pm;
+        if (x < np && ((pending >> x) & 1u)) v[u] = ld_relaxed64(xb.rslot + (int64_t)ps * Sp + k) ^ pm;
       }
 #pragma unroll
       for (int u = 0; u < PB; ++u) {
@@ -550,9 +559,33 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
   const int32_t unit = blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (unit >= a.n_units || unit == g.stall_unit) return;  // stall_unit: watchdog test hook
   constexpr bool PAIR = C >= 4 && !PR && !MS;  // (compute, TP) pairs in one iteration
-  const int32_t cells = g.pp * (g.d1 - g.d0);  // this shard's cells (all of them unsharded)
-  const int32_t cell = unit % cells, chunk = a.chunk0 + unit / cells;
-  const int32_t s = cell % g.pp, dpi = g.d0 + cell / g.pp;
+  // row e: this CTA's shard (a local-group launch covers every shard of the device, units grouped
+  // by shard) and its DP block, exchange buffer and output arrays
+  int32_t shard = SH ? a.L.self : 0, d0 = g.d0, d1 = g.d1, u = unit;
+  int64_t fnode0 = g.fin_node0;
+  if (SH && a.L.lg > 0) {
+    const int32_t per = a.n_units / a.L.lg, blk = g.dp / g.n_shards;
+    shard = unit / per;
+    u = unit - shard * per;
+    d0 = shard * blk;
+    d1 = d0 + blk;
+    // a DP block is one contiguous row range under TP_PP_DP; Megatron order keeps all rows
+    fnode0 = g.order == PRISM_ORDER_MEGATRON ? 0 : (int64_t)shard * g.fin_rows;
+    fin = a.L.lg_fin[shard];
+    gfin = a.L.lg_gfin[shard];
+    rank_end = a.L.lg_rank_end[shard];
+  }
+  XBuf xb{a.rslot, a.acc, a.rres, a.arrive, shard};
+  if (SH) {
+    unsigned char *eb = a.L.base[shard];
+    xb.rslot = (int64_t *)(eb + a.L.o_rslot);
+    xb.acc = (int64_t *)(eb + a.L.o_acc);
+    xb.rres = nullptr;
+    xb.arrive = (uint32_t *)(eb + a.L.o_arrive);
+  }
+  const int32_t cells = g.pp * (d1 - d0);  // this shard's cells (all of them unsharded)
+  const int32_t cell = u % cells, chunk = a.chunk0 + u / cells;
+  const int32_t s = cell % g.pp, dpi = d0 + cell / g.pp;
   const int32_t Sp = a.Sp;
   const int32_t k = chunk * SC + lane;
   __shared__ int64_t ts[C * 32];  // chain state of the cross-cell path (rolled over ranks)
@@ -627,7 +660,7 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
   }
   // fin rows of op i (graph.h fin_off): the cell's C ranks are C consecutive 32-lane rows of this
   // chunk, and op i + 1's rows follow: one moving pointer, rank r at the constant offset r * 32
-  int64_t *fp = fin ? fin + fin_off(g, (int64_t)rb[0], k, Sp) : nullptr;
+  int64_t *fp = fin ? fin + (((int64_t)(k / SC) * g.fin_rows + rb[0] - fnode0) * SC + (k % SC)) : nullptr;
   for (int32_t base = 0; base < len; base += 32) {
     const int32_t cnt = min(32, len - base);
     const uint32_t bcls = ncls;
@@ -767,9 +800,9 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
         // peer touches their ready slots in the local exchange buffer, so gpu scope suffices
         const bool lean = (C >= 4 || a.lean > 1) && a.lean &&
                           __all_sync(0xffffffffu, lane >= C * xo.ns || ((pre.meta & 0x8000FFFFu) == 2u &&
-                                                                        (!SH || pre.smask == (1u << a.L.self))));
-        const bool ok = lean ? cross_pairs<C>(p, a, gfin, ts, xo.ns, k, cs, pre, tl)
-                             : cross_all<SH, C>(g, p, a, gfin, ts, xo.ns, k, cs, pre, tl);
+                                                                        (!SH || pre.smask == (1u << xb.self))));
+        const bool ok = lean ? cross_pairs<C>(p, a, xb, gfin, ts, xo.ns, k, cs, pre, tl)
+                             : cross_all<SH, C>(g, p, a, xb, gfin, ts, xo.ns, k, cs, pre, tl);
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < C; ++r) t[r] = ts[r * 32 + lane];

@@ -234,9 +234,12 @@ constexpr int kMaxShards = 16;
 struct ShardLink {
   int32_t n, self;                 // shards, this shard (n = 0: unsharded)
   uint32_t epoch;                  // replays since prepare, 1-based (flags of this replay)
-  int32_t pad;
+  int32_t lg;                      // > 0: a local-group launch replaying shards 0..lg-1 of one device
+                                   // in ONE cooperative grid (prism_replay_local_shards)
   unsigned char *base[kMaxShards];  // exchange buffer of every shard (peer-mapped), own included
   int64_t o_rslot, o_acc, o_arrive, o_part, o_flag;  // byte offsets inside a buffer
+  // local-group launches: every shard's own output arrays (the structure is the same graph)
+  int64_t *lg_fin[kMaxShards], *lg_gfin[kMaxShards], *lg_rank_end[kMaxShards];
 };
 
 // Tile of a level launch: `cnt` concrete groups of quotient group `q` starting at instance `i0`.
@@ -258,13 +261,17 @@ cudaError_t launch_query(const DevGraph &g, const ScenParams &p, int32_t Sp, con
                          const int64_t *gfin, int32_t rank, int32_t scen, int64_t *start_out,
                          int64_t *finish_out, cudaStream_t st);
 // replay_cells.cu (cell kernel); cudaErrorCooperativeLaunchTooLarge = does not fit, use levels
-bool cells_fit(const DevGraph &g, int nchunks);
+// group > 1: a local-group launch covering `group` shards of one device (prism_replay_local_shards)
+bool cells_fit(const DevGraph &g, int nchunks, int group = 1);
 int cells_chunk_scenarios();
-int cells_chunks_per_launch(const DevGraph &g, int nchunks);
+int cells_chunks_per_launch(const DevGraph &g, int nchunks, int group = 1);
 cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc,
                          int64_t *rres, uint32_t *arrive, uint32_t *status, int parity, int64_t *fin,
                          int64_t *gfin, int64_t *rank_end, int chunk0, int nchunks_launch, int Sp,
                          const ShardLink *link, cudaStream_t st);
+// row e, local group: T_k = max over the shards' own ranks' rank_end (all on this device)
+cudaError_t launch_local_group_reduce(const DevGraph &g, const ShardLink &link, int32_t S, int32_t Sp,
+                                      int64_t *iter, cudaStream_t st);
 // row e: iteration times of a sharded replay (local partial max, peer exchange, global max)
 cudaError_t launch_shard_reduce(const DevGraph &g, const ShardLink &link, int32_t S, int32_t Sp,
                                 const int64_t *rank_end, int64_t *part_local, int64_t *iter,

@@ -214,6 +214,34 @@ __global__ void __launch_bounds__(256) shard_partial_kernel(DevGraph g, int32_t 
   }
 }
 
+// Row e, local-group launch (prism_replay_local_shards): every shard of the device wrote its own
+// ranks' rank_end rows into its own array; T_k = max over shards and their ranks (one block per
+// scenario).
+__global__ void __launch_bounds__(256) local_group_reduce_kernel(DevGraph g, ShardLink L, int32_t Sp,
+                                                                 int64_t *__restrict__ iter) {
+  const int32_t k = blockIdx.x;
+  const int32_t blk = g.dp / g.n_shards;
+  const int32_t nloc = g.tp * g.pp * blk;
+  int64_t m = 0;
+  for (int32_t sh = 0; sh < L.lg; ++sh) {
+    const int64_t *re = L.lg_rank_end[sh];
+    for (int32_t x = threadIdx.x; x < nloc; x += blockDim.x) {
+      const int32_t tpi = x % g.tp, s = (x / g.tp) % g.pp, dpi = sh * blk + x / (g.tp * g.pp);
+      const int32_t r = g.order == PRISM_ORDER_MEGATRON ? tpi + g.tp * (dpi + g.dp * s)
+                                                        : tpi + g.tp * (s + g.pp * dpi);
+      m = max(m, re[(int64_t)r * Sp + k]);
+    }
+  }
+  for (int off = 16; off; off >>= 1) m = max(m, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off));
+  __shared__ int64_t wm[8];
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) m = max(m, wm[w]);
+    iter[k] = max(m, wm[0]);
+  }
+}
+
 // Row e: exchange of the partials over peer memory, then T_k = max over shards. One block: store
 // this shard's S partials into slot [epoch & 1][self] of every shard's buffer, fence (system
 // scope), publish flag[self] = epoch at every shard, wait for every shard's flag, reduce. The two
@@ -519,12 +547,19 @@ cudaError_t preload_replay_kernels() {
   cudaFuncAttributes a;
   const void *fns[] = {(const void *)reduce_iter_kernel, (const void *)shard_partial_kernel,
                        (const void *)shard_exchange_kernel, (const void *)query_kernel,
-                       (const void *)peak_time_kernel, (const void *)replay_guard_kernel};
+                       (const void *)peak_time_kernel, (const void *)replay_guard_kernel,
+                       (const void *)local_group_reduce_kernel};
   for (const void *f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t launch_local_group_reduce(const DevGraph &g, const ShardLink &link, int32_t S, int32_t Sp,
+                                      int64_t *iter, cudaStream_t st) {
+  local_group_reduce_kernel<<<S, 256, 0, st>>>(g, link, Sp, iter);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_shard_reduce(const DevGraph &g, const ShardLink &link, int32_t S, int32_t Sp,

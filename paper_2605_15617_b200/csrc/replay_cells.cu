@@ -138,15 +138,15 @@ PollPolicy poll_policy() {
 // else the caller launches one chunk at a time (chunk groups of 1).
 int64_t cell_count(const DevGraph &g) { return (int64_t)g.pp * (g.d1 - g.d0); }
 
-bool cells_fit(const DevGraph &g, int nchunks) {
-  return cell_fit_units(g, cell_count(g), nullptr) && nchunks >= 1;
+bool cells_fit(const DevGraph &g, int nchunks, int group) {
+  return cell_fit_units(g, cell_count(g) * group, nullptr) && nchunks >= 1;
 }
 
 int cells_chunk_scenarios() { return SC; }
 
-int cells_chunks_per_launch(const DevGraph &g, int nchunks) {
+int cells_chunks_per_launch(const DevGraph &g, int nchunks, int group) {
   for (int c = nchunks; c > 1; --c)
-    if (nchunks % c == 0 && cell_fit_units(g, cell_count(g) * c, nullptr)) return c;
+    if (nchunks % c == 0 && cell_fit_units(g, cell_count(g) * c * group, nullptr)) return c;
   return 1;
 }
 
@@ -154,7 +154,8 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
                          int64_t *rres, uint32_t *arrive, uint32_t *status, int parity, int64_t *fin,
                          int64_t *gfin, int64_t *rank_end, int chunk0, int nchunks_launch, int Sp,
                          const ShardLink *link, cudaStream_t st) {
-  const int64_t units = cell_count(g) * nchunks_launch;
+  // a local-group launch (link->lg shards of this device) covers every shard's cells
+  const int64_t units = cell_count(g) * nchunks_launch * (link && link->lg > 0 ? link->lg : 1);
   int ctas = 0;
   if (!cell_fit_units(g, units, &ctas)) return cudaErrorCooperativeLaunchTooLarge;
   // the launch covers chunks [chunk0, chunk0 + nchunks_launch) of the replay's Sp / 32 chunks

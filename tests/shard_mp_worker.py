@@ -22,14 +22,14 @@ for rep in range(3):
     t0 = time.time()
     try:
         it = g.replay(S, amp_q16=6554, kind_mask=7)
-        print(rank, "rep", rep, "ok", it[:3].tolist(), round(time.time() - t0, 3), flush=True)
+        print(rank, "rep", rep, "ok", it.tolist(), round(time.time() - t0, 3), flush=True)
     except Exception as e:
         print(rank, "rep", rep, "err", e, round(time.time() - t0, 3), flush=True)
         g.shard_connect_dist(S)
     dist.barrier()
 if rank == 0:
     import oracle
-    print("ref", oracle.replay(tm, S, amp_q16=6554, kind_mask=7)["iter"][:3].tolist())
+    print("ref", oracle.replay(tm, S, amp_q16=6554, kind_mask=7, threads=8)["iter"].tolist())
 dist.barrier()
 g.close()
 dist.destroy_process_group()

@@ -194,25 +194,22 @@ def test_world_collectives_large_groups(prism, algo):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
-def test_full_size_sampled(prism, name):
-    """(auto schedule = the cell kernel at these sizes, as bench.py runs it)"""
-    """BASELINE.json full sizes in the bench launch configuration (S = 64, +-10% jitter): the
-    iteration time of sampled scenarios and every rank's peak equal the oracle's."""
+def test_full_size(prism, name):
+    """BASELINE.json full sizes in the bench launch configuration (auto schedule = the cell kernel,
+    S = 64, +-10% jitter): all 64 iteration times, every rank's last finish in the first and last
+    scenario, and every rank's peak equal the oracle's (the oracle on all host threads)."""
     tm = w.config(name)
     g = _graph(prism, tm)
     S = 64
     it = g.replay(S, amp_q16=6554, kind_mask=7)
     pk = g.peak_memory()
-    ks = [0, 1, 63]
-    res = [oracle.replay(tm, 1, scen_first=k, amp_q16=6554, kind_mask=7, peaks=(k == 0)) for k in ks]
-    for k, r in zip(ks, res):
-        assert it[k] == r["iter"][0], (name, k)
-    assert np.array_equal(pk, res[0]["peak"][0])
-    # per-rank end times of scenario 63 via query of sampled ranks
-    rp = g.export("rank_ptr")
-    for rk in np.random.default_rng(1).choice(tm.topo.world, 16, replace=False):
-        st, fi, _ = g.query_rank(int(rk), 63)
-        assert fi[-1] == res[2]["rank_end"][0, rk] if len(fi) else True
+    ref = oracle.replay(tm, S, amp_q16=6554, kind_mask=7, peaks=False, threads=NPROC)
+    assert np.array_equal(it, ref["iter"]), name
+    assert np.array_equal(pk, oracle.replay(tm, 1)["peak"][0])
+    for k in (0, S - 1):
+        for rk in range(tm.topo.world):
+            _, fi, _ = g.query_rank(rk, k)
+            assert (fi[-1] if len(fi) else 0) == ref["rank_end"][k, rk], (name, k, rk)
     g.close()
 
 

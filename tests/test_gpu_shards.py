@@ -1,7 +1,10 @@
 """Row e on the GPU: the rank-sharded replay (DP blocks, peer-memory exchange inside the cell
 kernel) against the CPU oracle, bit-exact. All shards of a test live in one process on cuda:0,
-each with its own stream, connected with prism_shard_connect_local; the multi-process path differs
-only in how the exchange buffers are mapped (CUDA IPC, prism_shard_connect)."""
+each with its own stream, connected with prism_shard_connect_local and replayed together by
+prism_replay_local_shards (one cooperative launch over every shard's cells, the cross-shard
+exchange through the same peer-memory protocol as across GPUs); the multi-process path differs
+in how the exchange buffers are mapped (CUDA IPC, prism_shard_connect) and in running one launch
+per process."""
 import os
 
 import numpy as np
@@ -41,12 +44,13 @@ def _sharded(P, tm, n, S):
 
 def _replay_all(gs, S, **kw):
     import torch
+    import paper_2605_15617_b200 as P
 
-    outs = [torch.full((S,), -1, dtype=torch.int64, device="cuda") for _ in gs]
-    for g, o in zip(gs, outs):
-        g.replay_async(o.data_ptr(), S, **kw)
+    out = torch.full((S,), -1, dtype=torch.int64, device="cuda")
+    P.replay_local_shards(gs, out.data_ptr(), S, **kw)
     torch.cuda.synchronize()
-    return [o.cpu().numpy() for o in outs]
+    gs[0].sync()
+    return [out.cpu().numpy()]
 
 
 def _check(P, tm, n, S, reps=2, times=True, node_dur=None):
@@ -124,6 +128,17 @@ def test_shard_errors(prism):
         g.replay(4)
     assert e.value.name == "PRISM_E_INVALID_ARG"  # not connected
     g.close()
+    gs, _ = _sharded(prism, tm, 2, 8)
+    with pytest.raises(prism.PrismError) as e:  # same-device shards never replay in separate launches
+        gs[0].replay(8)
+    assert e.value.name == "PRISM_E_INVALID_ARG"
+    import torch
+
+    out = torch.zeros(8, dtype=torch.int64, device="cuda")
+    with pytest.raises(prism.PrismError):  # scenario count differs from prepare's
+        prism.replay_local_shards(gs, out.data_ptr(), 4)
+    for g in gs:
+        g.close()
 
 
 def test_multiprocess_ipc(prism, tmp_path):
@@ -133,7 +148,7 @@ def test_multiprocess_ipc(prism, tmp_path):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, SHARD_DEVICE="0")
+    env = dict(os.environ, SHARD_DEVICE="0", PRISM_ALLOW_SAME_DEVICE_IPC="1")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", "29517",
                         os.path.join(root, "tests", "shard_mp_worker.py"), "C2"],
@@ -158,3 +173,28 @@ def test_sharded_multistream_and_durations(prism, seed):
     tm.multistream = True
     d = np.random.default_rng(seed).integers(0, 900, tm.n_nodes) if seed % 2 else None
     _check(prism, tm, 2, [1, 5, 33][seed % 3], node_dur=d)
+
+
+_C5_REF = {}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_sharded_full_c5(prism, n):
+    """Full-size C5 (8192 ranks) sharded over 2 / 4 / 8 DP blocks of one device: all 64 iteration
+    times and the owning shard's per-op times of sampled ranks equal the oracle's."""
+    tm = w.config("C5")
+    S = 64
+    if "ref" not in _C5_REF:
+        _C5_REF["ref"] = oracle.replay(tm, S, amp_q16=6554, kind_mask=7, peaks=False, threads=NPROC)
+    ref = _C5_REF["ref"]
+    gs, _ = _sharded(prism, tm, n, S)
+    out = _replay_all(gs, S, amp_q16=6554, kind_mask=7)[0]
+    assert np.array_equal(out, ref["iter"])
+    for i, g in enumerate(gs):
+        own = prism.shard_ranks(tm.topo, n, i)
+        for r in (own[0], own[len(own) // 2], own[-1]):
+            _, fi, _ = g.query_rank(int(r), S - 1)
+            assert fi[-1] == ref["rank_end"][S - 1, r]
+    for g in gs:
+        g.close()
