@@ -198,6 +198,7 @@ def run_prism(args):
     # every timed step replays the same workload: identical results, or a step went wrong
     assert (its == iters[None, :]).all(), "timed steps disagree"
     st = graphs[0].stats()
+    shard_axis = graphs[0].shard_info()["axis"] if sharded else "none"
     launches_per_step = st["replay_launches"] + 3 + 1  # expand: rank tables, nodes, groups; peak
     if ws > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -291,8 +292,8 @@ def run_prism(args):
             "memberships": st["memberships"], "levels": st["levels"], "scenarios": S,
             "amp_q16": args.amp, "record_times": True, "schedule": schedule,
             "parallelism": ("single-gpu" if ws == 1 else
-                            f"ranks sharded over {ws} GPUs by DP block, exchange fused in the replay kernel "
-                            f"(NVLink peer memory)" if sharded else f"replicas{ws}"),
+                            f"ranks sharded over {ws} GPUs by {shard_axis.upper()} block, exchange fused in the "
+                            f"replay kernel (NVLink peer memory)" if sharded else f"replicas{ws}"),
             "l2": "working set (fin[N][S] = %.1f GB) > 126 MB L2; no flush needed" % (st["nodes"] * S * 8 / 1e9),
         },
         "extra": {

@@ -135,16 +135,18 @@ typedef struct {
                              default stream)                                                  */
   int32_t device;         /* CUDA device ordinal, -1 = current                                 */
   int32_t n_shards;       /* >= 1: the replay is sharded over n_shards GPUs (row e; see the
-                             "multi-GPU" section below); dp % n_shards == 0, n_shards <= 16   */
-  int32_t shard_index;    /* 0 .. n_shards-1: this shard replays the ranks with
-                             dp_i in [shard_index*dp/n_shards, (shard_index+1)*dp/n_shards)  */
+                             "multi-GPU" section below); n_shards <= 16 divides dp or pp     */
+  int32_t shard_index;    /* 0 .. n_shards-1: this shard replays the ranks of block shard_index
+                             of the shard axis (DP blocks or PP-stage blocks, below)          */
   int32_t flags;          /* PRISM_BUILD_PROFILE: record CUDA events around every kernel group */
 } prism_build_opts;
 
 /* PRISM_BUILD_PROFILE: record CUDA events around every kernel group (prism_last_timing).
  * PRISM_BUILD_ASYNC: return once the expansion is queued on the stream (later calls on the same
- * stream are ordered after it); by default prism_build_graph waits for it. */
-enum { PRISM_BUILD_PROFILE = 1, PRISM_BUILD_ASYNC = 2 };
+ * stream are ordered after it); by default prism_build_graph waits for it.
+ * PRISM_BUILD_SHARD_DP / _PP: force the shard axis of a sharded build (default: the axis whose
+ * blocks cut the fewest group memberships; every shard must resolve the same axis). */
+enum { PRISM_BUILD_PROFILE = 1, PRISM_BUILD_ASYNC = 2, PRISM_BUILD_SHARD_DP = 4, PRISM_BUILD_SHARD_PP = 8 };
 
 /* Scenario batch for what-if sweeps (re-time without structural change).
  * Scenario k gets perturbed durations d' = (d * (65536 + delta)) >> 16 with
@@ -242,9 +244,12 @@ PRISM_API prism_status prism_peak_memory_at(prism_graph_t g, int32_t scenario, i
 
 /* ---- multi-GPU (row e): rank sharding with a fused peer-memory exchange ---------------------
  *
- * The ranks are partitioned by DP block: shard i owns every rank whose dp coordinate lies in
- * [i*dp/n, (i+1)*dp/n) (north_star: "Ranks are sharded across the 8 B200s of one box"). TP groups
- * and P2P messages never cross a DP block, so only DP / EP / EDP / WORLD collectives span shards.
+ * The ranks are partitioned into n blocks along one axis (north_star: "Ranks are sharded across
+ * the 8 B200s of one box"): DP blocks (shard i owns every rank whose dp coordinate lies in
+ * [i*dp/n, (i+1)*dp/n); TP groups and P2P messages stay inside a block, DP / EP / EDP / WORLD
+ * collectives may span shards) or PP-stage blocks (pp coordinate in [i*pp/n, (i+1)*pp/n); every
+ * collective but WORLD stays inside a block, P2P messages at block edges span shards; SURVEY §8(e)
+ * picks these for the MoE config, whose EP all-to-alls would otherwise all cross shards).
  * Every shard holds the whole (replicated, O(N)) graph structure and replays only its own cells;
  * the cell kernel pushes the ready time of a member of a cross-shard group straight into the
  * exchange buffer of every shard holding a member of that group (NVLink peer stores and red.max
@@ -273,6 +278,9 @@ PRISM_API prism_status prism_peak_memory_at(prism_graph_t g, int32_t scenario, i
  * last replay of every shard has completed. */
 #define PRISM_SHARD_HANDLE_BYTES 64
 
+/* out[0..3] = n_shards, shard index, shard axis (0 = DP blocks, 1 = PP-stage blocks), block size
+ * (dp or pp coordinates per shard; 0 unsharded). */
+PRISM_API prism_status prism_shard_info(prism_graph_t g, int32_t out[4]);
 PRISM_API prism_status prism_shard_prepare(prism_graph_t g, int32_t n_scenarios, void *handle_out);
 PRISM_API prism_status prism_shard_connect(prism_graph_t g, const void *handles);
 PRISM_API prism_status prism_shard_connect_local(prism_graph_t g, const prism_graph_t *shards);

@@ -27,7 +27,7 @@ EXPORTED_SYMBOLS = [
     "prism_debug_export", "prism_plan", "prism_last_timing", "prism_last_algo",
     "prism_shard_prepare", "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
     "prism_set_durations", "prism_critical_path", "prism_peak_memory_at", "prism_sync",
-    "prism_debug_set", "prism_set_moe_load", "prism_replay_local_shards",
+    "prism_debug_set", "prism_set_moe_load", "prism_replay_local_shards", "prism_shard_info",
 ]
 SHARD_HANDLE_BYTES = 64
 
@@ -131,6 +131,7 @@ def lib():
         L.prism_sync.argtypes = [P]
         L.prism_set_moe_load.argtypes = [P, P]
         L.prism_replay_local_shards.argtypes = [P, ctypes.c_int32, P, P]
+        L.prism_shard_info.argtypes = [P, P]
         L.prism_debug_set.argtypes = [P, ctypes.c_int32, ctypes.c_int64]
         for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
                      "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
@@ -138,7 +139,8 @@ def lib():
                      "prism_last_timing", "prism_last_algo", "prism_shard_prepare",
                      "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
                      "prism_set_durations", "prism_critical_path", "prism_peak_memory_at",
-                     "prism_sync", "prism_debug_set", "prism_set_moe_load", "prism_replay_local_shards"):
+                     "prism_sync", "prism_debug_set", "prism_set_moe_load", "prism_replay_local_shards",
+                     "prism_shard_info"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
     return _lib
@@ -209,13 +211,16 @@ def plan(templates) -> Dict[str, int]:
 class Graph:
     """An expanded execution graph resident on one GPU (prism_build_graph)."""
 
+    SHARD_AXES = {"auto": 0, "dp": 4, "pp": 8}
+
     def __init__(self, templates, *, stream: Optional[int] = None, device: int = -1,
-                 profile: bool = False, n_shards: int = 1, shard_index: int = 0, asynchronous: bool = False):
+                 profile: bool = False, n_shards: int = 1, shard_index: int = 0, asynchronous: bool = False,
+                 shard_axis: str = "auto"):
         L = lib()
         self.topo = templates.topo
         self.n_shards, self.shard_index = int(n_shards), int(shard_index)
         self._topo, self._tm, self._keep = _marshal(templates)
-        flags = (1 if profile else 0) | (2 if asynchronous else 0)
+        flags = (1 if profile else 0) | (2 if asynchronous else 0) | self.SHARD_AXES[shard_axis]
         self._opts = _BuildOpts(stream or 0, device, self.n_shards, self.shard_index, flags)
         h = ctypes.c_void_p()
         self._h = None
@@ -366,6 +371,18 @@ class Graph:
         return path[: n.value], int(T.value)
 
     # ---------------------------------------------------------------- row e: sharding
+    def shard_info(self) -> Dict[str, object]:
+        """n_shards, shard, axis ('dp' or 'pp' blocks) and block size of this graph."""
+        out = np.zeros(4, np.int32)
+        _check(lib().prism_shard_info(self._h, _ptr(out)))
+        return {"n_shards": int(out[0]), "shard": int(out[1]), "axis": "pp" if out[2] == 1 else "dp",
+                "block": int(out[3])}
+
+    def owned_ranks(self):
+        """The global ranks this shard replays (all of them unsharded)."""
+        info = self.shard_info()
+        return shard_ranks(self.topo, info["n_shards"], info["shard"], info["axis"])
+
     def shard_prepare(self, n_scenarios: int) -> bytes:
         """Allocate this shard's exchange buffer for replays of n_scenarios; returns its IPC handle."""
         h = ctypes.create_string_buffer(SHARD_HANDLE_BYTES)
@@ -445,12 +462,20 @@ def shard_dp_block(dp: int, n_shards: int, shard_index: int):
     return b * shard_index, b * (shard_index + 1)
 
 
-def shard_ranks(topo, n_shards: int, shard_index: int):
-    """The global ranks a shard owns (every (tp, pp) coordinate of its DP block, reading Z1)."""
-    d0, d1 = shard_dp_block(topo.dp, n_shards, shard_index)
+def shard_ranks(topo, n_shards: int, shard_index: int, axis: str = "dp"):
+    """The global ranks a shard owns: every (tp, pp) coordinate of its DP block, or every (tp, dp)
+    coordinate of its PP-stage block (axis 'pp'); rank numbering of reading Z1."""
+    if n_shards <= 1:
+        return list(range(topo.tp * topo.pp * topo.dp))
+    if axis == "pp":
+        s0, s1 = shard_dp_block(topo.pp, n_shards, shard_index)
+        d0, d1 = 0, topo.dp
+    else:
+        d0, d1 = shard_dp_block(topo.dp, n_shards, shard_index)
+        s0, s1 = 0, topo.pp
     out = []
     for dpi in range(d0, d1):
-        for s in range(topo.pp):
+        for s in range(s0, s1):
             for t in range(topo.tp):
                 out.append(t + topo.tp * (s + topo.pp * dpi) if getattr(topo, "rank_order", 0) == 0
                            else t + topo.tp * (dpi + topo.dp * s))

@@ -408,6 +408,52 @@ prism_status prism_set_allocator(prism_alloc_fn alloc, prism_free_fn free_fn, vo
   return PRISM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// Row e, SURVEY §8.4 planner: the shard axis whose blocks cut the fewest memberships. DP blocks
+// (shard of a rank = dp_i / (dp/n)) keep TP groups and P2P messages local and cut DP and WORLD
+// collectives, EP all-to-alls wider than a block and EDP groups; PP-stage blocks keep every
+// collective but WORLD local and cut the P2P messages at block edges. opts->flags may force one.
+prism_status choose_shard_axis(const Plan &P, int n, int flags, int &axis, std::string &err) {
+  const bool dp_ok = P.topo.dp % n == 0, pp_ok = P.topo.pp % n == 0;
+  const bool want_dp = flags & PRISM_BUILD_SHARD_DP, want_pp = flags & PRISM_BUILD_SHARD_PP;
+  if (want_dp && want_pp) {
+    err = "PRISM_BUILD_SHARD_DP and PRISM_BUILD_SHARD_PP are exclusive";
+    return PRISM_E_INVALID_ARG;
+  }
+  if ((want_dp && !dp_ok) || (want_pp && !pp_ok) || (!dp_ok && !pp_ok)) {
+    err = "the shard count must divide dp (DP blocks) or pp (PP-stage blocks)";
+    return PRISM_E_INVALID_SPEC;
+  }
+  if (want_dp || !pp_ok) {
+    axis = 0;
+    return PRISM_OK;
+  }
+  if (want_pp || !dp_ok) {
+    axis = 1;
+    return PRISM_OK;
+  }
+  const int64_t Bd = P.topo.dp / n, Bp = P.topo.pp / n, ep = P.topo.ep;
+  int64_t cut_dp = 0, cut_pp = 0;
+  for (const QGroup &q : P.q) {
+    const int64_t m = (int64_t)q.inst * q.size;
+    switch (q.type) {
+      case PRISM_ROLE_DP: cut_dp += m; break;
+      case PRISM_ROLE_WORLD: cut_dp += m; cut_pp += m; break;
+      case PRISM_ROLE_EP: if (ep > Bd || Bd % ep != 0) cut_dp += m; break;
+      case PRISM_ROLE_EDP: if (q.size > 1) cut_dp += m; break;
+      case PRISM_ROLE_P2P: if (q.stage / Bp != q.stage2 / Bp) cut_pp += m; break;
+      default: break;
+    }
+  }
+  axis = cut_pp < cut_dp ? 1 : 0;
+  return PRISM_OK;
+}
+}  // namespace
+
+extern "C" {
+
 prism_status prism_plan(const prism_topology *topo, const prism_templates *tmpl, int64_t out[8]) {
   if (!topo || !tmpl || !out) return fail(PRISM_E_INVALID_ARG, "null argument");
   trace("build: begin");
@@ -435,14 +481,17 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const int shard = opts ? opts->shard_index : 0;
   if (n_shards > kMaxShards || shard < 0 || shard >= n_shards)
     return fail(PRISM_E_INVALID_ARG, "n_shards must be in [1, 16] and shard_index in [0, n_shards)");
-  if (topo->dp < 1 || topo->dp % n_shards != 0)
-    return fail(PRISM_E_INVALID_SPEC, "dp must be a multiple of n_shards (ranks are sharded by DP block)");
   trace("build: begin");
   Plan plan;
   std::string err;
   prism_status st = plan_graph(*topo, *tmpl, plan, err);
   if (st != PRISM_OK) return fail(st, err);
   trace("build: planned");
+  int axis = 0;
+  if (n_shards > 1) {
+    st = choose_shard_axis(plan, n_shards, opts ? opts->flags : 0, axis, err);
+    if (st != PRISM_OK) return fail(st, err);
+  }
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -476,14 +525,18 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.nq = (int32_t)P.q.size();
   d.n_shards = n_shards;
   d.shard = shard;
-  d.d0 = P.topo.dp / n_shards * shard;
-  d.d1 = P.topo.dp / n_shards * (shard + 1);
+  d.shard_axis = axis;
+  d.d0 = axis == 0 ? P.topo.dp / n_shards * shard : 0;
+  d.d1 = axis == 0 ? P.topo.dp / n_shards * (shard + 1) : P.topo.dp;
+  d.s0 = axis == 1 ? P.topo.pp / n_shards * shard : 0;
+  d.s1 = axis == 1 ? P.topo.pp / n_shards * (shard + 1) : P.topo.pp;
   G->n_shards = n_shards;
   G->shard = shard;
-  {  // fin rows kept by this graph: its DP block is one contiguous node range under TP_PP_DP
+  {  // fin rows kept by this graph: a DP block is one contiguous node range under TP_PP_DP (a PP
+     // block is not: PP-sharded graphs keep all rows)
     int64_t per_replica = 0;
     for (int s2 = 0; s2 < P.topo.pp; ++s2) per_replica += P.stage_len[s2] * P.topo.tp;
-    if (n_shards > 1 && P.topo.order == PRISM_ORDER_TP_PP_DP) {
+    if (n_shards > 1 && axis == 0 && P.topo.order == PRISM_ORDER_TP_PP_DP) {
       G->fin_node0 = per_replica * d.d0;
       G->fin_rows = per_replica * (d.d1 - d.d0);
     } else {
@@ -1114,9 +1167,11 @@ prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, i
   }
   const int64_t n = P.stage_len[pp_i];
   if (n_ops_out) *n_ops_out = n;
-  if (G->n_shards > 1 && (dp_i < G->dg.d0 || dp_i >= G->dg.d1) && start_ns)
+  if (G->n_shards > 1 && start_ns &&
+      (dp_i < G->dg.d0 || dp_i >= G->dg.d1 || pp_i < G->dg.s0 || pp_i >= G->dg.s1))
     return fail(PRISM_E_INVALID_ARG, "rank " + std::to_string(rank) + " is replayed by shard " +
-                                         std::to_string(dp_i / (t.dp / G->n_shards)));
+                                         std::to_string(G->dg.shard_axis == 1 ? pp_i / (t.pp / G->n_shards)
+                                                                              : dp_i / (t.dp / G->n_shards)));
   if (!G->recorded) return fail(PRISM_E_NOT_REPLAYED, "no replay with record != 0 has run on this graph");
   if (scenario < 0 || scenario >= G->last.S) return fail(PRISM_E_INVALID_ARG, "scenario outside the last replay");
   if (cap < n || (n > 0 && (!start_ns || !finish_ns))) return fail(PRISM_E_INVALID_ARG, "output capacity too small");
@@ -1600,6 +1655,15 @@ prism_status prism_shard_adopt(prism_graph_t G, prism_graph_t from) {
   from->ex = nullptr;
   from->ipc_open.clear();
   from->connected = false;
+  return PRISM_OK;
+}
+
+prism_status prism_shard_info(prism_graph_t G, int32_t out[4]) {
+  if (!G || !out) return fail(PRISM_E_INVALID_ARG, "null argument");
+  out[0] = G->n_shards;
+  out[1] = G->shard;
+  out[2] = G->dg.shard_axis;
+  out[3] = G->n_shards > 1 ? (G->dg.shard_axis == 1 ? G->plan.topo.pp : G->plan.topo.dp) / G->n_shards : 0;
   return PRISM_OK;
 }
 

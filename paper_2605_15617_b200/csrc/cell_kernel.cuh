@@ -561,16 +561,23 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
   constexpr bool PAIR = C >= 4 && !PR && !MS;  // (compute, TP) pairs in one iteration
   // row e: this CTA's shard (a local-group launch covers every shard of the device, units grouped
   // by shard) and its DP block, exchange buffer and output arrays
-  int32_t shard = SH ? a.L.self : 0, d0 = g.d0, d1 = g.d1, u = unit;
+  int32_t shard = SH ? a.L.self : 0, d0 = g.d0, d1 = g.d1, s0 = g.s0, s1 = g.s1, u = unit;
   int64_t fnode0 = g.fin_node0;
   if (SH && a.L.lg > 0) {
-    const int32_t per = a.n_units / a.L.lg, blk = g.dp / g.n_shards;
+    const int32_t per = a.n_units / a.L.lg;
     shard = unit / per;
     u = unit - shard * per;
-    d0 = shard * blk;
-    d1 = d0 + blk;
-    // a DP block is one contiguous row range under TP_PP_DP; Megatron order keeps all rows
-    fnode0 = g.order == PRISM_ORDER_MEGATRON ? 0 : (int64_t)shard * g.fin_rows;
+    if (g.shard_axis == 1) {  // PP-stage blocks: every shard keeps all rows
+      const int32_t blk = g.pp / g.n_shards;
+      s0 = shard * blk;
+      s1 = s0 + blk;
+    } else {
+      const int32_t blk = g.dp / g.n_shards;
+      d0 = shard * blk;
+      d1 = d0 + blk;
+      // a DP block is one contiguous row range under TP_PP_DP; Megatron order keeps all rows
+      fnode0 = g.order == PRISM_ORDER_MEGATRON ? 0 : (int64_t)shard * g.fin_rows;
+    }
     fin = a.L.lg_fin[shard];
     gfin = a.L.lg_gfin[shard];
     rank_end = a.L.lg_rank_end[shard];
@@ -583,9 +590,10 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
     xb.rres = nullptr;
     xb.arrive = (uint32_t *)(eb + a.L.o_arrive);
   }
-  const int32_t cells = g.pp * (d1 - d0);  // this shard's cells (all of them unsharded)
+  const int32_t nst = s1 - s0;
+  const int32_t cells = nst * (d1 - d0);  // this shard's cells (all of them unsharded)
   const int32_t cell = u % cells, chunk = a.chunk0 + u / cells;
-  const int32_t s = cell % g.pp, dpi = d0 + cell / g.pp;
+  const int32_t s = s0 + cell % nst, dpi = d0 + cell / nst;
   const int32_t Sp = a.Sp;
   const int32_t k = chunk * SC + lane;
   __shared__ int64_t ts[C * 32];  // chain state of the cross-cell path (rolled over ranks)

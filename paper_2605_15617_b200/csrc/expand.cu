@@ -128,9 +128,18 @@ __device__ __forceinline__ uint64_t group_uid_packed(const DevGraph &g, uint64_t
 
 // Row e: the shards holding a member of the group of a rank with DP coordinates (dpi, epi, edpi)
 // under the DP-block sharding (shard of dp_i = dp_i / (dp / n_shards)); TP groups and P2P
-// messages stay inside one DP coordinate, hence inside one shard.
-__device__ __forceinline__ uint32_t shard_mask(const DevGraph &g, int32_t type, int32_t dpi, int32_t epi,
+// messages stay inside one DP coordinate, hence inside one shard. Under PP-stage blocks (shard of
+// pp_i = pp_i / (pp / n_shards)) every collective but WORLD stays inside its stage; a P2P message
+// joins the sender's and the receiver's stage blocks.
+__device__ __forceinline__ uint32_t shard_mask(const DevGraph &g, const QGroup &q, int32_t dpi, int32_t epi,
                                                int32_t edpi) {
+  const int32_t type = q.type;
+  if (g.shard_axis == 1) {
+    const int32_t Bp = g.pp / g.n_shards;
+    if (type == PRISM_ROLE_WORLD) return g.n_shards >= 32 ? 0xFFFFFFFFu : (1u << g.n_shards) - 1u;
+    if (type == PRISM_ROLE_P2P) return (1u << (q.stage / Bp)) | (1u << (q.stage2 / Bp));
+    return 1u << (q.stage / Bp);
+  }
   const int32_t B = g.dp / g.n_shards;
   switch (type) {
     case PRISM_ROLE_DP:
@@ -305,7 +314,7 @@ __global__ void __launch_bounds__(256, 2) expand_nodes_kernel(DevGraph g) {
         g.h_meta[h] = (uint32_t)min(q.size, 0xFFFF) | ((uint32_t)min(j, 0x7FFF) << 16) | (large ? 0x80000000u : 0u);
         g.h_dur[h] = q.dur;
         g.h_uid[h] = group_uid(g, q, inst);
-        if (g.h_smask) g.h_smask[h] = shard_mask(g, q.type, dpi, epi, edpi);
+        if (g.h_smask) g.h_smask[h] = shard_mask(g, q, dpi, epi, edpi);
       }
     }
   }

@@ -12,8 +12,9 @@ namespace prism {
 // Plain device pointers; passed by value to kernels.
 struct DevGraph {
   int32_t W, pp, tp, dp, ep, order;
-  // row e: this shard replays the ranks with dp_i in [d0, d1) (d0 = 0, d1 = dp unsharded)
-  int32_t n_shards, shard, d0, d1;
+  // row e: this shard replays the ranks with dp_i in [d0, d1) and pp_i in [s0, s1) (everything
+  // unsharded); shard_axis 0 = DP blocks (d0/d1 vary), 1 = PP-stage blocks (s0/s1 vary)
+  int32_t n_shards, shard, d0, d1, s0, s1, shard_axis;
   // rows f1/f3/f4: node_sdur / h_dur / node_dur / grp_dur point at per-node override arrays and
   // compute spans / chained collectives last their own rank's value (prism_set_durations)
   int32_t per_rank_dur;

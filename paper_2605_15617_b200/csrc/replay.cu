@@ -196,10 +196,11 @@ __global__ void __launch_bounds__(256) shard_partial_kernel(DevGraph g, int32_t 
                                                             const int64_t *__restrict__ rank_end,
                                                             int64_t *__restrict__ part) {
   const int32_t k = blockIdx.x;
-  const int32_t nloc = g.tp * g.pp * (g.d1 - g.d0);
+  const int32_t ns = g.s1 - g.s0;
+  const int32_t nloc = g.tp * ns * (g.d1 - g.d0);
   int64_t m = 0;
   for (int32_t x = threadIdx.x; x < nloc; x += blockDim.x) {
-    const int32_t tpi = x % g.tp, s = (x / g.tp) % g.pp, dpi = g.d0 + x / (g.tp * g.pp);
+    const int32_t tpi = x % g.tp, s = g.s0 + (x / g.tp) % ns, dpi = g.d0 + x / (g.tp * ns);
     const int32_t r = g.order == PRISM_ORDER_MEGATRON ? tpi + g.tp * (dpi + g.dp * s)
                                                       : tpi + g.tp * (s + g.pp * dpi);
     m = max(m, rank_end[(int64_t)r * Sp + k]);
@@ -220,13 +221,15 @@ __global__ void __launch_bounds__(256) shard_partial_kernel(DevGraph g, int32_t 
 __global__ void __launch_bounds__(256) local_group_reduce_kernel(DevGraph g, ShardLink L, int32_t Sp,
                                                                  int64_t *__restrict__ iter) {
   const int32_t k = blockIdx.x;
-  const int32_t blk = g.dp / g.n_shards;
-  const int32_t nloc = g.tp * g.pp * blk;
+  const bool ppx = g.shard_axis == 1;
+  const int32_t ns = ppx ? g.pp / g.n_shards : g.pp, nd = ppx ? g.dp : g.dp / g.n_shards;
+  const int32_t nloc = g.tp * ns * nd;
   int64_t m = 0;
   for (int32_t sh = 0; sh < L.lg; ++sh) {
     const int64_t *re = L.lg_rank_end[sh];
+    const int32_t s0 = ppx ? sh * ns : 0, d0 = ppx ? 0 : sh * nd;
     for (int32_t x = threadIdx.x; x < nloc; x += blockDim.x) {
-      const int32_t tpi = x % g.tp, s = (x / g.tp) % g.pp, dpi = sh * blk + x / (g.tp * g.pp);
+      const int32_t tpi = x % g.tp, s = s0 + (x / g.tp) % ns, dpi = d0 + x / (g.tp * ns);
       const int32_t r = g.order == PRISM_ORDER_MEGATRON ? tpi + g.tp * (dpi + g.dp * s)
                                                         : tpi + g.tp * (s + g.pp * dpi);
       m = max(m, re[(int64_t)r * Sp + k]);

@@ -136,7 +136,7 @@ PollPolicy poll_policy() {
 
 // Chunks of 32 scenarios per unit; every chunk of a replay runs in one launch when they all fit,
 // else the caller launches one chunk at a time (chunk groups of 1).
-int64_t cell_count(const DevGraph &g) { return (int64_t)g.pp * (g.d1 - g.d0); }
+int64_t cell_count(const DevGraph &g) { return (int64_t)(g.s1 - g.s0) * (g.d1 - g.d0); }
 
 bool cells_fit(const DevGraph &g, int nchunks, int group) {
   return cell_fit_units(g, cell_count(g) * group, nullptr) && nchunks >= 1;

@@ -30,11 +30,11 @@ def prism():
     return P
 
 
-def _sharded(P, tm, n, S):
+def _sharded(P, tm, n, S, axis="auto"):
     import torch
 
     streams = [torch.cuda.Stream() for _ in range(n)]
-    gs = [P.Graph(tm, stream=streams[i].cuda_stream, n_shards=n, shard_index=i) for i in range(n)]
+    gs = [P.Graph(tm, stream=streams[i].cuda_stream, n_shards=n, shard_index=i, shard_axis=axis) for i in range(n)]
     for g in gs:
         g.shard_prepare(S)
     for g in gs:
@@ -53,8 +53,8 @@ def _replay_all(gs, S, **kw):
     return [out.cpu().numpy()]
 
 
-def _check(P, tm, n, S, reps=2, times=True, node_dur=None):
-    gs, _ = _sharded(P, tm, n, S)
+def _check(P, tm, n, S, reps=2, times=True, node_dur=None, axis="auto"):
+    gs, _ = _sharded(P, tm, n, S, axis)
     if node_dur is not None:
         for g in gs:
             g.set_durations(node_dur=node_dur)
@@ -73,7 +73,7 @@ def _check(P, tm, n, S, reps=2, times=True, node_dur=None):
         W = tm.topo.world
         rp = P.Graph(tm).export("rank_ptr")
         for i, g in enumerate(gs):
-            own = P.shard_ranks(tm.topo, n, i)
+            own = g.owned_ranks()
             for r in rng.choice(own, min(8, len(own)), replace=False):
                 for k in (0, S - 1):
                     st, fi, c = g.query_rank(int(r), k)
@@ -94,8 +94,29 @@ def test_sharded_scaled_dense(prism, name):
 
 @pytest.mark.parametrize("n", [2, 4, 8])
 def test_sharded_moe_ep_edp(prism, n):
-    """C4-shaped MoE (dp 8, ep 4): EP all-to-alls and EDP groups span shards for n >= 2."""
-    _check(prism, w.scaled("C4"), n, 33)
+    """C4-shaped MoE (dp 8, ep 4) forced onto DP blocks: EP all-to-alls and EDP groups span shards."""
+    _check(prism, w.scaled("C4"), n, 33, axis="dp")
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_sharded_moe_pp_blocks(prism, n):
+    """the MoE config sharded by PP-stage blocks (the planner's choice: EP
+    all-to-alls stay inside a shard, only P2P messages at block edges cross)."""
+    tm = w.scaled("C4")
+    g = prism.Graph(tm, n_shards=n, shard_index=0)
+    assert g.shard_info()["axis"] == "pp"
+    g.close()
+    _check(prism, tm, n, 33)
+
+
+@pytest.mark.parametrize("axis", ["dp", "pp"])
+@pytest.mark.parametrize("seed", range(400, 412))
+def test_sharded_axes_random(prism, axis, seed):
+    """Both shard axes forced on random templates (WORLD / EP / EDP collectives, batched P2P)."""
+    tm = w.random_templates(seed, max_world=32, max_ops=40)
+    if tm.topo.tp > 8 or (axis == "dp" and tm.topo.dp % 2) or (axis == "pp" and tm.topo.pp % 2):
+        pytest.skip("needs an even block count on the axis and tp <= 8")
+    _check(prism, tm, 2, [1, 5, 32, 40][seed % 4], axis=axis)
 
 
 @pytest.mark.parametrize("n", [2, 4])
@@ -192,7 +213,7 @@ def test_sharded_full_c5(prism, n):
     out = _replay_all(gs, S, amp_q16=6554, kind_mask=7)[0]
     assert np.array_equal(out, ref["iter"])
     for i, g in enumerate(gs):
-        own = prism.shard_ranks(tm.topo, n, i)
+        own = g.owned_ranks()
         for r in (own[0], own[len(own) // 2], own[-1]):
             _, fi, _ = g.query_rank(int(r), S - 1)
             assert fi[-1] == ref["rank_end"][S - 1, r]
