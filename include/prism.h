@@ -239,7 +239,8 @@ PRISM_API prism_status prism_peak_memory_async(prism_graph_t g, int64_t *peak_by
  * computed). For single-stream graphs this equals prism_peak_memory (program order = time order,
  * reading Z6); prism_peak_memory / _async of a multi-stream graph compute it for scenario 0.
  * PRISM_E_NOT_REPLAYED without a recorded replay; PRISM_E_NEGATIVE_MEMORY if a running total
- * drops below zero in time order; PRISM_E_INVALID_ARG beyond 4096 ops per rank or when sharded. */
+ * drops below zero in time order; PRISM_E_INVALID_ARG beyond 4096 ops per rank, or on a sharded
+ * graph whose scenario was not gathered (prism_shard_gather). */
 PRISM_API prism_status prism_peak_memory_at(prism_graph_t g, int32_t scenario, int64_t *peak_bytes_out);
 
 /* ---- multi-GPU (row e): rank sharding with a fused peer-memory exchange ---------------------
@@ -273,11 +274,20 @@ PRISM_API prism_status prism_peak_memory_at(prism_graph_t g, int32_t scenario, i
  *      prism_replay_local_shards.
  * prism_peak_memory returns all world peaks on every shard (the structure is replicated);
  * prism_query_rank answers for the shard's own ranks (PRISM_E_INVALID_ARG names the owner
- * otherwise). Replaying a sharded graph before connect, or with n != S, is PRISM_E_INVALID_ARG.
+ * otherwise) and, after prism_shard_gather of the scenario, for every rank. Replaying a sharded graph before connect, or with n != S, is PRISM_E_INVALID_ARG.
  * The exchange buffer is released with the graph; peers must destroy their graphs only after the
  * last replay of every shard has completed. */
 #define PRISM_SHARD_HANDLE_BYTES 64
 
+/* Per-rank outputs of a sharded replay gathered to every shard ("per-rank outputs
+ * are gathered to each caller"): collective over the shards (SPMD, every shard calls it after the
+ * same replay), it copies every shard's recorded finish times of scenario `scenario` into every
+ * shard's gather columns over NVLink peer stores (epoch-flag barrier, device watchdog). Until the
+ * next replay, prism_query_rank (any rank), prism_critical_path and prism_peak_memory_at answer
+ * that scenario on every shard; other scenarios stay owner-only / PRISM_E_INVALID_ARG.
+ * Synchronizes the stream. Shards of one device gather together: prism_shard_gather_local. */
+PRISM_API prism_status prism_shard_gather(prism_graph_t g, int32_t scenario);
+PRISM_API prism_status prism_shard_gather_local(const prism_graph_t *shards, int32_t n, int32_t scenario);
 /* out[0..3] = n_shards, shard index, shard axis (0 = DP blocks, 1 = PP-stage blocks), block size
  * (dp or pp coordinates per shard; 0 unsharded). */
 PRISM_API prism_status prism_shard_info(prism_graph_t g, int32_t out[4]);

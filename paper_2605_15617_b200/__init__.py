@@ -28,6 +28,7 @@ EXPORTED_SYMBOLS = [
     "prism_shard_prepare", "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
     "prism_set_durations", "prism_critical_path", "prism_peak_memory_at", "prism_sync",
     "prism_debug_set", "prism_set_moe_load", "prism_replay_local_shards", "prism_shard_info",
+    "prism_shard_gather", "prism_shard_gather_local",
 ]
 SHARD_HANDLE_BYTES = 64
 
@@ -132,6 +133,8 @@ def lib():
         L.prism_set_moe_load.argtypes = [P, P]
         L.prism_replay_local_shards.argtypes = [P, ctypes.c_int32, P, P]
         L.prism_shard_info.argtypes = [P, P]
+        L.prism_shard_gather.argtypes = [P, ctypes.c_int32]
+        L.prism_shard_gather_local.argtypes = [P, ctypes.c_int32, ctypes.c_int32]
         L.prism_debug_set.argtypes = [P, ctypes.c_int32, ctypes.c_int64]
         for name in ("prism_set_allocator", "prism_build_graph", "prism_replay", "prism_replay_async",
                      "prism_peak_memory", "prism_peak_memory_async", "prism_query_rank",
@@ -140,7 +143,7 @@ def lib():
                      "prism_shard_connect", "prism_shard_connect_local", "prism_shard_adopt",
                      "prism_set_durations", "prism_critical_path", "prism_peak_memory_at",
                      "prism_sync", "prism_debug_set", "prism_set_moe_load", "prism_replay_local_shards",
-                     "prism_shard_info"):
+                     "prism_shard_info", "prism_shard_gather", "prism_shard_gather_local"):
             getattr(L, name).restype = ctypes.c_int32
         _lib = L
     return _lib
@@ -383,6 +386,11 @@ class Graph:
         info = self.shard_info()
         return shard_ranks(self.topo, info["n_shards"], info["shard"], info["axis"])
 
+    def shard_gather(self, scenario: int) -> None:
+        """Collective over the shards (one per process): every rank's recorded times of `scenario`
+        to every shard, so query_rank / critical_path / peak_memory_at answer for all ranks."""
+        _check(lib().prism_shard_gather(self._h, int(scenario)))
+
     def shard_prepare(self, n_scenarios: int) -> bytes:
         """Allocate this shard's exchange buffer for replays of n_scenarios; returns its IPC handle."""
         h = ctypes.create_string_buffer(SHARD_HANDLE_BYTES)
@@ -437,6 +445,12 @@ def replay_local_shards(graphs, iter_dev_ptr: int, n: int = 1, *, seed: int = 0x
     arr = (ctypes.c_void_p * len(graphs))(*[g._h.value for g in graphs])
     sc = Graph._scen(n, seed, amp_q16, kind_mask, record, "auto", first)
     _check(lib().prism_replay_local_shards(arr, len(graphs), ctypes.byref(sc), ctypes.c_void_p(iter_dev_ptr)))
+
+
+def shard_gather_local(graphs, scenario: int) -> None:
+    """prism_shard_gather for the shards of one device (graphs[i] = shard i), in one launch."""
+    arr = (ctypes.c_void_p * len(graphs))(*[g._h.value for g in graphs])
+    _check(lib().prism_shard_gather_local(arr, len(graphs), int(scenario)))
 
 
 def gather_handles(mine: bytes, n_shards: int, shard_index: int, group=None):

@@ -258,7 +258,9 @@ struct prism_graph_s {
   int32_t ex_S = 0, ex_Sp = 0;
   ShardLink link{};
   bool connected = false;
-  bool local_group = false;             // connected to peers on this same device: such shards can
+  bool local_group = false;
+  uint32_t gather_epoch = 0;            // prism_shard_gather calls since prepare
+  int32_t gathered_k = -1;              // scenario held in the gather columns (-1: none)             // connected to peers on this same device: such shards can
                                         // only replay together (prism_replay_local_shards)
   std::vector<void *> ipc_open;         // peer buffers opened with cudaIpcOpenMemHandle
   int64_t *part = nullptr;              // [S] local partial iteration times
@@ -908,6 +910,7 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   p.mod_magic = ~0ULL / (uint64_t)p.mod + 1;
   p.mod_m32 = p.mod > 1 ? (uint32_t)((((uint64_t)1 << 32) + (uint64_t)p.mod - 1) / (uint64_t)p.mod) : 0xFFFFFFFFu;
   G->recorded = 0;
+  G->gathered_k = -1;
   trace("replay: begin");
   if (p.record) {
     if (!G->ensure(G->fin, G->fin_bytes, (size_t)std::max<int64_t>(1, G->fin_rows) * Sp * 8))
@@ -1054,6 +1057,30 @@ prism_status prism_replay(prism_graph_t G, const prism_scenarios *sc, int64_t *i
   return check_status(G);
 }
 
+// What a reader of the recorded times (query, critical path, time-ordered peak) sees for scenario
+// k: the graph's own fin / gfin, or — for a sharded graph after prism_shard_gather(k) — the gather
+// columns (every rank's finishes of that one scenario: the Sp = 1 layout, all rows, local index 0,
+// perturbation key shifted to the gathered scenario).
+struct ReadView {
+  DevGraph g;
+  ScenParams p;
+  const int64_t *fin, *gfin;
+  int32_t Sp, k;
+};
+static ReadView read_view(prism_graph_t G, int32_t scenario) {
+  ReadView v{G->cur(), G->last, G->fin, G->gfin, G->last_Sp, scenario};
+  if (G->n_shards > 1 && G->gathered_k == scenario && G->ex) {
+    v.g.fin_node0 = 0;
+    v.g.fin_rows = G->plan.N;
+    v.p.first = G->last.first + scenario;
+    v.fin = (const int64_t *)(G->ex + G->link.o_gcol);
+    v.gfin = (const int64_t *)(G->ex + G->link.o_ggcol);
+    v.Sp = 1;
+    v.k = 0;
+  }
+  return v;
+}
+
 // Peak memory into a device array: program order (single-stream graphs, any time) or, for
 // multi-stream graphs and prism_peak_memory_at, time order of `scenario` of the recorded replay.
 static prism_status peak_impl(prism_graph_t G, int32_t scenario, bool time_ordered, int64_t *peak_dev) {
@@ -1067,7 +1094,9 @@ static prism_status peak_impl(prism_graph_t G, int32_t scenario, bool time_order
   if (!G->recorded)
     return fail(PRISM_E_NOT_REPLAYED, "time-ordered peak memory needs a replay with record != 0 (multi-stream graphs)");
   if (scenario < 0 || scenario >= G->last.S) return fail(PRISM_E_INVALID_ARG, "scenario outside the last replay");
-  if (G->n_shards > 1) return fail(PRISM_E_INVALID_ARG, "time-ordered peak memory of a sharded graph is not supported");
+  if (G->n_shards > 1 && G->gathered_k != scenario)
+    return fail(PRISM_E_INVALID_ARG, "sharded graph: gather the scenario first (prism_shard_gather)");
+  const ReadView v = read_view(G, scenario);
   int64_t max_len = 0;
   for (int s = 0; s < P.topo.pp; ++s) max_len = std::max(max_len, P.stage_len[s]);
   if (max_len > kMaxTimeOrderedOps)
@@ -1075,7 +1104,7 @@ static prism_status peak_impl(prism_graph_t G, int32_t scenario, bool time_order
   uint32_t *status = G->words + 2;
   CU(cudaMemsetAsync(status, 0, 4, G->stream));
   G->rec(6);
-  CU(launch_peak_time(G->cur(), G->last, G->last_Sp, G->fin, G->gfin, scenario, (int32_t)max_len,
+  CU(launch_peak_time(v.g, v.p, v.Sp, v.fin, v.gfin, v.k, (int32_t)max_len,
                       peak_dev, status, G->stream));
   G->rec(7);
   CU(cudaMemcpyAsync(G->h_status + 2, status, 4, cudaMemcpyDeviceToHost, G->stream));
@@ -1167,7 +1196,7 @@ prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, i
   }
   const int64_t n = P.stage_len[pp_i];
   if (n_ops_out) *n_ops_out = n;
-  if (G->n_shards > 1 && start_ns &&
+  if (G->n_shards > 1 && start_ns && G->gathered_k != scenario &&
       (dp_i < G->dg.d0 || dp_i >= G->dg.d1 || pp_i < G->dg.s0 || pp_i >= G->dg.s1))
     return fail(PRISM_E_INVALID_ARG, "rank " + std::to_string(rank) + " is replayed by shard " +
                                          std::to_string(G->dg.shard_axis == 1 ? pp_i / (t.pp / G->n_shards)
@@ -1179,7 +1208,8 @@ prism_status prism_query_rank(prism_graph_t G, int32_t rank, int32_t scenario, i
   CU(cudaSetDevice(G->device));
   const size_t bytes = (size_t)n * 16;
   if (!G->ensure(G->scratch, G->scratch_bytes, bytes)) return fail(PRISM_E_OOM, "scratch allocation failed");
-  CU(launch_query(G->cur(), G->last, G->last_Sp, G->fin, G->gfin, rank, scenario, G->scratch,
+  const ReadView v = read_view(G, scenario);
+  CU(launch_query(v.g, v.p, v.Sp, v.fin, v.gfin, rank, v.k, G->scratch,
                   G->scratch + n, G->stream));
   CU(cudaMemcpyAsync(start_ns, G->scratch, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaMemcpyAsync(finish_ns, G->scratch + n, (size_t)n * 8, cudaMemcpyDeviceToHost, G->stream));
@@ -1402,9 +1432,10 @@ prism_status prism_set_moe_load(prism_graph_t G, const prism_moe_load *m) {
 prism_status prism_critical_path(prism_graph_t G, int32_t scenario, int32_t *path_out, int64_t cap,
                                  int64_t *n_out, int64_t *T_out) {
   if (!G || !n_out) return fail(PRISM_E_INVALID_ARG, "null argument");
-  if (G->n_shards > 1) return fail(PRISM_E_INVALID_ARG, "critical path of a sharded graph is not supported");
   if (!G->recorded) return fail(PRISM_E_NOT_REPLAYED, "no replay with record != 0 has run on this graph");
   if (scenario < 0 || scenario >= G->last.S) return fail(PRISM_E_INVALID_ARG, "scenario outside the last replay");
+  if (G->n_shards > 1 && G->gathered_k != scenario)
+    return fail(PRISM_E_INVALID_ARG, "sharded graph: gather the scenario first (prism_shard_gather)");
   if (cap < 0 || (cap > 0 && !path_out)) return fail(PRISM_E_INVALID_ARG, "bad path capacity");
   CU(cudaSetDevice(G->device));
   const Plan &P = G->plan;
@@ -1416,11 +1447,11 @@ prism_status prism_critical_path(prism_graph_t G, int32_t scenario, int32_t *pat
   int32_t *startn = (int32_t *)(iter + G->last.S);
   int64_t *len = (int64_t *)(startn + 2);
   int32_t *path = (int32_t *)(len + 1);
-  CU(launch_reduce(P.W, G->last.S, G->last_Sp, G->rank_end, iter, G->stream));
-  CU(launch_critical_path(G->cur(), G->last, G->fin, G->last_Sp, scenario, iter, startn, path, pc, len, G->stream));
+  const ReadView v = read_view(G, scenario);
+  CU(launch_critical_path(v.g, v.p, v.fin, v.Sp, v.k, iter, startn, path, pc, len, G->stream));
   int64_t hl = 0, hT = 0;
   CU(cudaMemcpyAsync(&hl, len, 8, cudaMemcpyDeviceToHost, G->stream));
-  CU(cudaMemcpyAsync(&hT, iter + scenario, 8, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaMemcpyAsync(&hT, iter + v.k, 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaStreamSynchronize(G->stream));
   *n_out = hl;
   if (T_out) *T_out = hT;
@@ -1472,6 +1503,7 @@ prism_status prism_replay_local_shards(const prism_graph_t *shards, int32_t n, c
   for (int i = 0; i < n; ++i) {
     prism_graph_t G = shards[i];
     G->recorded = 0;
+    G->gathered_k = -1;
     if (p.record && !G->ensure(G->fin, G->fin_bytes, (size_t)std::max<int64_t>(1, G->fin_rows) * Sp * 8))
       return fail(PRISM_E_OOM, "fin allocation failed");
     if (!G->ensure(G->gfin, G->gfin_bytes, (size_t)P.G * Sp * 8)) return fail(PRISM_E_OOM, "gfin allocation failed");
@@ -1526,6 +1558,48 @@ prism_status prism_replay_local_shards(const prism_graph_t *shards, int32_t n, c
   return PRISM_OK;
 }
 
+prism_status prism_shard_gather(prism_graph_t G, int32_t scenario) {
+  if (!G) return fail(PRISM_E_INVALID_ARG, "null graph");
+  if (G->n_shards < 2 || !G->connected || !G->ex) return fail(PRISM_E_INVALID_ARG, "not a connected shard");
+  if (G->local_group) return fail(PRISM_E_INVALID_ARG, "shards of one device gather together (prism_shard_gather_local)");
+  if (!G->recorded) return fail(PRISM_E_NOT_REPLAYED, "no replay with record != 0 has run on this graph");
+  if (scenario < 0 || scenario >= G->last.S) return fail(PRISM_E_INVALID_ARG, "scenario outside the last replay");
+  CU(cudaSetDevice(G->device));
+  ShardLink L = G->link;
+  L.lg = 0;
+  CU(cudaMemsetAsync(G->words, 0, 4, G->stream));
+  CU(launch_gather(G->cur(), L, G->fin, G->gfin, G->last_Sp, scenario, ++G->gather_epoch, G->words, G->stream));
+  CU(cudaMemcpyAsync(G->h_status, G->words, 8, cudaMemcpyDeviceToHost, G->stream));
+  CU(cudaStreamSynchronize(G->stream));
+  prism_status st = check_status(G);
+  if (st) return st;
+  G->gathered_k = scenario;
+  return PRISM_OK;
+}
+
+prism_status prism_shard_gather_local(const prism_graph_t *shards, int32_t n, int32_t scenario) {
+  if (!shards || n < 2 || n > kMaxShards) return fail(PRISM_E_INVALID_ARG, "bad arguments");
+  prism_graph_t G0 = shards[0];
+  for (int i = 0; i < n; ++i) {
+    const prism_graph_t G = shards[i];
+    if (!G || G->n_shards != n || G->shard != i || !G->local_group || !G->recorded || G->device != G0->device ||
+        G->last_Sp != G0->last_Sp || scenario < 0 || scenario >= G->last.S)
+      return fail(PRISM_E_INVALID_ARG, "shard " + std::to_string(i) + " is not a recorded local shard of this group");
+  }
+  CU(cudaSetDevice(G0->device));
+  ShardLink L = G0->link;
+  L.lg = n;
+  for (int i = 0; i < n; ++i) {
+    L.lg_fin[i] = shards[i]->fin;
+    L.lg_gfin[i] = shards[i]->gfin;
+  }
+  for (int i = 1; i < n; ++i) CU(cudaStreamSynchronize(shards[i]->stream));
+  CU(launch_gather(G0->cur(), L, nullptr, nullptr, G0->last_Sp, scenario, 0, G0->words, G0->stream));
+  CU(cudaStreamSynchronize(G0->stream));
+  for (int i = 0; i < n; ++i) shards[i]->gathered_k = scenario;
+  return PRISM_OK;
+}
+
 prism_status prism_shard_prepare(prism_graph_t G, int32_t n_scenarios, void *handle_out) {
   if (!G || !handle_out) return fail(PRISM_E_INVALID_ARG, "null argument");
   if (G->n_shards < 2) return fail(PRISM_E_INVALID_ARG, "graph was not built with n_shards > 1");
@@ -1551,6 +1625,9 @@ prism_status prism_shard_prepare(prism_graph_t G, int32_t n_scenarios, void *han
   L.o_arrive = (int64_t)carve((size_t)P.G_large * nchunks * 4);
   L.o_part = (int64_t)carve((size_t)2 * G->n_shards * Sp * 8);
   L.o_flag = (int64_t)carve((size_t)G->n_shards * 4);
+  L.o_gcol = (int64_t)carve((size_t)P.N * 8);
+  L.o_ggcol = (int64_t)carve((size_t)P.G * 8);
+  L.o_gflag = (int64_t)carve((size_t)G->n_shards * 4);
   const size_t bytes = off;
   for (void *p : G->ipc_open) cudaIpcCloseMemHandle(p);
   G->ipc_open.clear();
@@ -1563,6 +1640,8 @@ prism_status prism_shard_prepare(prism_graph_t G, int32_t n_scenarios, void *han
   CU(cudaMemset(G->ex + L.o_rslot, 0xFF, (size_t)P.M_cross * Sp * 8));  // "not yet" under parity 0
   CU(cudaDeviceSynchronize());
   G->parity = 0;
+  G->gather_epoch = 0;
+  G->gathered_k = -1;
   G->ex_S = n_scenarios;
   G->ex_Sp = (int32_t)Sp;
   G->link = L;

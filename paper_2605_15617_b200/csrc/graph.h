@@ -239,6 +239,7 @@ struct ShardLink {
                                    // in ONE cooperative grid (prism_replay_local_shards)
   unsigned char *base[kMaxShards];  // exchange buffer of every shard (peer-mapped), own included
   int64_t o_rslot, o_acc, o_arrive, o_part, o_flag;  // byte offsets inside a buffer
+  int64_t o_gcol, o_ggcol, o_gflag;  // prism_shard_gather: finish column [N], group column [G], flags
   // local-group launches: every shard's own output arrays (the structure is the same graph)
   int64_t *lg_fin[kMaxShards], *lg_gfin[kMaxShards], *lg_rank_end[kMaxShards];
 };
@@ -270,6 +271,10 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
                          int64_t *rres, uint32_t *arrive, uint32_t *status, int parity, int64_t *fin,
                          int64_t *gfin, int64_t *rank_end, int chunk0, int nchunks_launch, int Sp,
                          const ShardLink *link, cudaStream_t st);
+// row e, prism_shard_gather: the shard's own finishes of scenario k into every shard's gather
+// columns, then (cross-process) the epoch flag barrier
+cudaError_t launch_gather(const DevGraph &g, const ShardLink &link, const int64_t *fin, const int64_t *gfin,
+                          int32_t Sp, int32_t k, uint32_t epoch, uint32_t *status, cudaStream_t st);
 // row e, local group: T_k = max over the shards' own ranks' rank_end (all on this device)
 cudaError_t launch_local_group_reduce(const DevGraph &g, const ShardLink &link, int32_t S, int32_t Sp,
                                       int64_t *iter, cudaStream_t st);
@@ -312,8 +317,9 @@ struct MoeIn {
 cudaError_t launch_durations(const DevGraph &g, const DurIn &in, const MoeIn &me, int64_t *eff, int64_t *eal,
                              int64_t *efr, int64_t *gdur, int64_t *sdur, int64_t *hdur, uint32_t *status,
                              cudaStream_t st);
+// iter[k] receives T_k (max finish over every node); the walk starts at the lowest node finishing at it
 cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const int64_t *fin, int32_t Sp, int32_t k,
-                                 const int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
+                                 int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
                                  cudaStream_t st);
 // Start of every waiting replay (cells / ranks): the previous replay's abort status (word 0) is
 // folded into the sticky word (1) and cleared; after an abort the ready / result slots are reset

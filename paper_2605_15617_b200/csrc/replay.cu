@@ -300,6 +300,81 @@ __global__ void __launch_bounds__(1024) shard_exchange_kernel(ShardLink L, int32
   }
 }
 
+// Row e, prism_shard_gather: every shard writes its own ranks' finish times of scenario k (and the
+// finishes of the batched-P2P groups whose first member it owns) into the gather columns of every
+// shard's exchange buffer (rows in fin_row order, one scenario: Sp = 1 layout), over NVLink peer
+// stores; a local-group launch (L.lg > 0) does it for every shard of the device at once.
+__device__ __forceinline__ bool owns_rank(const DevGraph &g, int32_t r, int32_t sh) {
+  const int32_t s = g.order == PRISM_ORDER_MEGATRON ? r / (g.tp * g.dp) : (r / g.tp) % g.pp;
+  const int32_t dpi = g.order == PRISM_ORDER_MEGATRON ? (r / g.tp) % g.dp : r / (g.tp * g.pp);
+  return g.shard_axis == 1 ? s / (g.pp / g.n_shards) == sh : dpi / (g.dp / g.n_shards) == sh;
+}
+
+__global__ void __launch_bounds__(256) gather_kernel(DevGraph g, ShardLink L, const int64_t *__restrict__ fin,
+                                                     const int64_t *__restrict__ gfin, int32_t Sp, int32_t k) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int32_t nsrc = L.lg > 0 ? L.lg : 1;
+  for (int32_t src = 0; src < nsrc; ++src) {
+    const int32_t sh = L.lg > 0 ? src : L.self;
+    const int64_t *f = L.lg > 0 ? L.lg_fin[src] : fin;
+    const int64_t *gf = L.lg > 0 ? L.lg_gfin[src] : gfin;
+    // the source shard's fin rows start at its own node0 (DP blocks under TP_PP_DP), else 0
+    const int64_t node0 = (g.shard_axis == 0 && g.order == PRISM_ORDER_TP_PP_DP) ? (int64_t)sh * g.fin_rows : 0;
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N; n += stride) {
+      if (!owns_rank(g, g.node_rank[n], sh)) continue;
+      const int64_t row = fin_row(g, (int32_t)n);
+      const int64_t v = f[((int64_t)(k / (Sp < 32 ? Sp : 32)) * g.fin_rows + row - node0) * (Sp < 32 ? Sp : 32) +
+                          k % (Sp < 32 ? Sp : 32)];
+      for (int m = 0; m < L.n; ++m) ((int64_t *)(L.base[m] + L.o_gcol))[row] = v;
+    }
+    // group finishes are recorded only for the groups of batched P2P nodes (several groups on one
+    // node), by each such member: a shard contributes the groups of its own batched members
+    for (int64_t grp = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; grp < g.G; grp += stride) {
+      bool mine = false;
+      for (int32_t j = g.grp_ptr[grp]; j < g.grp_ptr[grp + 1] && j < g.grp_ptr[grp] + 2; ++j) {
+        const int32_t mn = g.grp_mem[j];
+        mine |= g.node_gptr[mn + 1] - g.node_gptr[mn] > 1 && owns_rank(g, g.node_rank[mn], sh);
+      }
+      if (!mine) continue;
+      const int64_t v = gf[grp * Sp + k];
+      for (int m = 0; m < L.n; ++m) ((int64_t *)(L.base[m] + L.o_ggcol))[grp] = v;
+    }
+  }
+  __threadfence_system();
+}
+
+// Cross-process gather completion: publish flag[self] = epoch at every shard (release, system
+// scope; the gather kernel before it on the stream has completed its peer stores) and wait for
+// every shard's flag (acquire), with the device watchdog.
+__global__ void gather_sync_kernel(ShardLink L, uint32_t epoch, uint32_t *status, uint64_t watchdog_ns) {
+  __threadfence_system();
+  if (threadIdx.x < L.n) {
+    uint32_t *f = (uint32_t *)(L.base[threadIdx.x] + L.o_gflag) + L.self;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x < L.n) {
+    const uint32_t *f = (const uint32_t *)(L.base[L.self] + L.o_gflag) + threadIdx.x;
+    uint64_t t0 = 0;
+    uint32_t spins = 0;
+    while (true) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      if ((int32_t)(v - epoch) >= 0) break;
+      __nanosleep(200);
+      if ((++spins & 255) == 0) {
+        uint64_t now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (t0 == 0) t0 = now;
+        if (now - t0 > watchdog_ns) {
+          atomicCAS(status, 0u, (uint32_t)PRISM_E_DEADLOCK);
+          break;
+        }
+      }
+    }
+  }
+}
+
 // prism_query_rank: start/finish of one rank's ops in one scenario from fin/gfin (fin layout:
 // graph.h fin_off; a sharded replay keeps only its own ranks' rows).
 // Start time of node i (rank r, first node rb) in scenario k of a recorded replay: a compute span
@@ -551,12 +626,20 @@ cudaError_t preload_replay_kernels() {
   const void *fns[] = {(const void *)reduce_iter_kernel, (const void *)shard_partial_kernel,
                        (const void *)shard_exchange_kernel, (const void *)query_kernel,
                        (const void *)peak_time_kernel, (const void *)replay_guard_kernel,
-                       (const void *)local_group_reduce_kernel};
+                       (const void *)local_group_reduce_kernel, (const void *)gather_kernel,
+                       (const void *)gather_sync_kernel};
   for (const void *f : fns) {
     cudaError_t e = cudaFuncGetAttributes(&a, f);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t launch_gather(const DevGraph &g, const ShardLink &link, const int64_t *fin, const int64_t *gfin,
+                          int32_t Sp, int32_t k, uint32_t epoch, uint32_t *status, cudaStream_t st) {
+  gather_kernel<<<num_sms() * 8, 256, 0, st>>>(g, link, fin, gfin, Sp, k);
+  if (link.lg == 0) gather_sync_kernel<<<1, 32, 0, st>>>(link, epoch, status, g.watchdog_ns);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_local_group_reduce(const DevGraph &g, const ShardLink &link, int32_t S, int32_t Sp,

@@ -125,6 +125,17 @@ __global__ void __launch_bounds__(256) records_kernel(DevGraph g, const int64_t 
 }
 
 
+// Row f3, step 0: T_k = max over every node's finish (covers multi-stream ranks, whose last op in
+// issue order need not finish last).
+__global__ void __launch_bounds__(256) view_max_kernel(DevGraph g, const int64_t *__restrict__ fin, int32_t Sp,
+                                                       int32_t k, int64_t *__restrict__ T) {
+  int64_t m = 0;
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N; n += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, fin[fin_off(g, fin_row(g, (int32_t)n), k, Sp)]);
+  for (int off = 16; off; off >>= 1) m = max(m, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long *)T, (unsigned long long)m);
+}
+
 // Row f3, step 1: T_k and the lowest node finishing at T_k.
 __global__ void __launch_bounds__(256) crit_start_kernel(DevGraph g, const int64_t *__restrict__ fin,
                                                          int32_t Sp, int32_t k, const int64_t *__restrict__ iter,
@@ -229,10 +240,12 @@ cudaError_t launch_durations(const DevGraph &g, const DurIn &in, const MoeIn &me
 }
 
 cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const int64_t *fin, int32_t Sp, int32_t k,
-                                 const int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
+                                 int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
                                  cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(scratch, 0x7F, 4, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(iter + k, 0, 8, st);
   if (e != cudaSuccess) return e;
+  if (g.N > 0) view_max_kernel<<<num_sms() * 4, 256, 0, st>>>(g, fin, Sp, k, iter + k);
   if (g.N > 0) crit_start_kernel<<<num_sms() * 4, 256, 0, st>>>(g, fin, Sp, k, iter, scratch);
   crit_walk_kernel<<<1, 32, 0, st>>>(g, p, fin, Sp, k, scratch, path, cap, len_out);
   return cudaGetLastError();

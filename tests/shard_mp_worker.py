@@ -27,9 +27,20 @@ for rep in range(3):
         print(rank, "rep", rep, "err", e, round(time.time() - t0, 3), flush=True)
         g.shard_connect_dist(S)
     dist.barrier()
+# per-rank outputs gathered to every process (prism_shard_gather): a rank owned by the OTHER shard
+g.shard_gather(S - 1)
+other = [r for r in range(tm.topo.world) if r not in set(g.owned_ranks())][0]
+st, fi, _ = g.query_rank(other, S - 1)
+path, T = g.critical_path(S - 1)
+print(rank, "gathered", other, fi.tolist(), "T", T, "path", len(path), int(path.sum()), flush=True)
 if rank == 0:
     import oracle
-    print("ref", oracle.replay(tm, S, amp_q16=6554, kind_mask=7, threads=8)["iter"].tolist())
+    ref = oracle.replay(tm, S, amp_q16=6554, kind_mask=7, threads=8, times=True)
+    print("ref", ref["iter"].tolist())
+    rpath, rT = oracle.critical_path(tm, S - 1, amp_q16=6554, kind_mask=7)
+    rp = P.Graph(tm).export("rank_ptr")
+    for r in range(tm.topo.world):
+        print("reff", r, ref["finish"][S - 1, rp[r]:rp[r + 1]].tolist(), "T", rT, "path", len(rpath), int(rpath.sum()))
 dist.barrier()
 g.close()
 dist.destroy_process_group()

@@ -83,6 +83,23 @@ def _check(P, tm, n, S, reps=2, times=True, node_dur=None, axis="auto"):
             if other:
                 with pytest.raises(P.PrismError):
                     g.query_rank(int(other[0]), 0)
+        # gathered to every shard: any rank from any shard, and the critical path
+        k = S - 1
+        P.shard_gather_local(gs, k)
+        for i, g in enumerate(gs):
+            for r in rng.choice(W, min(6, W), replace=False):
+                st, fi, _ = g.query_rank(int(r), k)
+                a, b = rp[r], rp[r + 1]
+                assert np.array_equal(fi, ref["finish"][k, a:b]) and np.array_equal(st, ref["start"][k, a:b])
+        path, T = gs[-1].critical_path(k)
+        rpath, rT = oracle.critical_path(tm, k, amp_q16=6554, kind_mask=7, node_dur=node_dur)
+        assert T == rT == ref["iter"][k] and np.array_equal(path, rpath)
+        if getattr(tm, "multistream", False):
+            rt = oracle.replay(tm, 1, scen_first=k, amp_q16=6554, kind_mask=7, node_dur=node_dur)
+            assert np.array_equal(gs[0].peak_memory_at(k), rt["peak"][0])
+        if S > 1:
+            with pytest.raises(P.PrismError):  # another scenario was not gathered
+                gs[0].critical_path(0)
     for g in gs:
         g.close()
 
@@ -182,6 +199,12 @@ def test_multiprocess_ipc(prism, tmp_path):
     for l in r.stdout.splitlines():
         if " rep " in l:
             assert " ok " in l and want in l, l
+    reff = {int(l.split()[1]): l.split(" ", 2)[2] for l in r.stdout.splitlines() if l.startswith("reff")}
+    gathered = [l for l in r.stdout.splitlines() if " gathered " in l]
+    assert len(gathered) == 2
+    for l in gathered:  # "<rank> gathered <other> <finishes> T <T> path <len> <sum>"
+        other = int(l.split()[2])
+        assert l.split(" ", 3)[3] == reff[other], (l[:200], reff[other][:200])
 
 
 @pytest.mark.parametrize("seed", range(300, 316))
