@@ -365,13 +365,15 @@ class Graph:
         """(path [node ids, last first], T) of one scenario of the last recorded replay."""
         n = ctypes.c_int64(0)
         T = ctypes.c_int64(0)
-        st = lib().prism_critical_path(self._h, int(scenario), None, 0, ctypes.byref(n), ctypes.byref(T))
-        if st not in (0, 1):
-            _check(st)
-        path = np.zeros(max(1, n.value), np.int32)
-        _check(lib().prism_critical_path(self._h, int(scenario), _ptr(path), n.value, ctypes.byref(n),
-                                         ctypes.byref(T)))
-        return path[: n.value], int(T.value)
+        path = np.zeros(1 << 16, np.int32)  # one call in the common case; retried if the path is longer
+        st = lib().prism_critical_path(self._h, int(scenario), _ptr(path), len(path), ctypes.byref(n),
+                                       ctypes.byref(T))
+        if st == 1 and n.value > len(path):
+            path = np.zeros(n.value, np.int32)
+            st = lib().prism_critical_path(self._h, int(scenario), _ptr(path), len(path), ctypes.byref(n),
+                                           ctypes.byref(T))
+        _check(st)
+        return path[: n.value].copy(), int(T.value)
 
     # ---------------------------------------------------------------- row e: sharding
     def shard_info(self) -> Dict[str, object]:

@@ -145,85 +145,131 @@ __global__ void __launch_bounds__(256) crit_start_kernel(DevGraph g, const int64
     if (fin[fin_off(g, fin_row(g, (int32_t)n), k, Sp)] == T) atomicMin(out_node, (int32_t)n);
 }
 
-// Row f3, step 2: the walk back (one warp; lanes split a group's members). Rules = the oracle's
-// (oracle/prism_oracle.cpp oracle_critical_path): compute span <- stream predecessor; sync node <-
-// its group with the max (start + dur') (lowest uid on ties) <- that group's latest-ready member
-// (lowest node id on ties) <- the member's stream predecessor; stop when there is none.
-__global__ void __launch_bounds__(32) crit_walk_kernel(DevGraph g, ScenParams p, const int64_t *__restrict__ fin,
-                                                       int32_t Sp, int32_t k, const int32_t *__restrict__ start_node,
-                                                       int32_t *__restrict__ path, int64_t cap,
-                                                       int64_t *__restrict__ len_out) {
-  const int lane = threadIdx.x;
-  int32_t cur = *start_node;
-  if (cur < 0 || cur >= g.N) cur = -1;  // empty graph: empty path
-  int64_t len = 0;
-  // a node's directional predecessor: its stream predecessor (row f2: or its event source,
-  // whichever finished later, the lower id on ties)
-  auto pred = [&](int32_t n) -> int32_t {
-    if (!g.ms) return g.rank_ptr[g.node_rank[n]] == n ? -1 : n - 1;
-    const int32_t a = g.node_spred[n], b = g.node_esrc[n];
-    if (a < 0) return b;
-    if (b < 0) return a;
-    const int64_t fa = fin[fin_off(g, fin_row(g, a), k, Sp)], fb = fin[fin_off(g, fin_row(g, b), k, Sp)];
-    if (fa != fb) return fa > fb ? a : b;
-    return min(a, b);
-  };
-  auto ready = [&](int32_t m) -> int64_t {
-    const int32_t q = pred(m);
-    return q < 0 ? 0 : fin[fin_off(g, fin_row(g, q), k, Sp)];
-  };
-  while (cur >= 0) {
-    if (lane == 0 && len < cap) path[len] = cur;
-    ++len;
-    int32_t next = -1;
-    const int32_t h0 = g.node_gptr[cur], h1 = g.node_gptr[cur + 1];
-    if (h0 == h1) {
-      next = pred(cur);
-    } else {
-      int64_t bf = -1;
-      uint64_t buid = 0;
-      int32_t bg = -1;
-      for (int32_t h = h0; h < h1; ++h) {
-        const int32_t gi = g.node_grp[h];
-        int64_t gs = 0;
-        for (int32_t j = g.grp_ptr[gi] + lane; j < g.grp_ptr[gi + 1]; j += 32) gs = max(gs, ready(g.grp_mem[j]));
-        for (int off = 16; off; off >>= 1) gs = max(gs, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)gs, off));
-        const uint64_t uid = g.grp_uid[gi];
-        const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
-        int64_t d = g.grp_dur[gi];
-        const int32_t kg = p.first + k;  // global scenario index (perturbation key)
-        if ((p.mask & gb) && p.amp > 0 && kg > 0) d = perturb_x(d, p.seed ^ ((uint64_t)kg * K_GOLD) ^ (uid * K_MIX), p);
-        const int64_t f = gs + d;
-        if (f > bf || (f == bf && uid < buid)) {
-          bf = f;
-          buid = uid;
-          bg = gi;
-        }
+// Row f3, steps 2-4. The walk's rules are the oracle's (oracle/prism_oracle.cpp
+// oracle_critical_path, reading R6): compute span <- its directional predecessor; sync node <- its
+// group with the max (start + dur') (lowest uid on ties) <- that group's latest-ready member (lowest
+// node id on ties) <- the member's directional predecessor; the walk ends at a node without one.
+// Every choice depends only on the recorded times, so the parent of EVERY node is computed in
+// parallel (groups first, then nodes) and the walk is a chase through the parent array (held in
+// L2) instead of a serial scan of each group's members.
+//
+// A node's directional predecessor: its stream predecessor (row f2: or its event source,
+// whichever finished later, the lower id on ties).
+__device__ __forceinline__ int32_t crit_pred(const DevGraph &g, const int64_t *fin, int32_t Sp, int32_t k, int32_t n) {
+  if (!g.ms) return g.rank_ptr[g.node_rank[n]] == n ? -1 : n - 1;
+  const int32_t a = g.node_spred[n], b = g.node_esrc[n];
+  if (a < 0) return b;
+  if (b < 0) return a;
+  const int64_t fa = fin[fin_off(g, fin_row(g, a), k, Sp)], fb = fin[fin_off(g, fin_row(g, b), k, Sp)];
+  if (fa != fb) return fa > fb ? a : b;
+  return min(a, b);
+}
+
+// step 2: per group (one warp), start = max over members of ready(member) and the latest-ready
+// member (lowest node id on ties)
+__global__ void __launch_bounds__(256) crit_groups_kernel(DevGraph g, const int64_t *__restrict__ fin, int32_t Sp,
+                                                          int32_t k, int64_t *__restrict__ gstart,
+                                                          int32_t *__restrict__ gbest) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t gi = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); gi < g.G; gi += warps) {
+    int64_t br = -1;
+    int32_t bm = 0x7FFFFFFF;
+    for (int32_t j = g.grp_ptr[gi] + lane; j < g.grp_ptr[gi + 1]; j += 32) {
+      const int32_t m = g.grp_mem[j];
+      const int32_t q = crit_pred(g, fin, Sp, k, m);
+      const int64_t r = q < 0 ? 0 : fin[fin_off(g, fin_row(g, q), k, Sp)];
+      if (r > br || (r == br && m < bm)) {
+        br = r;
+        bm = m;
       }
-      // latest-ready member of the chosen group, lowest node id on ties
-      int64_t br = -1;
-      int32_t bm = 0x7FFFFFFF;
-      for (int32_t j = g.grp_ptr[bg] + lane; j < g.grp_ptr[bg + 1]; j += 32) {
-        const int32_t m = g.grp_mem[j];
-        const int64_t r = ready(m);
-        if (r > br || (r == br && m < bm)) {
-          br = r;
-          bm = m;
-        }
-      }
-      for (int off = 16; off; off >>= 1) {
-        const int64_t r2 = (int64_t)__shfl_xor_sync(0xffffffffu, (long long)br, off);
-        const int32_t m2 = __shfl_xor_sync(0xffffffffu, bm, off);
-        if (r2 > br || (r2 == br && m2 < bm)) {
-          br = r2;
-          bm = m2;
-        }
-      }
-      next = pred(bm);
     }
-    cur = next;
+    for (int off = 16; off; off >>= 1) {
+      const int64_t r2 = (int64_t)__shfl_xor_sync(0xffffffffu, (long long)br, off);
+      const int32_t m2 = __shfl_xor_sync(0xffffffffu, bm, off);
+      if (r2 > br || (r2 == br && m2 < bm)) {
+        br = r2;
+        bm = m2;
+      }
+    }
+    if (lane == 0) {
+      gstart[gi] = br;
+      gbest[gi] = bm;
+    }
   }
-  if (lane == 0) *len_out = len;
+}
+
+// step 3: the parent of every node (-1: none)
+__global__ void __launch_bounds__(256) crit_parent_kernel(DevGraph g, ScenParams p, const int64_t *__restrict__ fin,
+                                                          int32_t Sp, int32_t k, const int64_t *__restrict__ gstart,
+                                                          const int32_t *__restrict__ gbest, int32_t *__restrict__ parent) {
+  const int32_t kg = p.first + k;  // global scenario index (perturbation key)
+  for (int64_t nn = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; nn < g.N; nn += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t n = (int32_t)nn;
+    const int32_t h0 = g.node_gptr[n], h1 = g.node_gptr[n + 1];
+    if (h0 == h1) {
+      parent[n] = crit_pred(g, fin, Sp, k, n);
+      continue;
+    }
+    int64_t bf = -1;
+    uint64_t buid = 0;
+    int32_t bg = -1;
+    for (int32_t h = h0; h < h1; ++h) {
+      const int32_t gi = g.node_grp[h];
+      const uint64_t uid = g.grp_uid[gi];
+      const uint32_t gb = (uid >> 56) == PRISM_ROLE_P2P ? 4u : 2u;
+      int64_t d = g.grp_dur[gi];
+      if ((p.mask & gb) && p.amp > 0 && kg > 0) d = perturb_x(d, p.seed ^ ((uint64_t)kg * K_GOLD) ^ (uid * K_MIX), p);
+      const int64_t f = gstart[gi] + d;
+      if (f > bf || (f == bf && uid < buid)) {
+        bf = f;
+        buid = uid;
+        bg = gi;
+      }
+    }
+    parent[n] = crit_pred(g, fin, Sp, k, gbest[bg]);
+  }
+}
+
+// step 4: runs of stream predecessors. Inside a rank, a node whose parent is the node before it
+// continues the run of that node; run_start[n] = the first node of n's run (a warp per rank:
+// prefix max of the run-break positions), so the chase below needs two dependent loads per RUN
+// (one per hop between ranks / groups) instead of one per node.
+__global__ void __launch_bounds__(256) crit_runs_kernel(DevGraph g, const int32_t *__restrict__ parent,
+                                                        int32_t *__restrict__ run_start) {
+  const int lane = threadIdx.x & 31;
+  const int32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (int32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < g.W; r += warps) {
+    const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
+    int32_t carry = rb;
+    for (int32_t base = rb; base < re; base += 32) {
+      const int32_t i = base + lane;
+      int32_t x = (i < re && (i == rb || parent[i] != i - 1)) ? i : carry;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) x = max(x, __shfl_up_sync(0xffffffffu, x, off));
+      x = max(x, carry);
+      if (i < re) run_start[i] = x;
+      carry = __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+}
+
+// step 5: the chase from the lowest node finishing at T (one thread): each run is written out
+// without loads, then the walk continues at the parent of the run's first node
+__global__ void crit_chase_kernel(const int32_t *__restrict__ start_node, int32_t N, const int32_t *__restrict__ parent,
+                                  const int32_t *__restrict__ run_start, int32_t *__restrict__ path, int64_t cap,
+                                  int64_t *__restrict__ len_out) {
+  int32_t cur = *start_node;
+  if (cur < 0 || cur >= N) cur = -1;  // empty graph: empty path
+  int64_t len = 0;
+  while (cur >= 0) {
+    const int32_t rs = __ldcg(run_start + cur);
+    const int32_t nxt = __ldcg(parent + rs);
+    for (int32_t x = cur; x >= rs; --x, ++len)
+      if (len < cap) path[len] = x;
+    cur = nxt;
+  }
+  *len_out = len;
 }
 
 }  // namespace
@@ -241,13 +287,18 @@ cudaError_t launch_durations(const DevGraph &g, const DurIn &in, const MoeIn &me
 
 cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const int64_t *fin, int32_t Sp, int32_t k,
                                  int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
+                                 int64_t *gstart, int32_t *gbest, int32_t *parent, int32_t *run_start,
                                  cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(scratch, 0x7F, 4, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(iter + k, 0, 8, st);
   if (e != cudaSuccess) return e;
-  if (g.N > 0) view_max_kernel<<<num_sms() * 4, 256, 0, st>>>(g, fin, Sp, k, iter + k);
-  if (g.N > 0) crit_start_kernel<<<num_sms() * 4, 256, 0, st>>>(g, fin, Sp, k, iter, scratch);
-  crit_walk_kernel<<<1, 32, 0, st>>>(g, p, fin, Sp, k, scratch, path, cap, len_out);
+  const int blocks = num_sms() * 8;
+  if (g.N > 0) view_max_kernel<<<blocks, 256, 0, st>>>(g, fin, Sp, k, iter + k);
+  if (g.N > 0) crit_start_kernel<<<blocks, 256, 0, st>>>(g, fin, Sp, k, iter, scratch);
+  if (g.G > 0) crit_groups_kernel<<<blocks, 256, 0, st>>>(g, fin, Sp, k, gstart, gbest);
+  if (g.N > 0) crit_parent_kernel<<<blocks, 256, 0, st>>>(g, p, fin, Sp, k, gstart, gbest, parent);
+  if (g.W > 0) crit_runs_kernel<<<blocks, 256, 0, st>>>(g, parent, run_start);
+  crit_chase_kernel<<<1, 1, 0, st>>>(scratch, (int32_t)g.N, parent, run_start, path, cap, len_out);
   return cudaGetLastError();
 }
 
