@@ -494,6 +494,26 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     st = choose_shard_axis(plan, n_shards, opts ? opts->flags : 0, axis, err);
     if (st != PRISM_OK) return fail(st, err);
   }
+  {  // replica cells for tp = 1: R = 8 DP replicas per cell when the topology and
+     // the shard blocks allow it (PRISM_REPLICA_CELLS=0 keeps one rank per cell: experiments)
+    static const int env_rc = [] {
+      const char *e = std::getenv("PRISM_REPLICA_CELLS");
+      return e ? std::atoi(e) : 1;
+    }();
+    // EP CTAs: the 8 cells of an EP group (R = ep / 8 replicas each) share one CTA, so an EP
+    // all-to-all is a register + shared-memory max behind one barrier; a DP-block shard must then
+    // hold whole EP groups. PRISM_REPLICA_CELLS=2: replica cells of 8 without EP CTAs.
+    const int ks = 8;
+    const Topo &tt = plan.topo;
+    const bool cta = env_rc != 2 && tt.tp == 1 && tt.ep >= ks && tt.ep % ks == 0 && tt.ep / ks <= 8 &&
+                     (tt.ep / ks) * ks == tt.ep && (n_shards == 1 || axis == 1 || (tt.dp / n_shards) % tt.ep == 0);
+    const int R = cta ? tt.ep / ks : 8;
+    const bool blocks_ok = n_shards == 1 || axis == 1 || (tt.dp / n_shards) % R == 0;
+    if (env_rc && (cta || env_rc == 2) && blocks_ok && replica_cells_ok(tt, R) && (R == 1 || R == 2 || R == 4 || R == 8)) {
+      st = plan_replica_cells(plan, R, cta ? ks : 1, err);
+      if (st != PRISM_OK) return fail(st, err);
+    }
+  }
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -575,6 +595,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t o_tdur = carve(nops * 8), o_tal = carve(nops * 8), o_tfr = carve(nops * 8), o_tsd = carve(nops * 8);
   const size_t o_tlab = carve(nops * 4), o_tkind = carve(nops), o_tqi = carve(nops * 8);
   const size_t o_tms = ms ? carve(nops * 2) : 0, o_tsp2 = ms ? carve(nops * 4) : 0, o_tes = ms ? carve(nops * 4) : 0;
+  const size_t o_crp = P.cell_R > 1 ? carve((pp + 1) * 8) : 0;  // replica cells: cell-record offsets
   const size_t table_bytes = off;
   // graph arrays (written by the expand kernels)
   const size_t o_rp = carve((W + 1) * 4), o_rs = carve((W + 1) * 4), o_rst = carve(W * 4);
@@ -587,6 +608,8 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t o_hs = n_shards > 1 ? carve(M * 4) : 0;
   const size_t o_nmsk = ms ? carve(N * 2) : 0, o_nsp = ms ? carve(N * 4) : 0, o_nes = ms ? carve(N * 4) : 0;
   const size_t o_words = carve(16);
+  const size_t ncrec = P.cell_R > 1 ? (size_t)P.crec_ptr[pp] : 0;
+  const size_t o_cb = P.cell_R > 1 ? carve(ncrec * 4) : 0, o_cm = P.cell_R > 1 ? carve(ncrec * 4) : 0;
   const size_t total = off;
   trace("build: tables sized");
   unsigned char *base = G->take<unsigned char>(total);
@@ -659,6 +682,12 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.node_esrc = ms ? (int32_t *)at(o_nes) : nullptr;
   d.M_cross = P.M_cross;
   d.G_large = P.G_large;
+  d.cell_R = P.cell_R;
+  d.cta_ks = P.cta_ks;
+  d.Ltot = (int64_t)nops;
+  d.crec_ptr = P.cell_R > 1 ? (const int64_t *)at(o_crp) : nullptr;
+  d.c_base = P.cell_R > 1 ? (int32_t *)at(o_cb) : nullptr;
+  d.c_meta = P.cell_R > 1 ? (uint32_t *)at(o_cm) : nullptr;
   d.stall_unit = -1;
   d.watchdog_ns = 10ull * 1000 * 1000 * 1000;
   G->words = (uint32_t *)at(o_words);
@@ -715,6 +744,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
       }
     }
     put(o_xptr, P.x_ptr.data(), (pp + 1) * 4);
+    if (P.cell_R > 1) put(o_crp, P.crec_ptr.data(), (pp + 1) * 8);
     put(o_xops, P.x_ops.data(), P.x_ops.size() * sizeof(XOp));
     if (ms) {
       put(o_tms, P.t_ms.data(), nops * 2);
@@ -746,6 +776,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   if (!(G->h_status = pin_take())) return fail(PRISM_E_OOM, "pinned status words unavailable");
   G->rec(0);
   CU(launch_expand(d, s));
+  CU(launch_cell_records(d, s));
   G->rec(1);
   trace("build: expand launched");
   if (!(opts && (opts->flags & PRISM_BUILD_ASYNC))) CU(cudaStreamSynchronize(s));
@@ -863,7 +894,9 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   const int32_t S = sc->n;
   const Plan &P = G->plan;
   // one scenario: the lane = rank kernel when it applies (auto) or is asked for
-  if (sc->algo == PRISM_ALGO_RANKS || (sc->algo == PRISM_ALGO_AUTO && S == 1)) {
+  // (EP-CTA graphs stay on the cell kernel: its CTA-local all-to-alls beat the rank kernel's
+  // global rendezvous even for one scenario)
+  if (sc->algo == PRISM_ALGO_RANKS || (sc->algo == PRISM_ALGO_AUTO && S == 1 && G->dg.cta_ks <= 1)) {
     const bool fit = S == 1 && ranks_fit(G->cur(), nullptr);
     if (fit) return replay_ranks_impl(G, sc, iter_dev);
     if (sc->algo == PRISM_ALGO_RANKS)
@@ -1829,11 +1862,25 @@ extern "C" PRISM_API prism_status prism_debug_export(prism_graph_t G, int32_t wh
     CU(cudaMemcpyAsync(rp32.data(), d.rank_ptr, (size_t)(d.W + 1) * 4, cudaMemcpyDeviceToHost, G->stream));
     CU(cudaStreamSynchronize(G->stream));
     int64_t *out = (int64_t *)host_out;
+    const Plan &P = G->plan;
     for (int64_t r = 0; r < d.W; ++r) {
-      const int64_t tpi = r % d.tp, c0 = rp32[r - tpi];
+      // row of op 0 and row stride (graph.h cell_row0: TP cells, or replica cells with tp = 1)
+      int64_t c0, stride;
+      if (d.cell_R <= 1) {
+        const int64_t tpi = r % d.tp;
+        c0 = rp32[r - tpi] + tpi;
+        stride = d.tp;
+      } else {
+        const int64_t R = d.cell_R;
+        const bool meg = d.order == PRISM_ORDER_MEGATRON;
+        const int64_t s2 = meg ? r / d.dp : r % d.pp, dpi = meg ? r % d.dp : r / d.pp;
+        c0 = (meg ? (int64_t)d.dp * P.stage_op0[s2] + (dpi / R) * R * P.stage_len[s2]
+                  : R * ((dpi / R) * d.Ltot + P.stage_op0[s2])) + dpi % R;
+        stride = R;
+      }
       for (int64_t n = rp32[r]; n < rp32[r + 1]; ++n) {
         if (n < n0 || n >= n0 + rows) continue;
-        const int64_t row = c0 + (n - rp32[r]) * d.tp + tpi - n0;
+        const int64_t row = c0 + (n - rp32[r]) * stride - n0;
         for (int64_t k = 0; k < Sp; ++k) out[(n - n0) * Sp + k] = raw[(size_t)(((k / cw) * rows + row) * cw + k % cw)];
       }
     }

@@ -164,11 +164,24 @@ struct PreRec {
   uint64_t uid;
 };
 
+// crec: replica cells, the op's cell record (cell-full ops: one pair, the cell-level group).
 template <bool SH>
 __device__ __forceinline__ void prefetch_cross(const DevGraph &g, const XOp &xo, const int32_t *rsh, int C,
-                                               PreRec &pre) {
+                                               PreRec &pre, int64_t crec) {
   const int lane = threadIdx.x & 31;
   const int ns = xo.ns;
+  if (xo.flags & 1) {
+    if (lane == 0) {
+      const int32_t h = rsh[0] + xo.hoff;
+      pre.meta = g.c_meta[crec];
+      pre.base = g.c_base[crec];
+      pre.dur = g.h_dur[h];
+      pre.uid = g.h_uid[h];
+      pre.grp = 0;
+      pre.smask = SH ? g.h_smask[h] : 0u;
+    }
+    return;
+  }
   if (ns > 0 && lane < C * ns) {
     const int r = lane / ns, q = lane - r * ns;
     const int32_t h = rsh[r] + xo.hoff + q;
@@ -218,11 +231,10 @@ struct CrossScratch {
 template <bool SH, int C>
 __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p, const CellArgs &a, const XBuf &xb,
                                           int64_t *__restrict__ gfin, int64_t *ts, int32_t ns,
-                                          int32_t k, CrossScratch<C> &cs, const PreRec &pre, int tl) {
+                                          int32_t k, CrossScratch<C> &cs, const PreRec &pre, int tl, int np) {
   const int lane = threadIdx.x & 31;
   const int32_t Sp = a.Sp;
-  const int32_t ck = k / SC;
-  const int np = C * ns;  // <= 32
+  const int32_t ck = k / SC;  // np = C * ns pairs (<= 32), or 1 for a replica cell's cell-full op
   if (lane < np) {  // the op's sync records, prefetched into registers one cross op ahead
     cs.meta[lane] = pre.meta;
     cs.base[lane] = pre.base;
@@ -416,7 +428,7 @@ __device__ __forceinline__ bool cross_all(const DevGraph &g, const ScenParams &p
   if (tl >= 0 && lane == 0) g_tl[tl * 4 + 2] = globaltimer();
 #endif
   if (large_any && SH) fence_acq_rel_sys();
-  for (int r = 0; r < C; ++r) {
+  for (int r = 0; r < C && r * ns < np; ++r) {
     int64_t fr = 0;
     for (int32_t q = 0; q < ns; ++q) {
       const int x = r * ns + q;
@@ -544,20 +556,33 @@ __device__ __forceinline__ bool cross_pairs(const ScenParams &p, const CellArgs 
   return true;
 }
 
+// Dynamic shared memory of one warp of an EP CTA: cross scratch, chain state, membership slots.
+template <int C>
+__host__ __device__ constexpr size_t cta_warp_scratch() {
+  return (sizeof(CrossScratch<C>) + C * 32 * 8 + MAX_TP * 4 + 15) / 16 * 16;
+}
+
 // PR (rows f1/f3/f4): the graph carries per-node durations (prism_set_durations), so a compute
 // span or chained collective lasts its own rank's value node_sdur[rb[r] + i], loaded one op ahead.
 // MS (row f2, multi-stream ranks): besides its ranks' ready times the warp keeps, per rank, the
 // finish of the last op of each stream and the latest record of each (densely renumbered) event
 // slot in dynamic shared memory; an op starts at max(its stream's last finish, its awaited
 // event). The ranks of a cell still share one template, so TP collectives stay register-local.
-template <int C, bool SH, bool PR, bool MS>
-__global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
+// KS > 1 (EP CTAs, replica cells): the KS cells of one EP group are the KS warps of one CTA; an
+// EP collective (class 4) is the max over the CTA's ranks, formed in registers and shared memory
+// behind one CTA barrier. A warp of such a CTA never leaves the loop early (after an abort it
+// skips the remaining waits), so the CTA's barrier counts always match.
+template <int C, bool SH, bool PR, bool MS, int KS = 1>
+__global__ void __launch_bounds__(KS * 32, KS > 1 ? 2 : (C == 1 ? 28 : (C == 2 ? 24 : 16))) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
                                                          int64_t *__restrict__ fin,
                                                          int64_t *__restrict__ gfin,
                                                          int64_t *__restrict__ rank_end) {
   const int lane = threadIdx.x & 31;
-  const int32_t unit = blockIdx.x * WARPS + (threadIdx.x >> 5);
-  if (unit >= a.n_units || unit == g.stall_unit) return;  // stall_unit: watchdog test hook
+  const int sub = KS > 1 ? (int)(threadIdx.x >> 5) : 0;  // the warp's cell within the CTA
+  const int32_t unit = blockIdx.x;                        // CTA (KS cells)
+  if (unit >= a.n_units) return;  // the whole CTA
+  bool aborted = unit == g.stall_unit;  // stall_unit: watchdog test hook (no arrivals at all)
+  if (KS == 1 && aborted) return;
   constexpr bool PAIR = C >= 4 && !PR && !MS;  // (compute, TP) pairs in one iteration
   // row e: this CTA's shard (a local-group launch covers every shard of the device, units grouped
   // by shard) and its DP block, exchange buffer and output arrays
@@ -591,28 +616,55 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
     xb.arrive = (uint32_t *)(eb + a.L.o_arrive);
   }
   const int32_t nst = s1 - s0;
-  const int32_t cells = nst * (d1 - d0);  // this shard's cells (all of them unsharded)
+  const int32_t RC = g.cell_R > 1 ? g.cell_R : 1;  // replica cells: RC = C consecutive DP replicas
+  const int32_t cells = nst * (d1 - d0) / RC / KS;  // this shard's CTAs of one chunk
   const int32_t cell = u % cells, chunk = a.chunk0 + u / cells;
-  const int32_t s = s0 + cell % nst, dpi = d0 + cell / nst;
+  const int32_t s = s0 + cell % nst, dpi = d0 + ((cell / nst) * KS + sub) * RC;
+  // rank r of the cell: tp index r (TP cells) or DP replica dpi + r (replica cells, tp = 1)
+  auto cell_rank = [&](int32_t r) { return RC > 1 ? rank_of(g, 0, s, dpi + r) : rank_of(g, r, s, dpi); };
+  const int64_t crec0 = RC > 1 ? g.crec_ptr[s] + (int64_t)(dpi / RC) * (g.x_ptr[s + 1] - g.x_ptr[s]) - g.x_ptr[s] : 0;
   const int32_t Sp = a.Sp;
   const int32_t k = chunk * SC + lane;
-  __shared__ int64_t ts[C * 32];  // chain state of the cross-cell path (rolled over ranks)
-  __shared__ CrossScratch<C> cs;
-  __shared__ int32_t rsh[MAX_TP];       // first membership slot of each rank
+  // per-warp scratch: static for one warp per CTA, carved from dynamic shared memory for EP CTAs
+  // (KS warps' scratch exceeds the 48 KB of static shared memory)
+  __shared__ int64_t ts_s[KS == 1 ? C * 32 : 1];  // chain state of the cross-cell path
+  __shared__ CrossScratch<KS == 1 ? C : 1> cs_s;
+  __shared__ int32_t rsh_s[KS == 1 ? MAX_TP : 1];  // first membership slot of each rank
+  extern __shared__ __align__(16) unsigned char dsm[];
+  int64_t *ts;
+  CrossScratch<C> *csp;
+  int32_t *rsh;
+  int64_t *xm = nullptr;  // EP CTAs: [2][KS][32] partial maxima (double-buffered)
+  size_t dyn_used = 0;
+  if (KS == 1) {
+    ts = ts_s;
+    csp = reinterpret_cast<CrossScratch<C> *>(&cs_s);
+    rsh = rsh_s;
+  } else {
+    const size_t per = cta_warp_scratch<C>();
+    unsigned char *w = dsm + (size_t)sub * per;
+    csp = reinterpret_cast<CrossScratch<C> *>(w);
+    ts = reinterpret_cast<int64_t *>(w + sizeof(CrossScratch<C>));
+    rsh = reinterpret_cast<int32_t *>(w + sizeof(CrossScratch<C>) + C * 32 * 8);
+    xm = reinterpret_cast<int64_t *>(dsm + (size_t)KS * per);
+    dyn_used = (size_t)KS * per + 2 * KS * 32 * 8;
+  }
+  CrossScratch<C> &cs = *csp;
+  int xp = 0;
   int32_t rb[C];
   int32_t rs[C];   // first membership slot of each rank (node_gptr of its first node)
   uint32_t rkh[C];  // high word of (rank << 32) * K_MIX (its low word is zero): a compute span's
                     // uid mix is that + tidx * K_MIX (perturb_add_span)
 #pragma unroll
   for (int r = 0; r < C; ++r) {
-    const int32_t rr = rank_of(g, r, s, dpi);
+    const int32_t rr = cell_rank(r);
     rb[r] = g.rank_ptr[rr];
     rs[r] = g.node_gptr[rb[r]];
     rkh[r] = (uint32_t)((((uint64_t)rr << 32) * K_MIX) >> 32);
     if (lane == 0) rsh[r] = rs[r];
   }
   __syncwarp();
-  const int32_t len = g.rank_ptr[rank_of(g, 0, s, dpi) + 1] - rb[0];
+  const int32_t len = g.rank_ptr[cell_rank(0) + 1] - rb[0];
   const int32_t kg = p.first + k;  // global scenario index (perturbation key)
   const uint64_t sx = p.seed ^ ((uint64_t)kg * K_GOLD);
   // per-warp flags pinned in a register (an asm output cannot be rematerialised from the kernel
@@ -625,7 +677,8 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
 #pragma unroll
   for (int r = 0; r < C; ++r) t[r] = 0;
   // MS state: [stream][rank][lane] then [event][rank][lane] (g.ms_streams, g.ms_events)
-  extern __shared__ int64_t ms_dyn[];
+  int64_t *ms_dyn = reinterpret_cast<int64_t *>(dsm + dyn_used) +
+                    (KS > 1 ? (size_t)sub * (g.ms_streams + g.ms_events) * C * 32 : 0);
   if (MS) {
     for (int x = 0; x < (g.ms_streams + g.ms_events) * C; ++x) ms_dyn[x * 32 + lane] = 0;  // unrecorded: satisfied
   }
@@ -640,7 +693,7 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
   PreRec pre{0u, 0u, 0, 0, 0, 0};
   if (xk < xend) {
     xo = g.x_ops[xk];
-    prefetch_cross<SH>(g, xo, rsh, C, pre);
+    prefetch_cross<SH>(g, xo, rsh, C, pre, crec0 + xk);
   }
   int64_t pd[PR ? C : 1];  // PR: per-rank durations of the next op
   if (PR) {
@@ -668,7 +721,8 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
   }
   // fin rows of op i (graph.h fin_off): the cell's C ranks are C consecutive 32-lane rows of this
   // chunk, and op i + 1's rows follow: one moving pointer, rank r at the constant offset r * 32
-  int64_t *fp = fin ? fin + (((int64_t)(k / SC) * g.fin_rows + rb[0] - fnode0) * SC + (k % SC)) : nullptr;
+  int64_t *fp = fin ? fin + (((int64_t)(k / SC) * g.fin_rows + cell_row0(g, cell_rank(0)) - fnode0) * SC + (k % SC))
+                    : nullptr;
   for (int32_t base = 0; base < len; base += 32) {
     const int32_t cnt = min(32, len - base);
     const uint32_t bcls = ncls;
@@ -701,6 +755,7 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
     int64_t d_n = __shfl_sync(0xffffffffu, bd, 0);
     for (int32_t j = 0; j < cnt; ++j) {
       const uint32_t c = c_n & 0xFu;
+      const uint32_t cfl = c_n;  // class flags (0x10 pair, 0x20 / 0x40 replica-cell uid steps)
       // pair: this compute span is followed by a TP collective of this batch (plan flag 0x10);
       // both run in this iteration (plain variant only)
       const bool pair = PAIR && (c_n & 0x10u) && j + 1 < cnt;
@@ -765,6 +820,17 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
 #pragma unroll
           for (int r = 0; r < C; ++r) t[r] += PR ? dr[r] : d;
         }
+      } else if (KS > 1 && c == 4) {  // EP collective of an EP CTA: the group is this CTA's ranks
+        const uint64_t ux = __shfl_sync(0xffffffffu, bux, j);
+        int64_t m = tree_max<C>(t);
+        xm[(xp * KS + sub) * 32 + lane] = m;
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < KS; ++w) m = max(m, xm[(xp * KS + w) * 32 + lane]);
+        xp ^= 1;
+        m += gpert ? perturb_x(d, sx ^ (ux * K_MIX), p) : d;
+#pragma unroll
+        for (int r = 0; r < C; ++r) t[r] = m;
       } else if (c == 1) {  // in-cell TP collective: register-local segmented max
         const uint64_t ux = __shfl_sync(0xffffffffu, bux, j);
         int64_t m = tree_max<C>(t);
@@ -775,9 +841,15 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
                             // occurrence's shared finish, so start = own ready time (exact)
         const uint64_t ux = __shfl_sync(0xffffffffu, bux, j);
         if (gpert) {
-          // rank r's group uid = ux + r * 2^24 (gid = tp_i + ...), WORLD: one group
+          // rank r's group uid = ux + r * 2^24 (gid = tp_i + ...), WORLD: one group; replica cells:
+          // a per-replica group (flag 0x20, gid = s + pp * dp) steps by pp, a cell-full one (0x40)
+          // is one group for the whole cell
           const uint64_t um = ux * K_MIX;
-          const uint64_t stepm = ((ux >> 56) == PRISM_ROLE_WORLD ? 0ull : (1ull << 24)) * K_MIX;
+          const uint32_t cf = cfl;
+          const uint64_t step = (cf & 0x40u) ? 0ull
+                                : (cf & 0x20u) ? ((uint64_t)g.pp << 24)
+                                : ((ux >> 56) == PRISM_ROLE_WORLD ? 0ull : (1ull << 24));
+          const uint64_t stepm = step * K_MIX;
           int64_t dd[C];
           uint64_t xx[C];
 #pragma unroll
@@ -799,6 +871,14 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
         if (k < 32 && dpi == 0 && s < 16 && xk - g.x_ptr[s] < 128) tl = s * 128 + (xk - g.x_ptr[s]);
         if (tl >= 0 && lane == 0) g_tl[tl * 4 + 0] = globaltimer();
 #endif
+        // replica cells, cell-full group (DP / EP / WORLD over the cell's replicas): the cell's
+        // members reach it together, so the warp enters with their max as ONE member (pair 0)
+        const bool cfull = xo.flags & 1;
+        if (cfull) {
+          const int64_t m = tree_max<C>(t);
+#pragma unroll
+          for (int r = 0; r < C; ++r) t[r] = m;
+        }
 #pragma unroll
         for (int r = 0; r < C; ++r) ts[r * 32 + lane] = t[r];
         __syncwarp();
@@ -806,21 +886,27 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
         // TP = 1 / 2 cells it measured slower than cross_all on C4). Sharded: only groups whose
         // members are all on this shard (P2P messages never leave a DP block, reading R9) — no
         // peer touches their ready slots in the local exchange buffer, so gpu scope suffices
-        const bool lean = (C >= 4 || a.lean > 1) && a.lean &&
+        const bool lean = !cfull && (C >= 4 || a.lean > 1) && a.lean &&
                           __all_sync(0xffffffffu, lane >= C * xo.ns || ((pre.meta & 0x8000FFFFu) == 2u &&
                                                                         (!SH || pre.smask == (1u << xb.self))));
-        const bool ok = lean ? cross_pairs<C>(p, a, xb, gfin, ts, xo.ns, k, cs, pre, tl)
-                             : cross_all<SH, C>(g, p, a, xb, gfin, ts, xo.ns, k, cs, pre, tl);
+        // after an abort (watchdog, or the stall test hook) no more arrivals or waits: the warp
+        // runs to the end (EP CTAs keep their barriers matched), its results are invalid
+        const bool ok = aborted ? false
+                        : lean  ? cross_pairs<C>(p, a, xb, gfin, ts, xo.ns, k, cs, pre, tl)
+                                : cross_all<SH, C>(g, p, a, xb, gfin, ts, xo.ns, k, cs, pre, tl, cfull ? 1 : C * xo.ns);
         __syncwarp();
 #pragma unroll
-        for (int r = 0; r < C; ++r) t[r] = ts[r * 32 + lane];
+        for (int r = 0; r < C; ++r) t[r] = ts[(cfull ? 0 : r) * 32 + lane];
 #ifdef PRISM_CELL_STATS
         if (tl >= 0 && lane == 0) g_tl[tl * 4 + 3] = globaltimer();
 #endif
-        if (!ok) return;
+        if (!ok) {
+          if (KS == 1) return;
+          aborted = true;
+        }
         if (++xk < xend) {  // next cross op: its records load while the compute spans run
           xo = g.x_ops[xk];
-          prefetch_cross<SH>(g, xo, rsh, C, pre);
+          prefetch_cross<SH>(g, xo, rsh, C, pre, crec0 + xk);
         }
 #ifdef PRISM_CELL_STATS
         if (lane == 0) {
@@ -852,7 +938,7 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
       for (int x = 0; x < g.ms_streams; ++x) t[r] = max(t[r], ms_dyn[(x * C + r) * 32 + lane]);
   }
 #pragma unroll
-  for (int r = 0; r < C; ++r) rank_end[(int64_t)rank_of(g, r, s, dpi) * Sp + k] = t[r];
+  for (int r = 0; r < C; ++r) rank_end[(int64_t)cell_rank(r) * Sp + k] = t[r];
 #ifdef PRISM_CELL_STATS
   if (lane == 0) {
     STAT_ADD(0, clock64() - k_start);
@@ -863,7 +949,8 @@ __global__ void __launch_bounds__(WARPS * 32, C == 1 ? 28 : (C == 2 ? 24 : 16)) 
 
 }  // namespace
 
-// type-erased kernel pointer of one variant (cells_k_*.cu)
-const void *cell_kernel_get(int tp, bool sh, bool pr, bool ms);
+// type-erased kernel pointer of one variant (cells_k_*.cu): tp = cell width (tp, or the replicas
+// of a replica cell), ks = warps (cells) per CTA: 1, or 8 for EP CTAs (width 2, 4 or 8)
+const void *cell_kernel_get(int tp, bool sh, bool pr, bool ms, int ks);
 
 }  // namespace prism

@@ -5,7 +5,16 @@
 
 namespace prism {
 
-const void *cell_kernel_get_sto(int tp) {
+const void *cell_kernel_get_sto(int tp, int ks) {
+  if (ks == 8) {  // EP CTAs: eight replica cells of tp-width R per CTA
+    switch (tp) {
+      case 2: return (const void *)cell_kernel<2, true, false, false, 8>;
+      case 4: return (const void *)cell_kernel<4, true, false, false, 8>;
+      case 8: return (const void *)cell_kernel<8, true, false, false, 8>;
+      default: return nullptr;
+    }
+  }
+  if (ks != 1) return nullptr;
   switch (tp) {
     case 1: return (const void *)cell_kernel<1, true, false, false>;
     case 2: return (const void *)cell_kernel<2, true, false, false>;

@@ -5,7 +5,16 @@
 
 namespace prism {
 
-const void *cell_kernel_get_upm(int tp) {
+const void *cell_kernel_get_upm(int tp, int ks) {
+  if (ks == 8) {  // EP CTAs: eight replica cells of tp-width R per CTA
+    switch (tp) {
+      case 2: return (const void *)cell_kernel<2, false, true, true, 8>;
+      case 4: return (const void *)cell_kernel<4, false, true, true, 8>;
+      case 8: return (const void *)cell_kernel<8, false, true, true, 8>;
+      default: return nullptr;
+    }
+  }
+  if (ks != 1) return nullptr;
   switch (tp) {
     case 1: return (const void *)cell_kernel<1, false, true, true>;
     case 2: return (const void *)cell_kernel<2, false, true, true>;

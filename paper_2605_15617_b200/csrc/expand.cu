@@ -369,6 +369,41 @@ __global__ void __launch_bounds__(256) build_groups_kernel(DevGraph g) {
 
 }  // namespace
 
+// Replica cells: one thread per (stage, DP block, cross op of the stage); cell-full ops get their
+// group's cell-level slot (row a4 at cell granularity). The cell's member index in its group: DP
+// and EDP (ep = 1) groups number their cells by DP block, EP groups by the block within the EP
+// group, the WORLD group by (stage, block).
+__global__ void __launch_bounds__(256) cell_records_kernel(DevGraph g) {
+  const int32_t R = g.cell_R, nb = g.dp / R;
+  for (int32_t s = blockIdx.x; s < g.pp; s += gridDim.x) {
+    const int32_t x0 = g.x_ptr[s], nx = g.x_ptr[s + 1] - x0;
+    for (int32_t y = threadIdx.x; y < nb * nx; y += blockDim.x) {
+      const int32_t b = y / nx, x = x0 + y % nx;
+      const XOp xo = g.x_ops[x];
+      if (!(xo.flags & 1)) continue;
+      const QGroup q = ldg_q(g.q + __ldg(g.t_q0 + g.t_op0[s] + xo.tidx));
+      const int32_t dpi = b * R, epi = dpi % g.ep, edpi = dpi / g.ep;
+      const int32_t inst = group_inst(g, q.type, 0, dpi, epi, edpi);
+      const int32_t cz = q.size / R;
+      int32_t own;
+      switch (q.type) {
+        case PRISM_ROLE_EP: own = epi / R; break;
+        case PRISM_ROLE_WORLD: own = s * nb + b; break;
+        default: own = b; break;  // DP, EDP with ep = 1
+      }
+      const bool large = q.clbase >= 0;
+      const int64_t rec = g.crec_ptr[s] + (int64_t)b * nx + (x - x0);
+      g.c_meta[rec] = (uint32_t)min(cz, 0xFFFF) | ((uint32_t)min(own, 0x7FFF) << 16) | (large ? 0x80000000u : 0u);
+      g.c_base[rec] = large ? (int32_t)(q.clbase + inst) : (int32_t)(q.cxbase + (int64_t)inst * cz);
+    }
+  }
+}
+
+cudaError_t launch_cell_records(const DevGraph &g, cudaStream_t st) {
+  if (g.cell_R > 1 && g.pp > 0) cell_records_kernel<<<g.pp, 256, 0, st>>>(g);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_expand(const DevGraph &g, cudaStream_t st) {
   rank_tables_kernel<<<1, 1024, 0, st>>>(g);
   if (g.N > 0) {

@@ -25,6 +25,16 @@ struct DevGraph {
   uint64_t watchdog_ns;
   // fin rows kept by this graph: [fin_node0, fin_node0 + fin_rows) of the row order below
   int64_t fin_node0, fin_rows;
+  // replica cells (cell_R > 1, tp = 1): a cell is cell_R consecutive DP replicas of one stage;
+  // crec_ptr[s] + b * (x ops of stage s) + x = the cell record of cross op x of cell (s, b):
+  // c_meta = size in cells | own cell index << 16 | large << 31, c_base = first cell-level ready
+  // slot or the accumulator index of the op's group (cell-full ops, XOp flags bit 0)
+  int32_t cell_R;
+  int32_t cta_ks;            // EP CTAs: the cta_ks replica cells of one EP group share a CTA
+  int64_t Ltot;              // ops of all stage templates together
+  const int64_t *crec_ptr;   // [pp+1]
+  int32_t *c_base;
+  uint32_t *c_meta;
   // row f2: multi-stream ranks (per-node stream / event fields, directional predecessors, -1 =
   // none); streams and densely renumbered event slots used by the graph
   int32_t ms, ms_streams, ms_events;
@@ -111,11 +121,26 @@ struct DevGraph {
 // cell kernel warp (one cell, one 32-scenario chunk) thus writes op i of its ranks as C
 // consecutive 256-byte rows at constant offsets (no per-op address arithmetic), and its ops follow
 // each other contiguously.
+// Replica cells (cell_R = R > 1, tp = 1) interleave the R replicas instead: op i of replica rr of
+// cell (stage s, DP block b) is row base(s, b) + i R + rr with base = R (b Ltot + op0[s]) under
+// TP_PP_DP (cells b-major, then s) and dp op0[s] + b R len(s) under Megatron order.
 #ifdef __CUDACC__
+__device__ __forceinline__ int64_t cell_row0(const DevGraph &g, int32_t r) {  // row of rank r's op 0
+  if (g.cell_R <= 1) {
+    const int32_t tpi = r % g.tp;
+    return (int64_t)g.rank_ptr[r - tpi] + tpi;
+  }
+  const int32_t R = g.cell_R;
+  const bool meg = g.order == PRISM_ORDER_MEGATRON;
+  const int32_t s = meg ? r / g.dp : r % g.pp, dpi = meg ? r % g.dp : r / g.pp;
+  const int64_t base = meg ? (int64_t)g.dp * g.t_op0[s] + (int64_t)(dpi / R) * R * g.t_len[s]
+                           : (int64_t)R * ((int64_t)(dpi / R) * g.Ltot + g.t_op0[s]);
+  return base + dpi % R;
+}
+__device__ __forceinline__ int32_t cell_row_stride(const DevGraph &g) { return g.cell_R > 1 ? g.cell_R : g.tp; }
 __device__ __forceinline__ int64_t fin_row(const DevGraph &g, int32_t n) {
   const int32_t r = g.node_rank[n];
-  const int32_t tpi = r % g.tp;
-  return (int64_t)g.rank_ptr[r - tpi] + (int64_t)(n - g.rank_ptr[r]) * g.tp + tpi;
+  return cell_row0(g, r) + (int64_t)(n - g.rank_ptr[r]) * cell_row_stride(g);
 }
 __device__ __forceinline__ int64_t fin_off(const DevGraph &g, int64_t row, int32_t k, int32_t Sp) {
   const int32_t cw = Sp < 32 ? Sp : 32;
@@ -251,6 +276,8 @@ struct Tile {
 
 // expand.cu
 cudaError_t launch_expand(const DevGraph &g, cudaStream_t st);
+// replica cells: the cell records of the cell-full cross ops
+cudaError_t launch_cell_records(const DevGraph &g, cudaStream_t st);
 // replay.cu
 cudaError_t launch_level(const DevGraph &g, const ScenParams &p, const Tile *tiles, int32_t ntiles,
                          int32_t max_cnt, int64_t *fin, int64_t *gfin, int lanes, int nchunks,

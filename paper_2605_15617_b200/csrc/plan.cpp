@@ -429,6 +429,8 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     // other group exchanges ready times through global ready slots
     g.xbase = -1;
     g.lbase = -1;
+    g.cxbase = -1;
+    g.clbase = -1;
     if (g.type != PRISM_ROLE_TP) {
       if (g.size <= kSmallGroup) {
         g.xbase = X;
@@ -518,6 +520,71 @@ prism_status plan_graph(const prism_topology &tp_, const prism_templates &tm, Pl
     err = fmt("graph too large for int32 ids: N=%lld M=%lld G=%lld", N, M, G);
     return PRISM_E_INVALID_ARG;
   }
+  return PRISM_OK;
+}
+
+bool replica_cells_ok(const Topo &t, int32_t R) {
+  return R > 1 && t.tp == 1 && t.dp % R == 0 && (t.ep == 1 || t.ep % R == 0);
+}
+
+prism_status plan_replica_cells(Plan &P, int32_t R, int32_t ks, std::string &err) {
+  const Topo &t = P.topo;
+  if (!replica_cells_ok(t, R)) {
+    err = "replica cells need tp == 1, R | dp and (ep == 1 or R | ep)";
+    return PRISM_E_INVALID_ARG;
+  }
+  // does a group of this role hold all R replicas of a cell (else exactly one of them)?
+  auto full = [&](int role) {
+    switch (role) {
+      case PRISM_ROLE_DP:
+      case PRISM_ROLE_WORLD: return true;
+      case PRISM_ROLE_EP: return t.ep > 1;        // R | ep: the cell's replicas share edp
+      case PRISM_ROLE_EDP: return t.ep == 1;      // ep = 1: the EDP group is the DP group
+      default: return false;                      // TP / size-1 EP / P2P
+    }
+  };
+  const int pp = t.pp;
+  // classes: TP collectives (size-1 groups) become per-replica chained ops (flag 0x20: uid step
+  // pp << 24 between replicas, gid = s + pp * dp); chained collectives of full groups keep one uid
+  // for the whole cell (flag 0x40: step 0); the (compute, TP) pair flag disappears with class 1
+  P.x_ops.clear();
+  P.x_ptr.assign(pp + 1, 0);
+  P.crec_ptr.assign(pp + 1, 0);
+  for (int s = 0; s < pp; ++s) {
+    const int64_t a = P.stage_op0[s], b = a + P.stage_len[s];
+    for (int64_t i = a; i < b; ++i) {
+      uint8_t c = P.t_cls[i] & 0xF;
+      const int32_t q0 = P.t_q0[i];
+      const int role = q0 >= 0 ? P.q[q0].type : 0;
+      if (c == 1) c = 3 | 0x20;
+      else if (c == 3) c = 3 | (full(role) ? 0x40 : 0x20);
+      else if (c == 2 && ks > 1 && role == PRISM_ROLE_EP && t.ep == R * ks) c = 4;  // the CTA is the group
+      P.t_cls[i] = c;
+      if (c == 2)
+        P.x_ops.push_back(XOp{(int32_t)(i - a), P.t_slot_ptr[i], P.t_slots[i],
+                              (role != PRISM_ROLE_P2P && full(role)) ? 1 : 0});
+    }
+    P.x_ptr[s + 1] = (int32_t)P.x_ops.size();
+    P.crec_ptr[s + 1] = P.crec_ptr[s] + (int64_t)(t.dp / R) * (P.x_ptr[s + 1] - P.x_ptr[s]);
+  }
+  // cell-level slots of the full groups, after the rank-level ones (the rank kernel and the level
+  // path keep using those)
+  int64_t X = P.M_cross, LG = P.G_large;
+  for (QGroup &g : P.q) {
+    if (g.type == PRISM_ROLE_P2P || !full(g.type)) continue;
+    const int64_t cz = g.size / R;
+    if (cz <= kSmallGroup) {
+      g.cxbase = X;
+      X += (int64_t)g.inst * cz;
+    } else {
+      g.clbase = LG;
+      LG += g.inst;
+    }
+  }
+  P.M_cross = X;
+  P.G_large = LG;
+  P.cell_R = R;
+  P.cta_ks = ks;
   return PRISM_OK;
 }
 

@@ -50,11 +50,15 @@ struct QGroup {
   int64_t mbase;       // first membership index
   int64_t xbase;       // first ready slot (cell kernel, small cross-cell groups); -1 otherwise
   int64_t lbase;       // first accumulator index (cell kernel, large groups); -1 otherwise
+  // replica cells (Plan::cell_R > 1): a group holding all R replicas of a cell exchanges ONE value
+  // per cell: cell-level ready slots (size / R <= kSmallGroup) or accumulator; -1 otherwise
+  int64_t cxbase, clbase;
 };
 
-// A cross-cell op of a stage template: its template index, first slot offset and slot count.
+// A cross-cell op of a stage template: its template index, first slot offset and slot count;
+// flags bit 0 (replica cells): the op's group holds every rank of the cell (one member per cell).
 struct XOp {
-  int32_t tidx, hoff, ns, pad;
+  int32_t tidx, hoff, ns, flags;
 };
 
 struct Topo {
@@ -103,7 +107,25 @@ struct Plan {
   // group-side build chunks: (quotient group, first local membership), 2048 memberships each
   std::vector<int32_t> chunk_q;
   std::vector<int64_t> chunk_m;
+  // replica cells (tp = 1): a cell of the cell kernel is cell_R consecutive DP replicas of one
+  // stage instead of one TP group (1 = TP cells); per stage, the cell records of its cross ops
+  // start at crec_ptr[s] (cells x cross ops of the stage)
+  int32_t cell_R = 1;
+  int32_t cta_ks = 1;  // EP CTAs: cells per CTA (1 = one warp per CTA)
+  std::vector<int64_t> crec_ptr;
 };
+
+// Replica cells (row a6/a7): with tp = 1 the cell kernel's warps walk R consecutive
+// DP replicas of a stage. A collective whose group holds all R replicas (DP, WORLD, EP when R
+// divides ep, EDP when ep = 1) is reduced over the cell in registers and exchanged with ONE
+// value per cell; a group holding one replica per cell (TP and EP of size 1, EDP when R divides
+// ep, P2P messages) keeps its per-rank exchange. Rewrites the replay classes, marks the cell-full
+// cross ops and allocates cell-level slots. Requires tp == 1, R | dp and (ep == 1 or R | ep).
+// ks > 1 (EP CTAs): the ks cells of one EP group (ep = R ks) share a CTA, and an EP collective
+// becomes class 4: the group's max is formed in registers and shared memory behind one CTA
+// barrier, with no global exchange at all.
+prism_status plan_replica_cells(Plan &P, int32_t R, int32_t ks, std::string &err);
+bool replica_cells_ok(const Topo &t, int32_t R);
 
 // Returns PRISM_OK or an error status with *err filled.
 prism_status plan_graph(const prism_topology &topo, const prism_templates &tm, Plan &plan,

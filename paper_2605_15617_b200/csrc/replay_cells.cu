@@ -34,7 +34,15 @@ namespace prism {
 
 #ifdef PRISM_CELL_STATS
 template <bool SH, bool PR, bool MS>
-static const void *cell_kernel_tp(int tp) {
+static const void *cell_kernel_tp(int tp, int ks) {
+  if (ks == 8) {
+    switch (tp) {
+      case 2: return (const void *)cell_kernel<2, SH, PR, MS, 8>;
+      case 4: return (const void *)cell_kernel<4, SH, PR, MS, 8>;
+      case 8: return (const void *)cell_kernel<8, SH, PR, MS, 8>;
+      default: return nullptr;
+    }
+  }
   switch (tp) {
     case 1: return (const void *)cell_kernel<1, SH, PR, MS>;
     case 2: return (const void *)cell_kernel<2, SH, PR, MS>;
@@ -47,17 +55,17 @@ static const void *cell_kernel_tp(int tp) {
     default: return nullptr;
   }
 }
-const void *cell_kernel_get(int tp, bool sh, bool pr, bool ms) {
+const void *cell_kernel_get(int tp, bool sh, bool pr, bool ms, int ks) {
   const int v = (sh ? 1 : 0) | (pr ? 2 : 0) | (ms ? 4 : 0);
   switch (v) {
-    case 0: return cell_kernel_tp<false, false, false>(tp);
-    case 1: return cell_kernel_tp<true, false, false>(tp);
-    case 2: return cell_kernel_tp<false, true, false>(tp);
-    case 3: return cell_kernel_tp<true, true, false>(tp);
-    case 4: return cell_kernel_tp<false, false, true>(tp);
-    case 5: return cell_kernel_tp<true, false, true>(tp);
-    case 6: return cell_kernel_tp<false, true, true>(tp);
-    default: return cell_kernel_tp<true, true, true>(tp);
+    case 0: return cell_kernel_tp<false, false, false>(tp, ks);
+    case 1: return cell_kernel_tp<true, false, false>(tp, ks);
+    case 2: return cell_kernel_tp<false, true, false>(tp, ks);
+    case 3: return cell_kernel_tp<true, true, false>(tp, ks);
+    case 4: return cell_kernel_tp<false, false, true>(tp, ks);
+    case 5: return cell_kernel_tp<true, false, true>(tp, ks);
+    case 6: return cell_kernel_tp<false, true, true>(tp, ks);
+    default: return cell_kernel_tp<true, true, true>(tp, ks);
   }
 }
 #endif
@@ -69,24 +77,37 @@ namespace {
 // cells_k_*.cu units, compiled in parallel; PRISM_CELL_STATS builds instantiate them here so the
 // statistics arrays are one set).
 const void *cell_kernel_for(const DevGraph &g) {
-  return cell_kernel_get(g.tp, g.n_shards > 1, g.per_rank_dur != 0, g.ms != 0);
+  // cell width: the tp ranks of a TP cell, or the R replicas of a replica cell
+  return cell_kernel_get(g.cell_R > 1 ? g.cell_R : g.tp, g.n_shards > 1, g.per_rank_dur != 0, g.ms != 0,
+                         g.cta_ks > 1 ? g.cta_ks : 1);
 }
 // dynamic shared memory of the multi-stream state (0 otherwise)
 size_t cell_dyn_smem(const DevGraph &g) {
-  return g.ms ? (size_t)(g.ms_streams + g.ms_events) * g.tp * 32 * 8 : 0;
+  const int w = g.cell_R > 1 ? g.cell_R : g.tp, ks = g.cta_ks > 1 ? g.cta_ks : 1;
+  const size_t msb = g.ms ? (size_t)(g.ms_streams + g.ms_events) * w * 32 * 8 * ks : 0;
+  if (ks == 1) return msb;
+  size_t per = 0;
+  switch (w) {  // EP CTAs: per-warp scratch + the partial-max buffer, in dynamic shared memory
+    case 2: per = cta_warp_scratch<2>(); break;
+    case 4: per = cta_warp_scratch<4>(); break;
+    default: per = cta_warp_scratch<8>(); break;
+  }
+  return (size_t)ks * per + 2 * (size_t)ks * 32 * 8 + msb;
 }
 
 cudaError_t preload_cell_kernels() {
   cudaFuncAttributes a;
   for (int tp = 1; tp <= MAX_TP; ++tp)
-    for (int v = 0; v < 8; ++v) {
-      const void *f = cell_kernel_get(tp, v & 1, v & 2, v & 4);
-      cudaError_t e = cudaFuncGetAttributes(&a, f);
-      if (e != cudaSuccess) return e;
-      // allow the multi-stream state beyond the 48 KB default of dynamic shared memory
-      e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      if (e != cudaSuccess) return e;
-    }
+    for (int ks : {1, 8})
+      for (int v = 0; v < 8; ++v) {
+        const void *f = cell_kernel_get(tp, v & 1, v & 2, v & 4, ks);
+        if (!f) continue;
+        cudaError_t e = cudaFuncGetAttributes(&a, f);
+        if (e != cudaSuccess) return e;
+        // allow the multi-stream state / the EP CTAs' scratch beyond the 48 KB default
+        e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, ks > 1 ? 200 * 1024 : 96 * 1024);
+        if (e != cudaSuccess) return e;
+      }
   return cudaSuccess;
 }
 
@@ -99,11 +120,12 @@ bool cell_fit_units(const DevGraph &g, int64_t units, int *ctas) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
   if (!coop) return false;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, WARPS * 32, cell_dyn_smem(g)) != cudaSuccess) {
+  const int ks = g.cta_ks > 1 ? g.cta_ks : 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, ks * 32, cell_dyn_smem(g)) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  const int64_t need = (units + WARPS - 1) / WARPS;
+  const int64_t need = units;  // one CTA per unit (a cell, or the KS cells of an EP CTA)
   if (ctas) *ctas = (int)need;
   return need >= 1 && (int64_t)per_sm * sms >= need;
 }
@@ -136,7 +158,10 @@ PollPolicy poll_policy() {
 
 // Chunks of 32 scenarios per unit; every chunk of a replay runs in one launch when they all fit,
 // else the caller launches one chunk at a time (chunk groups of 1).
-int64_t cell_count(const DevGraph &g) { return (int64_t)(g.s1 - g.s0) * (g.d1 - g.d0); }
+// CTAs of one chunk: cells, or EP CTAs of cta_ks cells
+int64_t cell_count(const DevGraph &g) {
+  return (int64_t)(g.s1 - g.s0) * (g.d1 - g.d0) / (g.cell_R > 1 ? g.cell_R : 1) / (g.cta_ks > 1 ? g.cta_ks : 1);
+}
 
 bool cells_fit(const DevGraph &g, int nchunks, int group) {
   return cell_fit_units(g, cell_count(g) * group, nullptr) && nchunks >= 1;
@@ -167,7 +192,7 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
   ScenParams pp = p;
   int64_t *fin_g = fin;
   void *args[] = {&gg, &pp, &a, &fin_g, &gfin, &rank_end};
-  return cudaLaunchCooperativeKernel(cell_kernel_for(g), dim3(ctas), dim3(WARPS * 32), args,
+  return cudaLaunchCooperativeKernel(cell_kernel_for(g), dim3(ctas), dim3((g.cta_ks > 1 ? g.cta_ks : 1) * 32), args,
                                      cell_dyn_smem(g), st);
 }
 

@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(32, 16) rank_kernel(DevGraph g, ScenParams p, 
   const int32_t rb = active ? g.rank_ptr[r] : 0;
   // fin row of op i: cell-interleaved (graph.h fin_off; one scenario: row = element), so the tp
   // lanes of a cell store op i to consecutive words
-  const int64_t frow0 = active ? (int64_t)g.rank_ptr[r - tpi] + tpi - g.fin_node0 : 0;
+  const int64_t frow0 = active ? cell_row0(g, r) - g.fin_node0 : 0;
+  const int32_t fstride = cell_row_stride(g);
   const int32_t rs = active ? g.node_gptr[rb] : 0;  // the rank's first membership slot
   const int32_t s0 = s < g.pp ? s : 0;
   const int32_t len = (int32_t)g.t_len[s0];
@@ -233,7 +234,7 @@ __global__ void __launch_bounds__(32, 16) rank_kernel(DevGraph g, ScenParams p, 
         }
         if (active) t = fr;
       }
-      if (p.record && active) fin[frow0 + (int64_t)i * g.tp] = t;
+      if (p.record && active) fin[frow0 + (int64_t)i * fstride] = t;
     }
   }
   if (active) rank_end[r] = t;
