@@ -503,10 +503,16 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     // EP CTAs: the 8 cells of an EP group (R = ep / 8 replicas each) share one CTA, so an EP
     // all-to-all is a register + shared-memory max behind one barrier; a DP-block shard must then
     // hold whole EP groups. PRISM_REPLICA_CELLS=2: replica cells of 8 without EP CTAs.
-    const int ks = 8;
     const Topo &tt = plan.topo;
+    static const int env_ks = [] {
+      const char *e = std::getenv("PRISM_EP_CTA_KS");
+      return e ? std::atoi(e) : 0;
+    }();
+    // sixteen cells of ep / 16 replicas when that width is instantiated (2 or 4), else eight
+    const int ks = env_ks ? env_ks : ((tt.ep % 16 == 0 && (tt.ep / 16 == 2 || tt.ep / 16 == 4)) ? 16 : 8);
     const bool cta = env_rc != 2 && tt.tp == 1 && tt.ep >= ks && tt.ep % ks == 0 && tt.ep / ks <= 8 &&
-                     (tt.ep / ks) * ks == tt.ep && (n_shards == 1 || axis == 1 || (tt.dp / n_shards) % tt.ep == 0);
+                     (n_shards == 1 || axis == 1 || (tt.dp / n_shards) % tt.ep == 0) &&
+                     (ks == 8 || tt.ep / ks == 2 || tt.ep / ks == 4);
     const int R = cta ? tt.ep / ks : 8;
     const bool blocks_ok = n_shards == 1 || axis == 1 || (tt.dp / n_shards) % R == 0;
     if (env_rc && (cta || env_rc == 2) && blocks_ok && replica_cells_ok(tt, R) && (R == 1 || R == 2 || R == 4 || R == 8)) {

@@ -573,7 +573,7 @@ __host__ __device__ constexpr size_t cta_warp_scratch() {
 // behind one CTA barrier. A warp of such a CTA never leaves the loop early (after an abort it
 // skips the remaining waits), so the CTA's barrier counts always match.
 template <int C, bool SH, bool PR, bool MS, int KS = 1>
-__global__ void __launch_bounds__(KS * 32, KS > 1 ? 2 : (C == 1 ? 28 : (C == 2 ? 24 : 16))) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
+__global__ void __launch_bounds__(KS * 32, KS > 8 ? 1 : (KS > 1 ? 2 : (C == 1 ? 28 : (C == 2 ? 24 : 16)))) cell_kernel(DevGraph g, ScenParams p, CellArgs a,
                                                          int64_t *__restrict__ fin,
                                                          int64_t *__restrict__ gfin,
                                                          int64_t *__restrict__ rank_end) {
@@ -950,7 +950,7 @@ __global__ void __launch_bounds__(KS * 32, KS > 1 ? 2 : (C == 1 ? 28 : (C == 2 ?
 }  // namespace
 
 // type-erased kernel pointer of one variant (cells_k_*.cu): tp = cell width (tp, or the replicas
-// of a replica cell), ks = warps (cells) per CTA: 1, or 8 for EP CTAs (width 2, 4 or 8)
+// of a replica cell), ks = warps (cells) per CTA: 1, or 8 / 16 for EP CTAs (width 2, 4 or 8 / 2 or 4)
 const void *cell_kernel_get(int tp, bool sh, bool pr, bool ms, int ks);
 
 }  // namespace prism

@@ -14,6 +14,13 @@ const void *cell_kernel_get_sto(int tp, int ks) {
       default: return nullptr;
     }
   }
+  if (ks == 16) {  // EP CTAs of sixteen narrower replica cells
+    switch (tp) {
+      case 2: return (const void *)cell_kernel<2, true, false, false, 16>;
+      case 4: return (const void *)cell_kernel<4, true, false, false, 16>;
+      default: return nullptr;
+    }
+  }
   if (ks != 1) return nullptr;
   switch (tp) {
     case 1: return (const void *)cell_kernel<1, true, false, false>;

@@ -35,6 +35,13 @@ namespace prism {
 #ifdef PRISM_CELL_STATS
 template <bool SH, bool PR, bool MS>
 static const void *cell_kernel_tp(int tp, int ks) {
+  if (ks == 16) {
+    switch (tp) {
+      case 2: return (const void *)cell_kernel<2, SH, PR, MS, 16>;
+      case 4: return (const void *)cell_kernel<4, SH, PR, MS, 16>;
+      default: return nullptr;
+    }
+  }
   if (ks == 8) {
     switch (tp) {
       case 2: return (const void *)cell_kernel<2, SH, PR, MS, 8>;
@@ -98,7 +105,7 @@ size_t cell_dyn_smem(const DevGraph &g) {
 cudaError_t preload_cell_kernels() {
   cudaFuncAttributes a;
   for (int tp = 1; tp <= MAX_TP; ++tp)
-    for (int ks : {1, 8})
+    for (int ks : {1, 8, 16})
       for (int v = 0; v < 8; ++v) {
         const void *f = cell_kernel_get(tp, v & 1, v & 2, v & 4, ks);
         if (!f) continue;
