@@ -53,6 +53,8 @@ class Clocks:
         self.proc = None
 
     def __enter__(self):
+        if os.environ.get("PRISM_BENCH_NO_CLOCKS"):  # experiments only: the sampler's own cost
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -524,7 +526,9 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    # 50 steps by default (~0.2 s of GPU time): the first timed step carries the pipeline fill (its
+    # host build of ~2.5 ms runs with the device idle) and the clock sampler runs alongside
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
     ap.add_argument("--config", default="C5")

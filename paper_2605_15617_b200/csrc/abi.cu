@@ -221,7 +221,12 @@ struct prism_graph_s {
   void *ctx = nullptr;
   std::vector<std::pair<void *, size_t>> blocks;  // structure allocations
   int64_t structure_bytes = 0;
-  // replay state
+  // replay state: the arrays below live in ONE device block (`state`, carved per replay), so a
+  // replay allocates at most once through the allocator hooks (each hook call costs the Python
+  // binding tens of microseconds of host time on the bench step's critical path)
+  unsigned char *state = nullptr;
+  size_t state_cap = 0;
+  size_t state_off[8] = {}, state_len[8] = {};  // the current carve (offsets, bytes)
   int64_t *fin = nullptr;
   size_t fin_bytes = 0;
   int64_t *gfin = nullptr;
@@ -340,17 +345,10 @@ struct prism_graph_s {
   }
   ~prism_graph_s() {
     trace("destroy: begin");
-    dfree(fin);
-    dfree(gfin);
-    dfree(rank_end);
+    dfree(state);
     dfree(iter);
     dfree(scratch);
     dfree(tiles);
-    dfree(rslot);
-    dfree(acc);
-    dfree(rres);
-    dfree(sync_words);
-    dfree(part);
     dfree(ov);
     dfree(din_blk);
     dfree(moe_blk);
@@ -605,11 +603,13 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   const size_t table_bytes = off;
   // graph arrays (written by the expand kernels)
   const size_t o_rp = carve((W + 1) * 4), o_rs = carve((W + 1) * 4), o_rst = carve(W * 4);
-  const size_t o_nrank = carve(N * 4), o_ndur = carve(N * 8), o_nkind = carve(N), o_nlab = carve(N * 4);
-  const size_t o_nal = carve(N * 8), o_nfr = carve(N * 8), o_nps = carve(N * 4), o_ngp = carve((N + 1) * 4);
+  // per node only the structure (rank, previous sync node, slot pointer); a node's duration, kind,
+  // label, memory deltas and replay record are its template op's (graph.h nd_*, the cell kernel's
+  // record loads), looked up instead of written N times
+  const size_t o_nrank = carve(N * 4), o_nps = carve(N * 4), o_ngp = carve((N + 1) * 4);
   const size_t o_ngrp = carve(M * 4), o_gptr = carve((Gn + 1) * 4), o_gmem = carve(M * 4), o_gdur = carve(Gn * 8);
-  const size_t o_guid = carve(Gn * 8), o_glvl = carve(Gn * 4), o_nms = carve(M * 4), o_ncls = carve(N);
-  const size_t o_nsd = carve(N * 8), o_nuid = carve(N * 8), o_gxb = carve(Gn * 8), o_gli = carve(Gn * 4);
+  const size_t o_guid = carve(Gn * 8), o_glvl = carve(Gn * 4), o_nms = carve(M * 4);
+  const size_t o_gxb = carve(Gn * 8), o_gli = carve(Gn * 4);
   const size_t o_hb = carve(M * 4), o_hm = carve(M * 4), o_hd = carve(M * 8), o_hu = carve(M * 8);
   const size_t o_hs = n_shards > 1 ? carve(M * 4) : 0;
   const size_t o_nmsk = ms ? carve(N * 2) : 0, o_nsp = ms ? carve(N * 4) : 0, o_nes = ms ? carve(N * 4) : 0;
@@ -659,11 +659,11 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.rank_slot = (int32_t *)at(o_rs);
   d.rank_stage = (int32_t *)at(o_rst);
   d.node_rank = (int32_t *)at(o_nrank);
-  d.node_dur = (int64_t *)at(o_ndur);
-  d.node_kind = (uint8_t *)at(o_nkind);
-  d.node_label = (uint32_t *)at(o_nlab);
-  d.node_alloc = (int64_t *)at(o_nal);
-  d.node_free = (int64_t *)at(o_nfr);
+  d.node_dur = nullptr;  // template lookups (overrides replace them in dov)
+  d.node_kind = nullptr;
+  d.node_label = nullptr;
+  d.node_alloc = nullptr;
+  d.node_free = nullptr;
   d.node_prev_sync = (int32_t *)at(o_nps);
   d.node_gptr = (int32_t *)at(o_ngp);
   d.node_grp = (int32_t *)at(o_ngrp);
@@ -673,9 +673,9 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   d.grp_uid = (uint64_t *)at(o_guid);
   d.grp_level = (int32_t *)at(o_glvl);
   d.node_mslot = (int32_t *)at(o_nms);
-  d.node_cls = (uint8_t *)at(o_ncls);
-  d.node_sdur = (int64_t *)at(o_nsd);
-  d.node_uid = (uint64_t *)at(o_nuid);
+  d.node_cls = nullptr;
+  d.node_sdur = nullptr;
+  d.node_uid = nullptr;
   d.grp_xbase = (int64_t *)at(o_gxb);
   d.grp_lidx = (int32_t *)at(o_gli);
   d.h_base = (int32_t *)at(o_hb);
@@ -726,6 +726,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     put(o_chm, P.chunk_m.data(), nch * 8);
     put(o_tcls, P.t_cls.data(), nops);
     put(o_tq0, P.t_q0.data(), nops * 4);
+    trace("pack: plan tables copied");
     {
       int64_t *tdur = (int64_t *)(hb + o_tdur), *tal = (int64_t *)(hb + o_tal);
       int64_t *tfr = (int64_t *)(hb + o_tfr), *tsd = (int64_t *)(hb + o_tsd);
@@ -749,6 +750,7 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
         }
       }
     }
+    trace("pack: op fields");
     put(o_xptr, P.x_ptr.data(), (pp + 1) * 4);
     if (P.cell_R > 1) put(o_crp, P.crec_ptr.data(), (pp + 1) * 8);
     put(o_xops, P.x_ops.data(), P.x_ops.size() * sizeof(XOp));
@@ -793,6 +795,54 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
 }  // extern "C"
 
 namespace {
+
+// Replay state of one replay (bytes per array; 0 = not needed), carved from the graph's state block.
+struct StateReq {
+  size_t fin, gfin, rank_end, rslot, acc, rres, sync, part;
+};
+prism_status ensure_state(prism_graph_t G, const StateReq &q) {
+  const size_t want[8] = {q.fin, q.gfin, q.rank_end, q.rslot, q.acc, q.rres, q.sync, q.part};
+  size_t off = 0, o[8];
+  for (int i = 0; i < 8; ++i) {
+    off = (off + 255) & ~(size_t)255;
+    o[i] = off;
+    off += want[i];
+  }
+  const size_t total = std::max<size_t>(off, 256);
+  bool relayout = false;
+  for (int i = 0; i < 8; ++i) relayout |= G->state_off[i] != o[i] || G->state_len[i] != want[i];
+  if (total > G->state_cap || !G->state) {
+    G->dfree(G->state);
+    G->state = (unsigned char *)G->dalloc(total);
+    G->state_cap = G->state ? total : 0;
+    if (!G->state) return fail(PRISM_E_OOM, "replay-state allocation failed");
+    relayout = true;
+  }
+  // the ready / result slots must be reset when their memory or offsets changed
+  if (relayout) G->rslot_dirty = true;
+  for (int i = 0; i < 8; ++i) {
+    G->state_off[i] = o[i];
+    G->state_len[i] = want[i];
+  }
+  auto at = [&](int i) { return want[i] ? (void *)(G->state + o[i]) : nullptr; };
+  G->fin = (int64_t *)at(0);
+  G->fin_bytes = want[0];
+  G->gfin = (int64_t *)at(1);
+  G->gfin_bytes = want[1];
+  G->rank_end = (int64_t *)at(2);
+  G->rank_end_bytes = want[2];
+  G->rslot = (int64_t *)at(3);
+  G->rslot_bytes = want[3];
+  G->acc = (int64_t *)at(4);
+  G->acc_bytes = want[4];
+  G->rres = (int64_t *)at(5);
+  G->rres_bytes = want[5];
+  G->sync_words = (uint32_t *)at(6);
+  G->sync_bytes = want[6];
+  G->part = (int64_t *)at(7);
+  G->part_bytes = want[7];
+  return PRISM_OK;
+}
 
 // Tiles of every level for a team width of `lanes` (one membership per team per round).
 prism_status plan_tiles(prism_graph_s *G, int lanes) {
@@ -848,20 +898,16 @@ prism_status replay_ranks_impl(prism_graph_t G, const prism_scenarios *sc, int64
   p.mod_m32 = p.mod > 1 ? (uint32_t)((((uint64_t)1 << 32) + (uint64_t)p.mod - 1) / (uint64_t)p.mod) : 0xFFFFFFFFu;
   G->recorded = 0;
   const int32_t Sp = 1;
-  if (p.record && !G->ensure(G->fin, G->fin_bytes, (size_t)std::max<int64_t>(1, G->fin_rows) * 8))
-    return fail(PRISM_E_OOM, "fin allocation failed");
-  if (!G->ensure(G->gfin, G->gfin_bytes, (size_t)std::max<int64_t>(1, P.G) * 8)) return fail(PRISM_E_OOM, "gfin allocation failed");
-  if (!G->ensure(G->rank_end, G->rank_end_bytes, (size_t)P.W * 8)) return fail(PRISM_E_OOM, "rank_end allocation failed");
-  const size_t rs_bytes = std::max<size_t>(16, (size_t)P.M_cross * 8);
-  if (G->rslot_bytes < rs_bytes || G->rslot_Sp != Sp) G->rslot_dirty = true;
-  G->rslot_Sp = Sp;
-  if (!G->ensure(G->rslot, G->rslot_bytes, rs_bytes)) return fail(PRISM_E_OOM, "ready-slot allocation failed");
   const size_t lg = std::max<size_t>(16, (size_t)P.G_large * 8);
-  if (!G->ensure(G->acc, G->acc_bytes, lg)) return fail(PRISM_E_OOM, "accumulator allocation failed");
-  if (G->rres_bytes < lg) G->rslot_dirty = true;
-  if (!G->ensure(G->rres, G->rres_bytes, lg)) return fail(PRISM_E_OOM, "result-slot allocation failed");
   const size_t nwords = std::max<size_t>(1, (size_t)P.G_large);
-  if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
+  {
+    const StateReq q{p.record ? (size_t)std::max<int64_t>(1, G->fin_rows) * 8 : 0, (size_t)std::max<int64_t>(1, P.G) * 8,
+                     (size_t)P.W * 8, std::max<size_t>(16, (size_t)P.M_cross * 8), lg, lg, nwords * 4, 0};
+    prism_status st = ensure_state(G, q);
+    if (st) return st;
+  }
+  if (G->rslot_Sp != Sp) G->rslot_dirty = true;
+  G->rslot_Sp = Sp;
   if (G->rslot_dirty) {
     CU(cudaMemsetAsync(G->rslot, 0xFF, G->rslot_bytes, G->stream));
     CU(cudaMemsetAsync(G->rres, 0xFF, G->rres_bytes, G->stream));
@@ -951,19 +997,25 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
   G->recorded = 0;
   G->gathered_k = -1;
   trace("replay: begin");
-  if (p.record) {
-    if (!G->ensure(G->fin, G->fin_bytes, (size_t)std::max<int64_t>(1, G->fin_rows) * Sp * 8))
-      return fail(PRISM_E_OOM, "fin[N][S] allocation failed");
+  {
+    StateReq q{p.record ? (size_t)std::max<int64_t>(1, G->fin_rows) * Sp * 8 : 0, (size_t)std::max<int64_t>(1, P.G) * Sp * 8,
+               (size_t)P.W * Sp * 8, 0, 0, 0, 0, 0};
+    if (sharded) {
+      q.part = (size_t)Sp * 8;
+    } else if (cells) {
+      q.rslot = std::max<size_t>(16, (size_t)P.M_cross * Sp * 8);
+      q.acc = q.rres = std::max<size_t>(16, (size_t)P.G_large * Sp * 8);
+      q.sync = std::max<size_t>(1, (size_t)P.G_large * nchunks) * 4;
+    }
+    prism_status st = ensure_state(G, q);
+    if (st) return st;
   }
-  if (!G->ensure(G->gfin, G->gfin_bytes, (size_t)P.G * Sp * 8)) return fail(PRISM_E_OOM, "gfin allocation failed");
-  if (!G->ensure(G->rank_end, G->rank_end_bytes, (size_t)P.W * Sp * 8)) return fail(PRISM_E_OOM, "rank_end allocation failed");
   int64_t launches = 0;
   trace("replay: buffers ready");
   if (sharded) {
     // row e: ready slots / accumulators / counters live in the peer-mapped exchange buffer; they
     // were reset at prepare, and the accumulators and counters are reset again right after the
     // cell kernel, before this shard publishes its partial (the peers' next pushes wait for it)
-    if (!G->ensure(G->part, G->part_bytes, (size_t)Sp * 8)) return fail(PRISM_E_OOM, "partial allocation failed");
     // an abort leaves the peers' exchange state inconsistent: the graph is re-prepared instead of
     // reset (check_status disconnects it), so the guard only folds the status
     CU(launch_replay_guard(G->words, nullptr, 0, nullptr, 0, G->parity, G->stream));
@@ -994,17 +1046,9 @@ prism_status replay_impl(prism_graph_t G, const prism_scenarios *sc, int64_t *it
     trace("shard: status copy");
     launches += 2;
   } else if (cells) {
-    const size_t rs_bytes = std::max<size_t>(16, (size_t)P.M_cross * Sp * 8);
-    if (G->rslot_bytes < rs_bytes || G->rslot_Sp != Sp) G->rslot_dirty = true;
+    if (G->rslot_Sp != Sp) G->rslot_dirty = true;
     G->rslot_Sp = Sp;
-    if (!G->ensure(G->rslot, G->rslot_bytes, rs_bytes)) return fail(PRISM_E_OOM, "ready-slot allocation failed");
-    if (!G->ensure(G->acc, G->acc_bytes, std::max<size_t>(16, (size_t)P.G_large * Sp * 8)))
-      return fail(PRISM_E_OOM, "accumulator allocation failed");
-    const size_t rr_bytes = std::max<size_t>(16, (size_t)P.G_large * Sp * 8);
-    if (G->rres_bytes < rr_bytes) G->rslot_dirty = true;  // result slots share the ready slots' parity
-    if (!G->ensure(G->rres, G->rres_bytes, rr_bytes)) return fail(PRISM_E_OOM, "result-slot allocation failed");
-    const size_t nwords = std::max<size_t>(1, (size_t)P.G_large * nchunks);
-    if (!G->ensure(G->sync_words, G->sync_bytes, nwords * 4)) return fail(PRISM_E_OOM, "sync-word allocation failed");
+    const size_t nwords = G->sync_bytes / 4;
     if (G->rslot_dirty) {  // all slots read "not yet" under parity 0
       CU(cudaMemsetAsync(G->rslot, 0xFF, G->rslot_bytes, G->stream));
       CU(cudaMemsetAsync(G->rres, 0xFF, G->rres_bytes, G->stream));
@@ -1549,10 +1593,10 @@ prism_status prism_replay_local_shards(const prism_graph_t *shards, int32_t n, c
     prism_graph_t G = shards[i];
     G->recorded = 0;
     G->gathered_k = -1;
-    if (p.record && !G->ensure(G->fin, G->fin_bytes, (size_t)std::max<int64_t>(1, G->fin_rows) * Sp * 8))
-      return fail(PRISM_E_OOM, "fin allocation failed");
-    if (!G->ensure(G->gfin, G->gfin_bytes, (size_t)P.G * Sp * 8)) return fail(PRISM_E_OOM, "gfin allocation failed");
-    if (!G->ensure(G->rank_end, G->rank_end_bytes, (size_t)P.W * Sp * 8)) return fail(PRISM_E_OOM, "rank_end allocation failed");
+    const StateReq q{p.record ? (size_t)std::max<int64_t>(1, G->fin_rows) * Sp * 8 : 0, (size_t)P.G * Sp * 8,
+                     (size_t)P.W * Sp * 8, 0, 0, 0, 0, 0};
+    prism_status st = ensure_state(G, q);
+    if (st) return st;
     L.lg_fin[i] = p.record ? G->fin : nullptr;
     L.lg_gfin[i] = G->gfin;
     L.lg_rank_end[i] = G->rank_end;
@@ -1841,11 +1885,11 @@ extern "C" PRISM_API prism_status prism_debug_export(prism_graph_t G, int32_t wh
   switch (which) {
     case 0: src = d.rank_ptr; need = (d.W + 1) * 4; break;
     case 1: src = d.node_rank; need = d.N * 4; break;
-    case 2: src = d.node_dur; need = d.N * 8; break;
-    case 3: src = d.node_kind; need = d.N; break;
-    case 4: src = d.node_label; need = d.N * 4; break;
-    case 5: src = d.node_alloc; need = d.N * 8; break;
-    case 6: src = d.node_free; need = d.N * 8; break;
+    case 2: need = d.N * 8; break;  // 2-6: template fields, materialised below
+    case 3: need = d.N; break;
+    case 4: need = d.N * 4; break;
+    case 5: need = d.N * 8; break;
+    case 6: need = d.N * 8; break;
     case 7: src = d.node_prev_sync; need = d.N * 4; break;
     case 8: src = d.node_gptr; need = (d.N + 1) * 4; break;
     case 9: src = d.node_grp; need = d.M * 4; break;
@@ -1860,6 +1904,11 @@ extern "C" PRISM_API prism_status prism_debug_export(prism_graph_t G, int32_t wh
   if (bytes < need) return fail(PRISM_E_INVALID_ARG, "buffer too small: need " + std::to_string(need));
   if (need == 0) return PRISM_OK;
   CU(cudaSetDevice(G->device));
+  if (which >= 2 && which <= 6) {
+    if (!G->ensure(G->scratch, G->scratch_bytes, (size_t)need)) return fail(PRISM_E_OOM, "scratch allocation failed");
+    CU(launch_materialize(d, which, G->scratch, G->stream));
+    src = G->scratch;
+  }
   if (which == 15) {  // fin: device layout (graph.h fin_off) -> canonical [row = node][Sp], rank-major
     const int64_t rows = G->fin_rows, Sp = G->last_Sp, cw = Sp < 32 ? Sp : 32, n0 = G->fin_node0;
     std::vector<int64_t> raw((size_t)(rows * Sp));

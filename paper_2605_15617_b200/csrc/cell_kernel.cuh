@@ -700,25 +700,28 @@ __global__ void __launch_bounds__(KS * 32, KS > 8 ? 1 : (KS > 1 ? 2 : (C == 1 ? 
 #pragma unroll
     for (int r = 0; r < C; ++r) pd[r] = len > 0 ? __ldg(g.node_sdur + rb[r]) : 0;
   }
-  // op records of the cell's first rank (the template is shared; the per-rank part of a compute
-  // span's uid is rk[r]), 32 ops per coalesced round trip, next batch in flight
-  // The record pointers are loop-carried and each batch loads at a constant offset from them:
-  // address temporaries of the batch loads would be reused by the next op's shuffles, and a
-  // register still feeding an in-flight load's address stalls its next writer (long scoreboard at
-  // every op's dispatch in the v10 profile)
-  const uint8_t *p_cls = g.node_cls + rb[0] + lane;
-  const int64_t *p_sd = g.node_sdur + rb[0] + lane;
-  const uint64_t *p_uid = g.node_uid + rb[0] + lane;
-  const uint16_t *p_ms = MS ? g.node_ms + rb[0] + lane : nullptr;
+  // op records of the stage template (the cell's ranks share it; the per-rank part of a compute
+  // span's uid is rkh[r]): class, record duration (PR: the rank-0 node's override, e.g. a group's
+  // max over its members' overridden durations) and, for in-cell / chained / CTA-local group ops,
+  // the uid of the cell's rank-0 group (closed form from the template's packed group word),
+  // 32 ops per coalesced round trip from the L2-resident tables, next batch in flight
+  const int64_t top0 = g.t_op0[s];
+  const int32_t tp0 = 0, dp0 = dpi;  // coordinates of the cell's rank 0
+  auto load_rec = [&](int32_t i, uint32_t &cls, int64_t &d, uint64_t &ux, uint32_t &msv) {
+    const int64_t op = top0 + i;
+    cls = __ldg(g.t_cls + op);
+    d = PR ? __ldg(g.node_sdur + rb[0] + i) : __ldg(g.t_sdur + op);
+    ux = 0;
+    if ((cls & 0xFu) != 0 && (cls & 0xFu) != 2) {
+      const uint64_t qi = __ldg(g.t_qinfo + op);
+      ux = group_uid_packed(g, qi, group_inst(g, (int32_t)(qi & 0xFF), tp0, dp0, dp0 % g.ep, dp0 / g.ep));
+    }
+    if (MS) msv = __ldg(g.t_ms + op);
+  };
   uint32_t ncls = 2, nms = 0;
   int64_t nd = 0;
   uint64_t nux = 0;
-  if (lane < len) {
-    ncls = *p_cls;
-    nd = *p_sd;
-    nux = *p_uid;
-    if (MS) nms = *p_ms;
-  }
+  if (lane < len) load_rec(lane, ncls, nd, nux, nms);
   // fin rows of op i (graph.h fin_off): the cell's C ranks are C consecutive 32-lane rows of this
   // chunk, and op i + 1's rows follow: one moving pointer, rank r at the constant offset r * 32
   int64_t *fp = fin ? fin + (((int64_t)(k / SC) * g.fin_rows + cell_row0(g, cell_rank(0)) - fnode0) * SC + (k % SC))
@@ -729,26 +732,7 @@ __global__ void __launch_bounds__(KS * 32, KS > 8 ? 1 : (KS > 1 ? 2 : (C == 1 ? 
     const int64_t bd = nd;
     const uint64_t bux = nux;
     const uint32_t bms = nms;
-    if (base + 32 + lane < len) {
-      if (C >= 4 && !PR) {
-        ncls = p_cls[32];
-        nd = p_sd[32];
-        nux = p_uid[32];
-        if (MS) nms = p_ms[32];
-      } else {  // small cells, per-rank durations: fewer live registers (PR measured slower)
-        const int32_t n = rb[0] + base + 32 + lane;
-        ncls = g.node_cls[n];
-        nd = g.node_sdur[n];
-        nux = g.node_uid[n];
-        if (MS) nms = g.node_ms[n];
-      }
-    }
-    if (C >= 4 && !PR) {
-      p_cls += 32;
-      p_sd += 32;
-      p_uid += 32;
-      if (MS) p_ms += 32;
-    }
+    if (base + 32 + lane < len) load_rec(base + 32 + lane, ncls, nd, nux, nms);
     // op j's class / duration were fetched during op j-1 (software pipelined: the dispatch
     // branch of an op does not wait on its shuffles)
     uint32_t c_n = __shfl_sync(0xffffffffu, bcls, 0);

@@ -110,21 +110,6 @@ __device__ __forceinline__ uint64_t group_gid(const DevGraph &g, const QGroup &q
 __device__ __forceinline__ uint64_t group_uid(const DevGraph &g, const QGroup &q, int32_t inst) {
   return ((uint64_t)q.type << 56) | (group_gid(g, q, inst) << 24) | (uint64_t)q.occ;
 }
-// The same from a host-packed t_qinfo word (type | dir << 8 | stage << 16 | occurrence << 32).
-__device__ __forceinline__ uint64_t group_uid_packed(const DevGraph &g, uint64_t qi, int32_t inst) {
-  const int32_t type = (int32_t)(qi & 0xFF), dir = (int32_t)((qi >> 8) & 0xFF);
-  const int32_t s = (int32_t)((qi >> 16) & 0xFFFF);
-  uint64_t gid;
-  switch (type) {
-    case PRISM_ROLE_TP: gid = (uint64_t)s + (uint64_t)g.pp * inst; break;
-    case PRISM_ROLE_DP: gid = (uint64_t)inst + (uint64_t)g.tp * s; break;
-    case PRISM_ROLE_EP:
-    case PRISM_ROLE_EDP: gid = (uint64_t)(inst % g.tp) + (uint64_t)g.tp * (s + (uint64_t)g.pp * (inst / g.tp)); break;
-    case PRISM_ROLE_WORLD: gid = 0; break;
-    default: gid = (uint64_t)rank_of(g, inst % g.tp, s, inst / g.tp) * 2 + dir; break;
-  }
-  return ((uint64_t)type << 56) | (gid << 24) | (qi >> 32);
-}
 
 // Row e: the shards holding a member of the group of a rank with DP coordinates (dpi, epi, edpi)
 // under the DP-block sharding (shard of dp_i = dp_i / (dp / n_shards)); TP groups and P2P
@@ -175,41 +160,18 @@ __device__ __forceinline__ QGroup ldg_q(const QGroup *p) {
   return q;
 }
 
-// Instance of quotient group q that a rank with these coordinates joins (closed form, a2).
-__device__ __forceinline__ int32_t group_inst(const DevGraph &g, int32_t type, int32_t tpi, int32_t dpi,
-                                              int32_t epi, int32_t edpi) {
-  switch (type) {
-    case PRISM_ROLE_TP: return dpi;
-    case PRISM_ROLE_DP: return tpi;
-    case PRISM_ROLE_EP: return tpi + g.tp * edpi;
-    case PRISM_ROLE_EDP: return tpi + g.tp * epi;
-    case PRISM_ROLE_WORLD: return 0;
-    default: return tpi + g.tp * dpi;  // P2P message (sender or receiver: same tp/dp)
-  }
-}
 
-// Template fields of one op that the node-side expansion writes (expand_nodes_kernel).
+// Template fields of one op that the node-side expansion writes (expand_nodes_kernel): the
+// structure only (previous sync op, slot offset, stream / event edges); the op's own fields stay
+// in the template tables (graph.h nd_*).
 struct OpF {
-  int64_t dur, al, fr, sdur;
-  uint64_t qinfo;
-  int32_t tps, q0, tsp, sp, es;
-  uint32_t lab;
+  int32_t tps, tsp, sp, es;
   uint16_t msv;
-  uint8_t kind, cls;
 };
 __device__ __forceinline__ OpF load_opf(const DevGraph &g, int64_t ti) {
   OpF f;
   f.tps = __ldg(g.t_prev_sync + ti);
-  f.q0 = __ldg(g.t_q0 + ti);
-  f.dur = __ldg(g.t_dur + ti);
-  f.al = __ldg(g.t_alloc + ti);
-  f.fr = __ldg(g.t_free + ti);
-  f.sdur = __ldg(g.t_sdur + ti);
-  f.lab = __ldg(g.t_label + ti);
-  f.kind = __ldg(g.t_kind + ti);
-  f.cls = __ldg(g.t_cls + ti);
   f.tsp = __ldg(g.t_slot_ptr + ti);
-  f.qinfo = __ldg(g.t_qinfo + ti);
   f.sp = -1;
   f.es = -1;
   f.msv = 0;
@@ -257,32 +219,18 @@ __global__ void __launch_bounds__(256, 2) expand_nodes_kernel(DevGraph g) {
     for (int32_t i = threadIdx.x; i < len; i += blockDim.x) {
       OpF nxt;
       if (i + (int32_t)blockDim.x < len) nxt = load_opf(g, op0 + i + blockDim.x);
-      const int32_t qtype = (int32_t)(cur.qinfo & 0xFF);  // a sync node's first group (t_qinfo)
       for (int32_t j = 0; j < nr; ++j) {
         const int32_t r = s_r[j], rb = s_rb[j];
         const int32_t n = rb + i;
+        // the op's own fields (duration, kind, label, memory, replay record) are the template's:
+        // looked up by (stage, index) where needed (graph.h nd_*), not written per node
         g.node_rank[n] = r;
-        g.node_dur[n] = cur.dur;
-        g.node_kind[n] = cur.kind;
-        g.node_label[n] = cur.lab;
-        g.node_alloc[n] = cur.al;
-        g.node_free[n] = cur.fr;
         g.node_prev_sync[n] = cur.tps < 0 ? -1 : rb + cur.tps;
         g.node_gptr[n] = s_slot0[j] + cur.tsp;
         if (g.ms) {
           g.node_ms[n] = cur.msv;
           g.node_spred[n] = cur.sp < 0 ? -1 : rb + cur.sp;
           g.node_esrc[n] = cur.es < 0 ? -1 : rb + cur.es;
-        }
-        // replay record: a compute span carries its own duration and uid; a sync node its first
-        // group's (quotient group q0, instance from the rank's coordinates)
-        g.node_cls[n] = cur.cls;
-        g.node_sdur[n] = cur.sdur;
-        if (cur.q0 < 0) {
-          g.node_uid[n] = ((uint64_t)r << 32) | (uint32_t)i;
-        } else {
-          const int32_t dpi = s_dpi[j];
-          g.node_uid[n] = group_uid_packed(g, cur.qinfo, group_inst(g, qtype, s_tpi[j], dpi, dpi % g.ep, dpi / g.ep));
         }
       }
       cur = nxt;
@@ -397,6 +345,25 @@ __global__ void __launch_bounds__(256) cell_records_kernel(DevGraph g) {
       g.c_base[rec] = large ? (int32_t)(q.clbase + inst) : (int32_t)(q.cxbase + (int64_t)inst * cz);
     }
   }
+}
+
+// Test hook (prism_debug_export): the per-node template fields, materialised.
+__global__ void __launch_bounds__(256) materialize_kernel(DevGraph g, int32_t which, void *out) {
+  for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N; n += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t m = (int32_t)n;
+    switch (which) {
+      case 2: ((int64_t *)out)[n] = nd_dur(g, m); break;
+      case 3: ((uint8_t *)out)[n] = nd_kind(g, m); break;
+      case 4: ((uint32_t *)out)[n] = nd_label(g, m); break;
+      case 5: ((int64_t *)out)[n] = nd_alloc(g, m); break;
+      default: ((int64_t *)out)[n] = nd_free(g, m); break;
+    }
+  }
+}
+
+cudaError_t launch_materialize(const DevGraph &g, int32_t which, void *out, cudaStream_t st) {
+  if (g.N > 0) materialize_kernel<<<num_sms() * 4, 256, 0, st>>>(g, which, out);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_cell_records(const DevGraph &g, cudaStream_t st) {

@@ -148,6 +148,60 @@ __device__ __forceinline__ int64_t fin_off(const DevGraph &g, int64_t row, int32
 }
 #endif
 
+// ---- closed forms and template lookups shared by the kernels (rows a1-a4) ----------------------
+#ifdef __CUDACC__
+__device__ __forceinline__ int32_t dg_rank_of(const DevGraph &g, int32_t tp_i, int32_t pp_i, int32_t dp_i) {
+  return g.order == PRISM_ORDER_MEGATRON ? tp_i + g.tp * (dp_i + g.dp * pp_i) : tp_i + g.tp * (pp_i + g.pp * dp_i);
+}
+// Instance of quotient group q that a rank with these coordinates joins (closed form, a2).
+__device__ __forceinline__ int32_t group_inst(const DevGraph &g, int32_t type, int32_t tpi, int32_t dpi,
+                                              int32_t epi, int32_t edpi) {
+  switch (type) {
+    case PRISM_ROLE_TP: return dpi;
+    case PRISM_ROLE_DP: return tpi;
+    case PRISM_ROLE_EP: return tpi + g.tp * edpi;
+    case PRISM_ROLE_EDP: return tpi + g.tp * epi;
+    case PRISM_ROLE_WORLD: return 0;
+    default: return tpi + g.tp * dpi;  // P2P message (sender or receiver: same tp/dp)
+  }
+}
+// The same from a host-packed t_qinfo word (type | dir << 8 | stage << 16 | occurrence << 32).
+__device__ __forceinline__ uint64_t group_uid_packed(const DevGraph &g, uint64_t qi, int32_t inst) {
+  const int32_t type = (int32_t)(qi & 0xFF), dir = (int32_t)((qi >> 8) & 0xFF);
+  const int32_t s = (int32_t)((qi >> 16) & 0xFFFF);
+  uint64_t gid;
+  switch (type) {
+    case PRISM_ROLE_TP: gid = (uint64_t)s + (uint64_t)g.pp * inst; break;
+    case PRISM_ROLE_DP: gid = (uint64_t)inst + (uint64_t)g.tp * s; break;
+    case PRISM_ROLE_EP:
+    case PRISM_ROLE_EDP: gid = (uint64_t)(inst % g.tp) + (uint64_t)g.tp * (s + (uint64_t)g.pp * (inst / g.tp)); break;
+    case PRISM_ROLE_WORLD: gid = 0; break;
+    default: gid = (uint64_t)dg_rank_of(g, inst % g.tp, s, inst / g.tp) * 2 + dir; break;
+  }
+  return ((uint64_t)type << 56) | (gid << 24) | (qi >> 32);
+}
+
+// Per-node fields that are the node's template op's (every rank of a stage runs the stage's
+// template): looked up from the L2-resident per-stage tables instead of being written out
+// per node by the expansion; an override array (prism_set_durations / _set_moe_load) takes their
+// place when set.
+__device__ __forceinline__ int64_t node_op(const DevGraph &g, int32_t n) {
+  const int32_t r = g.node_rank[n];
+  return g.t_op0[g.rank_stage[r]] + (n - g.rank_ptr[r]);
+}
+__device__ __forceinline__ int64_t nd_dur(const DevGraph &g, int32_t n) {
+  return g.node_dur ? g.node_dur[n] : __ldg(g.t_dur + node_op(g, n));
+}
+__device__ __forceinline__ int64_t nd_alloc(const DevGraph &g, int32_t n) {
+  return g.node_alloc ? g.node_alloc[n] : __ldg(g.t_alloc + node_op(g, n));
+}
+__device__ __forceinline__ int64_t nd_free(const DevGraph &g, int32_t n) {
+  return g.node_free ? g.node_free[n] : __ldg(g.t_free + node_op(g, n));
+}
+__device__ __forceinline__ uint8_t nd_kind(const DevGraph &g, int32_t n) { return __ldg(g.t_kind + node_op(g, n)); }
+__device__ __forceinline__ uint32_t nd_label(const DevGraph &g, int32_t n) { return __ldg(g.t_label + node_op(g, n)); }
+#endif
+
 // Scenario parameters as seen by the kernels.
 struct ScenParams {
   int32_t S;         // scenarios
@@ -278,6 +332,8 @@ struct Tile {
 cudaError_t launch_expand(const DevGraph &g, cudaStream_t st);
 // replica cells: the cell records of the cell-full cross ops
 cudaError_t launch_cell_records(const DevGraph &g, cudaStream_t st);
+// test hook: per-node template field `which` (prism_debug_export 2..6) into a device array
+cudaError_t launch_materialize(const DevGraph &g, int32_t which, void *out, cudaStream_t st);
 // replay.cu
 cudaError_t launch_level(const DevGraph &g, const ScenParams &p, const Tile *tiles, int32_t ntiles,
                          int32_t max_cnt, int64_t *fin, int64_t *gfin, int lanes, int nchunks,

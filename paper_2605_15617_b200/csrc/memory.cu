@@ -21,13 +21,16 @@ __global__ void __launch_bounds__(256) peak_kernel(DevGraph g, int64_t *__restri
   const int32_t warps = gridDim.x * (blockDim.x >> 5);
   for (int32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < g.W; r += warps) {
     const int32_t rb = g.rank_ptr[r], re = g.rank_ptr[r + 1];
+    // the rank's memory deltas: its stage template's (L2-resident), or per-node overrides
+    const int64_t *al = g.node_alloc ? g.node_alloc + rb : g.t_alloc + g.t_op0[g.rank_stage[r]];
+    const int64_t *fr = g.node_free ? g.node_free + rb : g.t_free + g.t_op0[g.rank_stage[r]];
     int64_t carry = 0, best = 0;  // best: this lane's max of R_i + alloc_i (warp max at the end)
     for (int32_t base = rb; base < re; base += 32) {
       const int32_t i = base + lane;
       int64_t a = 0, f = 0;
       if (i < re) {
-        a = __ldcs(g.node_alloc + i);
-        f = __ldcs(g.node_free + i);
+        a = al[i - rb];
+        f = fr[i - rb];
       }
       int64_t x = a - f;  // inclusive scan of (alloc - free)
 #pragma unroll

@@ -70,7 +70,7 @@ __device__ __forceinline__ void walk_segment(const DevGraph &g, const ScenParams
   }
   const uint64_t rhi = (uint64_t)r << 32;
   for (int32_t i = (ps >= 0 ? ps + 1 : rb); i < end; ++i) {
-    const int64_t d = g.node_dur[i];
+    const int64_t d = nd_dur(g, i);
     const uint64_t uidx = (rhi | (uint32_t)(i - rb)) * K_MIX;
 #pragma unroll
     for (int j = 0; j < SPL; ++j) {
@@ -386,7 +386,7 @@ __device__ __forceinline__ int64_t node_start(const DevGraph &g, const ScenParam
   const int32_t h0 = g.node_gptr[i], h1 = g.node_gptr[i + 1];
   const int32_t kg = p.first + k;  // global scenario index (perturbation key)
   if (h0 == h1) {  // compute span: exact, finish = start + d'
-    int64_t d = g.node_dur[i];
+    int64_t d = nd_dur(g, i);
     if ((p.mask & 1u) && p.amp > 0 && kg > 0)
       d = perturb_x(d, p.seed ^ ((uint64_t)kg * K_GOLD) ^ ((((uint64_t)r << 32) | (uint32_t)(i - rb)) * K_MIX), p);
     return fin[fin_off(g, fin_row(g, i), k, Sp)] - d;
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(1024) peak_time_kernel(DevGraph g, ScenParams 
         const int64_t tm = fr ? fin[fin_off(g, fin_row(g, n), k, Sp)] : node_start(g, p, Sp, fin, gfin, r, rb, n, k);
         key[x] = (unsigned long long)tm;
         kix[x] = (uint16_t)x;
-        val[x] = fr ? -g.node_free[n] : g.node_alloc[n];
+        val[x] = fr ? -nd_free(g, n) : nd_alloc(g, n);
       } else {
         key[x] = ~0ull;
         kix[x] = 0xFFFF;

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(256) eff_kernel(DevGraph g, DurIn in, MoeIn me
                                                   int64_t *__restrict__ eal, int64_t *__restrict__ efr,
                                                   uint32_t *status) {
   for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < g.N; n += (int64_t)gridDim.x * blockDim.x) {
-    int64_t d = in.base ? in.base[n] : g.node_dur[n];
+    int64_t d = in.base ? in.base[n] : nd_dur(g, (int32_t)n);
     if (d < 0 || d > (1LL << 40)) atomicCAS(status, 0u, (uint32_t)PRISM_E_INVALID_ARG);
     const int32_t r = g.node_rank[n];
     int32_t b = 65536;  // br of the node's gating event on its EP rank (Q16), 1.0 if not routed
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(256) eff_kernel(DevGraph g, DurIn in, MoeIn me
     }
     if (me.scale & PRISM_MOE_DUR) d = (d * (int64_t)b) >> 16;
     if (in.n_labels > 0) {
-      const uint32_t L = g.node_label[n];
+      const uint32_t L = nd_label(g, (int32_t)n);
       int32_t lo = 0, hi = in.n_labels - 1;
       while (lo <= hi) {
         const int32_t mid = (lo + hi) >> 1;
@@ -64,10 +64,10 @@ __global__ void __launch_bounds__(256) eff_kernel(DevGraph g, DurIn in, MoeIn me
         else hi = mid - 1;
       }
     }
-    if (in.rank_f && g.node_kind[n] == PRISM_KIND_COMPUTE) d = (d * (int64_t)in.rank_f[r]) >> 16;
+    if (in.rank_f && nd_kind(g, (int32_t)n) == PRISM_KIND_COMPUTE) d = (d * (int64_t)in.rank_f[r]) >> 16;
     eff[n] = d;
     if (eal) {
-      int64_t a = in.al ? in.al[n] : g.node_alloc[n], f = in.fr ? in.fr[n] : g.node_free[n];
+      int64_t a = in.al ? in.al[n] : nd_alloc(g, (int32_t)n), f = in.fr ? in.fr[n] : nd_free(g, (int32_t)n);
       if (a < 0 || f < 0 || a > (1LL << 43) || f > (1LL << 43)) atomicCAS(status, 0u, (uint32_t)PRISM_E_INVALID_ARG);
       if (me.scale & PRISM_MOE_ALLOC) a = (a * (int64_t)b) >> 16;
       if (me.scale & PRISM_MOE_FREE) f = (f * (int64_t)b) >> 16;
