@@ -123,11 +123,20 @@ def run_prism(args):
     import workloads as w
 
     ws, rank, local = _dist()
+    # PRISM_BENCH_ONE_GPU=1 (plumbing check on a 1-GPU box only, never a measurement): every rank on
+    # cuda:0, gloo for the host-side collectives (NCCL needs one GPU per rank)
+    one_gpu = ws > 1 and os.environ.get("PRISM_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
+        os.environ.setdefault("PRISM_ALLOW_SAME_DEVICE_IPC", "1")
     torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     prism.use_torch_allocator()
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
@@ -203,7 +212,7 @@ def run_prism(args):
     shard_axis = graphs[0].shard_info()["axis"] if sharded else "none"
     launches_per_step = st["replay_launches"] + 3 + 1  # expand: rank tables, nodes, groups; peak
     if ws > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64, device="cpu" if one_gpu else "cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
@@ -253,7 +262,7 @@ def run_prism(args):
         e2e_ms = (time.perf_counter() - t0) * 1e3 / reps
         assert (it_host == iters).all()
     if ws > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cpu" if one_gpu else "cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_ms = float(t.item())
 

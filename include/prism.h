@@ -145,7 +145,8 @@ typedef struct {
  * PRISM_BUILD_ASYNC: return once the expansion is queued on the stream (later calls on the same
  * stream are ordered after it); by default prism_build_graph waits for it.
  * PRISM_BUILD_SHARD_DP / _PP: force the shard axis of a sharded build (default: the axis whose
- * blocks cut the fewest group memberships; every shard must resolve the same axis). */
+ * blocks cut the fewest exchanged synchronisations — template-level sync ops whose group spans
+ * shards, chained collectives excepted — SURVEY §8.4; every shard resolves the same axis). */
 enum { PRISM_BUILD_PROFILE = 1, PRISM_BUILD_ASYNC = 2, PRISM_BUILD_SHARD_DP = 4, PRISM_BUILD_SHARD_PP = 8 };
 
 /* Scenario batch for what-if sweeps (re-time without structural change).

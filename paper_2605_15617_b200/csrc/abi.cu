@@ -411,7 +411,7 @@ prism_status prism_set_allocator(prism_alloc_fn alloc, prism_free_fn free_fn, vo
 }  // extern "C"
 
 namespace {
-// Row e, SURVEY §8.4 planner: the shard axis whose blocks cut the fewest memberships. DP blocks
+// Row e, SURVEY §8.4 planner: the shard axis whose blocks cut the fewest exchanged synchronisations. DP blocks
 // (shard of a rank = dp_i / (dp/n)) keep TP groups and P2P messages local and cut DP and WORLD
 // collectives, EP all-to-alls wider than a block and EDP groups; PP-stage blocks keep every
 // collective but WORLD local and cut the P2P messages at block edges. opts->flags may force one.
@@ -434,10 +434,13 @@ prism_status choose_shard_axis(const Plan &P, int n, int flags, int &axis, std::
     axis = 1;
     return PRISM_OK;
   }
+  // cost of an axis = the template-level synchronisations it cuts that the replay must exchange
+  // (a chained collective, class 3, resolves locally): each one puts a cross-shard rendezvous on a
+  // rank's chain, whatever the number of its instances (they run side by side)
   const int64_t Bd = P.topo.dp / n, Bp = P.topo.pp / n, ep = P.topo.ep;
   int64_t cut_dp = 0, cut_pp = 0;
   for (const QGroup &q : P.q) {
-    const int64_t m = (int64_t)q.inst * q.size;
+    const int64_t m = (P.t_cls[P.stage_op0[q.stage] + q.tidx] & 0xF) == 3 ? 0 : 1;
     switch (q.type) {
       case PRISM_ROLE_DP: cut_dp += m; break;
       case PRISM_ROLE_WORLD: cut_dp += m; cut_pp += m; break;
