@@ -70,6 +70,13 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
         results = list(ex.map(compile_one, sources()))
+    keep = {os.path.abspath(o) for o, _ in results}
+    for old in glob.glob(os.path.join(OBJ, "*.o")):  # objects of earlier sources / flags
+        if os.path.abspath(old) not in keep:
+            try:
+                os.remove(old)
+            except OSError:
+                pass
     tmp = OUT + f".tmp{os.getpid()}"
     res = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
                           *[o for o, _ in results]], capture_output=True, text=True)

@@ -202,6 +202,28 @@ __device__ __forceinline__ uint8_t nd_kind(const DevGraph &g, int32_t n) { retur
 __device__ __forceinline__ uint32_t nd_label(const DevGraph &g, int32_t n) { return __ldg(g.t_label + node_op(g, n)); }
 #endif
 
+// ---- TMA (cp.async.bulk) 1-D copies global -> shared, completed on an mbarrier ------------------
+#ifdef __CUDACC__
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");  // visible to the async proxy
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+// bytes: a multiple of 16; src and dst 16-byte aligned
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}"
+      ::"r"(smem_addr(bar)), "r"(parity) : "memory");
+}
+#endif
+
 // Scenario parameters as seen by the kernels.
 struct ScenParams {
   int32_t S;         // scenarios

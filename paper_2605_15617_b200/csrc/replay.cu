@@ -97,8 +97,23 @@ __global__ void __launch_bounds__(256) level_kernel(DevGraph g, ScenParams p,
   const int64_t m0 = q.mbase + (int64_t)tl.i0 * z;
   const int32_t nmem = cnt * z;
   const int32_t Sp = gridDim.y * SC;
+  // the frontier tile's member list (a contiguous run of grp_mem) is staged in shared memory by a
+  // TMA bulk copy, completed on an mbarrier, while the threads clear the accumulators; a tile of a
+  // huge group (> kTileMem members) reads its members from global memory instead
+  constexpr int kTileMem = 512;
+  __shared__ __align__(16) int32_t mem_s[kTileMem + 8];
+  __shared__ __align__(8) uint64_t bar;
+  const int64_t a0 = m0 & ~(int64_t)3, a1 = (m0 + nmem + 3) & ~(int64_t)3;  // 16-byte aligned superset
+  const bool staged = a1 - a0 <= kTileMem + 8;
+  if (staged && threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (uint32_t)((a1 - a0) * 4));
+    tma_load_1d(mem_s, g.grp_mem + a0, (uint32_t)((a1 - a0) * 4), &bar);
+  }
   for (int x = threadIdx.x; x < cnt * SC; x += 256) acc[x] = 0ULL;
   __syncthreads();
+  if (staged) mbar_wait(&bar, 0);
+  const int32_t *mem = staged ? mem_s + (m0 - a0) : g.grp_mem + m0;
 
   const int team = threadIdx.x / L, lane = threadIdx.x % L;
   const int32_t k0 = blockIdx.y * SC + lane * SPL;
@@ -110,7 +125,7 @@ __global__ void __launch_bounds__(256) level_kernel(DevGraph g, ScenParams p,
     pj[j] = (p.mask & 1u) && p.amp > 0 && (p.first + k0 + j) > 0;
   }
   for (int32_t mm = team; mm < nmem; mm += TEAMS) {
-    const int32_t n = g.grp_mem[m0 + mm];
+    const int32_t n = mem[mm];
     const int32_t gl = mm / z;
     const int32_t r = g.node_rank[n];
     const int32_t ps = g.node_prev_sync[n];
