@@ -103,6 +103,7 @@ struct CellArgs {
   uint32_t poll_sleep_max; // ... up to this
   uint32_t fast_spin, fast_sleep0, fast_sleep_max;  // the fast wait's policy (fast_sleep_max 0: off)
   uint32_t lean;       // cross_pairs: 0 off, 1 TP >= 4 cells (default), 2 every cell (PRISM_LEAN, experiments)
+  uint32_t mix;        // CTA -> cell permutation stride (1 = identity; odd: a bijection mod a power of two)
   ShardLink L;         // row e: peer exchange buffers (sharded kernels only)
 };
 
@@ -618,7 +619,7 @@ __global__ void __launch_bounds__(KS * 32, KS > 8 ? 1 : (KS > 1 ? 2 : (C == 1 ? 
   const int32_t nst = s1 - s0;
   const int32_t RC = g.cell_R > 1 ? g.cell_R : 1;  // replica cells: RC = C consecutive DP replicas
   const int32_t cells = nst * (d1 - d0) / RC / KS;  // this shard's CTAs of one chunk
-  const int32_t cell = u % cells, chunk = a.chunk0 + u / cells;
+  const int32_t cell = (int32_t)(((uint64_t)(u % cells) * a.mix) % (uint64_t)cells), chunk = a.chunk0 + u / cells;
   const int32_t s = s0 + cell % nst, dpi = d0 + ((cell / nst) * KS + sub) * RC;
   // rank r of the cell: tp index r (TP cells) or DP replica dpi + r (replica cells, tp = 1)
   auto cell_rank = [&](int32_t r) { return RC > 1 ? rank_of(g, 0, s, dpi + r) : rank_of(g, r, s, dpi); };

@@ -30,6 +30,8 @@
 // GPU.
 #include "cell_kernel.cuh"
 
+#include <numeric>
+
 namespace prism {
 
 #ifdef PRISM_CELL_STATS
@@ -193,7 +195,19 @@ cudaError_t launch_cells(const DevGraph &g, const ScenParams &p, int64_t *rslot,
   // the launch covers chunks [chunk0, chunk0 + nchunks_launch) of the replay's Sp / 32 chunks
   static const PollPolicy pol = poll_policy();
   CellArgs a{rslot, acc, rres, arrive, status, g.watchdog_ns, parity, (int32_t)units, Sp, chunk0,
-             Sp / SC, pol.spin, pol.sleep0, pol.sleep_max, pol.fspin, pol.fsleep0, pol.fsleep_max, pol.lean, ShardLink{}};
+             Sp / SC, pol.spin, pol.sleep0, pol.sleep_max, pol.fspin, pol.fsleep0, pol.fsleep_max, pol.lean, 1u, ShardLink{}};
+  {  // CTA -> cell placement: CTAs are dealt to the SMs in index order, and with the identity map
+     // an SM holds warps of only a few pipeline stages (whose busy and idle phases coincide in a
+     // 1F1B schedule); a permutation of the cells by a stride coprime with their count mixes the
+     // stages per SM (C5 cell kernel 2.66 -> 2.58 ms, any of 16 strides tried within noise of each
+     // other, tools/exp/mix_sweep.sh). PRISM_CELL_MIX overrides it (1 = identity).
+    static const uint32_t mix = [] {
+      const char *e = std::getenv("PRISM_CELL_MIX");
+      return e ? (uint32_t)std::atoi(e) : 257u;
+    }();
+    const int64_t cells = units / nchunks_launch / (link && link->lg > 0 ? link->lg : 1);
+    if (mix > 1 && std::gcd((int64_t)mix, cells) == 1) a.mix = mix;
+  }
   if (link) a.L = *link;
   DevGraph gg = g;
   ScenParams pp = p;
