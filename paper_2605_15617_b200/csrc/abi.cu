@@ -511,12 +511,18 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
     }();
     // sixteen cells of ep / 16 replicas when that width is instantiated (2 or 4), else eight
     const int ks = env_ks ? env_ks : ((tt.ep % 16 == 0 && (tt.ep / 16 == 2 || tt.ep / 16 == 4)) ? 16 : 8);
-    const bool cta = env_rc != 2 && tt.tp == 1 && tt.ep >= ks && tt.ep % ks == 0 && tt.ep / ks <= 8 &&
+    const bool cta = env_rc != 2 && tt.tp == 1 && tt.ep >= 2 * ks && tt.ep % ks == 0 && tt.ep / ks <= 8 &&
                      (n_shards == 1 || axis == 1 || (tt.dp / n_shards) % tt.ep == 0) &&
                      (ks == 8 || tt.ep / ks == 2 || tt.ep / ks == 4);
     const int R = cta ? tt.ep / ks : 8;
     const bool blocks_ok = n_shards == 1 || axis == 1 || (tt.dp / n_shards) % R == 0;
-    if (env_rc && (cta || env_rc == 2) && blocks_ok && replica_cells_ok(tt, R) && (R == 1 || R == 2 || R == 4 || R == 8)) {
+    // without EP CTAs, plain replica cells when one-rank cells could not all be co-resident (more
+    // than ~4k ranks per shard at 28 warps per SM): 8-replica warps instead of the level-by-level
+    // fallback
+    const int64_t my_ranks = (int64_t)tt.tp * tt.pp * tt.dp / std::max(1, n_shards);
+    const bool wide = tt.tp == 1 && my_ranks > 4096;
+    if (env_rc && (cta || wide || env_rc == 2) && blocks_ok && replica_cells_ok(tt, R) &&
+        (R == 2 || R == 4 || R == 8)) {
       st = plan_replica_cells(plan, R, cta ? ks : 1, err);
       if (st != PRISM_OK) return fail(st, err);
     }

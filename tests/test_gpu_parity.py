@@ -317,3 +317,24 @@ def test_async_builds_pipelined(prism):
     for g in graphs:
         g.close()
     big.close()
+
+
+@pytest.mark.parametrize("ep", [1, 8])
+def test_tp1_8192_ranks_on_cells(prism, ep):
+    """TP = 1 at 8192 ranks (the paper's S.A/S.C/S.D shapes): one-rank cells cannot
+    all be co-resident, so the replay runs replica cells (8 DP replicas per warp; EP CTAs when ep
+    allows) instead of dropping to the level-by-level path; bit-exact against the oracle."""
+    tm = w.uniform_pipeline(1, 8, 1024, 4, f_ns=700, b_ns=1300, p2p_c=40, dense_tp_layout=False)
+    if ep > 1:
+        t = tm.topo
+        tm = w.Templates(w.Topology(t.tp, t.pp, t.dp, ep, t.vpp, t.rank_order), tm.ops, tm.tmpl_ptr, tm.static_mem)
+    g = _graph(prism, tm)
+    it = g.replay(64, amp_q16=6554, kind_mask=7)
+    assert g.last_algo() == "cells"
+    ref = oracle.replay(tm, 64, amp_q16=6554, kind_mask=7, threads=NPROC, times=True)
+    assert np.array_equal(it, ref["iter"])
+    assert np.array_equal(g.peak_memory(), ref["peak"][0])
+    rp = g.export("rank_ptr")
+    for r in (0, 4095, 8191):
+        st, fi, _ = g.query_rank(r, 63)
+        assert np.array_equal(fi, ref["finish"][63, rp[r]:rp[r + 1]])
