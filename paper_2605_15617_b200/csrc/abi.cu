@@ -1534,7 +1534,7 @@ prism_status prism_critical_path(prism_graph_t G, int32_t scenario, int32_t *pat
   const int64_t pc = std::min<int64_t>(cap, P.N + 1);
   // [S iter][start node (4B, padded)][len (8B)][gstart G x 8][gbest G x 4][parent N x 4][run_start N x 4][path]
   const size_t gn = (size_t)std::max<int64_t>(P.G, 1), nn = (size_t)std::max<int64_t>(P.N, 1);
-  const size_t need = (size_t)G->last.S * 8 + 16 + gn * 12 + nn * 8 + 16 + (size_t)std::max<int64_t>(pc, 1) * 4;
+  const size_t need = (size_t)G->last.S * 8 + 16 + gn * 12 + nn * 12 + 32 + (size_t)std::max<int64_t>(pc, 1) * 4;
   if (!G->ensure(G->crit, G->crit_bytes, need)) return fail(PRISM_E_OOM, "critical-path scratch allocation failed");
   int64_t *iter = (int64_t *)G->crit;
   int32_t *startn = (int32_t *)(iter + G->last.S);
@@ -1542,11 +1542,14 @@ prism_status prism_critical_path(prism_graph_t G, int32_t scenario, int32_t *pat
   int64_t *gstart = len + 1;
   int32_t *gbest = (int32_t *)(gstart + gn);
   int32_t *parent = gbest + gn;
-  int32_t *run_start = parent + nn + 2;
-  int32_t *path = run_start + nn + 2;
+  int32_t *run_start = (int32_t *)(((uintptr_t)(parent + nn) + 15) & ~(uintptr_t)15);  // 2 N words (int2)
+  int32_t *path = run_start + 2 * nn + 4;
   const ReadView v = read_view(G, scenario);
+  // T: the unsharded replay's rank ends (multi-stream ranks included) reduce to it directly
+  const bool have_T = G->n_shards == 1;
+  if (have_T) CU(launch_reduce(P.W, G->last.S, G->last_Sp, G->rank_end, iter, G->stream));
   CU(launch_critical_path(v.g, v.p, v.fin, v.Sp, v.k, iter, startn, path, pc, len, gstart, gbest, parent, run_start,
-                                 G->stream));
+                          have_T, G->stream));
   int64_t hl = 0, hT = 0;
   CU(cudaMemcpyAsync(&hl, len, 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaMemcpyAsync(&hT, iter + v.k, 8, cudaMemcpyDeviceToHost, G->stream));

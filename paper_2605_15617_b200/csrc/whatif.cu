@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(256) crit_parent_kernel(DevGraph g, ScenParams
 // prefix max of the run-break positions), so the chase below needs two dependent loads per RUN
 // (one per hop between ranks / groups) instead of one per node.
 __global__ void __launch_bounds__(256) crit_runs_kernel(DevGraph g, const int32_t *__restrict__ parent,
-                                                        int32_t *__restrict__ run_start) {
+                                                        int2 *__restrict__ run) {
   const int lane = threadIdx.x & 31;
   const int32_t warps = gridDim.x * (blockDim.x >> 5);
   for (int32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < g.W; r += warps) {
@@ -248,23 +248,22 @@ __global__ void __launch_bounds__(256) crit_runs_kernel(DevGraph g, const int32_
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) x = max(x, __shfl_up_sync(0xffffffffu, x, off));
       x = max(x, carry);
-      if (i < re) run_start[i] = x;
+      if (i < re) run[i] = make_int2(x, parent[x]);  // the run's first node and where it leads
       carry = __shfl_sync(0xffffffffu, x, 31);
     }
   }
 }
 
-// step 5: the chase from the lowest node finishing at T (one thread): each run is written out
-// without loads, then the walk continues at the parent of the run's first node
-__global__ void crit_chase_kernel(const int32_t *__restrict__ start_node, int32_t N, const int32_t *__restrict__ parent,
-                                  const int32_t *__restrict__ run_start, int32_t *__restrict__ path, int64_t cap,
-                                  int64_t *__restrict__ len_out) {
+// step 5: the chase from the lowest node finishing at T (one thread): one dependent 8-byte load per
+// run (its first node and that node's parent), the run itself written out without loads
+__global__ void crit_chase_kernel(const int32_t *__restrict__ start_node, int32_t N, const int2 *__restrict__ run,
+                                  int32_t *__restrict__ path, int64_t cap, int64_t *__restrict__ len_out) {
   int32_t cur = *start_node;
   if (cur < 0 || cur >= N) cur = -1;  // empty graph: empty path
   int64_t len = 0;
   while (cur >= 0) {
-    const int32_t rs = __ldcg(run_start + cur);
-    const int32_t nxt = __ldcg(parent + rs);
+    const int2 rn = __ldcg(run + cur);
+    const int32_t rs = rn.x, nxt = rn.y;
     for (int32_t x = cur; x >= rs; --x, ++len)
       if (len < cap) path[len] = x;
     cur = nxt;
@@ -288,17 +287,18 @@ cudaError_t launch_durations(const DevGraph &g, const DurIn &in, const MoeIn &me
 cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const int64_t *fin, int32_t Sp, int32_t k,
                                  int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
                                  int64_t *gstart, int32_t *gbest, int32_t *parent, int32_t *run_start,
-                                 cudaStream_t st) {
+                                 bool have_T, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(scratch, 0x7F, 4, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(iter + k, 0, 8, st);
+  if (e == cudaSuccess && !have_T) e = cudaMemsetAsync(iter + k, 0, 8, st);
   if (e != cudaSuccess) return e;
   const int blocks = num_sms() * 8;
-  if (g.N > 0) view_max_kernel<<<blocks, 256, 0, st>>>(g, fin, Sp, k, iter + k);
+  if (g.N > 0 && !have_T) view_max_kernel<<<blocks, 256, 0, st>>>(g, fin, Sp, k, iter + k);
   if (g.N > 0) crit_start_kernel<<<blocks, 256, 0, st>>>(g, fin, Sp, k, iter, scratch);
   if (g.G > 0) crit_groups_kernel<<<blocks, 256, 0, st>>>(g, fin, Sp, k, gstart, gbest);
   if (g.N > 0) crit_parent_kernel<<<blocks, 256, 0, st>>>(g, p, fin, Sp, k, gstart, gbest, parent);
-  if (g.W > 0) crit_runs_kernel<<<blocks, 256, 0, st>>>(g, parent, run_start);
-  crit_chase_kernel<<<1, 1, 0, st>>>(scratch, (int32_t)g.N, parent, run_start, path, cap, len_out);
+  int2 *run = reinterpret_cast<int2 *>(run_start);  // 8-byte aligned scratch of 2 N words
+  if (g.W > 0) crit_runs_kernel<<<blocks, 256, 0, st>>>(g, parent, run);
+  crit_chase_kernel<<<1, 1, 0, st>>>(scratch, (int32_t)g.N, run, path, cap, len_out);
   return cudaGetLastError();
 }
 
