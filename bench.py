@@ -421,8 +421,12 @@ def f_rows_extra(args, tm, sh):
     r = timed_replay(g, N)
     t0 = time.perf_counter()
     path, T = g.critical_path(0)
+    cp0_ms = (time.perf_counter() - t0) * 1e3  # first call: includes the scratch allocation
+    t0 = time.perf_counter()
+    path, T = g.critical_path(0)
     cp_ms = (time.perf_counter() - t0) * 1e3
-    out["f3_whatif"] = dict(r, critical_path_ms=round(cp_ms, 3), critical_path_nodes=int(len(path)),
+    out["f3_whatif"] = dict(r, critical_path_ms=round(cp_ms, 3), critical_path_first_call_ms=round(cp0_ms, 3),
+                            critical_path_nodes=int(len(path)),
                             iteration_ns=int(T), workload=f"{args.config}, ATTN_F -> 1 ns, rank {tm.topo.world // 2} x1.12")
     g.close()
     c4 = w.config("C4")

@@ -1532,24 +1532,19 @@ prism_status prism_critical_path(prism_graph_t G, int32_t scenario, int32_t *pat
   CU(cudaSetDevice(G->device));
   const Plan &P = G->plan;
   const int64_t pc = std::min<int64_t>(cap, P.N + 1);
-  // [S iter][start node (4B, padded)][len (8B)][gstart G x 8][gbest G x 4][parent N x 4][run_start N x 4][path]
-  const size_t gn = (size_t)std::max<int64_t>(P.G, 1), nn = (size_t)std::max<int64_t>(P.N, 1);
-  const size_t need = (size_t)G->last.S * 8 + 16 + gn * 12 + nn * 12 + 32 + (size_t)std::max<int64_t>(pc, 1) * 4;
+  const ReadView v = read_view(G, scenario);
+  // [S iter][the kernels' scratch (crit_scratch_bytes)]
+  const size_t need = (size_t)G->last.S * 8 + 64 + crit_scratch_bytes(v.g, pc);
   if (!G->ensure(G->crit, G->crit_bytes, need)) return fail(PRISM_E_OOM, "critical-path scratch allocation failed");
   int64_t *iter = (int64_t *)G->crit;
-  int32_t *startn = (int32_t *)(iter + G->last.S);
-  int64_t *len = (int64_t *)(startn + 2);
-  int64_t *gstart = len + 1;
-  int32_t *gbest = (int32_t *)(gstart + gn);
-  int32_t *parent = gbest + gn;
-  int32_t *run_start = (int32_t *)(((uintptr_t)(parent + nn) + 15) & ~(uintptr_t)15);  // 2 N words (int2)
-  int32_t *path = run_start + 2 * nn + 4;
-  const ReadView v = read_view(G, scenario);
+  void *scratch = (void *)(((uintptr_t)(iter + G->last.S) + 63) & ~(uintptr_t)63);
   // T: the unsharded replay's rank ends (multi-stream ranks included) reduce to it directly
   const bool have_T = G->n_shards == 1;
   if (have_T) CU(launch_reduce(P.W, G->last.S, G->last_Sp, G->rank_end, iter, G->stream));
-  CU(launch_critical_path(v.g, v.p, v.fin, v.Sp, v.k, iter, startn, path, pc, len, gstart, gbest, parent, run_start,
-                          have_T, G->stream));
+  int32_t *pls[3];
+  CU(launch_critical_path(v.g, v.p, v.fin, v.Sp, v.k, iter, have_T, scratch, pls, pc, G->stream));
+  int32_t *path = pls[0];
+  int64_t *len = (int64_t *)pls[1];
   int64_t hl = 0, hT = 0;
   CU(cudaMemcpyAsync(&hl, len, 8, cudaMemcpyDeviceToHost, G->stream));
   CU(cudaMemcpyAsync(&hT, iter + v.k, 8, cudaMemcpyDeviceToHost, G->stream));

@@ -423,11 +423,13 @@ cudaError_t launch_durations(const DevGraph &g, const DurIn &in, const MoeIn &me
                              int64_t *efr, int64_t *gdur, int64_t *sdur, int64_t *hdur, uint32_t *status,
                              cudaStream_t st);
 // iter[k] receives T_k (max finish over every node); the walk starts at the lowest node finishing at it;
-// gstart [G] / gbest [G] / parent [N] / run [2N, 8-byte aligned]: scratch; have_T: iter[k] already holds T of the parallel parent computation
+// Row f3: the critical path of scenario k into scratch (crit_scratch_bytes of it); have_T: iter[k]
+// already holds T. path_len_start receives the device addresses of the path, its length (int64)
+// and the start node inside scratch.
+size_t crit_scratch_bytes(const DevGraph &g, int64_t path_cap);
 cudaError_t launch_critical_path(const DevGraph &g, const ScenParams &p, const int64_t *fin, int32_t Sp, int32_t k,
-                                 int64_t *iter, int32_t *scratch, int32_t *path, int64_t cap, int64_t *len_out,
-                                 int64_t *gstart, int32_t *gbest, int32_t *parent, int32_t *run_start,
-                                 bool have_T, cudaStream_t st);
+                                 int64_t *iter, bool have_T, void *scratch, int32_t *path_len_start[3],
+                                 int64_t cap, cudaStream_t st);
 // Start of every waiting replay (cells / ranks): the previous replay's abort status (word 0) is
 // folded into the sticky word (1) and cleared; after an abort the ready / result slots are reset
 // to "not yet" under this replay's parity (fill), since the aborted replay left some unwritten.

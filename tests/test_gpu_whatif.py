@@ -137,10 +137,14 @@ def test_memory_deltas(prism):
     assert e.value.name == "PRISM_E_INVALID_ARG"
 
 
+@pytest.mark.parametrize("big", [False, True])
 @pytest.mark.parametrize("seed", range(20))
-def test_critical_path_random(prism, seed):
+def test_critical_path_random(prism, seed, big):
+    """big: durations in multiples of 2^36 ns with many ties, so T >= 2^38 and the group pass takes
+    its unpacked two-pass form (ready time, then the lowest member at it)."""
     tm = w.random_templates(seed, max_world=32, max_ops=40)
-    d = np.random.default_rng(seed).integers(0, 500, tm.n_nodes)
+    rng = np.random.default_rng(seed)
+    d = rng.integers(0, 4, tm.n_nodes) << 36 if big else rng.integers(0, 500, tm.n_nodes)
     g = _graph(prism, tm)
     g.set_durations(node_dur=d)
     S = 5
@@ -149,6 +153,7 @@ def test_critical_path_random(prism, seed):
         path, T = g.critical_path(k)
         rpath, rT = oracle.critical_path(tm, k, amp_q16=6554, kind_mask=7, node_dur=d)
         assert T == rT and np.array_equal(path, rpath)
+        assert not big or T >= 1 << 38 or len(path) < 4
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
