@@ -5,6 +5,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 import numpy as np, torch
 import paper_2605_15617_b200 as prism, workloads as w
 torch.cuda.set_device(0); prism.use_torch_allocator()
+if os.environ.get("L2G"):  # cudaLimitMaxL2FetchGranularity experiment
+    import ctypes
+    rt = ctypes.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libcudart.so.12") else None
+    rt = rt or ctypes.CDLL(torch.__path__[0] + "/lib/libcudart.so.12")
+    print("setlimit", rt.cudaDeviceSetLimit(5, ctypes.c_size_t(int(os.environ["L2G"]))))
+    v = ctypes.c_size_t(0); rt.cudaDeviceGetLimit(ctypes.byref(v), 5); print("L2 fetch granularity", v.value)
 tm = w.config(os.environ.get("CFG", "C5")); sh = torch.cuda.current_stream().cuda_stream
 g = prism.Graph(tm, stream=sh)
 labs = {int(l): 1 for l in np.unique(tm.ops["label"]) if (int(l) >> 24) == w.OPCODES["ATTN_F"]}
