@@ -397,8 +397,9 @@ def run_prism(args):
 
 def s1_line(args, tm, sh):
     """The S = 1 configuration of SURVEY §8.3 ("every run at S = 1 and S = 64"): one unperturbed
-    scenario of the same graph on the rank kernel (lane = rank), device-timed (CUDA events on the
-    graph's stream), best of 5, with its own roofline fraction on the same §8(d) bytes."""
+    scenario of the same graph on the single-scenario path (segment walks + rendezvous chain,
+    replay_ranks.cu), device-timed (CUDA events on the graph's stream), best of 5, with its own
+    roofline fraction on the same §8(d) bytes."""
     import paper_2605_15617_b200 as prism
 
     g = prism.Graph(tm, stream=sh, profile=True)

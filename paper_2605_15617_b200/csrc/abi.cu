@@ -911,7 +911,8 @@ prism_status replay_ranks_impl(prism_graph_t G, const prism_scenarios *sc, int64
   const size_t nwords = std::max<size_t>(1, (size_t)P.G_large);
   {
     const StateReq q{p.record ? (size_t)std::max<int64_t>(1, G->fin_rows) * 8 : 0, (size_t)std::max<int64_t>(1, P.G) * 8,
-                     (size_t)P.W * 8, std::max<size_t>(16, (size_t)P.M_cross * 8), lg, lg, nwords * 4, 0};
+                     (size_t)P.W * 8, std::max<size_t>(16, (size_t)P.M_cross * 8), lg, lg, nwords * 4,
+                     segs_scratch_bytes(G->cur(), (int64_t)P.x_ops.size())};
     prism_status st = ensure_state(G, q);
     if (st) return st;
   }
@@ -928,15 +929,17 @@ prism_status replay_ranks_impl(prism_graph_t G, const prism_scenarios *sc, int64
   CU(cudaMemsetAsync(G->sync_words, 0, nwords * 4, G->stream));
   uint32_t *status = G->words;
   G->rec(2);
+  int nl = 1;
   CU(launch_ranks(G->cur(), p, G->rslot, G->acc, G->rres, G->sync_words, status, G->parity,
-                  p.record ? G->fin : nullptr, G->gfin, G->rank_end, G->stream));
+                  p.record ? G->fin : nullptr, G->gfin, G->rank_end, G->part, (int64_t)P.x_ops.size(), &nl,
+                  G->stream));
   G->parity ^= 1;
   CU(cudaMemcpyAsync(G->h_status, G->words, 8, cudaMemcpyDeviceToHost, G->stream));
   G->rec(3);
   G->rec(4);
   CU(launch_reduce(P.W, 1, Sp, G->rank_end, iter_dev, G->stream));
   G->rec(5);
-  G->launches = 3;  // guard, rank kernel, reduce
+  G->launches = 2 + nl;  // guard, rank kernel or segment walk + chain (+ fin walk), reduce
   G->last = p;
   G->last_Sp = Sp;
   G->recorded = p.record;

@@ -396,9 +396,11 @@ cudaError_t launch_peak_time(const DevGraph &g, const ScenParams &p, int32_t Sp,
 // replay_ranks.cu (one scenario, lane = rank)
 bool ranks_fit(const DevGraph &g, int *blocks);
 cudaError_t preload_rank_kernels();
+// seg: scratch of segs_scratch_bytes (nullptr: the one-kernel rank path); launches: kernels queued
+size_t segs_scratch_bytes(const DevGraph &g, int64_t n_cross);
 cudaError_t launch_ranks(const DevGraph &g, const ScenParams &p, int64_t *rslot, int64_t *acc, int64_t *rres,
                          uint32_t *arrive, uint32_t *status, int parity, int64_t *fin, int64_t *gfin,
-                         int64_t *rank_end, cudaStream_t st);
+                         int64_t *rank_end, int64_t *seg, int64_t n_cross, int *launches, cudaStream_t st);
 // memory.cu
 cudaError_t launch_peak(const DevGraph &g, int64_t *peak, cudaStream_t st);
 // whatif.cu (rows f1/f3/f4): device copies of prism_set_durations' inputs ...
