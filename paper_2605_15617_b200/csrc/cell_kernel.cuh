@@ -773,12 +773,8 @@ __global__ void __launch_bounds__(KS * 32, KS > 8 ? 1 : (KS > 1 ? 2 : (C == 1 ? 
       if (pair) {  // compute span i, then the TP collective i + 1 (its hash beside the span chains)
         const uint64_t uxn = __shfl_sync(0xffffffffu, bux, (j + 1) & 31);
         int64_t tq = d_n;
-        if (cpert) {
-          int64_t dd[C];
-#pragma unroll
-          for (int r = 0; r < C; ++r) dd[r] = d;
-          if (gpert) tq = perturb_x(d_n, sx ^ (uxn * K_MIX), p);
-          perturb_add_span<C, false>(t, dd, sx, rkh, (uint64_t)i * K_MIX, p);
+        if (cpert) {  // the TP hash as a ninth chain beside the span's
+          tq = perturb_add_span_q<C>(t, d, sx, rkh, (uint64_t)i * K_MIX, d_n, sx ^ (uxn * K_MIX), gpert, p);
         } else {
           if (gpert) tq = perturb_x(d_n, sx ^ (uxn * K_MIX), p);
 #pragma unroll

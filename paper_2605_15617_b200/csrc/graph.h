@@ -328,6 +328,50 @@ __device__ __forceinline__ void perturb_add_span(int64_t (&t)[C], const int64_t 
     for (int r = 0; r < C; ++r) t[r] += (d[0] * (int64_t)(uint32_t)m[r] + dc) >> 16;
   }
 }
+
+// perturb_add_span<C, false> for a (compute span, TP collective) pair, with the TP collective's
+// perturbed duration perturb_x(dq, xq) formed as a ninth chain beside the span's C chains (emitted
+// on its own, ptxas scheduled it as one serial ~40-instruction chain ahead of the span's). Returns
+// the collective's duration (dq when tp_pert is false). Bit-identical to the separate calls.
+template <int C>
+__device__ __forceinline__ int64_t perturb_add_span_q(int64_t (&t)[C], int64_t d, uint64_t sx,
+                                                      const uint32_t (&rkhi)[C], uint64_t ix, int64_t dq,
+                                                      uint64_t xq, bool tp_pert, const ScenParams &p) {
+  const uint32_t xlo = (uint32_t)sx ^ (uint32_t)ix;
+  const uint32_t zlo = xlo + 0x7F4A7C15u;
+  const uint32_t cg = 0x9E3779B9u + (zlo < xlo ? 1u : 0u);
+  const uint32_t sxh = (uint32_t)(sx >> 32), ixh = (uint32_t)(ix >> 32);
+  const uint32_t zlo30 = zlo >> 30;
+  uint64_t z[C + 1];
+#pragma unroll
+  for (int r = 0; r < C; ++r) {
+    const uint32_t zh = (sxh ^ (ixh + rkhi[r])) + cg;
+    const uint32_t lo = zlo ^ (zlo30 | (zh << 2)), hi = zh ^ (zh >> 30);
+    z[r] = ((uint64_t)hi << 32 | lo) * 0xBF58476D1CE4E5B9ULL;
+  }
+  {
+    const uint64_t zq = xq + 0x9E3779B97F4A7C15ULL;
+    z[C] = (zq ^ (zq >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  }
+#pragma unroll
+  for (int r = 0; r <= C; ++r) z[r] = z[r] ^ (z[r] >> 27);
+  uint32_t v[C + 1];
+#pragma unroll
+  for (int r = 0; r <= C; ++r) {
+    const uint32_t lo = (uint32_t)z[r], hi = (uint32_t)(z[r] >> 32);
+    v[r] = (__umulhi(lo, 0x133111EBu) + lo * 0x94D049BBu + hi * 0x133111EBu) >> 8;
+  }
+  int32_t m[C + 1];
+#pragma unroll
+  for (int r = 0; r <= C; ++r) {
+    m[r] = (int32_t)(v[r] - __umulhi(v[r], p.mod_m32) * (uint32_t)p.mod);
+    m[r] += (int32_t)((uint32_t)m[r] >> 31) * p.mod;
+  }
+  const int64_t dc = d * (int64_t)(uint32_t)(65536 - p.amp);
+#pragma unroll
+  for (int r = 0; r < C; ++r) t[r] += (d * (int64_t)(uint32_t)m[r] + dc) >> 16;
+  return tp_pert ? (dq * (int64_t)((uint32_t)m[C] + (uint32_t)(65536 - p.amp))) >> 16 : dq;
+}
 #endif
 
 // Row e: the peer-memory exchange of a sharded replay. Every shard's exchange buffer has the
