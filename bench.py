@@ -260,10 +260,14 @@ def run_prism(args):
     if ws > 1:
         torch.distributed.barrier()
     gc.disable()
-    t0 = time.perf_counter()
     pending = None
     checked = 0
-    for i in range(reps + 1):
+    step_t = []
+    t0 = None
+    for i in range(-args.warmup, reps + 1):  # the first W steps are untimed warm-up (as above)
+        if i == 0:
+            t0 = time.perf_counter()
+        step_t.append(time.perf_counter())
         cur = None
         if i < reps:
             j = i % 2
@@ -282,7 +286,7 @@ def run_prism(args):
             pev, pg, pj = pending
             pev.synchronize()
             assert (pin_it[pj].numpy() == iters).all(), "e2e step disagrees with the timed steps"
-            checked += 1
+            checked += i > 0
             if cur is None:
                 pg.sync()  # the last graph: raises if the device watchdog aborted a replay
                 gp = pg    # kept open for the serial form's first build
@@ -290,6 +294,8 @@ def run_prism(args):
                 pg.close()
         pending = cur
     e2e_ms = (time.perf_counter() - t0) * 1e3 / reps
+    step_t.append(time.perf_counter())
+    e2e_step_ms = [round((b - a) * 1e3, 3) for a, b in zip(step_t[args.warmup:], step_t[args.warmup + 1:])]
     if gc_was:
         gc.enable()
     assert checked == reps
@@ -387,7 +393,8 @@ def run_prism(args):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
                 "mode": "pipelined: step i+1's build from host templates overlaps step i's replay; each "
                         "step's templates H2D and T / peak results D2H (pinned) inside the timed region",
-                "steps": reps, "serial_ms_per_step": round(e2e_serial_ms, 3)},
+                "steps": reps, "warmup": args.warmup, "step_ms_median": sorted(e2e_step_ms)[len(e2e_step_ms) // 2],
+                "serial_ms_per_step": round(e2e_serial_ms, 3)},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
