@@ -146,16 +146,21 @@ def run_prism(args):
     # replicas: GPU i sweeps its own block of scenarios (i*S .. i*S+S-1) of one what-if sweep
     kw = dict(amp_q16=args.amp, kind_mask=7, seed=0x5EED, algo=args.algo,
               first=(rank * args.scenarios if (ws > 1 and not sharded) else 0))
-    iter_dev = torch.zeros(S, dtype=torch.int64, device="cuda")
+    iter_dev = torch.zeros(2, S, dtype=torch.int64, device="cuda")
     iter_steps = torch.zeros(max(1, args.steps), S, dtype=torch.int64, device="cuda")  # per timed step
-    peak_dev = torch.zeros(tm.topo.world, dtype=torch.int64, device="cuda")
+    peak_dev = torch.zeros(2, tm.topo.world, dtype=torch.int64, device="cuda")
     comm = [None]  # sharded: the graph currently holding the connected exchange buffer
+    # Consecutive steps' graphs alternate between two streams (unsharded runs): step i+1's build
+    # (upload + expansion kernels, ordinary launches) fills SMs while step i's cooperative replay
+    # drains in its 1F1B ramp-down; the two replays still run one after the other (a cooperative
+    # grid starts once all of its CTAs fit). Sharded graphs share one exchange buffer: one stream.
+    streams = [stream] if sharded else [stream, torch.cuda.Stream()]
 
-    def new_graph(profile=False):
-        # asynchronous build: the expansion is queued on the stream and the replay follows it
-        # there without a host round trip
+    def new_graph(profile=False, i=0):
+        # asynchronous build: the expansion is queued on the graph's stream and the replay follows
+        # it there without a host round trip
         if not sharded:
-            return prism.Graph(tm, stream=sh, profile=profile, asynchronous=True)
+            return prism.Graph(tm, stream=streams[i % len(streams)].cuda_stream, profile=profile, asynchronous=True)
         g = prism.Graph(tm, stream=sh, profile=profile, n_shards=ws, shard_index=rank, asynchronous=True)
         if comm[0] is None:
             g.shard_connect_dist(S)  # once: exchange-buffer IPC handles over torch.distributed
@@ -166,26 +171,44 @@ def run_prism(args):
 
     graphs = []
     replay_events = []  # (start, end) CUDA events around each timed replay, on its stream
+    last_end = [None]   # end event of the latest replay
+
+    step_done = []  # end event of each queued step (after its peak scan), on its stream
 
     def step(timed=False, i=0):
+        # host pacing, as a serving loop does (the e2e loop below): step i's build is queued once
+        # step i-2 has finished, i.e. while step i-1's replay is resident — queued earlier, the
+        # expansion could take SMs before that replay's cooperative grid starts and delay it
+        if len(step_done) >= 2:
+            step_done.pop(0).synchronize()
         # build first (a sharded build adopts the previous graph's exchange buffer), then release
-        # the previous step's graph; the last one survives the timed region
-        g = new_graph()
-        while graphs:
-            graphs.pop().close()
-        if timed:
-            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            ev[0].record(stream)
-        out = iter_steps[i] if timed else iter_dev
+        # the graph of two steps back (the previous one may still run on the other stream); the
+        # last ones survive the timed region
+        g = new_graph(i=i)
+        while len(graphs) > len(streams) - 1:
+            graphs.pop(0).close()
+        st_i = streams[i % len(streams)]
+        # the replay waits for the previous one explicitly (the hardware would serialise the two
+        # cooperative grids anyway), so its CUDA events bracket the replay alone while this step's
+        # expansion, queued above, overlaps the previous replay
+        if last_end[0] is not None:
+            st_i.wait_event(last_end[0])
+        ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        ev[0].record(st_i)
+        out = iter_steps[i] if timed else iter_dev[i % 2]
         g.replay_async(out.data_ptr(), S, record=True, **kw)
+        ev[1].record(st_i)
+        last_end[0] = ev[1]
         if timed:
-            ev[1].record(stream)
             replay_events.append(ev)
-        g.peak_memory_async(peak_dev.data_ptr())
+        g.peak_memory_async(peak_dev[i % 2].data_ptr())
+        done = torch.cuda.Event()
+        done.record(st_i)
+        step_done.append(done)
         graphs.append(g)
 
-    for _ in range(args.warmup):
-        step()
+    for wi in range(args.warmup):
+        step(i=wi)
     torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
@@ -196,14 +219,19 @@ def run_prism(args):
     gc.disable()  # no collector pause inside the timed loop (host work is on the step's path)
     with Clocks(local) as clk:
         e0.record(stream)
+        for s_ in streams[1:]:
+            s_.wait_event(e0)
         for i in range(args.steps):
             step(timed=True, i=i)
+        for s_ in streams[1:]:
+            stream.wait_stream(s_)
         e1.record(stream)
         torch.cuda.synchronize()
     if gc_was:
         gc.enable()
     ms = e0.elapsed_time(e1)
-    graphs[0].sync()  # raises if the device watchdog aborted a replay (prism_sync)
+    for g_ in graphs:
+        g_.sync()  # raises if the device watchdog aborted a replay (prism_sync)
     its = iter_steps.cpu().numpy()
     iters = its[0].copy()
     # every timed step replays the same workload: identical results, or a step went wrong
@@ -226,8 +254,8 @@ def run_prism(args):
     graphs.clear()
     prof = {"expand": [], "levels": [], "tail": [], "reduce": [], "peak": []}
     for i in range(3):
-        gp.replay_async(iter_dev.data_ptr(), S, record=True, **kw)
-        gp.peak_memory_async(peak_dev.data_ptr())
+        gp.replay_async(iter_dev[0].data_ptr(), S, record=True, **kw)
+        gp.peak_memory_async(peak_dev[0].data_ptr())
         t = gp.last_timing()
         for k in ("levels", "tail", "reduce", "peak"):
             prof[k].append(t[k])
@@ -242,6 +270,7 @@ def run_prism(args):
     replay_ms = sum(a.elapsed_time(b) for a, b in replay_events) / len(replay_events)
     peak_bw, peak_src = _peaks()
     achieved = ab["replay"] / (replay_ms / 1e3) / 1e9
+    iso_ms = med["levels"] + med["tail"] + med["reduce"]
 
     # ---- e2e: the public API from HOST buffers (H2D of templates, D2H of results) -------------
     # Pipelined, as a serving loop runs it: every step builds its graph from the host templates
@@ -271,16 +300,18 @@ def run_prism(args):
         cur = None
         if i < reps:
             j = i % 2
-            g = new_graph()  # (a sharded build adopts the previous graph's exchange buffer)
+            st_i = streams[i % len(streams)]  # graphs alternate streams as in the timed loop
+            g = new_graph(i=i)  # (a sharded build adopts the previous graph's exchange buffer)
             if gp is not None:
                 gp.close()
                 gp = None
             g.replay_async(dev_it[j].data_ptr(), S, record=True, **kw)
             g.peak_memory_async(dev_pk[j].data_ptr())
-            pin_it[j].copy_(dev_it[j], non_blocking=True)
-            pin_pk[j].copy_(dev_pk[j], non_blocking=True)
+            with torch.cuda.stream(st_i):
+                pin_it[j].copy_(dev_it[j], non_blocking=True)
+                pin_pk[j].copy_(dev_pk[j], non_blocking=True)
             ev = torch.cuda.Event()
-            ev.record(stream)
+            ev.record(st_i)
             cur = (ev, g, j)
         if pending is not None:
             pev, pg, pj = pending
@@ -356,6 +387,7 @@ def run_prism(args):
                             f"ranks sharded over {ws} GPUs by {shard_axis.upper()} block, exchange fused in the "
                             f"replay kernel (NVLink peer memory)" if sharded else f"replicas{ws}"),
             "l2": "working set (fin[N][S] = %.1f GB) > 126 MB L2; no flush needed" % (st["nodes"] * S * 8 / 1e9),
+            "streams": len(streams),  # step graphs alternate between them (build overlaps the replay drain)
         },
         "extra": {
             "emulated_iterations_per_s": round(S * (1 if sharded else ws) / (ms_step / 1e3), 2),
@@ -388,11 +420,15 @@ def run_prism(args):
             "state_bytes_per_call": ab["replay_state"],
             "traffic": traffic,
             "traffic_source": (f"{traffic_src} (not measured in this run)" if traffic is not None else None),
+            # context: the same replay timed alone on one stream (the profiled graph after the timed
+            # loop); in the timed loop the next step's build shares the GPU with each replay's drain
+            "isolated": {"replay_ms": round(iso_ms, 4), "frac": round(ab["replay"] / (iso_ms / 1e3) / 1e9 / peak_bw, 4)},
         },
         "e2e": {"value": round(units / (e2e_ms / 1e3), 1), "unit": "node-scenarios/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 3),
-                "mode": "pipelined: step i+1's build from host templates overlaps step i's replay; each "
-                        "step's templates H2D and T / peak results D2H (pinned) inside the timed region",
+                "mode": "pipelined: step i+1's build from host templates overlaps step i's replay (graphs "
+                        "alternate between two streams when unsharded); each step's templates H2D and T / peak "
+                        "results D2H (pinned) inside the timed region",
                 "steps": reps, "warmup": args.warmup, "step_ms_median": sorted(e2e_step_ms)[len(e2e_step_ms) // 2],
                 "serial_ms_per_step": round(e2e_serial_ms, 3)},
         "gpu_launches": launches_per_step * args.steps,
