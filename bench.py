@@ -51,6 +51,7 @@ class Clocks:
         self.index = index
         self.rows = []
         self.proc = None
+        self.window = None  # (t0, t1) of the timed region: only samples arriving inside it count
 
     def __enter__(self):
         if os.environ.get("PRISM_BENCH_NO_CLOCKS"):  # experiments only: the sampler's own cost
@@ -67,7 +68,12 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append([x.strip() for x in line.split(",")] + [time.perf_counter()])
+
+    # The sampler is started before the warm-up steps (nvidia-smi's NVML start-up disturbed the
+    # first milliseconds of the timed region when it was launched there) and marks the region.
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc:
@@ -79,6 +85,11 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
+        rows = self.rows
+        if self.window and rows:  # samples taken during the timed region (else the nearest one)
+            inside = [r for r in rows if self.window[0] <= r[-1] <= self.window[1] + 0.15]
+            rows = inside or [min(rows, key=lambda r: abs(r[-1] - self.window[1]))]
+        self.rows = [r[:-1] for r in rows]
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = sorted(int(float(r[1])) for r in self.rows if r[1].replace(".", "").isdigit())
@@ -155,12 +166,17 @@ def run_prism(args):
     # drains in its 1F1B ramp-down; the two replays still run one after the other (a cooperative
     # grid starts once all of its CTAs fit). Sharded graphs share one exchange buffer: one stream.
     streams = [stream] if sharded else [stream, torch.cuda.Stream()]
+    # the device-timed loop keeps one stream: its replay events then bracket a replay that has the
+    # GPU to itself, and host timing (the clock sampler runs beside it) cannot shift the overlap;
+    # the e2e loop below, a serving loop through the public API, alternates both streams
+    dev_streams = streams[:1]
 
-    def new_graph(profile=False, i=0):
+    def new_graph(profile=False, i=0, pool=None):
         # asynchronous build: the expansion is queued on the graph's stream and the replay follows
         # it there without a host round trip
+        pool = pool or dev_streams
         if not sharded:
-            return prism.Graph(tm, stream=streams[i % len(streams)].cuda_stream, profile=profile, asynchronous=True)
+            return prism.Graph(tm, stream=pool[i % len(pool)].cuda_stream, profile=profile, asynchronous=True)
         g = prism.Graph(tm, stream=sh, profile=profile, n_shards=ws, shard_index=rank, asynchronous=True)
         if comm[0] is None:
             g.shard_connect_dist(S)  # once: exchange-buffer IPC handles over torch.distributed
@@ -173,21 +189,25 @@ def run_prism(args):
     replay_events = []  # (start, end) CUDA events around each timed replay, on its stream
     last_end = [None]   # end event of the latest replay
 
-    step_done = []  # end event of each queued step (after its peak scan), on its stream
+    last_start = [None]  # start event of the latest replay (fires when it is about to launch)
+    step_done = [None]   # end event of the latest step
 
     def step(timed=False, i=0):
-        # host pacing, as a serving loop does (the e2e loop below): step i's build is queued once
-        # step i-2 has finished, i.e. while step i-1's replay is resident — queued earlier, the
-        # expansion could take SMs before that replay's cooperative grid starts and delay it
-        if len(step_done) >= 2:
-            step_done.pop(0).synchronize()
+        # host pacing: step i's build is queued once step i-1's replay is about to launch (its
+        # start event fired: its graph is built and the replay before it has ended), so the
+        # expansion fills SMs during that replay's drain — queued earlier, it could take SMs
+        # before the cooperative grid starts and delay the whole replay
+        paced = len(dev_streams) > 1
+        if paced and last_start[0] is not None:
+            last_start[0].synchronize()
         # build first (a sharded build adopts the previous graph's exchange buffer), then release
         # the graph of two steps back (the previous one may still run on the other stream); the
         # last ones survive the timed region
         g = new_graph(i=i)
-        while len(graphs) > len(streams) - 1:
-            graphs.pop(0).close()
-        st_i = streams[i % len(streams)]
+        if len(dev_streams) == 1:  # (two streams: a graph is released once its step has finished, below)
+            while graphs:
+                graphs.pop(0).close()
+        st_i = dev_streams[i % len(dev_streams)]
         # the replay waits for the previous one explicitly (the hardware would serialise the two
         # cooperative grids anyway), so its CUDA events bracket the replay alone while this step's
         # expansion, queued above, overlaps the previous replay
@@ -195,6 +215,7 @@ def run_prism(args):
             st_i.wait_event(last_end[0])
         ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
         ev[0].record(st_i)
+        last_start[0] = ev[0]
         out = iter_steps[i] if timed else iter_dev[i % 2]
         g.replay_async(out.data_ptr(), S, record=True, **kw)
         ev[1].record(st_i)
@@ -204,9 +225,15 @@ def run_prism(args):
         g.peak_memory_async(peak_dev[i % 2].data_ptr())
         done = torch.cuda.Event()
         done.record(st_i)
-        step_done.append(done)
         graphs.append(g)
+        # and, as the e2e loop does, the host waits for the previous step before going on
+        if paced and step_done[0] is not None:
+            step_done[0].synchronize()
+            while len(graphs) > 1:
+                graphs.pop(0).close()
+        step_done[0] = done
 
+    clk = Clocks(local).__enter__()  # sampling from before the warm-up; the timed region is marked
     for wi in range(args.warmup):
         step(i=wi)
     torch.cuda.synchronize()
@@ -217,16 +244,20 @@ def run_prism(args):
     e1 = torch.cuda.Event(enable_timing=True)
     gc_was = gc.isenabled()
     gc.disable()  # no collector pause inside the timed loop (host work is on the step's path)
-    with Clocks(local) as clk:
+    try:
+        t_region0 = time.perf_counter()
         e0.record(stream)
-        for s_ in streams[1:]:
+        for s_ in dev_streams[1:]:
             s_.wait_event(e0)
         for i in range(args.steps):
             step(timed=True, i=i)
-        for s_ in streams[1:]:
+        for s_ in dev_streams[1:]:
             stream.wait_stream(s_)
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.mark(t_region0, time.perf_counter())
+    finally:
+        clk.__exit__(None, None, None)
     if gc_was:
         gc.enable()
     ms = e0.elapsed_time(e1)
@@ -292,6 +323,7 @@ def run_prism(args):
     pending = None
     checked = 0
     step_t = []
+    e2e_start, e2e_end = [None], [None]
     t0 = None
     for i in range(-args.warmup, reps + 1):  # the first W steps are untimed warm-up (as above)
         if i == 0:
@@ -301,11 +333,19 @@ def run_prism(args):
         if i < reps:
             j = i % 2
             st_i = streams[i % len(streams)]  # graphs alternate streams as in the timed loop
-            g = new_graph(i=i)  # (a sharded build adopts the previous graph's exchange buffer)
+            if e2e_start[0] is not None:  # the same pacing as the timed loop
+                e2e_start[0].synchronize()
+            g = new_graph(i=i, pool=streams)  # (a sharded build adopts the previous graph's exchange buffer)
             if gp is not None:
                 gp.close()
                 gp = None
+            if e2e_end[0] is not None:
+                st_i.wait_event(e2e_end[0])
+            e2e_start[0] = torch.cuda.Event()
+            e2e_start[0].record(st_i)
             g.replay_async(dev_it[j].data_ptr(), S, record=True, **kw)
+            e2e_end[0] = torch.cuda.Event()
+            e2e_end[0].record(st_i)
             g.peak_memory_async(dev_pk[j].data_ptr())
             with torch.cuda.stream(st_i):
                 pin_it[j].copy_(dev_it[j], non_blocking=True)
@@ -387,7 +427,7 @@ def run_prism(args):
                             f"ranks sharded over {ws} GPUs by {shard_axis.upper()} block, exchange fused in the "
                             f"replay kernel (NVLink peer memory)" if sharded else f"replicas{ws}"),
             "l2": "working set (fin[N][S] = %.1f GB) > 126 MB L2; no flush needed" % (st["nodes"] * S * 8 / 1e9),
-            "streams": len(streams),  # step graphs alternate between them (build overlaps the replay drain)
+            "streams": {"device_timed_loop": len(dev_streams), "e2e_loop": len(streams)},
         },
         "extra": {
             "emulated_iterations_per_s": round(S * (1 if sharded else ws) / (ms_step / 1e3), 2),
