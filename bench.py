@@ -169,7 +169,9 @@ def run_prism(args):
     # the device-timed loop keeps one stream: its replay events then bracket a replay that has the
     # GPU to itself, and host timing (the clock sampler runs beside it) cannot shift the overlap;
     # the e2e loop below, a serving loop through the public API, alternates both streams
-    dev_streams = streams[:1]
+    # (PRISM_BENCH_DEV_STREAMS=2, experiments: 3.01-3.77 ms/step over four runs — the overlap
+    # depends on when the host queues each build — vs 3.22-3.27 on one stream)
+    dev_streams = streams[:int(os.environ.get("PRISM_BENCH_DEV_STREAMS", "1"))]
 
     def new_graph(profile=False, i=0, pool=None):
         # asynchronous build: the expansion is queued on the graph's stream and the replay follows
