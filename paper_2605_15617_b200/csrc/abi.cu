@@ -453,6 +453,67 @@ prism_status choose_shard_axis(const Plan &P, int n, int flags, int &axis, std::
   axis = cut_pp < cut_dp ? 1 : 0;
   return PRISM_OK;
 }
+// Plan cache (host): a build whose topology, template bytes and shard options equal an earlier
+// build's reuses that build's validated plan (plan_graph, the shard axis and the replica-cell
+// rewrite: O(template ops), ~1.6 ms for C5) — a serving loop rebuilding one workload then pays a
+// byte comparison and a copy. The key is the inputs themselves (exact; no hash), four entries,
+// least recently used first out. PRISM_PLAN_CACHE=0 turns it off.
+struct PlanCacheEntry {
+  std::vector<unsigned char> key;
+  Plan plan;
+  int axis = 0;
+};
+std::mutex g_plan_mu;
+std::vector<PlanCacheEntry> g_plan_cache;  // most recently used last
+constexpr size_t kPlanCacheEntries = 4;
+
+bool plan_key(const prism_topology &t, const prism_templates &tm, int n_shards, int shard, uint32_t flags,
+              int env_a, int env_b, std::vector<unsigned char> &key) {
+  static const bool off = [] {
+    const char *e = std::getenv("PRISM_PLAN_CACHE");
+    return e && std::atoi(e) == 0;
+  }();
+  // only well-formed inputs are keyed (plan_graph reports everything else)
+  if (off || t.pp < 1 || t.pp > (1 << 16) || tm.n_ops < 0 || tm.n_ops > (int64_t(1) << 28) ||
+      (tm.n_ops > 0 && !tm.ops) || !tm.tmpl_ptr || !tm.static_mem)
+    return false;
+  const size_t nops = (size_t)tm.n_ops * sizeof(prism_op), nptr = (size_t)(t.pp + 1) * 8, nst = (size_t)t.pp * 8;
+  key.resize(sizeof t + 8 + 5 * 4 + nops + nptr + nst);
+  unsigned char *k = key.data();
+  const int32_t o[5] = {n_shards, shard, (int32_t)flags, env_a, env_b};
+  std::memcpy(k, &t, sizeof t);
+  k += sizeof t;
+  std::memcpy(k, &tm.n_ops, 8);
+  k += 8;
+  std::memcpy(k, o, sizeof o);
+  k += sizeof o;
+  if (nops) std::memcpy(k, tm.ops, nops);
+  k += nops;
+  std::memcpy(k, tm.tmpl_ptr, nptr);
+  k += nptr;
+  std::memcpy(k, tm.static_mem, nst);
+  return true;
+}
+
+bool plan_cache_get(const std::vector<unsigned char> &key, Plan &plan, int &axis) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  for (size_t i = g_plan_cache.size(); i-- > 0;) {
+    PlanCacheEntry &e = g_plan_cache[i];
+    if (e.key.size() == key.size() && std::memcmp(e.key.data(), key.data(), key.size()) == 0) {
+      plan = e.plan;
+      axis = e.axis;
+      if (i + 1 != g_plan_cache.size()) std::rotate(g_plan_cache.begin() + i, g_plan_cache.begin() + i + 1, g_plan_cache.end());
+      return true;
+    }
+  }
+  return false;
+}
+
+void plan_cache_put(std::vector<unsigned char> &&key, const Plan &plan, int axis) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  if (g_plan_cache.size() >= kPlanCacheEntries) g_plan_cache.erase(g_plan_cache.begin());
+  g_plan_cache.push_back(PlanCacheEntry{std::move(key), plan, axis});
+}
 }  // namespace
 
 extern "C" {
@@ -487,45 +548,53 @@ prism_status prism_build_graph(const prism_topology *topo, const prism_templates
   trace("build: begin");
   Plan plan;
   std::string err;
-  prism_status st = plan_graph(*topo, *tmpl, plan, err);
-  if (st != PRISM_OK) return fail(st, err);
-  trace("build: planned");
+  prism_status st = PRISM_OK;
   int axis = 0;
-  if (n_shards > 1) {
-    st = choose_shard_axis(plan, n_shards, opts ? opts->flags : 0, axis, err);
+  static const int env_rc = [] {
+    const char *e = std::getenv("PRISM_REPLICA_CELLS");
+    return e ? std::atoi(e) : 1;
+  }();
+  static const int env_ks = [] {
+    const char *e = std::getenv("PRISM_EP_CTA_KS");
+    return e ? std::atoi(e) : 0;
+  }();
+  std::vector<unsigned char> pkey;
+  const bool keyed = plan_key(*topo, *tmpl, n_shards, shard, opts ? opts->flags : 0, env_rc, env_ks, pkey);
+  const bool cached = keyed && plan_cache_get(pkey, plan, axis);
+  if (cached) trace("build: plan from the cache");
+  if (!cached) {
+    st = plan_graph(*topo, *tmpl, plan, err);
     if (st != PRISM_OK) return fail(st, err);
-  }
-  {  // replica cells for tp = 1: R = 8 DP replicas per cell when the topology and
-     // the shard blocks allow it (PRISM_REPLICA_CELLS=0 keeps one rank per cell: experiments)
-    static const int env_rc = [] {
-      const char *e = std::getenv("PRISM_REPLICA_CELLS");
-      return e ? std::atoi(e) : 1;
-    }();
-    // EP CTAs: the 8 cells of an EP group (R = ep / 8 replicas each) share one CTA, so an EP
-    // all-to-all is a register + shared-memory max behind one barrier; a DP-block shard must then
-    // hold whole EP groups. PRISM_REPLICA_CELLS=2: replica cells of 8 without EP CTAs.
-    const Topo &tt = plan.topo;
-    static const int env_ks = [] {
-      const char *e = std::getenv("PRISM_EP_CTA_KS");
-      return e ? std::atoi(e) : 0;
-    }();
-    // sixteen cells of ep / 16 replicas when that width is instantiated (2 or 4), else eight
-    const int ks = env_ks ? env_ks : ((tt.ep % 16 == 0 && (tt.ep / 16 == 2 || tt.ep / 16 == 4)) ? 16 : 8);
-    const bool cta = env_rc != 2 && tt.tp == 1 && tt.ep >= 2 * ks && tt.ep % ks == 0 && tt.ep / ks <= 8 &&
-                     (n_shards == 1 || axis == 1 || (tt.dp / n_shards) % tt.ep == 0) &&
-                     (ks == 8 || tt.ep / ks == 2 || tt.ep / ks == 4);
-    const int R = cta ? tt.ep / ks : 8;
-    const bool blocks_ok = n_shards == 1 || axis == 1 || (tt.dp / n_shards) % R == 0;
-    // without EP CTAs, plain replica cells when one-rank cells could not all be co-resident (more
-    // than ~4k ranks per shard at 28 warps per SM): 8-replica warps instead of the level-by-level
-    // fallback
-    const int64_t my_ranks = (int64_t)tt.tp * tt.pp * tt.dp / std::max(1, n_shards);
-    const bool wide = tt.tp == 1 && my_ranks > 4096;
-    if (env_rc && (cta || wide || env_rc == 2) && blocks_ok && replica_cells_ok(tt, R) &&
-        (R == 2 || R == 4 || R == 8)) {
-      st = plan_replica_cells(plan, R, cta ? ks : 1, err);
+    trace("build: planned");
+    if (n_shards > 1) {
+      st = choose_shard_axis(plan, n_shards, opts ? opts->flags : 0, axis, err);
       if (st != PRISM_OK) return fail(st, err);
     }
+    {  // replica cells for tp = 1: R = 8 DP replicas per cell when the topology and
+       // the shard blocks allow it (PRISM_REPLICA_CELLS=0 keeps one rank per cell: experiments)
+      // EP CTAs: the 8 cells of an EP group (R = ep / 8 replicas each) share one CTA, so an EP
+      // all-to-all is a register + shared-memory max behind one barrier; a DP-block shard must then
+      // hold whole EP groups. PRISM_REPLICA_CELLS=2: replica cells of 8 without EP CTAs.
+      const Topo &tt = plan.topo;
+      // sixteen cells of ep / 16 replicas when that width is instantiated (2 or 4), else eight
+      const int ks = env_ks ? env_ks : ((tt.ep % 16 == 0 && (tt.ep / 16 == 2 || tt.ep / 16 == 4)) ? 16 : 8);
+      const bool cta = env_rc != 2 && tt.tp == 1 && tt.ep >= 2 * ks && tt.ep % ks == 0 && tt.ep / ks <= 8 &&
+                       (n_shards == 1 || axis == 1 || (tt.dp / n_shards) % tt.ep == 0) &&
+                       (ks == 8 || tt.ep / ks == 2 || tt.ep / ks == 4);
+      const int R = cta ? tt.ep / ks : 8;
+      const bool blocks_ok = n_shards == 1 || axis == 1 || (tt.dp / n_shards) % R == 0;
+      // without EP CTAs, plain replica cells when one-rank cells could not all be co-resident (more
+      // than ~4k ranks per shard at 28 warps per SM): 8-replica warps instead of the level-by-level
+      // fallback
+      const int64_t my_ranks = (int64_t)tt.tp * tt.pp * tt.dp / std::max(1, n_shards);
+      const bool wide = tt.tp == 1 && my_ranks > 4096;
+      if (env_rc && (cta || wide || env_rc == 2) && blocks_ok && replica_cells_ok(tt, R) &&
+          (R == 2 || R == 4 || R == 8)) {
+        st = plan_replica_cells(plan, R, cta ? ks : 1, err);
+        if (st != PRISM_OK) return fail(st, err);
+      }
+    }
+    if (keyed) plan_cache_put(std::move(pkey), plan, axis);
   }
 
   int ndev = 0;
