@@ -196,7 +196,10 @@ PRISM_API prism_status prism_set_allocator(prism_alloc_fn alloc, prism_free_fn f
  *   PRISM_E_DEADLOCK           the synchronization structure has a cycle
  *   PRISM_E_NEGATIVE_MEMORY    a template's running allocation drops below zero (program order)
  * On success *out owns the graph. Blocks until the device work is complete unless
- * opts.flags has PRISM_BUILD_ASYNC. */
+ * opts.flags has PRISM_BUILD_ASYNC. Host plan cache: a build whose topology, template arrays
+ * (ops, tmpl_ptr, static_mem, compared byte for byte) and shard options (n_shards, shard_index,
+ * flags) equal one of the last four successful builds' reuses that build's validated plan instead
+ * of planning again (same result; the environment variable PRISM_PLAN_CACHE=0 disables it). */
 PRISM_API prism_status prism_build_graph(const prism_topology *topo, const prism_templates *tmpl,
                                const prism_build_opts *opts, prism_graph_t *out);
 
