@@ -330,7 +330,9 @@ PRISM_API prism_status prism_shard_adopt(prism_graph_t g, prism_graph_t from);
  *   routed (prism_set_moe_load);  d = label_dur[i] if label(n) == labels[i];
  *   d = (d * rank_slow_q16[rank(n)]) >> 16 if node n is a compute span.
  * A synchronization group lasts the max of its members' effective durations (reading Z2), and
- * scenario perturbation (prism_scenarios) applies on top. Arrays are host, copied. Applies to all
+ * scenario perturbation (prism_scenarios) applies on top. Arrays are copied: node_dur, node_alloc
+ * and node_free may be host or device pointers (unified addressing; measured durations already on
+ * the GPU are copied device to device), the label arrays and rank_slow_q16 are host. Applies to all
  * later replays / peak scans until reset with d == NULL (or all fields empty); invalidates the
  * recorded replay. Errors: PRISM_E_INVALID_ARG (duration outside [0, 2^40], memory delta outside
  * [0, 2^43], factor outside [0, 2^20], duplicate label), PRISM_E_UNKNOWN_LABEL (no node carries a

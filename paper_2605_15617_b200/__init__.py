@@ -340,12 +340,24 @@ class Graph:
             keep.append(a)
             return a.ctypes.data
 
+        def node_arr(a):  # per-node arrays: host (numpy) or a CUDA int64 tensor (copied on the device)
+            if a is not None and type(a).__module__.startswith("torch") and getattr(a, "is_cuda", False):
+                import torch
+
+                if a.dtype != torch.int64 or a.dim() != 1 or not a.is_contiguous():
+                    raise ValueError("per-node device arrays must be contiguous 1-D int64 CUDA tensors")
+                if a.numel() != self.stats()["nodes"]:
+                    raise ValueError("per-node arrays need one entry per node")
+                keep.append(a)
+                return a.data_ptr()
+            return arr(a, np.int64)
+
         labs = sorted((label_dur or {}).items())
         la = np.array([int(k) for k, _ in labs], np.uint32)
         ld = np.array([int(v) for _, v in labs], np.int64)
-        d = _Durations(arr(node_dur, np.int64), arr(la, np.uint32) if len(la) else None,
+        d = _Durations(node_arr(node_dur), arr(la, np.uint32) if len(la) else None,
                        arr(ld, np.int64) if len(ld) else None, len(labs), 0, arr(rank_slow_q16, np.int32),
-                       arr(node_alloc, np.int64), arr(node_free, np.int64))
+                       node_arr(node_alloc), node_arr(node_free))
         _check(lib().prism_set_durations(self._h, ctypes.byref(d)))
 
     def set_moe_load(self, op_event=None, br_q16=None, scale: int = MOE_DUR | MOE_ALLOC | MOE_FREE) -> None:

@@ -1515,8 +1515,10 @@ prism_status prism_set_durations(prism_graph_t G, const prism_durations *d) {
     hd[i] = lab[i].second;
   }
   cudaError_t e = cudaSuccess;
+  // cudaMemcpyDefault (unified addressing): node_dur / node_alloc / node_free may be device arrays
+  // (measured durations already on the GPU: a device-to-device copy instead of a pageable upload)
   auto up = [&](size_t o, const void *src, size_t bytes) {
-    if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(B + o, src, bytes, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(B + o, src, bytes, cudaMemcpyDefault, st);
   };
   if (d->node_dur) up(o_base, d->node_dur, N * 8);
   up(o_lab, hl.data(), L * 4);

@@ -270,3 +270,29 @@ def test_moe_two_rank_golden(prism):
     assert g.replay(1)[0] == G["iter"][0]
     assert g.peak_memory().tolist() == G["peak"]
     assert g.query_rank(0)[1].tolist() == G["finish_rank0"] and g.query_rank(1)[1].tolist() == G["finish_rank1"]
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_device_arrays_equal_host_arrays(prism, name):
+    """prism_set_durations with per-node arrays already on the GPU (a CUDA int64 tensor, copied
+    device to device) replays exactly as the same values from host memory, and as the oracle."""
+    import torch
+
+    tm = w.scaled(name)
+    nt = oracle.node_table(tm)
+    rng = np.random.default_rng(11)
+    d = (nt["dur"] * rng.integers(90, 111, tm.n_nodes)) // 100
+    al = rng.integers(0, 1000, tm.n_nodes)  # every node frees what it allocated: totals stay >= 0
+    fr = al.copy()
+    g_host, ref = _check(prism, tm, 33, d, node_alloc=al, node_free=fr, times=False)
+    g = _graph(prism, tm)
+    g.set_durations(node_dur=torch.from_numpy(np.ascontiguousarray(d, np.int64)).cuda(),
+                    node_alloc=torch.from_numpy(np.ascontiguousarray(al, np.int64)).cuda(),
+                    node_free=torch.from_numpy(np.ascontiguousarray(fr, np.int64)).cuda())
+    it = g.replay(33, amp_q16=6554, kind_mask=7)
+    assert np.array_equal(it, ref["iter"])
+    assert np.array_equal(g.peak_memory(), ref["peak"][0])
+    with pytest.raises(ValueError):
+        g.set_durations(node_dur=torch.zeros(3, dtype=torch.int64, device="cuda"))
+    with pytest.raises(ValueError):
+        g.set_durations(node_dur=torch.zeros(tm.n_nodes, dtype=torch.int32, device="cuda"))
