@@ -81,6 +81,7 @@ struct XRec {
   int32_t hb[kMaxSlots];
   int64_t dur[kMaxSlots];
   uint64_t uid[kMaxSlots];
+  int32_t grp[kMaxSlots];  // batched P2P nodes (ns > 1): each group's id, for its finish in gfin
 };
 __device__ __forceinline__ void load_xrec(const DevGraph &g, XRec &x, int32_t h0, int32_t ns) {
   x.h0 = h0;
@@ -91,11 +92,14 @@ __device__ __forceinline__ void load_xrec(const DevGraph &g, XRec &x, int32_t h0
     x.hb[q] = 0;
     x.dur[q] = 0;
     x.uid[q] = 0;
+    x.grp[q] = 0;
     if (q < ns) {
       x.meta[q] = g.h_meta[h0 + q];
       x.hb[q] = g.h_base[h0 + q];
       x.dur[q] = g.h_dur[h0 + q];
       x.uid[q] = g.h_uid[h0 + q];
+      // loaded with the rest (one cross op ahead): the finish's gfin store then waits for no load
+      if (ns > 1) x.grp[q] = g.node_grp[h0 + q];
     }
   }
 }
@@ -181,7 +185,7 @@ __device__ __forceinline__ bool cross_sync(const DevGraph &g, const ScenParams &
     if (pr) gd = perturb_x(gd, sx ^ (uid * K_MIX), p);
     const int64_t f = val[q] + gd;
     fr = max(fr, f);
-    if (x.ns > 1) gfin[g.node_grp[x.h0 + q]] = f;  // batched P2P groups' finishes, for queries
+    if (x.ns > 1) gfin[x.grp[q]] = f;  // batched P2P groups' finishes, for queries
   }
   *out = fr;
   return true;
