@@ -467,11 +467,13 @@ __global__ void __launch_bounds__(32, 16) seg_chain_kernel(DevGraph g, ScenParam
   };
   XRec xr, xn;  // this cross op's records and the next one's (loaded a rendezvous ahead)
   int32_t ti = 0, tn = 0;  // their template indices
-  auto load_x = [&](int32_t j, XRec &x, int32_t &ti_) {
+  // the slot records of op j are addressed by its XOp entry, which is loaded one rendezvous
+  // earlier still (xq): loading both at once made the warp wait for the entry before its deposit
+  XOp xq{0, 0, 0, 0};
+  auto load_x = [&](int32_t j, const XOp &xo, XRec &x, int32_t &ti_) {
     int32_t h0 = 0, ns = 0;
     ti_ = 0;
     if (j < nx) {
-      const XOp xo = g.x_ops[xs + j];
       h0 = rs + xo.hoff;
       ns = active ? min(xo.ns, kMaxSlots) : 0;
       ti_ = xo.tidx;
@@ -480,7 +482,9 @@ __global__ void __launch_bounds__(32, 16) seg_chain_kernel(DevGraph g, ScenParam
   };
   int64_t fl, dT, pre, end;
   load_sum(0, fl, dT, pre, end);
-  load_x(0, xn, tn);
+  if (0 < nx) xq = g.x_ops[xs];
+  load_x(0, xq, xn, tn);
+  if (1 < nx) xq = g.x_ops[xs + 1];
   int64_t t = 0;  // the current segment's start s_r
   for (int32_t j = 0; j <= nx; ++j) {
     int64_t m = t + pre;
@@ -493,9 +497,11 @@ __global__ void __launch_bounds__(32, 16) seg_chain_kernel(DevGraph g, ScenParam
     xr = xn;
     ti = tn;
     const int32_t i = ti;
-    // the next segment's summary and cross op records load during this rendezvous
+    // the next segment's summary and cross op records load during this rendezvous, and the XOp
+    // entry of the op after
     load_sum(j + 1, fl, dT, pre, end);
-    load_x(j + 1, xn, tn);
+    load_x(j + 1, xq, xn, tn);
+    if (j + 2 < nx) xq = g.x_ops[xs + j + 2];
     int64_t fr = 0;
     if (!cross_sync(g, p, a, xr, ready, sx, gpert, ppert, gfin, &fr)) return;
     t = fr;
