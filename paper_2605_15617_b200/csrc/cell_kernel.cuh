@@ -696,6 +696,10 @@ __global__ void __launch_bounds__(KS * 32, KS > 8 ? 1 : (KS > 1 ? 2 : (C == 1 ? 
     xo = g.x_ops[xk];
     prefetch_cross<SH>(g, xo, rsh, C, pre, crec0 + xk);
   }
+  // the XOp entry of the cross op after next, loaded a cross op early: prefetching the next op's
+  // records right after a cross op then does not first wait for its entry
+  XOp xq{len, 0, 0, 0};
+  if (xk + 1 < xend) xq = g.x_ops[xk + 1];
   int64_t pd[PR ? C : 1];  // PR: per-rank durations of the next op
   if (PR) {
 #pragma unroll
@@ -886,8 +890,9 @@ __global__ void __launch_bounds__(KS * 32, KS > 8 ? 1 : (KS > 1 ? 2 : (C == 1 ? 
           aborted = true;
         }
         if (++xk < xend) {  // next cross op: its records load while the compute spans run
-          xo = g.x_ops[xk];
+          xo = xq;
           prefetch_cross<SH>(g, xo, rsh, C, pre, crec0 + xk);
+          if (xk + 1 < xend) xq = g.x_ops[xk + 1];
         }
 #ifdef PRISM_CELL_STATS
         if (lane == 0) {
