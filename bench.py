@@ -59,7 +59,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -192,6 +192,7 @@ def run_prism(args):
     last_end = [None]   # end event of the latest replay
 
     last_start = [None]  # start event of the latest replay (fires when it is about to launch)
+    build_events = []    # timed steps: recorded before each build is queued
     step_done = [None]   # end event of the latest step
 
     def step(timed=False, i=0):
@@ -205,6 +206,10 @@ def run_prism(args):
         # build first (a sharded build adopts the previous graph's exchange buffer), then release
         # the graph of two steps back (the previous one may still run on the other stream); the
         # last ones survive the timed region
+        if timed:  # the step's device work starts with its build (upload + expansion)
+            eb = torch.cuda.Event(enable_timing=True)
+            eb.record(dev_streams[i % len(dev_streams)])
+            build_events.append(eb)
         g = new_graph(i=i)
         if len(dev_streams) == 1:  # (two streams: a graph is released once its step has finished, below)
             while graphs:
@@ -246,18 +251,24 @@ def run_prism(args):
     e1 = torch.cuda.Event(enable_timing=True)
     gc_was = gc.isenabled()
     gc.disable()  # no collector pause inside the timed loop (host work is on the step's path)
+    mem0 = torch.cuda.memory_stats()
     try:
         t_region0 = time.perf_counter()
         e0.record(stream)
         for s_ in dev_streams[1:]:
             s_.wait_event(e0)
+        host_t = []
         for i in range(args.steps):
+            host_t.append(time.perf_counter())
             step(timed=True, i=i)
+        host_t.append(time.perf_counter())
         for s_ in dev_streams[1:]:
             stream.wait_stream(s_)
         e1.record(stream)
         torch.cuda.synchronize()
         clk.mark(t_region0, time.perf_counter())
+        host_step_ms = sorted((b - a) * 1e3 for a, b in zip(host_t, host_t[1:]))
+        mem1 = torch.cuda.memory_stats()
     finally:
         clk.__exit__(None, None, None)
     if gc_was:
@@ -301,6 +312,7 @@ def run_prism(args):
     # the roofline's duration: the replay launches of the timed steps themselves (CUDA events on
     # the launching stream, averaged); the profiled graph's split is reported beside it
     replay_ms = sum(a.elapsed_time(b) for a, b in replay_events) / len(replay_events)
+    bt = [b.elapsed_time(r[0]) for b, r in zip(build_events, replay_events)]
     peak_bw, peak_src = _peaks()
     achieved = ab["replay"] / (replay_ms / 1e3) / 1e9
     iso_ms = med["levels"] + med["tail"] + med["reduce"]
@@ -436,6 +448,17 @@ def run_prism(args):
             "iteration_time_ns_scenario0": int(iters[0]),
             "device_ms": {k: round(v, 4) for k, v in med.items()},
             "replay_ms_timed_steps": round(replay_ms, 4),
+            # host time to queue one step (build from host templates + replay + peak calls): the
+            # device step is only fed when this stays below it
+            "host_queue_ms": {"median": round(host_step_ms[len(host_step_ms) // 2], 3),
+                              "p90": round(host_step_ms[int(len(host_step_ms) * 0.9)], 3),
+                              "max": round(host_step_ms[-1], 3)},
+            # device time of each timed step from the event before its build to its replay's start
+            # (upload + expansion + any gap), median / max
+            "build_to_replay_ms": {"median": round(sorted(bt)[len(bt) // 2], 3), "max": round(max(bt), 3)},
+            # caching-allocator segments created (cudaMalloc) inside the timed region
+            "timed_region_new_segments": int(mem1.get("segment.all.allocated", 0) - mem0.get("segment.all.allocated", 0)),
+            "timed_region_alloc_retries": int(mem1.get("num_alloc_retries", 0) - mem0.get("num_alloc_retries", 0)),
             "s1": s1,
             "next_rows": frows,
             "paper_context": {
