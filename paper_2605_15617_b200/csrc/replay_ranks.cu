@@ -339,9 +339,21 @@ __global__ void __launch_bounds__(128) seg_walk_kernel(DevGraph g, ScenParams p,
   const int64_t wid = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   if (wid >= (int64_t)nsegs * dchunks) return;  // whole warps only
   const int32_t gs = (int32_t)(wid / dchunks), chunk = (int32_t)(wid % dchunks);
-  int32_t s = 0;
-  while (s + 1 < g.pp && g.x_ptr[s + 1] + s + 1 <= gs) ++s;
-  const int32_t xs = g.x_ptr[s], nx = g.x_ptr[s + 1] - xs, j = gs - xs - s;
+  // the segment's stage: the last s whose first segment x_ptr[s] + s is <= gs. pp <= 32: one
+  // coalesced load of x_ptr and a ballot (the scan below costs a dependent round trip per stage)
+  int32_t s = 0, xs, nx;
+  if (g.pp <= 31) {
+    const int32_t xv = lane <= g.pp ? g.x_ptr[lane] + lane : 0x7FFFFFFF;
+    const uint32_t m = __ballot_sync(0xffffffffu, lane < g.pp && xv <= gs);
+    s = 31 - __clz((int)m);
+    xs = __shfl_sync(0xffffffffu, xv, s) - s;
+    nx = __shfl_sync(0xffffffffu, xv, s + 1) - (s + 1) - xs;
+  } else {
+    while (s + 1 < g.pp && g.x_ptr[s + 1] + s + 1 <= gs) ++s;
+    xs = g.x_ptr[s];
+    nx = g.x_ptr[s + 1] - xs;
+  }
+  const int32_t j = gs - xs - s;
   const int32_t len = (int32_t)g.t_len[s];
   const int32_t i0 = j == 0 ? 0 : g.x_ops[xs + j - 1].tidx + 1;
   const int32_t i1 = j < nx ? g.x_ops[xs + j].tidx : len;
