@@ -189,7 +189,7 @@ __device__ __forceinline__ OpF load_opf(const DevGraph &g, int64_t ti) {
 // version moved 2.3 GB of template reads through L2 for 1.3 GB of graph writes on C5).
 constexpr int kRanksPerBlock = 8;
 
-__global__ void __launch_bounds__(256, 2) expand_nodes_kernel(DevGraph g) {
+__global__ void __launch_bounds__(256, 4) expand_nodes_kernel(DevGraph g) {
   __shared__ int32_t s_r[kRanksPerBlock], s_rb[kRanksPerBlock], s_slot0[kRanksPerBlock];
   __shared__ int32_t s_tpi[kRanksPerBlock], s_dpi[kRanksPerBlock];
   const int32_t per_stage = g.W / g.pp;  // tp * dp ranks run each stage template
