@@ -291,6 +291,25 @@ def test_single_scenario_full_size_c5(prism):
     assert it[0] == oracle.replay(tm, 1, scen_first=3, amp_q16=6554, kind_mask=7, peaks=False)["iter"][0]
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_single_scenario_full_size_configs(prism, name):
+    """One perturbed scenario of the full-size configs (segment path for C2 / C3, the cell kernel
+    for C4's EP-CTA plan): T and every rank's last finish against the oracle."""
+    tm = w.config(name)
+    g = _graph(prism, tm)
+    it = g.replay(1, amp_q16=6554, kind_mask=7, first=5)
+    assert g.last_algo() == ("cells" if name == "C4" else "ranks")
+    ref = oracle.replay(tm, 1, scen_first=5, amp_q16=6554, kind_mask=7, threads=NPROC)
+    assert it[0] == ref["iter"][0]
+    rp = g.export("rank_ptr")
+    W = tm.topo.world
+    for r in np.random.default_rng(5).choice(W, 48, replace=False):
+        st, fi, _ = g.query_rank(int(r), 0)
+        assert fi[-1] == ref["rank_end"][0, r], (name, r)
+    assert np.array_equal(g.peak_memory(), ref["peak"][0])  # program order: any scenario's
+
+
 # ------------------------------------------------------------------ asynchronous build pipeline
 def test_async_builds_pipelined(prism):
     """Ten graphs built back to back with asynchronous builds on one stream (more than the four
