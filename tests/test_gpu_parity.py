@@ -213,6 +213,28 @@ def test_full_size(prism, name):
     g.close()
 
 
+@pytest.mark.slow
+def test_full_size_c5_per_op_times(prism):
+    """C5 at full size in the bench launch configuration (S = 64, cell kernel): every op's start and
+    finish of sampled ranks (all stages, both scenario chunks) equal the oracle's, scenario by
+    scenario (the oracle's per-node times of all 64 scenarios would take 18 GB: single scenarios)."""
+    tm = w.config("C5")
+    g = _graph(prism, tm)
+    S = 64
+    g.replay(S, amp_q16=6554, kind_mask=7)
+    assert g.last_algo() == "cells"
+    rp = g.export("rank_ptr")
+    rng = np.random.default_rng(64)
+    ranks = sorted(set(rng.choice(tm.topo.world, 12, replace=False).tolist()) | {0, tm.topo.world - 1})
+    for k in (0, 37, 63):
+        ref = oracle.replay(tm, 1, scen_first=k, amp_q16=6554, kind_mask=7, times=True, peaks=False)
+        for r in ranks:
+            st, fi, _ = g.query_rank(r, k)
+            a, b = rp[r], rp[r + 1]
+            assert np.array_equal(st, ref["start"][0, a:b]) and np.array_equal(fi, ref["finish"][0, a:b]), (k, r)
+    g.close()
+
+
 def test_wide_tp_uses_levels(prism):
     """tp > 8 has no cell-kernel instantiation: the auto schedule falls back to one launch per
     frontier level, bit-exact as well; a multi-stream graph with tp > 8 is refused."""
