@@ -89,19 +89,19 @@ class Clocks:
         if self.window and rows:  # samples taken during the timed region (else the nearest one)
             inside = [r for r in rows if self.window[0] <= r[-1] <= self.window[1] + 0.15]
             rows = inside or [min(rows, key=lambda r: abs(r[-1] - self.window[1]))]
-        self.rows = [r[:-1] for r in rows]
-        if not self.rows:
+        rows = [r[:-1] for r in rows]  # (the arrival time is the last field)
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(int(float(r[1])) for r in self.rows if r[1].replace(".", "").isdigit())
-        mx = max(int(float(r[2])) for r in self.rows if r[2].replace(".", "").isdigit())
+        sm = sorted(int(float(r[1])) for r in rows if r[1].replace(".", "").isdigit())
+        mxs = [int(float(r[2])) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             for i, n in enumerate(names):
                 if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
                     reasons.add(n)
-        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": max(mxs) if mxs else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
 
 
 def _dist():

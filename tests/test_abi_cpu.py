@@ -129,3 +129,27 @@ def test_bench_reference_arm_runs():
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_clock_window():
+    """bench.Clocks keeps the samples that arrived during the timed region (else the nearest one),
+    reports the median SM clock and any throttle reason, and can be summarised twice."""
+    import importlib.util
+    import os
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(root, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    c = bench.Clocks(0)
+    row = lambda sm, t, slow="Not Active": ["0", str(sm), "1965", "700.0", "0x0", slow, "Not Active",
+                                             "Not Active", "Not Active", t]
+    c.rows = [row(1000, 0.5), row(1965, 10.0), row(1950, 10.1), row(1965, 10.2, "Active"), row(900, 20.0)]
+    c.mark(9.95, 10.25)
+    s1 = c.summary()
+    assert s1 == {"sm_mhz": 1965, "sm_max_mhz": 1965, "reasons": ["hw_slowdown"], "samples": 3}
+    assert c.summary() == s1
+    c.mark(30.0, 30.1)  # no sample inside: the nearest one
+    assert c.summary()["samples"] == 1 and c.summary()["sm_mhz"] == 900
+    c.rows = []
+    assert c.summary()["reasons"] == ["unsampled"]
