@@ -185,16 +185,25 @@ struct PinnedStage {
       S.dev = dev;
     }
     if (S.cap < bytes) {
-      if (S.p) cudaFreeHost(S.p);
-      S.p = nullptr;
-      S.cap = 0;
+      // every slot is (re)allocated at once, at the size this build needs: pinning host memory
+      // (cudaMallocHost) takes tens of milliseconds, and a slot first used by a later build stalled
+      // that build's host thread (a serving loop's 4th build: one 47 ms stall in a timed region)
       const size_t cap = std::max(bytes + bytes / 4, (size_t)1 << 20);
-      if (cudaMallocHost((void **)&S.p, cap) != cudaSuccess) {
-        S.p = nullptr;
-        cudaGetLastError();
-        return;
+      for (int k = 0; k < 4; ++k) {
+        PinnedRing::Slot &T = R.slot[(i + k) % 4];
+        if (T.cap >= bytes) continue;
+        if (T.ev && k > 0) cudaEventSynchronize(T.ev);  // its previous copy has completed
+        if (T.p) cudaFreeHost(T.p);
+        T.p = nullptr;
+        T.cap = 0;
+        if (cudaMallocHost((void **)&T.p, cap) != cudaSuccess) {
+          T.p = nullptr;
+          cudaGetLastError();
+          if (k == 0) return;
+          continue;
+        }
+        T.cap = cap;
       }
-      S.cap = cap;
     }
     R.next = (i + 1) % 4;
     idx = i;
