@@ -169,8 +169,8 @@ def run_prism(args):
     # the device-timed loop keeps one stream: its replay events then bracket a replay that has the
     # GPU to itself, and host timing (the clock sampler runs beside it) cannot shift the overlap;
     # the e2e loop below, a serving loop through the public API, alternates both streams
-    # (PRISM_BENCH_DEV_STREAMS=2, experiments: 3.01-3.77 ms/step over four runs — the overlap
-    # depends on when the host queues each build — vs 3.22-3.27 on one stream)
+    # (PRISM_BENCH_DEV_STREAMS=2, experiments: 2.90-3.31 ms/step over five runs, the replays'
+    # own events at 0.46-0.51 of the roofline, vs 3.05-3.07 ms and 0.54 on one stream)
     dev_streams = streams[:int(os.environ.get("PRISM_BENCH_DEV_STREAMS", "1"))]
 
     def new_graph(profile=False, i=0, pool=None):
