@@ -330,7 +330,9 @@ class Graph:
                       node_free=None) -> None:
         """Per-node durations (f1 calibration input), label overrides {label: ns} and per-rank
         compute slowdown in Q16 (f3 what-if / fault injection), per-node memory deltas (f4); no
-        arguments = back to the templates. Applies to later replays (prism_set_durations)."""
+        arguments = back to the templates. Applies to later replays (prism_set_durations).
+        node_dur / node_alloc / node_free: numpy arrays or contiguous 1-D int64 CUDA tensors (one
+        entry per node; copied on the device, no host upload)."""
         keep = []
 
         def arr(a, dt):
